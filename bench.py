@@ -1,0 +1,283 @@
+"""Benchmark: k-means Lloyd iterations/s on BASELINE config 1 (5M x 18 fp32, k=8,
+20 iterations), split=0 over N GPUs (strong scaling), plus the roofline of the
+dominant kernel and the reference CPU path timed on this box's host cores.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one kmeans_fit (validation pass + init + 20 Lloyd iterations + the
+f64 centroids back on the host) on the synthetic input already resident in
+HBM.  Under torchrun (N > 1) every rank holds its chunk_map shard; the timed
+region is bracketed by a barrier + device synchronize and the reported time is
+the max over ranks.  L2 is flushed (a 512 MB write) before every step; inside a
+step the 20 iterations re-read X, as the algorithm does.
+
+`--impl reference` times the reference's own implementation (oracle/_ref =
+the unmodified /root/reference sources compiled by oracle/Makefile) on the
+host cores with its own bench protocol (tools/bench.cpp:84-112).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ROWS, N_FEAT, K, ITERS, SEED = 5_000_000, 18, 8, 20, 42
+METRIC = "k-means Lloyd iters/s (5M x 18 fp32, k=8, 20 iters/fit)"
+UNIT = "iters/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def config(n_gpus):
+    return {"workload": "BASELINE configs[0]: k-means k=8, 20 Lloyd iterations, synthetic 5M x 18 fp32 "
+                        "(random_uniform<float> seed 42), split=0",
+            "rows": N_ROWS, "features": N_FEAT, "k": K, "iters_per_step": ITERS, "seed": SEED,
+            "parallelism": f"row shards over {n_gpus} GPU(s) (chunk_map), one f64 stats exchange/iter",
+            "l2": "flushed (512 MB write) before every step; X re-read by the 20 iterations inside a step"}
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------- reference
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.bind import Reference
+
+    if not Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdndref.so not built"}))
+        return
+    cores = host_cores()
+    # bound each step: the full 5M x 18 input, all host cores as rank-threads;
+    # fewer Lloyd iterations per step when the box has few cores
+    iters = ITERS if cores >= 32 else 5
+    R = Reference()
+    secs, chk = R.bench(0, N_ROWS, N_FEAT, K, iters, SEED, cores, args.warmup, args.steps)
+    mean = float(statistics.fmean(secs))
+    value = iters / mean
+    sample = (f"kmeans_fit(5M x 18 f64 of random_uniform<float>, k=8, {iters} iters, tol 0) per step, "
+              f"run_world({cores}) loopback rank-threads, tools/bench.cpp protocol")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config(args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "std_seconds": float(statistics.pstdev(secs)), "checksum": chk,
+    }))
+
+
+def cpu_baseline():
+    """oracle/_ref on a bounded sample (rank 0, N=1 only)."""
+    from oracle.bind import Reference
+
+    if not Reference.available():
+        return None
+    cores = host_cores()
+    iters = 3
+    R = Reference()
+    secs, _ = R.bench(0, N_ROWS, N_FEAT, K, iters, SEED, cores, 0, 1)
+    return {"value": iters / float(secs[0]), "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"kmeans_fit on the full 5M x 18 input with {iters} Lloyd iterations "
+                      f"(init included), run_world({cores}) rank-threads, one timed run"}
+
+
+# ---------------------------------------------------------------------- ours
+class ClockSampler:
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_bench_{os.getpid()}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            f = [c.strip() for c in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic():
+    """dram bytes per launch of the assign kernel from the committed ncu summary."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_kmeans_assign.json")))
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    import paper_2007_13552_b200.api as dnd
+    from paper_2007_13552_b200 import _lib
+
+    comm = dnd.Communicator.from_torch_distributed(local) if world > 1 else dnd.Communicator(local)
+    x = dnd.random_uniform((N_ROWS, N_FEAT), 0, SEED, comm)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        model = dnd.kmeans_fit(x, K, ITERS, 0.0, SEED)
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = comm.launches
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)  # L2 flush, outside the timed window
+        starts[i].record(stream)
+        model = dnd.kmeans_fit(x, K, ITERS, 0.0, SEED)
+        ends[i].record(stream)
+    barrier()
+    launches = comm.launches - launches0
+    clk = clocks.stop()
+    t_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if dist:
+        t = torch.tensor([t_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    value = ITERS * args.steps / (t_ms / 1e3)
+
+    # ---- e2e through the public API with host buffers: pinned H2D of this
+    # rank's shard + fit + f64 centroids back, every step
+    host_x = x.tile.cpu().pin_memory()
+    dev_x = torch.empty_like(x.tile)
+    xe = dnd.DndArray(x.shape, 0, comm, dev_x)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        dev_x.copy_(host_x, non_blocking=True)
+        model_e = dnd.kmeans_fit(xe, K, ITERS, 0.0, SEED)
+    e1.record(stream)
+    barrier()
+    te_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([te_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        te_ms = float(t.item())
+    e2e = {"value": ITERS * args.steps / (te_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": int(host_x.numel() * 4) * world,
+           "d2h_bytes_per_step": int((K * N_FEAT + ITERS) * 8) * world,
+           "path": "paper_2007_13552_b200.api.kmeans_fit -> dndc_kmeans_fit_f32 (C-ABI), pinned host X"}
+    assert abs(model_e.inertia_trace[-1] - model.inertia_trace[-1]) <= 1e-9 * model.inertia_trace[-1]
+
+    # ---- roofline of the dominant kernel (assign + accumulate), timed alone
+    import ctypes as C
+
+    ms, byt = C.c_double(), C.c_double()
+    _lib.check(_lib.lib().dndc_kmeans_time_assign_f32(comm.handle, x.tile.data_ptr(), x.tile.shape[0], N_FEAT, K,
+                                                      50, C.byref(ms), C.byref(byt)))
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured" if peak else "fallback"
+    peak = peak or 6650.0
+    achieved = byt.value / (ms.value * 1e-3) / 1e9
+    iter_us = t_ms * 1e3 / (ITERS * args.steps)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": ncu_traffic(), "kernel": "kmeans_assign_kernel<float,18>",
+            "algorithmic_bytes_per_launch": byt.value, "avg_launch_ms": ms.value,
+            "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json copy bandwidth)",
+            "iteration_us": iter_us,
+            "iteration_frac_of_hbm_floor": (byt.value / (peak * 1e9)) / (iter_us * 1e-6)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config(world), "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
+            "cpu_baseline": cpu, "clocks": clk, "refined_rows_last_fit": model.refined_rows,
+            "final_inertia": model.inertia_trace[-1],
+        }))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,424 @@
+"""Python mirror of the reference's C++ API for the hot path.
+
+Names, argument meaning and error behaviour follow proj/include/dnd/*.hpp so
+the parity tests read like the reference's own tests (tests/test_pairwise.cpp,
+test_cluster.cpp, test_moments.cpp).  Every compute call goes through the
+C-ABI of include/dndc.h (libdndc.so, CUDA kernels for sm_100a + NCCL); shards
+live in HBM as torch CUDA tensors, which are used only as device memory.
+
+  reference                                   here
+  ------------------------------------------  -----------------------------------
+  Communicator / run_world (transport.hpp)    Communicator (one per GPU / rank)
+  chunk_map (chunking.hpp:27)                 chunk_map
+  DndArray<T> (ndarray.hpp:58-91)             DndArray (split 0 or None)
+  random_uniform / from_global / gather       random_uniform / from_global / gather
+  detail::row_norms / distance_block          row_norms / distance_block
+  cdist / cdist_xy (pairwise.hpp:15-19)       cdist / cdist_xy
+  kmeans_* (cluster.hpp:25-42)                kmeans_init_indices / _centroids / fit / predict
+  mean_axis / var_axis / stddev_axis          same names (axis 0 = the split axis)
+  (not in the reference)                      kmeanspp_indices (BASELINE config 5)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import TransportError, check, lib
+
+__all__ = [
+    "Communicator", "DndArray", "KMeansModel", "MomentState", "TransportError", "chunk_map",
+    "random_uniform", "from_global", "gather", "row_norms", "distance_block", "cdist", "cdist_xy",
+    "kmeans_init_indices", "kmeans_init_centroids", "kmeans_fit", "kmeans_predict", "mean_axis",
+    "var_axis", "stddev_axis", "moments_axis0", "kmeanspp_indices",
+]
+
+_SUFFIX = {torch.float32: "f32", torch.float64: "f64"}
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+class Communicator:
+    """Rank handle over one GPU (dnd::Communicator, transport.hpp:85-217).
+
+    world == 1 needs nothing; world > 1 shares an NCCL unique id, normally via
+    `Communicator.from_torch_distributed()` (one process per GPU, torchrun).
+    """
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None):
+        self.device = int(device)
+        self._rank, self._world = int(rank), int(world)
+        h = C.c_void_p()
+        uid = None
+        if unique_id is not None:
+            uid = C.create_string_buffer(bytes(unique_id), _lib.UNIQUE_ID_BYTES)
+        torch.cuda.set_device(self.device)
+        check(lib().dndc_create(self.device, self._rank, self._world, uid, C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(_lib.UNIQUE_ID_BYTES)
+        check(lib().dndc_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch_distributed(cls, device: int | None = None) -> "Communicator":
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        if device is None:
+            device = torch.cuda.current_device()
+        obj = [cls.unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        return cls(device, rank, world, obj[0] if world > 1 else None)
+
+    # -- handle plumbing
+    @property
+    def handle(self):
+        lib().dndc_set_stream(self._h, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+        return self._h
+
+    def rank(self) -> int:
+        return self._rank
+
+    def size(self) -> int:
+        return self._world
+
+    def counters(self) -> dict:
+        c = _lib.Counters()
+        check(lib().dndc_get_counters(self._h, C.byref(c)))
+        return {n: getattr(c, n) for n, _ in c._fields_}
+
+    @property
+    def launches(self) -> int:
+        return int(lib().dndc_launch_count(self._h))
+
+    def synchronize(self) -> None:
+        check(lib().dndc_synchronize(self.handle))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().dndc_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def chunk_map(n: int, p: int) -> tuple[np.ndarray, np.ndarray]:
+    """Balanced split of n rows over p ranks (chunking.cpp:9-30)."""
+    off = np.empty(max(p, 1), np.int64)
+    ext = np.empty(max(p, 1), np.int64)
+    check(lib().dndc_chunk_map(int(n), int(p), off.ctypes.data, ext.ctypes.data))
+    return off, ext
+
+
+@dataclass
+class DndArray:
+    """A 2-D (or 1-D) array split along axis 0 (or replicated, split=None)."""
+
+    shape: tuple
+    split: int | None
+    comm: Communicator
+    tile: torch.Tensor  # this rank's rows, contiguous, on the rank's GPU
+
+    def ndim(self) -> int:
+        return len(self.shape)
+
+    def lshape(self) -> tuple:
+        return tuple(self.tile.shape)
+
+    def split_chunks(self):
+        if self.split is None:
+            raise ValueError("split_chunks: array is not split")
+        return chunk_map(self.shape[0], self.comm.size())
+
+    def row_offset(self) -> int:
+        return 0 if self.split is None else int(self.split_chunks()[0][self.comm.rank()])
+
+
+def _check_split(shape, split):
+    if any(e < 0 for e in shape):
+        raise ValueError(f"negative extent in shape {tuple(shape)}")
+    if split is not None and split != 0:
+        raise ValueError("the B200 hot path supports split=0 or replicated arrays (SURVEY.md 8(f) F1)")
+
+
+def random_uniform(shape, split, seed: int, comm: Communicator, dtype=torch.float32) -> DndArray:
+    """dnd::random_uniform<T> (ndarray.hpp:154-169), generated on the GPU."""
+    shape = tuple(int(s) for s in shape)
+    _check_split(shape, split)
+    n = shape[0]
+    m = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+    if split is None:
+        row0, rows = 0, n
+    else:
+        off, ext = chunk_map(n, comm.size())
+        row0, rows = int(off[comm.rank()]), int(ext[comm.rank()])
+    tile = torch.empty((rows,) + shape[1:], dtype=dtype, device=f"cuda:{comm.device}")
+    fn = getattr(lib(), f"dndc_fill_uniform_{_SUFFIX[dtype]}")
+    check(fn(comm.handle, int(seed) & 0xFFFFFFFFFFFFFFFF, row0, rows, m, _ptr(tile)))
+    return DndArray(shape, split, comm, tile)
+
+
+def from_global(data, shape, split, comm: Communicator, dtype=None) -> DndArray:
+    """dnd::from_global (ndarray.hpp:173-188): every rank passes the same data."""
+    shape = tuple(int(s) for s in shape)
+    _check_split(shape, split)
+    arr = np.asarray(data)
+    if dtype is None:
+        dtype = torch.float64 if arr.dtype == np.float64 else torch.float32
+    if arr.size != int(np.prod(shape)):
+        raise ValueError(f"from_global: data holds {arr.size} elements, shape {shape} needs "
+                         f"{int(np.prod(shape))}")
+    arr = arr.reshape(shape)
+    if split is not None:
+        off, ext = chunk_map(shape[0], comm.size())
+        arr = arr[off[comm.rank()]: off[comm.rank()] + ext[comm.rank()]]
+    np_dtype = np.float64 if dtype == torch.float64 else (np.int32 if dtype == torch.int32 else np.float32)
+    tile = torch.from_numpy(np.ascontiguousarray(arr, dtype=np_dtype)).to(f"cuda:{comm.device}")
+    return DndArray(shape, split, comm, tile)
+
+
+def gather(a: DndArray) -> np.ndarray:
+    """Full global content on every rank (dnd::gather, ndarray.hpp:389-393)."""
+    local = a.tile.detach().cpu().numpy()
+    if a.split is None or a.comm.size() == 1:
+        return local.reshape(a.shape)
+    import torch.distributed as dist
+
+    parts = [None] * a.comm.size()
+    dist.all_gather_object(parts, local)
+    return np.concatenate(parts, axis=0).reshape(a.shape)
+
+
+def _fn(name: str, t: torch.Tensor):
+    return getattr(lib(), f"{name}_{_SUFFIX[t.dtype]}")
+
+
+def row_norms(tile: torch.Tensor) -> torch.Tensor:
+    """detail::row_norms (pairwise.cpp:10-20)."""
+    tile = tile.contiguous()
+    comm_dev = tile.device.index
+    out = torch.empty(tile.shape[0], dtype=tile.dtype, device=tile.device)
+    ctx = _device_ctx(comm_dev)
+    check(_fn("dndc_row_norms", tile)(ctx.handle, _ptr(tile), tile.shape[0], tile.shape[1], _ptr(out)))
+    return out
+
+
+def distance_block(a: torch.Tensor, na: torch.Tensor, b: torch.Tensor, nb: torch.Tensor) -> torch.Tensor:
+    """detail::distance_block (pairwise.cpp:22-33)."""
+    out = torch.empty((a.shape[0], b.shape[0]), dtype=a.dtype, device=a.device)
+    ctx = _device_ctx(a.device.index)
+    check(_fn("dndc_cdist_tile", a)(ctx.handle, _ptr(a), _ptr(na), a.shape[0], _ptr(b), _ptr(nb), b.shape[0],
+                                    a.shape[1], _ptr(out), b.shape[0], 0, -1))
+    return out
+
+
+_DEVICE_CTX: dict[int, Communicator] = {}
+
+
+def _device_ctx(device: int) -> Communicator:
+    """A world-1 handle per device for communication-free helpers."""
+    if device not in _DEVICE_CTX:
+        _DEVICE_CTX[device] = Communicator(device)
+    return _DEVICE_CTX[device]
+
+
+def _require_2d(x: DndArray, who: str):
+    if x.ndim() != 2:
+        raise ValueError(f"{who}: input must be 2-D")
+
+
+def cdist(x: DndArray) -> DndArray:
+    """Ring self-distance (pairwise.cpp:37-85): world-1 exchanges per rank."""
+    _require_2d(x, "cdist")
+    if x.shape[0] == 0:
+        raise ValueError("cdist: input has no rows")
+    if x.split is None:
+        raise ValueError("cdist: replicated input; redistribute to split=0 (SURVEY.md 8(f) F1)")
+    n, m = x.shape
+    out = torch.empty((x.tile.shape[0], n), dtype=x.tile.dtype, device=x.tile.device)
+    check(_fn("dndc_cdist", x.tile)(x.comm.handle, _ptr(x.tile), x.tile.shape[0], n, m, _ptr(out)))
+    return DndArray((n, n), 0, x.comm, out)
+
+
+def cdist_xy(x: DndArray, y: DndArray) -> DndArray:
+    """cdist_xy (pairwise.cpp:87-100).  y replicated: communication-free;
+    y split=0: its shards travel the ring (BASELINE config 2)."""
+    if x.ndim() != 2 or y.ndim() != 2:
+        raise ValueError("cdist_xy: inputs must be 2-D")
+    if x.shape[1] != y.shape[1]:
+        raise ValueError(f"cdist_xy: feature counts {x.shape[1]} and {y.shape[1]} do not match")
+    m = x.shape[1]
+    nx_local = x.tile.shape[0] if x.split == 0 else x.shape[0]
+    out = torch.empty((nx_local, y.shape[0]), dtype=x.tile.dtype, device=x.tile.device)
+    if y.split is None:
+        check(_fn("dndc_cdist_xy", x.tile)(x.comm.handle, _ptr(x.tile), nx_local, _ptr(y.tile), y.shape[0], m,
+                                           _ptr(out)))
+    else:
+        if x.tile.dtype != torch.float32:
+            raise ValueError("cdist_xy: the ring over split y is implemented for float32")
+        check(lib().dndc_cdist_xy_ring_f32(x.comm.handle, _ptr(x.tile), nx_local, _ptr(y.tile), y.tile.shape[0],
+                                           y.shape[0], m, _ptr(out)))
+    return DndArray((x.shape[0], y.shape[0]), x.split, x.comm, out)
+
+
+@dataclass
+class KMeansModel:
+    """cluster.hpp:14-21."""
+
+    k: int = 0
+    n_features: int = 0
+    centroids: np.ndarray = field(default_factory=lambda: np.zeros((0, 0)))
+    inertia_trace: list = field(default_factory=list)
+    iterations_run: int = 0
+    seed: int = 0
+    refined_rows: int = 0  # rows re-decided in f64 during the last iteration set
+
+
+def kmeans_init_indices(n: int, k: int, seed: int) -> np.ndarray:
+    """cluster.cpp:60-75."""
+    out = np.empty(max(k, 1), np.int64)
+    check(lib().dndc_kmeans_init_indices(int(n), int(k), int(seed) & 0xFFFFFFFFFFFFFFFF, out.ctypes.data))
+    return out[:k]
+
+
+def _shard(x: DndArray):
+    """(handle owner, local rows, global rows).  A replicated input is
+    processed whole by every rank on a world-1 handle (the reference
+    resplits it first, cluster.cpp:91; results are identical)."""
+    n_local = x.tile.shape[0]
+    if x.split == 0:
+        return x.comm, n_local, x.shape[0]
+    return (_device_ctx(x.comm.device) if x.comm.size() > 1 else x.comm), n_local, n_local
+
+
+def kmeans_init_centroids(x: DndArray, k: int, seed: int) -> np.ndarray:
+    """cluster.cpp:77-81 (rows replicated to every rank, f64)."""
+    _require_2d(x, "kmeans_init_centroids")
+    comm, n_local, n_global = _shard(x)
+    m = x.shape[1]
+    out = np.empty((max(k, 1), m), np.float64)
+    if x.tile.dtype != torch.float32:
+        idx = kmeans_init_indices(n_global, k, seed)
+        full = gather(x)
+        return full[idx].astype(np.float64)
+    check(lib().dndc_kmeans_init_centroids_f32(comm.handle, _ptr(x.tile), n_local, n_global, m, int(k),
+                                               int(seed) & 0xFFFFFFFFFFFFFFFF, out.ctypes.data))
+    return out[:k]
+
+
+def kmeans_fit(x: DndArray, k: int, max_iter: int, tol: float, seed: int, init=None) -> KMeansModel:
+    """Lloyd's algorithm (cluster.cpp:83-153) on the fused GPU kernels."""
+    _require_2d(x, "kmeans_fit")
+    comm, n_local, n_global = _shard(x)
+    m = x.shape[1]
+    if k < 1:
+        raise ValueError(f"kmeans_fit: k must be positive, got {k}")
+    if k > n_global:
+        raise ValueError(f"kmeans_fit: k={k} exceeds the {n_global} available samples")
+    if max_iter < 1:
+        raise ValueError(f"kmeans_fit: max_iter must be positive, got {max_iter}")
+    cent = np.empty((k, m), np.float64)
+    trace = np.zeros(max_iter, np.float64)
+    iters = C.c_int(0)
+    init_ptr = None
+    if init is not None:
+        init = np.ascontiguousarray(init, np.float64).reshape(k, m)
+        init_ptr = init.ctypes.data
+    check(_fn("dndc_kmeans_fit", x.tile)(comm.handle, _ptr(x.tile), n_local, n_global, m, int(k), int(max_iter),
+                                         float(tol), int(seed) & 0xFFFFFFFFFFFFFFFF, init_ptr, cent.ctypes.data,
+                                         trace.ctypes.data, C.byref(iters)))
+    refined = C.c_int64(0)
+    lib().dndc_kmeans_last_refined(comm._h, C.byref(refined))
+    return KMeansModel(k, m, cent, list(trace[: iters.value]), iters.value, seed, refined.value)
+
+
+def kmeans_predict(model: KMeansModel, x: DndArray) -> DndArray:
+    """cluster.cpp:155-172 (ties to the lowest centroid index)."""
+    _require_2d(x, "kmeans_predict")
+    if x.shape[1] != model.n_features:
+        raise ValueError(f"kmeans_predict: input has {x.shape[1]} features, model expects {model.n_features}")
+    n_local = x.tile.shape[0]
+    labels = torch.empty(n_local, dtype=torch.int32, device=x.tile.device)
+    c = np.ascontiguousarray(model.centroids, np.float64)
+    check(_fn("dndc_kmeans_predict", x.tile)(x.comm.handle, _ptr(x.tile), n_local, x.shape[1], c.ctypes.data,
+                                             int(model.k), _ptr(labels)))
+    return DndArray((x.shape[0],), x.split, x.comm, labels)
+
+
+@dataclass
+class MomentState:
+    """moments.hpp:14-24 (count, per-slot mean and M2)."""
+
+    count: int
+    mean: np.ndarray
+    m2: np.ndarray
+
+
+def moments_axis0(a: DndArray) -> MomentState:
+    """local_moments_axis + rank-order combine (moments.cpp:41-52)."""
+    _require_2d(a, "moments")
+    m = a.shape[1]
+    cnt = np.zeros(1, np.int64)
+    mean = np.zeros(max(m, 1), np.float64)
+    m2 = np.zeros(max(m, 1), np.float64)
+    fn_ctx = _shard(a)[0]
+    check(_fn("dndc_moments_axis0", a.tile)(fn_ctx.handle, _ptr(a.tile), a.tile.shape[0], m, cnt.ctypes.data,
+                                            mean.ctypes.data, m2.ctypes.data))
+    return MomentState(int(cnt[0]), mean[:m].copy(), m2[:m].copy())
+
+
+def _variance_from(s: MomentState, ddof: int, who: str) -> np.ndarray:
+    if s.count - ddof <= 0:
+        raise ValueError(f"{who}: need more than ddof={ddof} samples, got {s.count}")
+    return s.m2 / float(s.count - ddof)
+
+
+def _replicated(values: np.ndarray, comm: Communicator) -> DndArray:
+    return DndArray((values.shape[0],), None, comm, torch.from_numpy(values).to(f"cuda:{comm.device}"))
+
+
+def mean_axis(a: DndArray, axis: int = 0) -> DndArray:
+    if axis != 0:
+        raise ValueError("mean_axis: the B200 path reduces along the split axis 0")
+    return _replicated(moments_axis0(a).mean, a.comm)
+
+
+def var_axis(a: DndArray, axis: int = 0, ddof: int = 0) -> DndArray:
+    if axis != 0:
+        raise ValueError("var_axis: the B200 path reduces along the split axis 0")
+    return _replicated(_variance_from(moments_axis0(a), ddof, "var_axis"), a.comm)
+
+
+def stddev_axis(a: DndArray, axis: int = 0, ddof: int = 0) -> DndArray:
+    if axis != 0:
+        raise ValueError("stddev_axis: the B200 path reduces along the split axis 0")
+    return _replicated(np.sqrt(_variance_from(moments_axis0(a), ddof, "stddev_axis")), a.comm)
+
+
+def kmeanspp_indices(x: DndArray, k: int, seed: int) -> np.ndarray:
+    """k-means++ seeding (BASELINE config 5; definition in DESIGN.md)."""
+    _require_2d(x, "kmeanspp")
+    if x.tile.dtype != torch.float32:
+        raise ValueError("kmeanspp: float32 input required")
+    comm, n_local, n_global = _shard(x)
+    out = np.empty(max(k, 1), np.int64)
+    check(lib().dndc_kmeanspp_indices_f32(comm.handle, _ptr(x.tile), n_local, n_global, x.shape[1], int(k),
+                                          int(seed) & 0xFFFFFFFFFFFFFFFF, out.ctypes.data))
+    return out[:k]
+
+
+del math

@@ -1,0 +1,383 @@
+// cdist.cu -- A3-A7: row norms, the distance tile and the ring exchange.
+//
+// Reference: detail::row_norms / distance_block / cdist / cdist_xy
+// (pairwise.cpp:10-100), matmul_local (ndarray.hpp:400-418), place_chunk
+// (tile.hpp:90-107).
+//
+// f32 (the performance path, small feature counts): a register-blocked FFMA
+// tile (128x128 per CTA, 8x8 per thread) computing
+//     d = sqrt(max(xn_i + yn_j - 2 * x_i.y_j, 0))
+// with the dot product accumulated by a sequential fmaf chain over k -- the
+// same chain row_norms_f32 uses, so a row's distance to itself cancels to an
+// exact 0 (test_pairwise.cpp:135-144 relies on that).  The epilogue writes the
+// column window [col_off, col_off + ny) of an ld_out-wide row block directly
+// (place_chunk without the temporary) with streaming (evict-first) vector
+// stores.  The feature-rich case (d = 1024, BASELINE config 4) goes to the
+// tcgen05 3xTF32 kernel in cdist_tc.cu.
+//
+// f64: the reference's arithmetic bit for bit (products rounded before adds,
+// IEEE sqrt), used by the drop-in f64 API.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace dndc {
+
+bool cdist_tc_eligible(int64_t nx, int64_t ny, int64_t m);
+void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn, int64_t nx, const float* y,
+                       const float* yn, int64_t ny, int64_t m, float* out, int64_t ld_out,
+                       int64_t col_off, int64_t diag_offset, cudaStream_t stream);
+
+// ------------------------------------------------------------- row norms
+__global__ void row_norms_f32_kernel(const float* __restrict__ x, int64_t rows, int m,
+                                     float* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const float* row = x + i * m;
+    float acc = 0.f;
+    for (int k = 0; k < m; ++k) acc = fmaf(row[k], row[k], acc);
+    out[i] = acc;
+}
+
+__global__ void row_norms_f64_kernel(const double* __restrict__ x, int64_t rows, int m,
+                                     double* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const double* row = x + i * m;
+    double acc = 0.0;
+    for (int k = 0; k < m; ++k) acc = add_rn(acc, mul_rn(row[k], row[k]));
+    out[i] = acc;
+}
+
+template <typename T>
+void row_norms(dndc_ctx* ctx, const T* x, int64_t rows, int64_t m, T* out, cudaStream_t stream) {
+    if (rows <= 0) return;
+    const int threads = 256;
+    const unsigned blocks = static_cast<unsigned>(ceil_div(rows, threads));
+    if constexpr (sizeof(T) == 4)
+        row_norms_f32_kernel<<<blocks, threads, 0, stream>>>(x, rows, static_cast<int>(m), out);
+    else
+        row_norms_f64_kernel<<<blocks, threads, 0, stream>>>(x, rows, static_cast<int>(m), out);
+    DNDC_LAUNCHED(ctx);
+}
+
+template void row_norms<float>(dndc_ctx*, const float*, int64_t, int64_t, float*, cudaStream_t);
+template void row_norms<double>(dndc_ctx*, const double*, int64_t, int64_t, double*, cudaStream_t);
+
+// --------------------------------------------------------- f32 FFMA tile
+namespace ffma {
+constexpr int BM = 128, BN = 128, BK = 32, THREADS = 256;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(ffma::THREADS)
+    cdist_tile_f32_kernel(const float* __restrict__ x, const float* __restrict__ xn, int64_t nx,
+                          const float* __restrict__ y, const float* __restrict__ yn, int64_t ny,
+                          int m, float* __restrict__ out, int64_t ld, int64_t col_off,
+                          int64_t diag_offset, int64_t row_block0) {
+    using namespace ffma;
+    __shared__ __align__(16) float xs[BK][BM];
+    __shared__ __align__(16) float ys[BK][BN];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int64_t row0 = (row_block0 + blockIdx.y) * BM;
+    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * BN;
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    for (int k0 = 0; k0 < m; k0 += BK) {
+        const int kc = min(BK, m - k0);
+        // r fastest: conflict-free transposed smem stores; the global reads of
+        // a 128 x kc slab stay within a few L1 lines per row.
+        for (int idx = tid; idx < BM * kc; idx += THREADS) {
+            const int r = idx % BM, kk = idx / BM;
+            const int64_t gr = row0 + r, gc = col0 + r;
+            xs[kk][r] = gr < nx ? __ldg(x + gr * m + k0 + kk) : 0.f;
+            ys[kk][r] = gc < ny ? __ldg(y + gc * m + k0 + kk) : 0.f;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&xs[kk][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&xs[kk][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&ys[kk][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&ys[kk][64 + tx * 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+
+    float ynv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int64_t gj = col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+        ynv[j] = gj < ny ? __ldg(yn + gj) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t gi = row0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+        if (gi >= nx) continue;
+        const float xni = __ldg(xn + gi);
+        float* orow = out + gi * ld + col_off;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t c = col0 + h * 64 + tx * 4;
+            float v[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const float s = fmaxf(fmaf(-2.f, acc[i][h * 4 + jj], xni + ynv[h * 4 + jj]), 0.f);
+                v[jj] = (c + jj == gi + diag_offset) ? 0.f : sqrt_approx(s);
+            }
+            if (VEC && c + 3 < ny) {
+                st_stream4(orow + c, v[0], v[1], v[2], v[3]);
+            } else {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                    if (c + jj < ny) st_stream(orow + c + jj, v[jj]);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------- f64 exact tile
+namespace f64t {
+constexpr int BM = 64, BN = 64, BK = 16;
+}
+
+__global__ void __launch_bounds__(256)
+    cdist_tile_f64_kernel(const double* __restrict__ x, const double* __restrict__ xn, int64_t nx,
+                          const double* __restrict__ y, const double* __restrict__ yn, int64_t ny,
+                          int m, double* __restrict__ out, int64_t ld, int64_t col_off,
+                          int64_t diag_offset, int64_t row_block0) {
+    using namespace f64t;
+    __shared__ double xs[BK][BM + 1];
+    __shared__ double ys[BK][BN + 1];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int64_t row0 = (row_block0 + blockIdx.y) * BM;
+    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * BN;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = 0; k0 < m; k0 += BK) {
+        const int kc = min(BK, m - k0);
+        for (int idx = tid; idx < BM * kc; idx += 256) {
+            const int r = idx % BM, kk = idx / BM;
+            const int64_t gr = row0 + r, gc = col0 + r;
+            xs[kk][r] = gr < nx ? x[gr * m + k0 + kk] : 0.0;
+            ys[kk][r] = gc < ny ? y[gc * m + k0 + kk] : 0.0;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    acc[i][j] = add_rn(acc[i][j], mul_rn(xs[kk][ty + 16 * i], ys[kk][tx + 16 * j]));
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t gi = row0 + ty + 16 * i;
+        if (gi >= nx) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t gj = col0 + tx + 16 * j;
+            if (gj >= ny) continue;
+            const double d = (gj == gi + diag_offset) ? 0.0 : ref_distance(xn[gi], yn[gj], acc[i][j]);
+            out[gi * ld + col_off + gj] = d;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- driver
+template <typename T>
+void cdist_tile(dndc_ctx* ctx, const T* x, const T* xn, int64_t nx, const T* y, const T* yn,
+                int64_t ny, int64_t m, T* out, int64_t ld_out, int64_t col_off,
+                int64_t diag_offset, cudaStream_t stream) {
+    if (nx <= 0 || ny <= 0) return;
+    if (m > (1 << 30)) value_error("cdist: feature count too large");
+    if constexpr (sizeof(T) == 4) {
+        if (cdist_tc_eligible(nx, ny, m)) {
+            cdist_tile_tc_f32(ctx, x, xn, nx, y, yn, ny, m, out, ld_out, col_off, diag_offset, stream);
+            return;
+        }
+        const bool vec = (ld_out % 4 == 0) && (col_off % 4 == 0) &&
+                         (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+        const int64_t row_blocks = ceil_div(nx, ffma::BM);
+        const unsigned gx = static_cast<unsigned>(ceil_div(ny, ffma::BN));
+        for (int64_t rb = 0; rb < row_blocks; rb += 65535) {
+            dim3 grid(gx, static_cast<unsigned>(std::min<int64_t>(65535, row_blocks - rb)));
+            if (vec)
+                cdist_tile_f32_kernel<true><<<grid, ffma::THREADS, 0, stream>>>(
+                    x, xn, nx, y, yn, ny, static_cast<int>(m), out, ld_out, col_off, diag_offset, rb);
+            else
+                cdist_tile_f32_kernel<false><<<grid, ffma::THREADS, 0, stream>>>(
+                    x, xn, nx, y, yn, ny, static_cast<int>(m), out, ld_out, col_off, diag_offset, rb);
+            DNDC_LAUNCHED(ctx);
+        }
+    } else {
+        const int64_t row_blocks = ceil_div(nx, f64t::BM);
+        const unsigned gx = static_cast<unsigned>(ceil_div(ny, f64t::BN));
+        for (int64_t rb = 0; rb < row_blocks; rb += 65535) {
+            dim3 grid(gx, static_cast<unsigned>(std::min<int64_t>(65535, row_blocks - rb)));
+            cdist_tile_f64_kernel<<<grid, 256, 0, stream>>>(x, xn, nx, y, yn, ny, static_cast<int>(m),
+                                                           out, ld_out, col_off, diag_offset, rb);
+            DNDC_LAUNCHED(ctx);
+        }
+    }
+}
+
+// The ring (pairwise.cpp:54-83): round t computes against the block that
+// originated at (rank - t) mod p and fills that origin's column window, while
+// the same block is already travelling to rank+1 on the comm stream (double
+// buffer: compute reads buf[cur], NCCL receives into buf[1-cur]).  The packet
+// is the block's rows followed by their norms, as in pairwise.cpp:73-74.
+template <typename T>
+void cdist_ring(dndc_ctx* ctx, const T* x_local, int64_t nx_local, const T* y_local,
+                int64_t ny_local, int64_t ny_global, int64_t m, T* out, bool self) {
+    const int p = ctx->world, r = ctx->rank;
+    std::vector<int64_t> yoff, yext;
+    chunk_map(ny_global, p, yoff, yext);
+    if (ny_local != yext[r])
+        value_error("cdist: local block has " + std::to_string(ny_local) + " rows, chunk_map gives " +
+                    std::to_string(yext[r]));
+    cudaStream_t s = ctx->stream;
+    T* xn = static_cast<T*>(ctx->slot("cd_xn", std::max<int64_t>(nx_local, 1) * sizeof(T)));
+    row_norms<T>(ctx, x_local, nx_local, m, xn, s);
+    if (p == 1) {
+        const T* yn = xn;
+        if (!self) {
+            T* ynb = static_cast<T*>(ctx->slot("cd_yn", std::max<int64_t>(ny_local, 1) * sizeof(T)));
+            row_norms<T>(ctx, y_local, ny_local, m, ynb, s);
+            yn = ynb;
+        }
+        cdist_tile<T>(ctx, x_local, xn, nx_local, y_local, yn, ny_local, m, out, ny_global, 0,
+                      self ? 0 : -1, s);
+        return;
+    }
+    const int64_t maxext = *std::max_element(yext.begin(), yext.end());
+    const size_t pkt = static_cast<size_t>(std::max<int64_t>(maxext, 1)) * (m + 1) * sizeof(T);
+    T* buf[2] = {static_cast<T*>(ctx->slot("cd_ring0", pkt)), static_cast<T*>(ctx->slot("cd_ring1", pkt))};
+    if (ny_local > 0) {
+        DNDC_CUDA(cudaMemcpyAsync(buf[0], y_local, ny_local * m * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        if (self)
+            DNDC_CUDA(cudaMemcpyAsync(buf[0] + ny_local * m, xn, ny_local * sizeof(T),
+                                      cudaMemcpyDeviceToDevice, s));
+        else
+            row_norms<T>(ctx, y_local, ny_local, m, buf[0] + ny_local * m, s);
+    }
+    const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
+    int origin = r, cur = 0;
+    for (int round = 0; round < p; ++round) {
+        const int64_t rows = yext[origin];
+        const bool more = round + 1 < p;
+        if (more) {
+            const int src_origin = (origin + p - 1) % p;
+            const int64_t in_rows = yext[src_origin];
+            DNDC_CUDA(cudaEventRecord(ctx->ev_a, s));
+            DNDC_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
+            DNDC_NCCL(ncclGroupStart());
+            if (rows > 0)
+                DNDC_NCCL(ncclSend(buf[cur], rows * (m + 1), dt, (r + 1) % p, ctx->comm, ctx->comm_stream));
+            if (in_rows > 0)
+                DNDC_NCCL(ncclRecv(buf[1 - cur], in_rows * (m + 1), dt, (r + p - 1) % p, ctx->comm,
+                                   ctx->comm_stream));
+            DNDC_NCCL(ncclGroupEnd());
+            DNDC_CUDA(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
+            ctx->counters.sendrecvs++;
+        }
+        cdist_tile<T>(ctx, x_local, xn, nx_local, buf[cur], buf[cur] + rows * m, rows, m, out,
+                      ny_global, yoff[origin], (self && origin == r) ? 0 : -1, s);
+        if (more) {
+            DNDC_CUDA(cudaStreamWaitEvent(s, ctx->ev_b, 0));
+            cur = 1 - cur;
+            origin = (origin + p - 1) % p;
+        }
+    }
+}
+
+template <typename T>
+void cdist_xy_replicated(dndc_ctx* ctx, const T* x_local, int64_t n_local, const T* y, int64_t ny,
+                         int64_t m, T* out) {
+    cudaStream_t s = ctx->stream;
+    T* xn = static_cast<T*>(ctx->slot("cd_xn", std::max<int64_t>(n_local, 1) * sizeof(T)));
+    T* yn = static_cast<T*>(ctx->slot("cd_yn", std::max<int64_t>(ny, 1) * sizeof(T)));
+    row_norms<T>(ctx, x_local, n_local, m, xn, s);
+    row_norms<T>(ctx, y, ny, m, yn, s);
+    cdist_tile<T>(ctx, x_local, xn, n_local, y, yn, ny, m, out, ny, 0, -1, s);
+}
+
+}  // namespace dndc
+
+using dndc::guard;
+
+extern "C" {
+
+int dndc_row_norms_f32(dndc_ctx* ctx, const float* x, int64_t rows, int64_t m, float* out) {
+    return guard([&] { dndc::row_norms<float>(ctx, x, rows, m, out, ctx->stream); });
+}
+int dndc_row_norms_f64(dndc_ctx* ctx, const double* x, int64_t rows, int64_t m, double* out) {
+    return guard([&] { dndc::row_norms<double>(ctx, x, rows, m, out, ctx->stream); });
+}
+
+int dndc_cdist_tile_f32(dndc_ctx* ctx, const float* x, const float* xn, int64_t nx, const float* y,
+                        const float* yn, int64_t ny, int64_t m, float* out, int64_t ld_out,
+                        int64_t col_off, int64_t diag_offset) {
+    return guard([&] {
+        dndc::cdist_tile<float>(ctx, x, xn, nx, y, yn, ny, m, out, ld_out, col_off, diag_offset,
+                                ctx->stream);
+    });
+}
+int dndc_cdist_tile_f64(dndc_ctx* ctx, const double* x, const double* xn, int64_t nx,
+                        const double* y, const double* yn, int64_t ny, int64_t m, double* out,
+                        int64_t ld_out, int64_t col_off, int64_t diag_offset) {
+    return guard([&] {
+        dndc::cdist_tile<double>(ctx, x, xn, nx, y, yn, ny, m, out, ld_out, col_off, diag_offset,
+                                 ctx->stream);
+    });
+}
+
+int dndc_cdist_f32(dndc_ctx* ctx, const float* x_local, int64_t n_local, int64_t n_global,
+                   int64_t m, float* out) {
+    return guard([&] {
+        if (n_global == 0) dndc::value_error("cdist: input has no rows");
+        dndc::cdist_ring<float>(ctx, x_local, n_local, x_local, n_local, n_global, m, out, true);
+    });
+}
+int dndc_cdist_f64(dndc_ctx* ctx, const double* x_local, int64_t n_local, int64_t n_global,
+                   int64_t m, double* out) {
+    return guard([&] {
+        if (n_global == 0) dndc::value_error("cdist: input has no rows");
+        dndc::cdist_ring<double>(ctx, x_local, n_local, x_local, n_local, n_global, m, out, true);
+    });
+}
+
+int dndc_cdist_xy_f32(dndc_ctx* ctx, const float* x_local, int64_t n_local, const float* y,
+                      int64_t ny, int64_t m, float* out) {
+    return guard([&] { dndc::cdist_xy_replicated<float>(ctx, x_local, n_local, y, ny, m, out); });
+}
+int dndc_cdist_xy_f64(dndc_ctx* ctx, const double* x_local, int64_t n_local, const double* y,
+                      int64_t ny, int64_t m, double* out) {
+    return guard([&] { dndc::cdist_xy_replicated<double>(ctx, x_local, n_local, y, ny, m, out); });
+}
+
+int dndc_cdist_xy_ring_f32(dndc_ctx* ctx, const float* x_local, int64_t nx_local,
+                           const float* y_local, int64_t ny_local, int64_t ny_global, int64_t m,
+                           float* out) {
+    return guard([&] {
+        dndc::cdist_ring<float>(ctx, x_local, nx_local, y_local, ny_local, ny_global, m, out, false);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,929 @@
+// kmeans.cu -- A8-A12: the fused Lloyd iteration.
+//
+// Reference: kmeans_fit / assign_local / gather_rows / kmeans_predict
+// (cluster.cpp:27-172) on top of cdist_xy (pairwise.cpp:87-100).
+//
+// One iteration on one GPU is three launches, all captured in one CUDA graph
+// for the whole fit (tol == 0 never needs the host; tol > 0 sets a device
+// `done` flag that turns the remaining launches into no-ops):
+//
+//   assign   persistent CTAs stream X once through a cp.async ring in shared
+//            memory.  Phase 1: lane = row; fp32 scores s_j = |c_j|^2 - 2 x.c_j
+//            against centroids staged in smem, top-2 tracking, and a rigorous
+//            fp32 error bound: rows whose top-2 gap falls inside it are
+//            re-decided with the reference's exact f64 arithmetic
+//            (distance_block + assign_local, products rounded before adds,
+//            strict < so the lowest index wins ties).  Phase 2: lane = feature;
+//            warp w owns clusters j = w, w+8, ...; per 32-row chunk a ballot
+//            selects the chunk's rows of cluster j and their features are summed
+//            in fp32 (<= 32 rows), then added into the CTA's f64 accumulators.
+//            No atomics: the result is deterministic for a given grid.
+//   reduce   per-stat sum over the CTA partials in CTA order (f64).
+//   update   [world > 1: after an NCCL allgather of the k*m + k stats] one CTA
+//            folds the ranks in order 0..p-1 (transport.hpp:136-148), forms
+//            the new f64 master centroids (empty clusters keep theirs,
+//            cluster.cpp:125-133), the inertia of the assignment just made,
+//            the displacement (cluster.cpp:139-150) and the fp32 tables of the
+//            next iteration.
+//
+// Inertia is not accumulated per row: with S_j, n_j the new sums/counts and c_j
+// the centroids used for the assignment,
+//     sum_i |x_i - c_l(i)|^2 = sum_i |x_i|^2 + sum_j (n_j |c_j|^2 - 2 c_j.S_j),
+// and sum_i |x_i|^2 is computed once per fit by the validation pass that the
+// reference performs anyway (the isfinite scan, cluster.cpp:88-89).
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace dndc {
+
+constexpr int KM_THREADS = 256;
+constexpr int KM_WARPS = KM_THREADS / 32;
+constexpr int KM_TILE = 256;  // rows per tile: one per thread in phase 1
+constexpr unsigned FULL = 0xffffffffu;
+
+struct KMeansState {
+    cudaGraphExec_t exec = nullptr;
+    std::string key;
+};
+
+void destroy_kmeans_state(KMeansState* st) {
+    if (!st) return;
+    if (st->exec) cudaGraphExecDestroy(st->exec);
+    delete st;
+}
+
+// Device buffers of the Lloyd state (ctx slots, stable addresses for graphs).
+struct KmBuffers {
+    double* c64;       // k*m f64 master centroids
+    double* cn64;      // k   reference-order |c|^2 of c64
+    float* ct;         // k*dpad  -2 * float(c64)
+    float* cn32;       // k   float(|float(c)|^2)
+    float* bounds;     // [0] max_j |c_j|, [1] max_j cn32_j
+    double* stats;     // S = k*m + k local reduced stats
+    double* gathered;  // world * S
+    double* partials;  // G * S
+    double* trace;     // max_iter
+    double* disp;      // max_iter
+    int* flags;        // [0] done, [1] iterations_run
+    double* sx2;       // [0] local sum x^2, [1] non-finite count, [2] global sum x^2
+    double* pre;       // validation partials
+    unsigned long long* refined;
+};
+
+static int dpad_of(int m) { return (m + 3) / 4 * 4; }
+
+// Row stride of a staged tile in shared memory.  Rows whose 16-byte chunks are
+// whole (m % 4 == 0) are padded so that lane = row reads hit distinct bank
+// groups (stride/4 odd); other widths are copied contiguously (m = 18 reads
+// conflict-free as 8-byte pairs).
+static int srow_of(int m) {
+    if (m % 4 != 0) return m;
+    return ((m / 4) % 2 == 0) ? m + 4 : m;
+}
+
+struct SmemLayout {
+    size_t acc, cnt, cts, cns, lbl, total;
+};
+
+__host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
+
+__host__ __device__ inline SmemLayout smem_layout(size_t elem, int k, int d, int srow, int dpad,
+                                                  int stages) {
+    SmemLayout l;
+    l.acc = align16(static_cast<size_t>(stages) * KM_TILE * srow * elem);
+    l.cnt = align16(l.acc + static_cast<size_t>(k) * d * sizeof(double));
+    l.cts = align16(l.cnt + static_cast<size_t>(k) * sizeof(long long));
+    const size_t ctab = elem == 4 ? static_cast<size_t>(k) * dpad * sizeof(float) : 0;
+    l.cns = align16(l.cts + ctab);
+    l.lbl = align16(l.cns + (elem == 4 ? static_cast<size_t>(k) * sizeof(float) : 0));
+    l.total = align16(l.lbl + KM_TILE * sizeof(int));
+    return l;
+}
+
+struct AssignParams {
+    const void* x;
+    int64_t n;
+    int d, k, dpad, srow, stages;
+    bool aligned16;
+    const float* ct;
+    const float* cn32;
+    const float* bounds;
+    const double* c64;
+    const double* cn64;
+    double* partials;  // null: predict only
+    int32_t* labels;   // optional
+    unsigned long long* refined;
+    const int* done;
+};
+
+// Exact reference decision for one row held in shared memory (cluster.cpp:44-56
+// over pairwise.cpp:22-33 and :96-97).
+template <typename T>
+__device__ int ref_argmin(const T* xr, int d, const double* __restrict__ c64,
+                          const double* __restrict__ cn64, int k) {
+    double xn = 0.0;
+    for (int f = 0; f < d; ++f) {
+        const double v = static_cast<double>(xr[f]);
+        xn = add_rn(xn, mul_rn(v, v));
+    }
+    int best = 0;
+    double bd = 0.0;
+    for (int j = 0; j < k; ++j) {
+        const double* c = c64 + static_cast<int64_t>(j) * d;
+        double g = 0.0;
+        for (int f = 0; f < d; ++f) g = add_rn(g, mul_rn(static_cast<double>(xr[f]), c[f]));
+        const double dj = ref_distance(xn, cn64[j], g);
+        if (j == 0 || dj < bd) {
+            bd = dj;
+            best = j;
+        }
+    }
+    return best;
+}
+
+template <typename T>
+__device__ __forceinline__ void load_tile(T* dst, const T* __restrict__ x, int64_t n, int d, int srow,
+                                          int64_t tile, bool aligned16) {
+    const int64_t row0 = tile * KM_TILE;
+    const int64_t rows = min(static_cast<int64_t>(KM_TILE), n - row0);
+    const T* src = x + row0 * d;
+    constexpr int V = 16 / sizeof(T);  // elements per 16-byte chunk
+    if (aligned16 && srow == d) {
+        const int64_t valid = rows * d * static_cast<int64_t>(sizeof(T));
+        const int chunks = KM_TILE * d * static_cast<int>(sizeof(T)) / 16;
+        for (int c = threadIdx.x; c < chunks; c += KM_THREADS) {
+            const int64_t rem = valid - static_cast<int64_t>(c) * 16;
+            const int bytes = rem >= 16 ? 16 : (rem > 0 ? static_cast<int>(rem) : 0);
+            cp_async16(dst + c * V, bytes > 0 ? src + c * V : x, bytes);
+        }
+    } else if (aligned16 && d % V == 0) {
+        const int per_row = d / V;
+        for (int c = threadIdx.x; c < KM_TILE * per_row; c += KM_THREADS) {
+            const int r = c / per_row, q = c % per_row;
+            const bool ok = r < rows;
+            cp_async16(dst + r * srow + q * V, ok ? src + static_cast<int64_t>(r) * d + q * V : x,
+                       ok ? 16 : 0);
+        }
+    } else {
+        for (int e = threadIdx.x; e < KM_TILE * d; e += KM_THREADS) {
+            const int r = e / d, f = e % d;
+            if (r < rows) {
+                if constexpr (sizeof(T) == 4)
+                    cp_async4(dst + r * srow + f, src + static_cast<int64_t>(r) * d + f);
+                else
+                    cp_async8(dst + r * srow + f, src + static_cast<int64_t>(r) * d + f);
+            }
+            else
+                dst[r * srow + f] = T(0);
+        }
+    }
+}
+
+// D > 0: compile-time feature count (row kept in registers); D == 0: runtime.
+template <typename T, int D>
+__global__ void __launch_bounds__(KM_THREADS) kmeans_assign_kernel(AssignParams p) {
+    if (p.done && *p.done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int d = D > 0 ? D : p.d;
+    const int k = p.k;
+    const int srow = p.srow;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // ---- carve shared memory (layout shared with assign_smem on the host)
+    const SmemLayout lay = smem_layout(sizeof(T), k, d, srow, p.dpad, p.stages);
+    T* xs = reinterpret_cast<T*>(smem_raw);
+    const size_t stage_elems = static_cast<size_t>(KM_TILE) * srow;
+    double* acc = reinterpret_cast<double*>(smem_raw + lay.acc);
+    long long* cnt = reinterpret_cast<long long*>(smem_raw + lay.cnt);
+    float* cts = reinterpret_cast<float*>(smem_raw + lay.cts);
+    float* cns = reinterpret_cast<float*>(smem_raw + lay.cns);
+    int* lbl = reinterpret_cast<int*>(smem_raw + lay.lbl);
+
+    const bool accumulate = p.partials != nullptr;
+    if (accumulate) {
+        for (int e = threadIdx.x; e < k * d; e += KM_THREADS) acc[e] = 0.0;
+        for (int j = threadIdx.x; j < k; j += KM_THREADS) cnt[j] = 0;
+    }
+    if constexpr (sizeof(T) == 4) {
+        for (int e = threadIdx.x; e < k * p.dpad; e += KM_THREADS) cts[e] = p.ct[e];
+        for (int j = threadIdx.x; j < k; j += KM_THREADS) cns[j] = p.cn32[j];
+    }
+    const float cmax = sizeof(T) == 4 ? p.bounds[0] : 0.f;
+    const float cnmax = sizeof(T) == 4 ? p.bounds[1] : 0.f;
+    const float tau_scale = 4.f * static_cast<float>(d + 3) * 0x1.0p-24f;
+
+    const T* __restrict__ x = static_cast<const T*>(p.x);
+    const int64_t ntiles = ceil_div(p.n, KM_TILE);
+    const int64_t my_tiles =
+        blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    // prologue: stages-1 tiles in flight
+    for (int s = 0; s < p.stages - 1; ++s) {
+        if (s < my_tiles)
+            load_tile<T>(xs + s * stage_elems, x, p.n, d, srow, blockIdx.x + s * gridDim.x, p.aligned16);
+        cp_async_commit();
+    }
+    unsigned long long refined = 0;
+
+    for (int64_t it = 0; it < my_tiles; ++it) {
+        const int64_t tile = blockIdx.x + it * gridDim.x;
+        const int stage = static_cast<int>(it % p.stages);
+        // wait until at most stages-2 younger groups are pending -> tile `it` landed
+        if (p.stages == 2) cp_async_wait<0>();
+        else if (p.stages == 3) cp_async_wait<1>();
+        else cp_async_wait<2>();
+        __syncthreads();
+        {
+            const int64_t nxt = it + p.stages - 1;
+            if (nxt < my_tiles)
+                load_tile<T>(xs + ((it + p.stages - 1) % p.stages) * stage_elems, x, p.n, d, srow,
+                             blockIdx.x + nxt * gridDim.x, p.aligned16);
+            cp_async_commit();
+        }
+        const T* xt = xs + stage * stage_elems;
+
+        // ---------------- phase 1: lane = row
+        const int row = threadIdx.x;
+        const int64_t grow = tile * KM_TILE + row;
+        int label = -1;
+        if (grow < p.n) {
+            const T* xr = xt + row * srow;
+            if constexpr (sizeof(T) == 4) {
+                float b1 = FLT_MAX, b2 = FLT_MAX, xx = 0.f;
+                int i1 = 0;
+                if constexpr (D > 0) {
+                    float xv[D];
+                    if constexpr (D % 2 == 0) {
+#pragma unroll
+                        for (int f = 0; f < D; f += 2) {
+                            const float2 v = *reinterpret_cast<const float2*>(xr + f);
+                            xv[f] = v.x;
+                            xv[f + 1] = v.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int f = 0; f < D; ++f) xv[f] = xr[f];
+                    }
+#pragma unroll
+                    for (int f = 0; f < D; ++f) xx = fmaf(xv[f], xv[f], xx);
+                    for (int j = 0; j < k; ++j) {
+                        const float* c = cts + j * p.dpad;
+                        float s = cns[j];
+#pragma unroll
+                        for (int f = 0; f < (D & ~3); f += 4) {
+                            const float4 cv = *reinterpret_cast<const float4*>(c + f);
+                            s = fmaf(xv[f], cv.x, s);
+                            s = fmaf(xv[f + 1], cv.y, s);
+                            s = fmaf(xv[f + 2], cv.z, s);
+                            s = fmaf(xv[f + 3], cv.w, s);
+                        }
+#pragma unroll
+                        for (int f = D & ~3; f < D; ++f) s = fmaf(xv[f], c[f], s);
+                        if (s < b1) {
+                            b2 = b1;
+                            b1 = s;
+                            i1 = j;
+                        } else if (s < b2) {
+                            b2 = s;
+                        }
+                    }
+                } else {
+                    for (int f = 0; f < d; ++f) xx = fmaf(xr[f], xr[f], xx);
+                    for (int j = 0; j < k; ++j) {
+                        const float* c = cts + j * p.dpad;
+                        float s = cns[j];
+                        for (int f = 0; f < d; ++f) s = fmaf(xr[f], c[f], s);
+                        if (s < b1) {
+                            b2 = b1;
+                            b1 = s;
+                            i1 = j;
+                        } else if (s < b2) {
+                            b2 = s;
+                        }
+                    }
+                }
+                label = i1;
+                // |s_j - exact_j| <= (d+3) u (|c_j|^2 + 2 |x||c_j|) for both
+                // candidates; 2x safety on the sum of the two bounds.
+                const float tau = tau_scale * (cnmax + 2.f * sqrtf(xx) * cmax);
+                if (k > 1 && !(b2 - b1 > tau)) {
+                    label = ref_argmin<T>(xr, d, p.c64, p.cn64, k);
+                    ++refined;
+                }
+            } else {
+                label = ref_argmin<T>(xr, d, p.c64, p.cn64, k);
+            }
+            if (p.labels) p.labels[grow] = label;
+        }
+        lbl[row] = label;
+        __syncthreads();
+
+        // ---------------- phase 2: lane = feature, warp owns clusters
+        if (accumulate) {
+            for (int j = warp; j < k; j += KM_WARPS) {
+                long long cj = 0;
+#pragma unroll 1
+                for (int c = 0; c < KM_TILE / 32; ++c) {
+                    const unsigned mask = __ballot_sync(FULL, lbl[c * 32 + lane] == j);
+                    if (mask == 0u) continue;
+                    cj += __popc(mask);
+                    for (int fb = 0; fb < d; fb += 32) {
+                        const int f = fb + lane;
+                        if (f < d) {
+                            T part = T(0);
+                            unsigned mm = mask;
+                            while (mm) {
+                                const int r = __ffs(mm) - 1;
+                                mm &= mm - 1;
+                                part += xt[(c * 32 + r) * srow + f];
+                            }
+                            acc[j * d + f] += static_cast<double>(part);
+                        }
+                    }
+                }
+                if (lane == 0) cnt[j] += cj;
+            }
+        }
+    }
+    cp_async_wait<0>();
+    if (refined) atomicAdd(p.refined, refined);
+    if (!accumulate) return;
+    __syncthreads();
+    const int S = k * d + k;
+    double* out = p.partials + static_cast<int64_t>(blockIdx.x) * S;
+    for (int e = threadIdx.x; e < k * d; e += KM_THREADS) out[e] = acc[e];
+    for (int j = threadIdx.x; j < k; j += KM_THREADS) out[k * d + j] = static_cast<double>(cnt[j]);
+}
+
+// Per-stat sum over CTA partials in CTA order.
+__global__ void reduce_partials_kernel(const double* __restrict__ partials, int G, int S,
+                                       double* __restrict__ stats, const int* done) {
+    if (done && *done) return;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= S) return;
+    double s = 0.0;
+    for (int g = 0; g < G; ++g) s += partials[static_cast<int64_t>(g) * S + e];
+    stats[e] = s;
+}
+
+// Deterministic block reductions (fixed tree over the thread index).
+__device__ double block_sum(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+__device__ double block_max(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+// Recomputes the derived tables of cluster j from c64 (f64 master copy).
+__device__ void derive_cluster(int j, int d, int dpad, const double* c64, double* cn64, float* ct,
+                               float* cn32, double& cnorm, double& cn32v) {
+    double n64 = 0.0, n32 = 0.0;
+    for (int f = 0; f < d; ++f) {
+        const double c = c64[static_cast<int64_t>(j) * d + f];
+        n64 = add_rn(n64, mul_rn(c, c));  // row_norms order (pairwise.cpp:13-18)
+        const float c32 = static_cast<float>(c);
+        ct[static_cast<int64_t>(j) * dpad + f] = -2.f * c32;
+        n32 += static_cast<double>(c32) * static_cast<double>(c32);
+    }
+    for (int f = d; f < dpad; ++f) ct[static_cast<int64_t>(j) * dpad + f] = 0.f;
+    cn64[j] = n64;
+    cn32[j] = static_cast<float>(n32);
+    cnorm = sqrt(n32);
+    cn32v = static_cast<double>(static_cast<float>(n32));
+}
+
+__global__ void derive_tables_kernel(int k, int d, int dpad, const double* c64, double* cn64,
+                                     float* ct, float* cn32, float* bounds) {
+    __shared__ double sh[256];
+    double cmax = 0.0, cnmax = 0.0;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        double cnorm, cnv;
+        derive_cluster(j, d, dpad, c64, cn64, ct, cn32, cnorm, cnv);
+        cmax = fmax(cmax, cnorm);
+        cnmax = fmax(cnmax, cnv);
+    }
+    cmax = block_max(cmax, sh);
+    cnmax = block_max(cnmax, sh);
+    if (threadIdx.x == 0) {
+        bounds[0] = static_cast<float>(cmax) * (1.f + 0x1.0p-20f);
+        bounds[1] = static_cast<float>(cnmax) * (1.f + 0x1.0p-20f);
+    }
+}
+
+// One CTA: rank-order fold, centroid update, inertia, displacement, tables.
+__global__ void kmeans_update_kernel(int k, int d, int dpad, int world, const double* gathered,
+                                     double* c64, double* cn64, float* ct, float* cn32, float* bounds,
+                                     const double* sx2, double* trace, double* disp, int* flags,
+                                     int iter, double tol) {
+    if (flags[0]) return;
+    __shared__ double sh[256];
+    const int S = k * d + k;
+    double inertia_part = 0.0, dmax = 0.0, cmax = 0.0, cnmax = 0.0;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        // allreduce(plus_vec) from the zero identity in rank order
+        double count = 0.0;
+        for (int r = 0; r < world; ++r) count += gathered[static_cast<int64_t>(r) * S + k * d + j];
+        double dot = 0.0, dsq = 0.0;
+        for (int f = 0; f < d; ++f) {
+            double s = 0.0;
+            for (int r = 0; r < world; ++r) s += gathered[static_cast<int64_t>(r) * S + j * d + f];
+            const double old = c64[static_cast<int64_t>(j) * d + f];
+            dot += old * s;
+            const double nxt = count > 0.0 ? s / count : old;
+            const double diff = nxt - old;
+            dsq = add_rn(dsq, mul_rn(diff, diff));  // cluster.cpp:142-146 order
+            c64[static_cast<int64_t>(j) * d + f] = nxt;
+        }
+        inertia_part += count * cn64[j] - 2.0 * dot;  // uses the old |c_j|^2
+        dmax = fmax(dmax, __dsqrt_rn(dsq));
+        double cnorm, cnv;
+        derive_cluster(j, d, dpad, c64, cn64, ct, cn32, cnorm, cnv);
+        cmax = fmax(cmax, cnorm);
+        cnmax = fmax(cnmax, cnv);
+    }
+    const double inertia = block_sum(inertia_part, sh);
+    dmax = block_max(dmax, sh);
+    cmax = block_max(cmax, sh);
+    cnmax = block_max(cnmax, sh);
+    if (threadIdx.x == 0) {
+        trace[iter] = sx2[2] + inertia;
+        disp[iter] = dmax;
+        flags[1] = iter + 1;
+        if (dmax < tol) flags[0] = 1;
+        bounds[0] = static_cast<float>(cmax) * (1.f + 0x1.0p-20f);
+        bounds[1] = static_cast<float>(cnmax) * (1.f + 0x1.0p-20f);
+    }
+}
+
+// Validation pass (cluster.cpp:88-89) fused with sum |x|^2.
+template <typename T>
+__global__ void validate_kernel(const T* __restrict__ x, int64_t count, double* out) {
+    __shared__ double sh[256];
+    double s = 0.0, bad = 0.0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += stride) {
+        const double v = static_cast<double>(x[e]);
+        if (!isfinite(v)) bad += 1.0;
+        else s += v * v;
+    }
+    s = block_sum(s, sh);
+    bad = block_sum(bad, sh);
+    if (threadIdx.x == 0) {
+        out[2 * blockIdx.x] = s;
+        out[2 * blockIdx.x + 1] = bad;
+    }
+}
+
+__global__ void validate_final_kernel(const double* pre, int G, double* sx2) {
+    if (threadIdx.x != 0) return;
+    double s = 0.0, bad = 0.0;
+    for (int g = 0; g < G; ++g) {
+        s += pre[2 * g];
+        bad += pre[2 * g + 1];
+    }
+    sx2[0] = s;
+    sx2[1] = bad;
+}
+
+// gather_rows (cluster.cpp:27-42): rows owned by this rank into a zero-filled
+// k x m f64 buffer (the allreduce-sum across ranks is then exact).
+template <typename T>
+__global__ void gather_rows_kernel(const T* __restrict__ x, int64_t lo, int64_t hi, int m,
+                                   const int64_t* idx, int k, double* c64) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * m; e += gridDim.x * blockDim.x) {
+        const int j = e / m, f = e % m;
+        const int64_t g = idx[j];
+        c64[e] = (g >= lo && g < hi) ? static_cast<double>(x[(g - lo) * m + f]) : 0.0;
+    }
+}
+
+__global__ void kmeans_reset_kernel(int* flags, unsigned long long* refined) {
+    flags[0] = 0;
+    flags[1] = 0;
+    *refined = 0ull;
+}
+
+// ----------------------------------------------------------------- host
+static KmBuffers buffers(dndc_ctx* ctx, int k, int m, int max_iter, int G) {
+    KmBuffers b;
+    const size_t S = static_cast<size_t>(k) * m + k;
+    b.c64 = static_cast<double*>(ctx->slot("km_c64", sizeof(double) * k * m));
+    b.cn64 = static_cast<double*>(ctx->slot("km_cn64", sizeof(double) * k));
+    b.ct = static_cast<float*>(ctx->slot("km_ct", sizeof(float) * k * dpad_of(m)));
+    b.cn32 = static_cast<float*>(ctx->slot("km_cn32", sizeof(float) * k));
+    b.bounds = static_cast<float*>(ctx->slot("km_bounds", sizeof(float) * 4));
+    b.stats = static_cast<double*>(ctx->slot("km_stats", sizeof(double) * S));
+    b.gathered = static_cast<double*>(ctx->slot("km_gathered", sizeof(double) * S * ctx->world));
+    b.partials = static_cast<double*>(ctx->slot("km_partials", sizeof(double) * S * std::max(G, 1)));
+    b.trace = static_cast<double*>(ctx->slot("km_trace", sizeof(double) * std::max(max_iter, 1)));
+    b.disp = static_cast<double*>(ctx->slot("km_disp", sizeof(double) * std::max(max_iter, 1)));
+    b.flags = static_cast<int*>(ctx->slot("km_flags", sizeof(int) * 4));
+    b.sx2 = static_cast<double*>(ctx->slot("km_sx2", sizeof(double) * 4));
+    b.pre = static_cast<double*>(ctx->slot("km_pre", sizeof(double) * 2 * 4096));
+    b.refined = static_cast<unsigned long long*>(ctx->slot("km_refined", sizeof(unsigned long long)));
+    return b;
+}
+
+template <typename T>
+struct AssignLaunch {
+    void (*fn)(AssignParams);
+    size_t smem;
+    int grid;
+    int stages;
+};
+
+template <typename T, int D>
+static void pick(AssignLaunch<T>& L) {
+    L.fn = kmeans_assign_kernel<T, D>;
+}
+
+template <typename T>
+static size_t assign_smem(int k, int d, int stages) {
+    return smem_layout(sizeof(T), k, d, srow_of(d), dpad_of(d), stages).total;
+}
+
+template <typename T>
+static AssignLaunch<T> plan_assign(dndc_ctx* ctx, int k, int d, int64_t n) {
+    AssignLaunch<T> L{};
+    if constexpr (sizeof(T) == 4) {
+        switch (d) {
+            case 2: pick<T, 2>(L); break;
+            case 3: pick<T, 3>(L); break;
+            case 4: pick<T, 4>(L); break;
+            case 8: pick<T, 8>(L); break;
+            case 16: pick<T, 16>(L); break;
+            case 18: pick<T, 18>(L); break;
+            case 32: pick<T, 32>(L); break;
+            case 64: pick<T, 64>(L); break;
+            default: pick<T, 0>(L); break;
+        }
+    } else {
+        pick<T, 0>(L);
+    }
+    int stages = 4;
+    while (stages > 2 && assign_smem<T>(k, d, stages) > 200 * 1024) --stages;
+    L.stages = stages;
+    L.smem = assign_smem<T>(k, d, stages);
+    if (L.smem > 227 * 1024)
+        throw Error(DNDC_EVALUE, "kmeans: k*m too large for the shared-memory accumulator (k=" +
+                                     std::to_string(k) + ", m=" + std::to_string(d) + ")");
+    DNDC_CUDA(cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(L.smem)));
+    int per_sm = 1;
+    DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.fn, KM_THREADS, L.smem));
+    per_sm = std::max(per_sm, 1);
+    const int64_t tiles = std::max<int64_t>(ceil_div(n, KM_TILE), 1);
+    L.grid = static_cast<int>(std::min<int64_t>(tiles, static_cast<int64_t>(ctx->num_sms) * per_sm));
+    return L;
+}
+
+template <typename T>
+static AssignParams assign_params(const KmBuffers& b, const T* x, int64_t n, int d, int k,
+                                  int stages, bool accumulate, int32_t* labels, bool use_done) {
+    AssignParams p{};
+    p.x = x;
+    p.n = n;
+    p.d = d;
+    p.k = k;
+    p.dpad = dpad_of(d);
+    p.srow = srow_of(d);
+    p.stages = stages;
+    p.aligned16 = reinterpret_cast<uintptr_t>(x) % 16 == 0;
+    p.ct = b.ct;
+    p.cn32 = b.cn32;
+    p.bounds = b.bounds;
+    p.c64 = b.c64;
+    p.cn64 = b.cn64;
+    p.partials = accumulate ? b.partials : nullptr;
+    p.labels = labels;
+    p.refined = b.refined;
+    p.done = use_done ? b.flags : nullptr;
+    return p;
+}
+
+static void validate_k(int64_t n, int k, const char* who) {
+    if (k < 1) value_error(std::string(who) + ": k must be positive, got " + std::to_string(k));
+    if (static_cast<int64_t>(k) > n)
+        value_error(std::string(who) + ": k=" + std::to_string(k) + " exceeds the " + std::to_string(n) +
+                    " available samples");
+}
+
+std::vector<int64_t> init_indices(int64_t n, int k, uint64_t seed) {
+    // cluster.cpp:60-75 without the O(n) pool: only swapped positions differ
+    // from the identity.
+    if (k < 1 || static_cast<int64_t>(k) > n)
+        value_error("kmeans_init_indices: k=" + std::to_string(k) + " out of range for n=" +
+                    std::to_string(n));
+    std::map<int64_t, int64_t> pool;
+    auto get = [&](int64_t i) {
+        auto it = pool.find(i);
+        return it == pool.end() ? i : it->second;
+    };
+    for (int j = 0; j < k; ++j) {
+        const uint64_t draw = splitmix64(seed ^ splitmix64(0x6b8b4567u + static_cast<uint64_t>(j)));
+        const int64_t pick = j + static_cast<int64_t>(draw % static_cast<uint64_t>(n - j));
+        const int64_t a = get(j), b = get(pick);
+        pool[j] = b;
+        pool[pick] = a;
+    }
+    std::vector<int64_t> out(k);
+    for (int j = 0; j < k; ++j) out[j] = get(j);
+    return out;
+}
+
+template <typename T>
+static void init_centroids(dndc_ctx* ctx, const KmBuffers& b, const T* x_local, int64_t lo,
+                           int64_t n_local, int m, int k, uint64_t seed, int64_t n_global) {
+    const auto idx = init_indices(n_global, k, seed);
+    int64_t* didx = static_cast<int64_t*>(ctx->slot("km_idx", sizeof(int64_t) * k));
+    int64_t* hidx = static_cast<int64_t*>(ctx->host_staging(sizeof(int64_t) * k));
+    std::memcpy(hidx, idx.data(), sizeof(int64_t) * k);
+    DNDC_CUDA(cudaMemcpyAsync(didx, hidx, sizeof(int64_t) * k, cudaMemcpyHostToDevice, ctx->stream));
+    gather_rows_kernel<T><<<std::max(1, std::min(1024, (k * m + 255) / 256)), 256, 0, ctx->stream>>>(
+        x_local, lo, lo + n_local, m, didx, k, b.c64);
+    DNDC_LAUNCHED(ctx);
+    allreduce_sum_f64(ctx, b.c64, static_cast<size_t>(k) * m, ctx->stream);
+    // the pinned staging buffer is reused by later calls: finish the copy first
+    DNDC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+static void derive_tables(dndc_ctx* ctx, const KmBuffers& b, int k, int m) {
+    derive_tables_kernel<<<1, 256, 0, ctx->stream>>>(k, m, dpad_of(m), b.c64, b.cn64, b.ct, b.cn32,
+                                                     b.bounds);
+    DNDC_LAUNCHED(ctx);
+}
+
+template <typename T>
+static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t n_global, int64_t m64,
+                       int k, int max_iter, double tol, uint64_t seed, const double* init_host,
+                       double* cent_host, double* trace_host, int* iters_host) {
+    validate_k(n_global, k, "kmeans_fit");
+    if (max_iter < 1) value_error("kmeans_fit: max_iter must be positive, got " + std::to_string(max_iter));
+    std::vector<int64_t> off, ext;
+    chunk_map(n_global, ctx->world, off, ext);
+    if (n_local != ext[ctx->rank])
+        value_error("kmeans_fit: local shard has " + std::to_string(n_local) + " rows, chunk_map gives " +
+                    std::to_string(ext[ctx->rank]));
+    const int m = static_cast<int>(m64);
+    cudaStream_t s = ctx->stream;
+    AssignLaunch<T> L = plan_assign<T>(ctx, k, m, n_local);
+    const KmBuffers b = buffers(ctx, k, m, max_iter, L.grid);
+    const int S = k * m + k;
+
+    // ---- validation + sum |x|^2 (one pass), agreed by every rank
+    {
+        const int64_t count = n_local * m;
+        const int G = static_cast<int>(std::min<int64_t>(std::max<int64_t>(ceil_div(count, 256 * 8), 1), 4096));
+        validate_kernel<T><<<G, 256, 0, s>>>(x_local, count, b.pre);
+        DNDC_LAUNCHED(ctx);
+        validate_final_kernel<<<1, 32, 0, s>>>(b.pre, G, b.sx2);
+        DNDC_LAUNCHED(ctx);
+        double* all = b.gathered;  // scratch: world x 2
+        allgather_f64(ctx, b.sx2, all, 2, s);
+        double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * 2 * ctx->world));
+        DNDC_CUDA(cudaMemcpyAsync(h, all, sizeof(double) * 2 * ctx->world, cudaMemcpyDeviceToHost, s));
+        DNDC_CUDA(cudaStreamSynchronize(s));
+        double sx2 = 0.0, bad = 0.0;
+        for (int r = 0; r < ctx->world; ++r) {
+            sx2 += h[2 * r];
+            bad += h[2 * r + 1];
+        }
+        if (bad > 0.0) value_error("kmeans_fit: input contains non-finite values");
+        h[0] = 0.0;
+        h[1] = 0.0;
+        h[2] = sx2;
+        DNDC_CUDA(cudaMemcpyAsync(b.sx2, h, sizeof(double) * 3, cudaMemcpyHostToDevice, s));
+        DNDC_CUDA(cudaStreamSynchronize(s));
+    }
+
+    // ---- initial centroids
+    if (init_host) {
+        double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * k * m));
+        std::memcpy(h, init_host, sizeof(double) * k * m);
+        DNDC_CUDA(cudaMemcpyAsync(b.c64, h, sizeof(double) * k * m, cudaMemcpyHostToDevice, s));
+        DNDC_CUDA(cudaStreamSynchronize(s));
+    } else {
+        init_centroids<T>(ctx, b, x_local, off[ctx->rank], n_local, m, k, seed, n_global);
+    }
+    derive_tables(ctx, b, k, m);
+
+    // ---- the Lloyd loop, one graph per (shape, buffers, max_iter, tol)
+    const AssignParams ap = assign_params<T>(b, x_local, n_local, m, k, L.stages, true, nullptr, true);
+    auto record = [&](cudaStream_t st) {
+        kmeans_reset_kernel<<<1, 1, 0, st>>>(b.flags, b.refined);
+        for (int it = 0; it < max_iter; ++it) {
+            L.fn<<<L.grid, KM_THREADS, L.smem, st>>>(ap);
+            reduce_partials_kernel<<<(S + 255) / 256, 256, 0, st>>>(b.partials, L.grid, S, b.stats, b.flags);
+            if (ctx->world > 1) allgather_f64(ctx, b.stats, b.gathered, S, st);
+            kmeans_update_kernel<<<1, 256, 0, st>>>(k, m, dpad_of(m), ctx->world,
+                                                   ctx->world > 1 ? b.gathered : b.stats, b.c64, b.cn64,
+                                                   b.ct, b.cn32, b.bounds, b.sx2, b.trace, b.disp, b.flags,
+                                                   it, tol);
+        }
+    };
+    if (!ctx->km) ctx->km = new KMeansState();
+    char keybuf[256];
+    std::snprintf(keybuf, sizeof(keybuf), "%p/%lld/%d/%d/%d/%.17g/%p/%d/%d", (const void*)x_local,
+                  (long long)n_local, m, k, max_iter, tol, (void*)s, L.grid, ctx->world);
+    const std::string key = std::string(sizeof(T) == 4 ? "f32/" : "f64/") + keybuf;
+    if (ctx->km->key != key || !ctx->km->exec) {
+        if (ctx->km->exec) {
+            cudaGraphExecDestroy(ctx->km->exec);
+            ctx->km->exec = nullptr;
+        }
+        const uint64_t before = ctx->counters.allgathers;
+        cudaGraph_t graph;
+        DNDC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            record(s);
+        } catch (...) {
+            cudaStreamEndCapture(s, &graph);
+            throw;
+        }
+        DNDC_CUDA(cudaStreamEndCapture(s, &graph));
+        ctx->counters.allgathers = before;  // counted per replay below
+        DNDC_CUDA(cudaGraphInstantiate(&ctx->km->exec, graph, 0));
+        DNDC_CUDA(cudaGraphDestroy(graph));
+        ctx->km->key = key;
+    }
+    DNDC_CUDA(cudaGraphLaunch(ctx->km->exec, s));
+    ctx->launches += 1 + 3ull * max_iter;
+    if (ctx->world > 1) ctx->counters.allgathers += max_iter;
+
+    // ---- results
+    const size_t hb = sizeof(double) * (k * m + max_iter) + 64;
+    unsigned char* h = static_cast<unsigned char*>(ctx->host_staging(hb));
+    DNDC_CUDA(cudaMemcpyAsync(h, b.c64, sizeof(double) * k * m, cudaMemcpyDeviceToHost, s));
+    DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * k * m, b.trace, sizeof(double) * max_iter,
+                              cudaMemcpyDeviceToHost, s));
+    DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * (k * m + max_iter), b.flags, sizeof(int) * 2,
+                              cudaMemcpyDeviceToHost, s));
+    DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * (k * m + max_iter) + 16, b.refined,
+                              sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    DNDC_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(cent_host, h, sizeof(double) * k * m);
+    const int* flags = reinterpret_cast<const int*>(h + sizeof(double) * (k * m + max_iter));
+    const int iters = flags[1];
+    std::memcpy(trace_host, h + sizeof(double) * k * m, sizeof(double) * max_iter);
+    *iters_host = iters;
+    ctx->last_refined = static_cast<int64_t>(
+        *reinterpret_cast<const unsigned long long*>(h + sizeof(double) * (k * m + max_iter) + 16));
+}
+
+template <typename T>
+static void kmeans_predict(dndc_ctx* ctx, const T* x, int64_t n, int64_t m64, const double* cent_host,
+                           int k, int32_t* labels) {
+    if (k < 1) value_error("kmeans_predict: k must be positive");
+    const int m = static_cast<int>(m64);
+    cudaStream_t s = ctx->stream;
+    AssignLaunch<T> L = plan_assign<T>(ctx, k, m, n);
+    const KmBuffers b = buffers(ctx, k, m, 1, L.grid);
+    double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * k * m));
+    std::memcpy(h, cent_host, sizeof(double) * k * m);
+    DNDC_CUDA(cudaMemcpyAsync(b.c64, h, sizeof(double) * k * m, cudaMemcpyHostToDevice, s));
+    DNDC_CUDA(cudaMemsetAsync(b.refined, 0, sizeof(unsigned long long), s));
+    derive_tables(ctx, b, k, m);
+    if (n > 0) {
+        const AssignParams ap = assign_params<T>(b, x, n, m, k, L.stages, false, labels, false);
+        L.fn<<<L.grid, KM_THREADS, L.smem, s>>>(ap);
+        DNDC_LAUNCHED(ctx);
+    }
+    unsigned long long* hr = reinterpret_cast<unsigned long long*>(h);
+    DNDC_CUDA(cudaMemcpyAsync(hr, b.refined, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    DNDC_CUDA(cudaStreamSynchronize(s));
+    ctx->last_refined = static_cast<int64_t>(*hr);
+}
+
+template <typename T>
+static void init_centroids_api(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t n_global,
+                               int64_t m, int k, uint64_t seed, double* out_host) {
+    validate_k(n_global, k, "kmeans_init_centroids");
+    std::vector<int64_t> off, ext;
+    chunk_map(n_global, ctx->world, off, ext);
+    if (n_local != ext[ctx->rank]) value_error("kmeans_init_centroids: shard does not match chunk_map");
+    const KmBuffers b = buffers(ctx, k, static_cast<int>(m), 1, 1);
+    init_centroids<T>(ctx, b, x_local, off[ctx->rank], n_local, static_cast<int>(m), k, seed, n_global);
+    double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * k * m));
+    DNDC_CUDA(cudaMemcpyAsync(h, b.c64, sizeof(double) * k * m, cudaMemcpyDeviceToHost, ctx->stream));
+    DNDC_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(out_host, h, sizeof(double) * k * m);
+}
+
+// Times the dominant kernel (assign + accumulate) alone: `reps` back-to-back
+// launches bracketed by CUDA events on the context's stream, against the
+// centroid tables of the last fit (or the first k rows when there was none).
+static void time_assign(dndc_ctx* ctx, const float* x, int64_t n, int64_t m64, int k, int reps, double* ms,
+                        double* bytes) {
+    const int m = static_cast<int>(m64);
+    cudaStream_t s = ctx->stream;
+    AssignLaunch<float> L = plan_assign<float>(ctx, k, m, n);
+    const bool fresh = ctx->slots.find("km_c64") == ctx->slots.end();
+    const KmBuffers b = buffers(ctx, k, m, 1, L.grid);
+    if (fresh) {
+        std::vector<int64_t> idx(k);
+        for (int j = 0; j < k; ++j) idx[j] = j;
+        int64_t* didx = static_cast<int64_t*>(ctx->slot("km_idx", sizeof(int64_t) * k));
+        DNDC_CUDA(cudaMemcpy(didx, idx.data(), sizeof(int64_t) * k, cudaMemcpyHostToDevice));
+        gather_rows_kernel<float><<<1, 256, 0, s>>>(x, 0, n, m, didx, k, b.c64);
+        derive_tables(ctx, b, k, m);
+    }
+    const AssignParams ap = assign_params<float>(b, x, n, m, k, L.stages, true, nullptr, false);
+    cudaEvent_t e0, e1;
+    DNDC_CUDA(cudaEventCreate(&e0));
+    DNDC_CUDA(cudaEventCreate(&e1));
+    L.fn<<<L.grid, KM_THREADS, L.smem, s>>>(ap);  // warm
+    DNDC_CUDA(cudaEventRecord(e0, s));
+    for (int r = 0; r < reps; ++r) L.fn<<<L.grid, KM_THREADS, L.smem, s>>>(ap);
+    DNDC_CUDA(cudaEventRecord(e1, s));
+    DNDC_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    DNDC_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ctx->launches += reps + 1;
+    *ms = static_cast<double>(t) / reps;
+    *bytes = static_cast<double>(n) * m * sizeof(float);
+}
+
+}  // namespace dndc
+
+using dndc::guard;
+
+extern "C" {
+
+int dndc_kmeans_init_indices(int64_t n, int k, uint64_t seed, int64_t* out_host) {
+    return guard([&] {
+        const auto v = dndc::init_indices(n, k, seed);
+        std::memcpy(out_host, v.data(), v.size() * sizeof(int64_t));
+    });
+}
+
+int dndc_kmeans_init_centroids_f32(dndc_ctx* ctx, const float* x_local, int64_t n_local,
+                                   int64_t n_global, int64_t m, int k, uint64_t seed,
+                                   double* centroids_host) {
+    return guard([&] {
+        dndc::init_centroids_api<float>(ctx, x_local, n_local, n_global, m, k, seed, centroids_host);
+    });
+}
+
+int dndc_kmeans_fit_f32(dndc_ctx* ctx, const float* x_local, int64_t n_local, int64_t n_global,
+                        int64_t m, int k, int max_iter, double tol, uint64_t seed,
+                        const double* init_centroids_host, double* centroids_host,
+                        double* inertia_trace_host, int* iterations_run) {
+    return guard([&] {
+        dndc::kmeans_fit<float>(ctx, x_local, n_local, n_global, m, k, max_iter, tol, seed,
+                                init_centroids_host, centroids_host, inertia_trace_host, iterations_run);
+    });
+}
+
+int dndc_kmeans_fit_f64(dndc_ctx* ctx, const double* x_local, int64_t n_local, int64_t n_global,
+                        int64_t m, int k, int max_iter, double tol, uint64_t seed,
+                        const double* init_centroids_host, double* centroids_host,
+                        double* inertia_trace_host, int* iterations_run) {
+    return guard([&] {
+        dndc::kmeans_fit<double>(ctx, x_local, n_local, n_global, m, k, max_iter, tol, seed,
+                                 init_centroids_host, centroids_host, inertia_trace_host, iterations_run);
+    });
+}
+
+int dndc_kmeans_predict_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m,
+                            const double* centroids_host, int k, int32_t* labels) {
+    return guard([&] { dndc::kmeans_predict<float>(ctx, x, n, m, centroids_host, k, labels); });
+}
+
+int dndc_kmeans_predict_f64(dndc_ctx* ctx, const double* x, int64_t n, int64_t m,
+                            const double* centroids_host, int k, int32_t* labels) {
+    return guard([&] { dndc::kmeans_predict<double>(ctx, x, n, m, centroids_host, k, labels); });
+}
+
+int dndc_kmeans_time_assign_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m, int k, int reps,
+                                double* ms_per_launch, double* algorithmic_bytes) {
+    return guard([&] { dndc::time_assign(ctx, x, n, m, k, reps, ms_per_launch, algorithmic_bytes); });
+}
+
+int dndc_kmeans_last_refined(const dndc_ctx* ctx, int64_t* rows_refined) {
+    *rows_refined = ctx->last_refined;
+    return DNDC_OK;
+}
+
+}  // extern "C"

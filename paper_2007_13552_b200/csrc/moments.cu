@@ -1,0 +1,164 @@
+// moments.cu -- A13/A14: per-column count/mean/M2 along the split axis 0.
+//
+// Reference: welford_update, local_moments_axis, combine, axis_statistic,
+// mean_axis / var_axis / stddev_axis (moments.cpp:10-140).
+//
+// One pass over the shard.  Thread (column c, row-lane r) walks rows r,
+// r + R, ... of its CTA's row range in chunks of KC rows: inside a chunk it
+// keeps f64 sums of (x - K) and (x - K)^2 around the chunk's first value K
+// (exact differences for fp32 input, no per-element division), converts the
+// chunk to (count, mean, M2) and merges it into its running state with the
+// reference's combine formula (Chan et al., moments.cpp:69-89).  States are
+// then merged in a fixed order: row-lanes inside the CTA, CTAs in a second
+// kernel, ranks on the host in rank order 0..p-1 from the identity -- the
+// reference's allreduce(combine) fold (moments.cpp:45-47, transport.hpp:140-146).
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace dndc {
+
+constexpr int MO_THREADS = 256;
+constexpr int MO_KC = 32;  // rows per shifted-sum chunk
+
+struct Moment {
+    double n, mean, m2;
+};
+
+// combine(a, b) of moments.cpp:69-89 for one slot (identity = n == 0).
+__host__ __device__ inline Moment combine1(Moment a, Moment b) {
+    if (a.n == 0.0) return b;
+    if (b.n == 0.0) return a;
+    Moment o;
+    o.n = a.n + b.n;
+    const double delta = b.mean - a.mean;
+    o.mean = a.mean + delta * b.n / o.n;
+    o.m2 = a.m2 + b.m2 + delta * delta * a.n * b.n / o.n;
+    return o;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(MO_THREADS)
+    moments_partial_kernel(const T* __restrict__ x, int64_t n, int m, int cols, int lanes,
+                           int64_t rows_per_cta, double* __restrict__ partials) {
+    // partials: [gridDim.x][3][m] as (n, mean, m2) per column
+    __shared__ Moment sh[MO_THREADS];
+    const int c_local = threadIdx.x % cols;
+    const int rl = threadIdx.x / cols;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_cta;
+    const int64_t r1 = min(n, r0 + rows_per_cta);
+    for (int cb = 0; cb < m; cb += cols) {
+        const int c = cb + c_local;
+        Moment run{0.0, 0.0, 0.0};
+        const bool active = rl < lanes && c < m;
+        if (active) {
+            int64_t i = r0 + rl;
+            while (i < r1) {
+                const double K = static_cast<double>(x[i * m + c]);
+                double s1 = 0.0, s2 = 0.0;
+                int cnt = 0;
+                for (; cnt < MO_KC && i < r1; ++cnt, i += lanes) {
+                    const double v = static_cast<double>(x[i * m + c]) - K;
+                    s1 += v;
+                    s2 = fma(v, v, s2);
+                }
+                const double nc = static_cast<double>(cnt);
+                Moment ch;
+                ch.n = nc;
+                ch.mean = K + s1 / nc;
+                ch.m2 = fmax(s2 - s1 * s1 / nc, 0.0);
+                run = combine1(run, ch);
+            }
+        }
+        sh[threadIdx.x] = run;
+        __syncthreads();
+        if (rl == 0 && c < m) {
+            Moment acc = sh[c_local];
+            for (int l = 1; l < lanes; ++l) acc = combine1(acc, sh[l * cols + c_local]);
+            double* out = partials + static_cast<int64_t>(blockIdx.x) * 3 * m;
+            out[c] = acc.n;
+            out[m + c] = acc.mean;
+            out[2 * m + c] = acc.m2;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void moments_final_kernel(const double* __restrict__ partials, int G, int m,
+                                     double* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= m) return;
+    Moment acc{0.0, 0.0, 0.0};
+    for (int g = 0; g < G; ++g) {
+        const double* p = partials + static_cast<int64_t>(g) * 3 * m;
+        acc = combine1(acc, Moment{p[c], p[m + c], p[2 * m + c]});
+    }
+    out[c] = acc.n;
+    out[m + c] = acc.mean;
+    out[2 * m + c] = acc.m2;
+}
+
+template <typename T>
+static void moments_axis0(dndc_ctx* ctx, const T* x, int64_t n_local, int64_t m64, int64_t* count_host,
+                          double* mean_host, double* m2_host) {
+    if (m64 < 0 || n_local < 0) value_error("moments: negative extent");
+    const int m = static_cast<int>(m64);
+    cudaStream_t s = ctx->stream;
+    const size_t rec = 3 * static_cast<size_t>(std::max(m, 1));
+    double* local = static_cast<double*>(ctx->slot("mo_local", sizeof(double) * rec));
+    double* all = static_cast<double*>(ctx->slot("mo_all", sizeof(double) * rec * ctx->world));
+    if (n_local > 0 && m > 0) {
+        const int cols = std::min(m, MO_THREADS);
+        const int lanes = MO_THREADS / cols;
+        // enough CTAs to fill the GPU, each with at least a few chunks per lane
+        const int64_t min_rows = static_cast<int64_t>(lanes) * MO_KC * 4;
+        const int64_t G = std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, ceil_div(n_local, min_rows)));
+        const int64_t rows_per_cta = ceil_div(n_local, G);
+        double* partials = static_cast<double*>(ctx->slot("mo_partials", sizeof(double) * rec * G));
+        moments_partial_kernel<T><<<static_cast<unsigned>(G), MO_THREADS, 0, s>>>(x, n_local, m, cols, lanes,
+                                                                                rows_per_cta, partials);
+        DNDC_LAUNCHED(ctx);
+        moments_final_kernel<<<(m + 127) / 128, 128, 0, s>>>(partials, static_cast<int>(G), m, local);
+        DNDC_LAUNCHED(ctx);
+    } else {
+        DNDC_CUDA(cudaMemsetAsync(local, 0, sizeof(double) * rec, s));
+    }
+    allgather_f64(ctx, local, all, rec, s);
+    double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * rec * ctx->world));
+    DNDC_CUDA(cudaMemcpyAsync(h, all, sizeof(double) * rec * ctx->world, cudaMemcpyDeviceToHost, s));
+    DNDC_CUDA(cudaStreamSynchronize(s));
+    // rank-order fold from the identity (moments.cpp:45-47), on every rank
+    int64_t count = 0;
+    std::vector<Moment> acc(std::max(m, 0), Moment{0.0, 0.0, 0.0});
+    for (int r = 0; r < ctx->world; ++r) {
+        const double* p = h + rec * r;
+        const int64_t rc = m > 0 ? static_cast<int64_t>(p[0]) : 0;
+        if (rc == 0) continue;  // combine(a, identity) == a exactly
+        for (int c = 0; c < m; ++c) acc[c] = combine1(acc[c], Moment{p[c], p[m + c], p[2 * m + c]});
+        count += rc;
+    }
+    *count_host = m > 0 ? count : 0;
+    for (int c = 0; c < m; ++c) {
+        mean_host[c] = acc[c].mean;
+        m2_host[c] = acc[c].m2;
+    }
+}
+
+}  // namespace dndc
+
+extern "C" {
+
+int dndc_moments_axis0_f32(dndc_ctx* ctx, const float* x_local, int64_t n_local, int64_t m,
+                           int64_t* count_host, double* mean_host, double* m2_host) {
+    return dndc::guard(
+        [&] { dndc::moments_axis0<float>(ctx, x_local, n_local, m, count_host, mean_host, m2_host); });
+}
+
+int dndc_moments_axis0_f64(dndc_ctx* ctx, const double* x_local, int64_t n_local, int64_t m,
+                           int64_t* count_host, double* mean_host, double* m2_host) {
+    return dndc::guard(
+        [&] { dndc::moments_axis0<double>(ctx, x_local, n_local, m, count_host, mean_host, m2_host); });
+}
+
+}  // extern "C"

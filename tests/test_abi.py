@@ -1,0 +1,72 @@
+"""The C-ABI boundary (include/dndc.h) without a GPU: the library loads, exports
+every declared symbol, and its host-only entry points behave like the
+reference functions they replace."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2007_13552_b200 import _lib
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    declared = _lib.header_symbols()
+    assert len(declared) >= 30
+    missing = [s for s in declared if not hasattr(L, s)]
+    assert not missing, missing
+    # the binding table covers the header exactly
+    assert sorted(_lib._SIGS) == declared
+
+
+def test_library_is_built_for_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_chunk_map_host(oracle):
+    for n, p in [(5, 3), (3, 5), (200_000, 8), (0, 2)]:
+        off = np.empty(p, np.int64)
+        ext = np.empty(p, np.int64)
+        assert _lib.lib().dndc_chunk_map(n, p, off.ctypes.data, ext.ctypes.data) == 0
+        o2, e2 = oracle.chunk_map(n, p)
+        assert np.array_equal(off, o2) and np.array_equal(ext, e2)
+    assert _lib.lib().dndc_chunk_map(5, 0, None, None) == _lib.DNDC_EVALUE
+    assert b"rank count" in _lib.lib().dndc_last_error()
+
+
+@pytest.mark.parametrize("n,k,s", [(100, 8, 21), (6, 6, 77), (100_000_000, 8, 42), (50_000_000, 64, 42)])
+def test_init_indices_host(golden, n, k, s):
+    out = np.empty(k, np.int64)
+    assert _lib.lib().dndc_kmeans_init_indices(n, k, s, out.ctypes.data) == 0
+    assert np.array_equal(out, golden[f"init_{n}_{k}_{s}"])
+
+
+def test_value_errors_map_to_python():
+    out = np.empty(4, np.int64)
+    with pytest.raises(ValueError, match="out of range"):
+        _lib.check(_lib.lib().dndc_kmeans_init_indices(3, 4, 1, out.ctypes.data))
+
+
+def test_create_rejects_bad_rank_without_touching_cuda():
+    h = C.c_void_p()
+    rc = _lib.lib().dndc_create(0, 3, 2, None, C.byref(h))
+    assert rc == _lib.DNDC_EVALUE
+    with pytest.raises(ValueError):
+        _lib.check(rc)
+
+
+def test_product_package_never_uses_the_oracle():
+    """The oracle is the checker only: no import, link or symbol use in the product."""
+    import pathlib
+    import re
+    import subprocess
+
+    pkg = pathlib.Path(_lib.HERE)
+    bad = re.compile(r"(from|import)\s+oracle|liboracle|libdndref|\bdno_|\bref_(kmeans|cdist|bench)")
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
+        assert not bad.search(f.read_text()), f
+    deps = subprocess.run(["ldd", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "oracle" not in deps and "dndref" not in deps
