@@ -54,12 +54,3 @@ def comm():
     import paper_2007_13552_b200.api as dnd
 
     return dnd.Communicator(0)
-
-
-def rel_dev(a, ref):
-    """tools/verify.cpp:20-33: max |a - ref| / max(1, |ref|)."""
-    a = np.asarray(a, np.float64)
-    ref = np.asarray(ref, np.float64)
-    if a.size == 0:
-        return 0.0
-    return float(np.max(np.abs(a - ref) / np.maximum(1.0, np.abs(ref))))

@@ -10,7 +10,7 @@ import pytest
 import torch
 
 import paper_2007_13552_b200.api as dnd
-from tests.conftest import rel_dev
+from _parity import rel_dev
 
 pytestmark = pytest.mark.gpu
 
