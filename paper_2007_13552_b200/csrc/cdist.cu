@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(ffma::THREADS)
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
                 const float s = fmaxf(fmaf(-2.f, acc[i][h * 4 + jj], xni + ynv[h * 4 + jj]), 0.f);
-                v[jj] = (c + jj == gi + diag_offset) ? 0.f : sqrt_approx(s);
+                v[jj] = (diag_offset >= 0 && c + jj == gi + diag_offset) ? 0.f : sqrt_approx(s);
             }
             if (VEC && c + 3 < ny) {
                 st_stream4(orow + c, v[0], v[1], v[2], v[3]);
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256)
         for (int j = 0; j < 4; ++j) {
             const int64_t gj = col0 + tx + 16 * j;
             if (gj >= ny) continue;
-            const double d = (gj == gi + diag_offset) ? 0.0 : ref_distance(xn[gi], yn[gj], acc[i][j]);
+            const double d = (diag_offset >= 0 && gj == gi + diag_offset) ? 0.0 : ref_distance(xn[gi], yn[gj], acc[i][j]);
             out[gi * ld + col_off + gj] = d;
         }
     }

@@ -79,6 +79,7 @@ struct dndc_ctx {
     dndc_counters counters{};
     uint64_t launches = 0;
     int64_t last_refined = 0;
+    int km_slot = 0;  // constant-memory centroid table slot (kmeans.cu)
 
     // Growable device workspace, carved by named slots so repeated calls reuse
     // the same addresses (CUDA-graph friendly).

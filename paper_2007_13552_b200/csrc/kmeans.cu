@@ -71,6 +71,7 @@ struct KmBuffers {
     int* flags;        // [0] done, [1] iterations_run
     double* sx2;       // [0] local sum x^2, [1] non-finite count, [2] global sum x^2
     double* pre;       // validation partials
+    float* ctab;       // K*D + K constant-bank layout of the fp32 table
     unsigned long long* refined;
 };
 
@@ -136,6 +137,29 @@ __device__ int ref_argmin(const T* xr, int d, const double* __restrict__ c64,
         const double* c = c64 + static_cast<int64_t>(j) * d;
         double g = 0.0;
         for (int f = 0; f < d; ++f) g = add_rn(g, mul_rn(static_cast<double>(xr[f]), c[f]));
+        const double dj = ref_distance(xn, cn64[j], g);
+        if (j == 0 || dj < bd) {
+            bd = dj;
+            best = j;
+        }
+    }
+    return best;
+}
+
+// Same decision for a row held in registers (compile-time width).
+template <int D>
+__device__ __noinline__ int ref_argmin_regs(const float (&xv)[D], const double* __restrict__ c64,
+                                            const double* __restrict__ cn64, int k) {
+    double xn = 0.0;
+#pragma unroll
+    for (int f = 0; f < D; ++f) xn = add_rn(xn, mul_rn(static_cast<double>(xv[f]), static_cast<double>(xv[f])));
+    int best = 0;
+    double bd = 0.0;
+    for (int j = 0; j < k; ++j) {
+        const double* c = c64 + static_cast<int64_t>(j) * D;
+        double g = 0.0;
+#pragma unroll
+        for (int f = 0; f < D; ++f) g = add_rn(g, mul_rn(static_cast<double>(xv[f]), c[f]));
         const double dj = ref_distance(xn, cn64[j], g);
         if (j == 0 || dj < bd) {
             bd = dj;
@@ -231,20 +255,21 @@ __global__ void __launch_bounds__(KM_THREADS) kmeans_assign_kernel(AssignParams 
 
     for (int64_t it = 0; it < my_tiles; ++it) {
         const int64_t tile = blockIdx.x + it * gridDim.x;
-        const int stage = static_cast<int>(it % p.stages);
+        const int stage = p.stages ? static_cast<int>(it % p.stages) : 0;
         // wait until at most stages-2 younger groups are pending -> tile `it` landed
         if (p.stages == 2) cp_async_wait<0>();
         else if (p.stages == 3) cp_async_wait<1>();
         else cp_async_wait<2>();
         __syncthreads();
-        {
+        if (p.stages > 0) {
             const int64_t nxt = it + p.stages - 1;
             if (nxt < my_tiles)
                 load_tile<T>(xs + ((it + p.stages - 1) % p.stages) * stage_elems, x, p.n, d, srow,
                              blockIdx.x + nxt * gridDim.x, p.aligned16);
             cp_async_commit();
         }
-        const T* xt = xs + stage * stage_elems;
+        // stages == 0 (rows too wide to stage): read the tile straight from HBM/L2
+        const T* xt = p.stages ? xs + stage * stage_elems : x + tile * KM_TILE * d;
 
         // ---------------- phase 1: lane = row
         const int row = threadIdx.x;
@@ -359,6 +384,260 @@ __global__ void __launch_bounds__(KM_THREADS) kmeans_assign_kernel(AssignParams 
     for (int j = threadIdx.x; j < k; j += KM_THREADS) out[k * d + j] = static_cast<double>(cnt[j]);
 }
 
+// ============================================================================
+// Specialised assign/accumulate for small compile-time (D, K) -- BASELINE
+// config 1 (D = 18, K = 8) and the 32-feature config 5 data.
+//
+//  * X tiles (256 rows) stream HBM -> smem through a 4-stage ring of 1-D bulk
+//    copies (cp.async.bulk + mbarrier complete_tx), issued by one thread.
+//  * The centroid table (-2 c_j, |c_j|^2 in fp32) lives in the constant bank,
+//    refreshed per iteration by a D2D memcpy node of the graph, so every score
+//    FFMA reads its centroid operand from c[][] (no shared-memory traffic).
+//  * Phase 1 (lane = row): K*D FFMA, top-2, the fp32 error bound and the f64
+//    re-decision of near-ties (same rule as the generic kernel; the bound uses
+//    the per-shard max |x_e| * sqrt(D) instead of |x_i|).
+//  * Phase 2: a CTA-wide counting sort of the tile by label (ballots, a
+//    per-warp prefix over the count table, one row scatter), then warp w sums
+//    the sorted positions [32w, 32w+32): runs of one cluster, read as float2 by
+//    groups of D/2 lanes, fp32 within the run (<= 32 rows), f64 per warp.
+// Deterministic: every sum has a fixed order for a given grid.
+// ============================================================================
+constexpr int KS_SLOTS = 4;
+constexpr int KS_TABLE = 1152;  // floats per slot (K*D + K)
+__constant__ float c_km_table[KS_SLOTS * KS_TABLE];
+
+struct SmallParams {
+    const float* x;
+    int64_t n;
+    const double* c64;
+    const double* cn64;
+    const float* bounds;  // [0] max |c_j|, [1] max |c_j|^2
+    const double* xabs;   // max |x_e| of the shard
+    double* partials;     // null: predict only
+    int32_t* labels;
+    unsigned long long* refined;
+    const int* done;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// One thread: stream `bytes` (any multiple of 4) of global memory into smem,
+// completing on `bar`.  The 16-byte-aligned body goes through the bulk-copy
+// engine; a <16-byte tail is stored directly before the arrive.
+__device__ __forceinline__ void bulk_load(float* dst, const float* src, uint32_t bytes, uint64_t* bar) {
+    const uint32_t body = bytes & ~15u;
+    for (uint32_t b = body; b < bytes; b += 4) dst[b / 4] = src[b / 4];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(body)
+                 : "memory");
+    if (body)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(dst)),
+            "l"(src), "r"(body), "r"(smem_u32(bar))
+            : "memory");
+}
+
+template <int D, int K, int SLOT>
+__global__ void __launch_bounds__(KM_THREADS, 2) kmeans_small_kernel(SmallParams p) {
+    static_assert(D % 2 == 0 && D <= 64 && K <= 32, "small kernel shape");
+    constexpr int TILE = KM_TILE, S = 4;
+    constexpr int L = D / 2;                  // lanes per row in phase 2 (float2 each)
+    constexpr int G = L <= 32 ? 32 / L : 1;   // rows summed in parallel per warp
+    constexpr int KD = K * D;
+    if (p.done && *p.done) return;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* tiles = reinterpret_cast<float*>(smem_raw);                 // S x TILE x D
+    float* sorted = tiles + S * TILE * D;                              // TILE x D
+    double* acc = reinterpret_cast<double*>(sorted + TILE * D);        // KM_WARPS x K x D
+    int* cnt = reinterpret_cast<int*>(acc + KM_WARPS * KD);            // KM_WARPS x K
+    uint64_t* bars = reinterpret_cast<uint64_t*>(cnt + ((KM_WARPS * K + 1) & ~1));
+
+    const float* CT = c_km_table + SLOT * KS_TABLE;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const float tau = 4.f * static_cast<float>(D + 3) * 0x1.0p-24f *
+                      (p.bounds[1] + 2.f * sqrtf(static_cast<float>(D)) * static_cast<float>(*p.xabs) * p.bounds[0]);
+
+    const bool accumulate = p.partials != nullptr;
+    for (int e = tid; e < KM_WARPS * KD; e += KM_THREADS) acc[e] = 0.0;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int64_t ntiles = ceil_div(p.n, TILE);
+    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto issue = [&](int64_t it) {
+        const int64_t tile = blockIdx.x + it * gridDim.x;
+        const int64_t rows = min(static_cast<int64_t>(TILE), p.n - tile * TILE);
+        bulk_load(tiles + (it % S) * TILE * D, p.x + tile * TILE * D, static_cast<uint32_t>(rows * D * 4),
+                  &bars[it % S]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < S - 1 && s < my_tiles; ++s) issue(s);
+
+    long long count_acc = 0;  // warp 0, lane j: rows of cluster j
+    unsigned long long refined = 0;
+    const int g = lane / L, q = lane % L;
+
+    for (int64_t it = 0; it < my_tiles; ++it) {
+        const int64_t tile = blockIdx.x + it * gridDim.x;
+        const int64_t row0 = tile * TILE;
+        const float* xt = tiles + (it % S) * TILE * D;
+        mbar_wait(&bars[it % S], static_cast<uint32_t>((it / S) & 1));
+
+        // ---------------- phase 1: lane = row
+        const int row = tid;
+        const bool valid = row0 + row < p.n;
+        float xv[D];
+#pragma unroll
+        for (int f = 0; f < D; f += 2) {
+            const float2 v = *reinterpret_cast<const float2*>(xt + row * D + f);
+            xv[f] = v.x;
+            xv[f + 1] = v.y;
+        }
+        int label = K;  // invalid rows sort last
+        if (valid) {
+            float b1 = FLT_MAX, b2 = FLT_MAX;
+            int i1 = 0;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                float sc = CT[KD + j];
+#pragma unroll
+                for (int f = 0; f < D; ++f) sc = fmaf(xv[f], CT[j * D + f], sc);
+                const bool lt = sc < b1;
+                b2 = fminf(b2, fmaxf(b1, sc));
+                b1 = fminf(b1, sc);
+                i1 = lt ? j : i1;
+            }
+            label = i1;
+            if (K > 1 && !(b2 - b1 > tau)) {
+                label = ref_argmin_regs<D>(xv, p.c64, p.cn64, K);
+                ++refined;
+            }
+            if (p.labels) p.labels[row0 + row] = label;
+        }
+        if (!accumulate) {
+            __syncthreads();  // every warp is done with the previous tile's stage
+            if (tid == 0 && it + S - 1 < my_tiles) issue(it + S - 1);
+            continue;
+        }
+
+        // ---------------- phase 2a: per-warp counts and ranks
+        unsigned mine = 0;
+        int wcnt = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const unsigned m = __ballot_sync(FULL, label == j);
+            if (label == j) mine = m;
+            if (lane == j) wcnt = __popc(m);
+        }
+        if (lane < K) cnt[warp * K + lane] = wcnt;
+        const int rank = __popc(mine & ((1u << lane) - 1u));
+        __syncthreads();  // counts visible; every warp is done with the previous tile
+        if (tid == 0 && it + S - 1 < my_tiles) issue(it + S - 1);
+
+        // lane j: start of cluster j in the sorted tile, and this warp's offset in it
+        int total = 0, before = 0;
+        if (lane < K)
+            for (int w = 0; w < KM_WARPS; ++w) {
+                const int c = cnt[w * K + lane];
+                total += c;
+                before += w < warp ? c : 0;
+            }
+        int start = total;  // exclusive scan over lanes 0..K-1
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, start, o);
+            if (lane >= o) start += v;
+        }
+        start -= total;
+        const int nvalid = __shfl_sync(FULL, start + total, K - 1);
+        if (warp == 0 && lane < K) count_acc += total;
+
+        // ---------------- phase 2b: scatter rows into label order
+        const int pos = __shfl_sync(FULL, start + before, label < K ? label : 0) + rank;
+        if (label < K) {
+#pragma unroll
+            for (int f = 0; f < D; f += 2)
+                *reinterpret_cast<float2*>(sorted + pos * D + f) = make_float2(xv[f], xv[f + 1]);
+        }
+        __syncthreads();
+
+        // ---------------- phase 2c: warp w sums sorted positions [32w, 32w+32)
+        int t = warp * 32;
+        const int seg_end = min(t + 32, nvalid);
+        double* wacc = acc + warp * KD;
+        while (t < seg_end) {
+            // cluster of position t: the highest j whose start is <= t
+            const unsigned le = __ballot_sync(FULL, lane < K && start <= t);
+            const int j = 31 - __clz(le);
+            const int run_end = min(seg_end, __shfl_sync(FULL, start + total, j));
+            float2 part = make_float2(0.f, 0.f);
+            if (g < G && q < L) {
+#pragma unroll 4
+                for (int r = t + g; r < run_end; r += G) {
+                    const float2 v = *reinterpret_cast<const float2*>(sorted + r * D + 2 * q);
+                    part.x += v.x;
+                    part.y += v.y;
+                }
+            }
+#pragma unroll
+            for (int s2 = 1; s2 < G; ++s2) {
+                const float ox = __shfl_down_sync(FULL, part.x, s2 * L);
+                const float oy = __shfl_down_sync(FULL, part.y, s2 * L);
+                if (g == 0) {
+                    part.x += ox;
+                    part.y += oy;
+                }
+            }
+            if (g == 0 && q < L) {
+                double2* a = reinterpret_cast<double2*>(wacc + j * D + 2 * q);
+                double2 v = *a;
+                v.x += static_cast<double>(part.x);
+                v.y += static_cast<double>(part.y);
+                *a = v;
+            }
+            t = run_end;
+        }
+    }
+    if (refined) atomicAdd(p.refined, refined);
+    if (!accumulate) return;
+    __syncthreads();
+    const int Sst = KD + K;
+    double* out = p.partials + static_cast<int64_t>(blockIdx.x) * Sst;
+    for (int e = tid; e < KD; e += KM_THREADS) {
+        double v = 0.0;
+        for (int w = 0; w < KM_WARPS; ++w) v += acc[w * KD + e];
+        out[e] = v;
+    }
+    if (warp == 0 && lane < K) out[KD + lane] = static_cast<double>(count_acc);
+}
+
+template <int D, int K>
+static size_t small_smem() {
+    return static_cast<size_t>(4 + 1) * KM_TILE * D * 4 + static_cast<size_t>(KM_WARPS) * K * D * 8 +
+           static_cast<size_t>((KM_WARPS * K + 1) & ~1) * 4 + 4 * 8;
+}
+
 // Per-stat sum over CTA partials in CTA order.
 __global__ void reduce_partials_kernel(const double* __restrict__ partials, int G, int S,
                                        double* __restrict__ stats, const int* done) {
@@ -395,16 +674,18 @@ __device__ double block_max(double v, double* sh) {
 }
 
 // Recomputes the derived tables of cluster j from c64 (f64 master copy).
-__device__ void derive_cluster(int j, int d, int dpad, const double* c64, double* cn64, float* ct,
-                               float* cn32, double& cnorm, double& cn32v) {
+__device__ void derive_cluster(int j, int k, int d, int dpad, const double* c64, double* cn64, float* ct,
+                               float* cn32, float* ctab, double& cnorm, double& cn32v) {
     double n64 = 0.0, n32 = 0.0;
     for (int f = 0; f < d; ++f) {
         const double c = c64[static_cast<int64_t>(j) * d + f];
         n64 = add_rn(n64, mul_rn(c, c));  // row_norms order (pairwise.cpp:13-18)
         const float c32 = static_cast<float>(c);
         ct[static_cast<int64_t>(j) * dpad + f] = -2.f * c32;
+        if (ctab) ctab[static_cast<int64_t>(j) * d + f] = -2.f * c32;
         n32 += static_cast<double>(c32) * static_cast<double>(c32);
     }
+    if (ctab) ctab[static_cast<int64_t>(k) * d + j] = static_cast<float>(n32);
     for (int f = d; f < dpad; ++f) ct[static_cast<int64_t>(j) * dpad + f] = 0.f;
     cn64[j] = n64;
     cn32[j] = static_cast<float>(n32);
@@ -413,12 +694,12 @@ __device__ void derive_cluster(int j, int d, int dpad, const double* c64, double
 }
 
 __global__ void derive_tables_kernel(int k, int d, int dpad, const double* c64, double* cn64,
-                                     float* ct, float* cn32, float* bounds) {
+                                     float* ct, float* cn32, float* ctab, float* bounds) {
     __shared__ double sh[256];
     double cmax = 0.0, cnmax = 0.0;
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
         double cnorm, cnv;
-        derive_cluster(j, d, dpad, c64, cn64, ct, cn32, cnorm, cnv);
+        derive_cluster(j, k, d, dpad, c64, cn64, ct, cn32, ctab, cnorm, cnv);
         cmax = fmax(cmax, cnorm);
         cnmax = fmax(cnmax, cnv);
     }
@@ -432,7 +713,7 @@ __global__ void derive_tables_kernel(int k, int d, int dpad, const double* c64, 
 
 // One CTA: rank-order fold, centroid update, inertia, displacement, tables.
 __global__ void kmeans_update_kernel(int k, int d, int dpad, int world, const double* gathered,
-                                     double* c64, double* cn64, float* ct, float* cn32, float* bounds,
+                                     double* c64, double* cn64, float* ct, float* cn32, float* ctab, float* bounds,
                                      const double* sx2, double* trace, double* disp, int* flags,
                                      int iter, double tol) {
     if (flags[0]) return;
@@ -457,7 +738,7 @@ __global__ void kmeans_update_kernel(int k, int d, int dpad, int world, const do
         inertia_part += count * cn64[j] - 2.0 * dot;  // uses the old |c_j|^2
         dmax = fmax(dmax, __dsqrt_rn(dsq));
         double cnorm, cnv;
-        derive_cluster(j, d, dpad, c64, cn64, ct, cn32, cnorm, cnv);
+        derive_cluster(j, k, d, dpad, c64, cn64, ct, cn32, ctab, cnorm, cnv);
         cmax = fmax(cmax, cnorm);
         cnmax = fmax(cnmax, cnv);
     }
@@ -479,30 +760,38 @@ __global__ void kmeans_update_kernel(int k, int d, int dpad, int world, const do
 template <typename T>
 __global__ void validate_kernel(const T* __restrict__ x, int64_t count, double* out) {
     __shared__ double sh[256];
-    double s = 0.0, bad = 0.0;
+    double s = 0.0, bad = 0.0, mx = 0.0;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += stride) {
         const double v = static_cast<double>(x[e]);
-        if (!isfinite(v)) bad += 1.0;
-        else s += v * v;
+        if (!isfinite(v)) {
+            bad += 1.0;
+        } else {
+            s += v * v;
+            mx = fmax(mx, fabs(v));
+        }
     }
     s = block_sum(s, sh);
     bad = block_sum(bad, sh);
+    mx = block_max(mx, sh);
     if (threadIdx.x == 0) {
-        out[2 * blockIdx.x] = s;
-        out[2 * blockIdx.x + 1] = bad;
+        out[3 * blockIdx.x] = s;
+        out[3 * blockIdx.x + 1] = bad;
+        out[3 * blockIdx.x + 2] = mx;
     }
 }
 
 __global__ void validate_final_kernel(const double* pre, int G, double* sx2) {
     if (threadIdx.x != 0) return;
-    double s = 0.0, bad = 0.0;
+    double s = 0.0, bad = 0.0, mx = 0.0;
     for (int g = 0; g < G; ++g) {
-        s += pre[2 * g];
-        bad += pre[2 * g + 1];
+        s += pre[3 * g];
+        bad += pre[3 * g + 1];
+        mx = fmax(mx, pre[3 * g + 2]);
     }
     sx2[0] = s;
     sx2[1] = bad;
+    sx2[3] = mx;
 }
 
 // gather_rows (cluster.cpp:27-42): rows owned by this rank into a zero-filled
@@ -539,7 +828,8 @@ static KmBuffers buffers(dndc_ctx* ctx, int k, int m, int max_iter, int G) {
     b.disp = static_cast<double*>(ctx->slot("km_disp", sizeof(double) * std::max(max_iter, 1)));
     b.flags = static_cast<int*>(ctx->slot("km_flags", sizeof(int) * 4));
     b.sx2 = static_cast<double*>(ctx->slot("km_sx2", sizeof(double) * 4));
-    b.pre = static_cast<double*>(ctx->slot("km_pre", sizeof(double) * 2 * 4096));
+    b.pre = static_cast<double*>(ctx->slot("km_pre", sizeof(double) * 3 * 4096));
+    b.ctab = static_cast<float*>(ctx->slot("km_ctab", sizeof(float) * (k * m + k)));
     b.refined = static_cast<unsigned long long*>(ctx->slot("km_refined", sizeof(unsigned long long)));
     return b;
 }
@@ -582,6 +872,7 @@ static AssignLaunch<T> plan_assign(dndc_ctx* ctx, int k, int d, int64_t n) {
     }
     int stages = 4;
     while (stages > 2 && assign_smem<T>(k, d, stages) > 200 * 1024) --stages;
+    if (assign_smem<T>(k, d, stages) > 200 * 1024) stages = 0;  // unstaged: rows read from global
     L.stages = stages;
     L.smem = assign_smem<T>(k, d, stages);
     if (L.smem > 227 * 1024)
@@ -606,7 +897,7 @@ static AssignParams assign_params(const KmBuffers& b, const T* x, int64_t n, int
     p.d = d;
     p.k = k;
     p.dpad = dpad_of(d);
-    p.srow = srow_of(d);
+    p.srow = stages ? srow_of(d) : d;
     p.stages = stages;
     p.aligned16 = reinterpret_cast<uintptr_t>(x) % 16 == 0;
     p.ct = b.ct;
@@ -619,6 +910,78 @@ static AssignParams assign_params(const KmBuffers& b, const T* x, int64_t n, int
     p.refined = b.refined;
     p.done = use_done ? b.flags : nullptr;
     return p;
+}
+
+// Chooses the assign/accumulate kernel for a shape and launches it.
+template <typename T>
+struct Assigner {
+    bool small = false;
+    AssignLaunch<T> gen{};
+    void (*sfn)(SmallParams) = nullptr;
+    size_t ssmem = 0;
+    int sgrid = 0, slot = 0;
+
+    int grid() const { return small ? sgrid : gen.grid; }
+
+    void launch(const KmBuffers& b, const T* x, int64_t n, int d, int k, bool accumulate, int32_t* labels,
+                bool use_done, cudaStream_t st) const {
+        if (small) {
+            DNDC_CUDA(cudaMemcpyToSymbolAsync(c_km_table, b.ctab, sizeof(float) * (k * d + k),
+                                              sizeof(float) * KS_TABLE * slot, cudaMemcpyDeviceToDevice, st));
+            SmallParams sp{};
+            sp.x = reinterpret_cast<const float*>(x);
+            sp.n = n;
+            sp.c64 = b.c64;
+            sp.cn64 = b.cn64;
+            sp.bounds = b.bounds;
+            sp.xabs = b.sx2 + 3;
+            sp.partials = accumulate ? b.partials : nullptr;
+            sp.labels = labels;
+            sp.refined = b.refined;
+            sp.done = use_done ? b.flags : nullptr;
+            sfn<<<sgrid, KM_THREADS, ssmem, st>>>(sp);
+        } else {
+            const AssignParams ap = assign_params<T>(b, x, n, d, k, gen.stages, accumulate, labels, use_done);
+            gen.fn<<<gen.grid, KM_THREADS, gen.smem, st>>>(ap);
+        }
+    }
+};
+
+template <int D, int K>
+static bool pick_small(void (*&fn)(SmallParams), size_t& smem, int slot) {
+    switch (slot) {
+        case 0: fn = kmeans_small_kernel<D, K, 0>; break;
+        case 1: fn = kmeans_small_kernel<D, K, 1>; break;
+        case 2: fn = kmeans_small_kernel<D, K, 2>; break;
+        default: fn = kmeans_small_kernel<D, K, 3>; break;
+    }
+    smem = small_smem<D, K>();
+    return true;
+}
+
+template <typename T>
+static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n) {
+    Assigner<T> A;
+    if constexpr (sizeof(T) == 4) {
+        const int slot = ctx->km_slot % KS_SLOTS;
+        bool ok = false;
+        if (d == 18 && k == 8) ok = pick_small<18, 8>(A.sfn, A.ssmem, slot);
+        else if (d == 32 && k == 8) ok = pick_small<32, 8>(A.sfn, A.ssmem, slot);
+        if (ok) {
+            A.small = true;
+            A.slot = slot;
+            DNDC_CUDA(cudaFuncSetAttribute(A.sfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(A.ssmem)));
+            int per_sm = 1;
+            DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, A.sfn, KM_THREADS, A.ssmem));
+            per_sm = std::max(per_sm, 1);
+            const int64_t tiles = std::max<int64_t>(ceil_div(n, KM_TILE), 1);
+            A.sgrid = static_cast<int>(std::min<int64_t>(tiles, static_cast<int64_t>(ctx->num_sms) * per_sm));
+            return A;
+        }
+    }
+    A.gen = plan_assign<T>(ctx, k, d, n);
+    return A;
 }
 
 static void validate_k(int64_t n, int k, const char* who) {
@@ -667,9 +1030,19 @@ static void init_centroids(dndc_ctx* ctx, const KmBuffers& b, const T* x_local, 
     DNDC_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// validation pass: sum x^2, non-finite count and max |x| of the shard -> b.sx2[0, 1, 3]
+template <typename T>
+static void scan_input(dndc_ctx* ctx, const KmBuffers& b, const T* x, int64_t count, cudaStream_t s) {
+    const int G = static_cast<int>(std::min<int64_t>(std::max<int64_t>(ceil_div(count, 256 * 8), 1), 4096));
+    validate_kernel<T><<<G, 256, 0, s>>>(x, count, b.pre);
+    DNDC_LAUNCHED(ctx);
+    validate_final_kernel<<<1, 32, 0, s>>>(b.pre, G, b.sx2);
+    DNDC_LAUNCHED(ctx);
+}
+
 static void derive_tables(dndc_ctx* ctx, const KmBuffers& b, int k, int m) {
     derive_tables_kernel<<<1, 256, 0, ctx->stream>>>(k, m, dpad_of(m), b.c64, b.cn64, b.ct, b.cn32,
-                                                     b.bounds);
+                                                     b.ctab, b.bounds);
     DNDC_LAUNCHED(ctx);
 }
 
@@ -686,21 +1059,16 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
                     std::to_string(ext[ctx->rank]));
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
-    AssignLaunch<T> L = plan_assign<T>(ctx, k, m, n_local);
-    const KmBuffers b = buffers(ctx, k, m, max_iter, L.grid);
+    const Assigner<T> A = plan<T>(ctx, k, m, n_local);
+    const KmBuffers b = buffers(ctx, k, m, max_iter, A.grid());
     const int S = k * m + k;
 
     // ---- validation + sum |x|^2 (one pass), agreed by every rank
     {
-        const int64_t count = n_local * m;
-        const int G = static_cast<int>(std::min<int64_t>(std::max<int64_t>(ceil_div(count, 256 * 8), 1), 4096));
-        validate_kernel<T><<<G, 256, 0, s>>>(x_local, count, b.pre);
-        DNDC_LAUNCHED(ctx);
-        validate_final_kernel<<<1, 32, 0, s>>>(b.pre, G, b.sx2);
-        DNDC_LAUNCHED(ctx);
+        scan_input<T>(ctx, b, x_local, n_local * m, s);
         double* all = b.gathered;  // scratch: world x 2
         allgather_f64(ctx, b.sx2, all, 2, s);
-        double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * 2 * ctx->world));
+        double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * std::max(4, 2 * ctx->world)));
         DNDC_CUDA(cudaMemcpyAsync(h, all, sizeof(double) * 2 * ctx->world, cudaMemcpyDeviceToHost, s));
         DNDC_CUDA(cudaStreamSynchronize(s));
         double sx2 = 0.0, bad = 0.0;
@@ -728,23 +1096,23 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     derive_tables(ctx, b, k, m);
 
     // ---- the Lloyd loop, one graph per (shape, buffers, max_iter, tol)
-    const AssignParams ap = assign_params<T>(b, x_local, n_local, m, k, L.stages, true, nullptr, true);
     auto record = [&](cudaStream_t st) {
         kmeans_reset_kernel<<<1, 1, 0, st>>>(b.flags, b.refined);
         for (int it = 0; it < max_iter; ++it) {
-            L.fn<<<L.grid, KM_THREADS, L.smem, st>>>(ap);
-            reduce_partials_kernel<<<(S + 255) / 256, 256, 0, st>>>(b.partials, L.grid, S, b.stats, b.flags);
+            A.launch(b, x_local, n_local, m, k, true, nullptr, true, st);
+            reduce_partials_kernel<<<(S + 255) / 256, 256, 0, st>>>(b.partials, A.grid(), S, b.stats, b.flags);
             if (ctx->world > 1) allgather_f64(ctx, b.stats, b.gathered, S, st);
             kmeans_update_kernel<<<1, 256, 0, st>>>(k, m, dpad_of(m), ctx->world,
                                                    ctx->world > 1 ? b.gathered : b.stats, b.c64, b.cn64,
-                                                   b.ct, b.cn32, b.bounds, b.sx2, b.trace, b.disp, b.flags,
+                                                   b.ct, b.cn32, b.ctab, b.bounds, b.sx2, b.trace, b.disp, b.flags,
                                                    it, tol);
         }
     };
     if (!ctx->km) ctx->km = new KMeansState();
+    cudaStream_t gs = ctx->own_stream;
     char keybuf[256];
     std::snprintf(keybuf, sizeof(keybuf), "%p/%lld/%d/%d/%d/%.17g/%p/%d/%d", (const void*)x_local,
-                  (long long)n_local, m, k, max_iter, tol, (void*)s, L.grid, ctx->world);
+                  (long long)n_local, m, k, max_iter, tol, (void*)s, A.grid(), ctx->world);
     const std::string key = std::string(sizeof(T) == 4 ? "f32/" : "f64/") + keybuf;
     if (ctx->km->key != key || !ctx->km->exec) {
         if (ctx->km->exec) {
@@ -753,21 +1121,27 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
         }
         const uint64_t before = ctx->counters.allgathers;
         cudaGraph_t graph;
-        DNDC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        // capture on the context's own (non-legacy) stream: the legacy default
+        // stream that torch hands us cannot be captured
+        DNDC_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
         try {
-            record(s);
+            record(gs);
         } catch (...) {
-            cudaStreamEndCapture(s, &graph);
+            cudaStreamEndCapture(gs, &graph);
             throw;
         }
-        DNDC_CUDA(cudaStreamEndCapture(s, &graph));
+        DNDC_CUDA(cudaStreamEndCapture(gs, &graph));
         ctx->counters.allgathers = before;  // counted per replay below
         DNDC_CUDA(cudaGraphInstantiate(&ctx->km->exec, graph, 0));
         DNDC_CUDA(cudaGraphDestroy(graph));
         ctx->km->key = key;
     }
-    DNDC_CUDA(cudaGraphLaunch(ctx->km->exec, s));
-    ctx->launches += 1 + 3ull * max_iter;
+    DNDC_CUDA(cudaEventRecord(ctx->ev_a, s));
+    DNDC_CUDA(cudaStreamWaitEvent(gs, ctx->ev_a, 0));
+    DNDC_CUDA(cudaGraphLaunch(ctx->km->exec, gs));
+    DNDC_CUDA(cudaEventRecord(ctx->ev_b, gs));
+    DNDC_CUDA(cudaStreamWaitEvent(s, ctx->ev_b, 0));
+    ctx->launches += 1 + 3ull * max_iter + (A.small ? max_iter : 0);  // + table copies
     if (ctx->world > 1) ctx->counters.allgathers += max_iter;
 
     // ---- results
@@ -796,16 +1170,16 @@ static void kmeans_predict(dndc_ctx* ctx, const T* x, int64_t n, int64_t m64, co
     if (k < 1) value_error("kmeans_predict: k must be positive");
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
-    AssignLaunch<T> L = plan_assign<T>(ctx, k, m, n);
-    const KmBuffers b = buffers(ctx, k, m, 1, L.grid);
+    const Assigner<T> A = plan<T>(ctx, k, m, n);
+    const KmBuffers b = buffers(ctx, k, m, 1, A.grid());
     double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * k * m));
     std::memcpy(h, cent_host, sizeof(double) * k * m);
     DNDC_CUDA(cudaMemcpyAsync(b.c64, h, sizeof(double) * k * m, cudaMemcpyHostToDevice, s));
     DNDC_CUDA(cudaMemsetAsync(b.refined, 0, sizeof(unsigned long long), s));
     derive_tables(ctx, b, k, m);
     if (n > 0) {
-        const AssignParams ap = assign_params<T>(b, x, n, m, k, L.stages, false, labels, false);
-        L.fn<<<L.grid, KM_THREADS, L.smem, s>>>(ap);
+        if (A.small) scan_input<T>(ctx, b, x, n * m, s);
+        A.launch(b, x, n, m, k, false, labels, false, s);
         DNDC_LAUNCHED(ctx);
     }
     unsigned long long* hr = reinterpret_cast<unsigned long long*>(h);
@@ -836,9 +1210,9 @@ static void time_assign(dndc_ctx* ctx, const float* x, int64_t n, int64_t m64, i
                         double* bytes) {
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
-    AssignLaunch<float> L = plan_assign<float>(ctx, k, m, n);
+    const Assigner<float> A = plan<float>(ctx, k, m, n);
     const bool fresh = ctx->slots.find("km_c64") == ctx->slots.end();
-    const KmBuffers b = buffers(ctx, k, m, 1, L.grid);
+    const KmBuffers b = buffers(ctx, k, m, 1, A.grid());
     if (fresh) {
         std::vector<int64_t> idx(k);
         for (int j = 0; j < k; ++j) idx[j] = j;
@@ -847,13 +1221,13 @@ static void time_assign(dndc_ctx* ctx, const float* x, int64_t n, int64_t m64, i
         gather_rows_kernel<float><<<1, 256, 0, s>>>(x, 0, n, m, didx, k, b.c64);
         derive_tables(ctx, b, k, m);
     }
-    const AssignParams ap = assign_params<float>(b, x, n, m, k, L.stages, true, nullptr, false);
+    scan_input<float>(ctx, b, x, n * m, s);
     cudaEvent_t e0, e1;
     DNDC_CUDA(cudaEventCreate(&e0));
     DNDC_CUDA(cudaEventCreate(&e1));
-    L.fn<<<L.grid, KM_THREADS, L.smem, s>>>(ap);  // warm
+    A.launch(b, x, n, m, k, true, nullptr, false, s);  // warm
     DNDC_CUDA(cudaEventRecord(e0, s));
-    for (int r = 0; r < reps; ++r) L.fn<<<L.grid, KM_THREADS, L.smem, s>>>(ap);
+    for (int r = 0; r < reps; ++r) A.launch(b, x, n, m, k, true, nullptr, false, s);
     DNDC_CUDA(cudaEventRecord(e1, s));
     DNDC_CUDA(cudaEventSynchronize(e1));
     float t = 0.f;

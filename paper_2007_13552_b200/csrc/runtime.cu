@@ -10,6 +10,7 @@
 //   - sendrecv is a grouped ncclSend/ncclRecv pair (transport.hpp:122-129);
 //   - TransportCounters are kept per rank (transport.hpp:19-27).
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
@@ -118,6 +119,14 @@ int dndc_create(int device, int rank, int world, const void* unique_id, dndc_ctx
         DNDC_CUDA(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
         DNDC_CUDA(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
         ctx->stream = ctx->own_stream;
+        {
+            // constant-bank centroid table slot (kmeans.cu), distinct per context
+            // on a device for up to DNDC_KM_SLOTS concurrent contexts
+            static std::mutex mu;
+            static std::map<int, int> next_slot;
+            std::lock_guard<std::mutex> lock(mu);
+            ctx->km_slot = next_slot[device]++ % 4;
+        }
         if (world > 1) {
             ncclUniqueId id;
             std::memcpy(&id, unique_id, sizeof(id));
@@ -146,7 +155,8 @@ int dndc_destroy(dndc_ctx* ctx) {
 
 int dndc_set_stream(dndc_ctx* ctx, void* cuda_stream) {
     return guard([&] {
-        ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+        // NULL is the legacy default stream (torch's default), not our own stream
+        ctx->stream = static_cast<cudaStream_t>(cuda_stream);
     });
 }
 
