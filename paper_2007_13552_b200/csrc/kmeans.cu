@@ -466,8 +466,7 @@ __global__ void __launch_bounds__(KM_THREADS, 2) kmeans_small_kernel(SmallParams
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* tiles = reinterpret_cast<float*>(smem_raw);                 // S x TILE x D
     float* sorted = tiles + S * TILE * D;                              // TILE x D
-    double* acc = reinterpret_cast<double*>(sorted + TILE * D);        // KM_WARPS x K x D
-    int* cnt = reinterpret_cast<int*>(acc + KM_WARPS * KD);            // KM_WARPS x K
+    int* cnt = reinterpret_cast<int*>(sorted + TILE * D);              // KM_WARPS x K
     uint64_t* bars = reinterpret_cast<uint64_t*>(cnt + ((KM_WARPS * K + 1) & ~1));
 
     const float* CT = c_km_table + SLOT * KS_TABLE;
@@ -476,7 +475,6 @@ __global__ void __launch_bounds__(KM_THREADS, 2) kmeans_small_kernel(SmallParams
                       (p.bounds[1] + 2.f * sqrtf(static_cast<float>(D)) * static_cast<float>(*p.xabs) * p.bounds[0]);
 
     const bool accumulate = p.partials != nullptr;
-    for (int e = tid; e < KM_WARPS * KD; e += KM_THREADS) acc[e] = 0.0;
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -497,6 +495,9 @@ __global__ void __launch_bounds__(KM_THREADS, 2) kmeans_small_kernel(SmallParams
     long long count_acc = 0;  // warp 0, lane j: rows of cluster j
     unsigned long long refined = 0;
     const int g = lane / L, q = lane % L;
+    double2 wsum[(K + KM_WARPS - 1) / KM_WARPS];
+#pragma unroll
+    for (int jj = 0; jj < (K + KM_WARPS - 1) / KM_WARPS; ++jj) wsum[jj] = make_double2(0.0, 0.0);
 
     for (int64_t it = 0; it < my_tiles; ++it) {
         const int64_t tile = blockIdx.x + it * gridDim.x;
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(KM_THREADS, 2) kmeans_small_kernel(SmallParams
             }
             label = i1;
             if (K > 1 && !(b2 - b1 > tau)) {
-                label = ref_argmin_regs<D>(xv, p.c64, p.cn64, K);
+                label = ref_argmin<float>(xt + row * D, D, p.c64, p.cn64, K);
                 ++refined;
             }
             if (p.labels) p.labels[row0 + row] = label;
@@ -582,60 +583,54 @@ __global__ void __launch_bounds__(KM_THREADS, 2) kmeans_small_kernel(SmallParams
         }
         __syncthreads();
 
-        // ---------------- phase 2c: warp w sums sorted positions [32w, 32w+32)
-        int t = warp * 32;
-        const int seg_end = min(t + 32, nvalid);
-        double* wacc = acc + warp * KD;
-        while (t < seg_end) {
-            // cluster of position t: the highest j whose start is <= t
-            const unsigned le = __ballot_sync(FULL, lane < K && start <= t);
-            const int j = 31 - __clz(le);
-            const int run_end = min(seg_end, __shfl_sync(FULL, start + total, j));
+        // ---------------- phase 2c: warp w sums the sorted run of clusters w, w+8, ...
+#pragma unroll
+        for (int jj = 0; jj < (K + KM_WARPS - 1) / KM_WARPS; ++jj) {
+            const int j = warp + jj * KM_WARPS;
+            if (j >= K) break;
+            const int r0 = __shfl_sync(FULL, start, j);
+            const int r1 = r0 + __shfl_sync(FULL, total, j);
             float2 part = make_float2(0.f, 0.f);
-            if (g < G && q < L) {
+            if (g < G) {
+                const float* src = sorted + 2 * q;
 #pragma unroll 4
-                for (int r = t + g; r < run_end; r += G) {
-                    const float2 v = *reinterpret_cast<const float2*>(sorted + r * D + 2 * q);
+                for (int r = r0 + g; r < r1; r += G) {
+                    const float2 v = *reinterpret_cast<const float2*>(src + r * D);
                     part.x += v.x;
                     part.y += v.y;
                 }
             }
+            // tree over the G groups; a source beyond the last group contributes nothing
 #pragma unroll
-            for (int s2 = 1; s2 < G; ++s2) {
-                const float ox = __shfl_down_sync(FULL, part.x, s2 * L);
-                const float oy = __shfl_down_sync(FULL, part.y, s2 * L);
-                if (g == 0) {
-                    part.x += ox;
-                    part.y += oy;
+            for (int o = 1; o < G; o <<= 1) {
+                const float vx = __shfl_down_sync(FULL, part.x, o * L);
+                const float vy = __shfl_down_sync(FULL, part.y, o * L);
+                if (g + o < G) {
+                    part.x += vx;
+                    part.y += vy;
                 }
             }
-            if (g == 0 && q < L) {
-                double2* a = reinterpret_cast<double2*>(wacc + j * D + 2 * q);
-                double2 v = *a;
-                v.x += static_cast<double>(part.x);
-                v.y += static_cast<double>(part.y);
-                *a = v;
-            }
-            t = run_end;
+            // lanes of group 0 own features 2q, 2q+1 of cluster j (f64, registers)
+            wsum[jj].x += static_cast<double>(part.x);
+            wsum[jj].y += static_cast<double>(part.y);
         }
     }
     if (refined) atomicAdd(p.refined, refined);
     if (!accumulate) return;
-    __syncthreads();
     const int Sst = KD + K;
     double* out = p.partials + static_cast<int64_t>(blockIdx.x) * Sst;
-    for (int e = tid; e < KD; e += KM_THREADS) {
-        double v = 0.0;
-        for (int w = 0; w < KM_WARPS; ++w) v += acc[w * KD + e];
-        out[e] = v;
+#pragma unroll
+    for (int jj = 0; jj < (K + KM_WARPS - 1) / KM_WARPS; ++jj) {
+        const int j = warp + jj * KM_WARPS;
+        if (j < K && g == 0 && q < L)
+            *reinterpret_cast<double2*>(out + j * D + 2 * q) = wsum[jj];
     }
     if (warp == 0 && lane < K) out[KD + lane] = static_cast<double>(count_acc);
 }
 
 template <int D, int K>
 static size_t small_smem() {
-    return static_cast<size_t>(4 + 1) * KM_TILE * D * 4 + static_cast<size_t>(KM_WARPS) * K * D * 8 +
-           static_cast<size_t>((KM_WARPS * K + 1) & ~1) * 4 + 4 * 8;
+    return static_cast<size_t>(4 + 1) * KM_TILE * D * 4 + static_cast<size_t>((KM_WARPS * K + 1) & ~1) * 4 + 4 * 8;
 }
 
 // Per-stat sum over CTA partials in CTA order.
