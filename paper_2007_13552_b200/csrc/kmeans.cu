@@ -454,26 +454,38 @@ __device__ __forceinline__ void bulk_load(float* dst, const float* src, uint32_t
             : "memory");
 }
 
+// CTA shape of the small kernel: 128 threads (4 warps), each thread deciding
+// KS_R rows per tile (KS_R * 128-row tiles): the constant-bank operands, the
+// per-tile scan and the per-cluster loops are amortised over more rows while
+// the per-tile barriers stay cheap (4 warps).
+constexpr int KS_THREADS = 128;
+constexpr int KS_WARPS = KS_THREADS / 32;
+constexpr int KS_R = 2;
+constexpr int KS_TILE = KS_THREADS * KS_R;
+constexpr int KS_STAGES = 2;
+constexpr int KS_MIN_CTAS = 4;
+constexpr int KS_VW = KS_WARPS * KS_R;  // 32-row groups per tile
+
 template <int D, int K, int SLOT>
-__global__ void __launch_bounds__(KM_THREADS, 2) kmeans_small_kernel(SmallParams p) {
+__global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(SmallParams p) {
     static_assert(D % 2 == 0 && D <= 64 && K <= 32, "small kernel shape");
-    constexpr int TILE = KM_TILE, S = 4;
+    constexpr int TILE = KS_TILE, S = KS_STAGES, W = KS_WARPS, R = KS_R, VW = KS_VW;
     constexpr int L = D / 2;                  // lanes per row in phase 2 (float2 each)
     constexpr int G = L <= 32 ? 32 / L : 1;   // rows summed in parallel per warp
     constexpr int KD = K * D;
+    constexpr int JW = (K + W - 1) / W;       // clusters owned per warp
     if (p.done && *p.done) return;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* tiles = reinterpret_cast<float*>(smem_raw);                 // S x TILE x D
     float* sorted = tiles + S * TILE * D;                              // TILE x D
-    int* cnt = reinterpret_cast<int*>(sorted + TILE * D);              // KM_WARPS x K
-    uint64_t* bars = reinterpret_cast<uint64_t*>(cnt + ((KM_WARPS * K + 1) & ~1));
+    int* cnt = reinterpret_cast<int*>(sorted + TILE * D);              // VW x K
+    uint64_t* bars = reinterpret_cast<uint64_t*>(cnt + ((VW * K + 1) & ~1));
 
     const float* CT = c_km_table + SLOT * KS_TABLE;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const float tau = 4.f * static_cast<float>(D + 3) * 0x1.0p-24f *
                       (p.bounds[1] + 2.f * sqrtf(static_cast<float>(D)) * static_cast<float>(*p.xabs) * p.bounds[0]);
-
     const bool accumulate = p.partials != nullptr;
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -492,49 +504,72 @@ __global__ void __launch_bounds__(KM_THREADS, 2) kmeans_small_kernel(SmallParams
     if (tid == 0)
         for (int s = 0; s < S - 1 && s < my_tiles; ++s) issue(s);
 
-    long long count_acc = 0;  // warp 0, lane j: rows of cluster j
+    long long count_acc = 0;  // lane j < K of warp 0: rows of cluster j
     unsigned long long refined = 0;
     const int g = lane / L, q = lane % L;
-    double2 wsum[(K + KM_WARPS - 1) / KM_WARPS];
+    double2 wsum[JW];
 #pragma unroll
-    for (int jj = 0; jj < (K + KM_WARPS - 1) / KM_WARPS; ++jj) wsum[jj] = make_double2(0.0, 0.0);
+    for (int jj = 0; jj < JW; ++jj) wsum[jj] = make_double2(0.0, 0.0);
 
     for (int64_t it = 0; it < my_tiles; ++it) {
-        const int64_t tile = blockIdx.x + it * gridDim.x;
-        const int64_t row0 = tile * TILE;
+        const int64_t row0 = (blockIdx.x + it * gridDim.x) * TILE;
         const float* xt = tiles + (it % S) * TILE * D;
         mbar_wait(&bars[it % S], static_cast<uint32_t>((it / S) & 1));
 
-        // ---------------- phase 1: lane = row
-        const int row = tid;
-        const bool valid = row0 + row < p.n;
-        float xv[D];
+        // ---------------- phase 1: rows tid + h * 128 (h < R), lane = row
+        float xv[R][D];
+        int label[R];
 #pragma unroll
-        for (int f = 0; f < D; f += 2) {
-            const float2 v = *reinterpret_cast<const float2*>(xt + row * D + f);
-            xv[f] = v.x;
-            xv[f + 1] = v.y;
+        for (int h = 0; h < R; ++h) {
+            const int row = tid + h * KS_THREADS;
+#pragma unroll
+            for (int f = 0; f < D; f += 2) {
+                const float2 v = *reinterpret_cast<const float2*>(xt + row * D + f);
+                xv[h][f] = v.x;
+                xv[h][f + 1] = v.y;
+            }
         }
-        int label = K;  // invalid rows sort last
-        if (valid) {
-            float b1 = FLT_MAX, b2 = FLT_MAX;
-            int i1 = 0;
+        {
+            float b1[R], b2[R];
+            int i1[R];
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                b1[h] = FLT_MAX;
+                b2[h] = FLT_MAX;
+                i1[h] = 0;
+            }
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-                float sc = CT[KD + j];
+                float sc[R];
 #pragma unroll
-                for (int f = 0; f < D; ++f) sc = fmaf(xv[f], CT[j * D + f], sc);
-                const bool lt = sc < b1;
-                b2 = fminf(b2, fmaxf(b1, sc));
-                b1 = fminf(b1, sc);
-                i1 = lt ? j : i1;
+                for (int h = 0; h < R; ++h) sc[h] = CT[KD + j];
+#pragma unroll
+                for (int f = 0; f < D; ++f) {
+                    const float c = CT[j * D + f];
+#pragma unroll
+                    for (int h = 0; h < R; ++h) sc[h] = fmaf(xv[h][f], c, sc[h]);
+                }
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                    const bool lt = sc[h] < b1[h];
+                    b2[h] = fminf(b2[h], fmaxf(b1[h], sc[h]));
+                    b1[h] = fminf(b1[h], sc[h]);
+                    i1[h] = lt ? j : i1[h];
+                }
             }
-            label = i1;
-            if (K > 1 && !(b2 - b1 > tau)) {
-                label = ref_argmin<float>(xt + row * D, D, p.c64, p.cn64, K);
-                ++refined;
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                const int row = tid + h * KS_THREADS;
+                label[h] = K;  // rows past the end sort last
+                if (row0 + row < p.n) {
+                    label[h] = i1[h];
+                    if (K > 1 && !(b2[h] - b1[h] > tau)) {
+                        label[h] = ref_argmin<float>(xt + row * D, D, p.c64, p.cn64, K);
+                        ++refined;
+                    }
+                    if (p.labels) p.labels[row0 + row] = label[h];
+                }
             }
-            if (p.labels) p.labels[row0 + row] = label;
         }
         if (!accumulate) {
             __syncthreads();  // every warp is done with the previous tile's stage
@@ -542,51 +577,62 @@ __global__ void __launch_bounds__(KM_THREADS, 2) kmeans_small_kernel(SmallParams
             continue;
         }
 
-        // ---------------- phase 2a: per-warp counts and ranks
-        unsigned mine = 0;
-        int wcnt = 0;
+        // ---------------- phase 2a: counts per 32-row group vw = h * W + warp
+        unsigned mine[R];
+        int rank[R];
+        if (lane < K) {
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const unsigned m = __ballot_sync(FULL, label == j);
-            if (label == j) mine = m;
-            if (lane == j) wcnt = __popc(m);
+            for (int h = 0; h < R; ++h) cnt[(h * W + warp) * K + lane] = 0;
         }
-        if (lane < K) cnt[warp * K + lane] = wcnt;
-        const int rank = __popc(mine & ((1u << lane) - 1u));
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+            mine[h] = __match_any_sync(FULL, label[h]);
+            rank[h] = __popc(mine[h] & ((1u << lane) - 1u));
+            if (rank[h] == 0 && label[h] < K) cnt[(h * W + warp) * K + label[h]] = __popc(mine[h]);
+        }
         __syncthreads();  // counts visible; every warp is done with the previous tile
         if (tid == 0 && it + S - 1 < my_tiles) issue(it + S - 1);
 
-        // lane j: start of cluster j in the sorted tile, and this warp's offset in it
-        int total = 0, before = 0;
-        if (lane < K)
-            for (int w = 0; w < KM_WARPS; ++w) {
-                const int c = cnt[w * K + lane];
-                total += c;
-                before += w < warp ? c : 0;
-            }
-        int start = total;  // exclusive scan over lanes 0..K-1
+        // lane j: start of cluster j in the sorted tile and the offsets of this
+        // warp's groups inside it
+        int total = 0, before[R];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
+        for (int h = 0; h < R; ++h) before[h] = 0;
+        if (lane < K) {
+#pragma unroll
+            for (int v = 0; v < VW; ++v) {
+                const int c = cnt[v * K + lane];
+                total += c;
+#pragma unroll
+                for (int h = 0; h < R; ++h) before[h] += v < h * W + warp ? c : 0;
+            }
+        }
+        int start = total;  // inclusive scan over lanes 0..K-1
+#pragma unroll
+        for (int o = 1; o < K; o <<= 1) {
             const int v = __shfl_up_sync(FULL, start, o);
             if (lane >= o) start += v;
         }
         start -= total;
-        const int nvalid = __shfl_sync(FULL, start + total, K - 1);
         if (warp == 0 && lane < K) count_acc += total;
 
         // ---------------- phase 2b: scatter rows into label order
-        const int pos = __shfl_sync(FULL, start + before, label < K ? label : 0) + rank;
-        if (label < K) {
 #pragma unroll
-            for (int f = 0; f < D; f += 2)
-                *reinterpret_cast<float2*>(sorted + pos * D + f) = make_float2(xv[f], xv[f + 1]);
+        for (int h = 0; h < R; ++h) {
+            const int pos = __shfl_sync(FULL, start + before[h], label[h] < K ? label[h] : 0) + rank[h];
+            if (label[h] < K) {
+#pragma unroll
+                for (int f = 0; f < D; f += 2)
+                    *reinterpret_cast<float2*>(sorted + pos * D + f) = make_float2(xv[h][f], xv[h][f + 1]);
+            }
         }
         __syncthreads();
 
-        // ---------------- phase 2c: warp w sums the sorted run of clusters w, w+8, ...
+        // ---------------- phase 2c: warp w sums the sorted runs of clusters w, w+W, ...
 #pragma unroll
-        for (int jj = 0; jj < (K + KM_WARPS - 1) / KM_WARPS; ++jj) {
-            const int j = warp + jj * KM_WARPS;
+        for (int jj = 0; jj < JW; ++jj) {
+            const int j = warp + jj * W;
             if (j >= K) break;
             const int r0 = __shfl_sync(FULL, start, j);
             const int r1 = r0 + __shfl_sync(FULL, total, j);
@@ -620,68 +666,86 @@ __global__ void __launch_bounds__(KM_THREADS, 2) kmeans_small_kernel(SmallParams
     const int Sst = KD + K;
     double* out = p.partials + static_cast<int64_t>(blockIdx.x) * Sst;
 #pragma unroll
-    for (int jj = 0; jj < (K + KM_WARPS - 1) / KM_WARPS; ++jj) {
-        const int j = warp + jj * KM_WARPS;
-        if (j < K && g == 0 && q < L)
-            *reinterpret_cast<double2*>(out + j * D + 2 * q) = wsum[jj];
+    for (int jj = 0; jj < JW; ++jj) {
+        const int j = warp + jj * W;
+        if (j < K && g == 0 && q < L) *reinterpret_cast<double2*>(out + j * D + 2 * q) = wsum[jj];
     }
     if (warp == 0 && lane < K) out[KD + lane] = static_cast<double>(count_acc);
 }
 
 template <int D, int K>
 static size_t small_smem() {
-    return static_cast<size_t>(4 + 1) * KM_TILE * D * 4 + static_cast<size_t>((KM_WARPS * K + 1) & ~1) * 4 + 4 * 8;
+    return static_cast<size_t>(KS_STAGES + 1) * KS_TILE * D * 4 +
+           static_cast<size_t>((KS_VW * K + 1) & ~1) * 4 + KS_STAGES * 8;
 }
 
-// Per-stat sum over CTA partials in CTA order.
-__global__ void reduce_partials_kernel(const double* __restrict__ partials, int G, int S,
-                                       double* __restrict__ stats, const int* done) {
+// Per-stat sum over the CTA partials: one block per stat, a fixed strided
+// split over 256 threads and a fixed tree (deterministic for a given grid).
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __restrict__ partials, int G, int S,
+                                                              double* __restrict__ stats, const int* done) {
     if (done && *done) return;
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= S) return;
-    double s = 0.0;
-    for (int g = 0; g < G; ++g) s += partials[static_cast<int64_t>(g) * S + e];
-    stats[e] = s;
-}
-
-// Deterministic block reductions (fixed tree over the thread index).
-__device__ double block_sum(double v, double* sh) {
+    __shared__ double sh[256];
+    const int e = blockIdx.x;
+    double v = 0.0;
+    for (int g = threadIdx.x; g < G; g += 256) v += partials[static_cast<int64_t>(g) * S + e];
     sh[threadIdx.x] = v;
     __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+#pragma unroll
+    for (int o = 128; o > 0; o >>= 1) {
         if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
         __syncthreads();
     }
-    const double r = sh[0];
+    if (threadIdx.x == 0) stats[e] = sh[0];
+}
+
+// Deterministic block reductions: a fixed xor-butterfly inside each warp, then
+// warp 0 combines the per-warp values in a fixed order.  `sh` holds >= 32 doubles.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int nw = (blockDim.x + 31) / 32;
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = v;
+    __syncthreads();
+    double r = 0.0;
+    for (int w = 0; w < nw; ++w) r += sh[w];
     __syncthreads();
     return r;
 }
 __device__ double block_max(double v, double* sh) {
-    sh[threadIdx.x] = v;
+    v = warp_max(v);
+    const int nw = (blockDim.x + 31) / 32;
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = v;
     __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
-        __syncthreads();
-    }
-    const double r = sh[0];
+    double r = sh[0];
+    for (int w = 1; w < nw; ++w) r = fmax(r, sh[w]);
     __syncthreads();
     return r;
 }
 
-// Recomputes the derived tables of cluster j from c64 (f64 master copy).
-__device__ void derive_cluster(int j, int k, int d, int dpad, const double* c64, double* cn64, float* ct,
+// Derived tables of cluster j from its f64 centroid row `c` (smem or global):
+// reference-order |c|^2 (pairwise.cpp:13-18), the fp32 score tables, bounds.
+__device__ void derive_cluster(int j, int k, int d, int dpad, const double* c, double* cn64, float* ct,
                                float* cn32, float* ctab, double& cnorm, double& cn32v) {
     double n64 = 0.0, n32 = 0.0;
     for (int f = 0; f < d; ++f) {
-        const double c = c64[static_cast<int64_t>(j) * d + f];
-        n64 = add_rn(n64, mul_rn(c, c));  // row_norms order (pairwise.cpp:13-18)
-        const float c32 = static_cast<float>(c);
+        const double cf = c[f];
+        n64 = add_rn(n64, mul_rn(cf, cf));
+        const float c32 = static_cast<float>(cf);
         ct[static_cast<int64_t>(j) * dpad + f] = -2.f * c32;
         if (ctab) ctab[static_cast<int64_t>(j) * d + f] = -2.f * c32;
         n32 += static_cast<double>(c32) * static_cast<double>(c32);
     }
-    if (ctab) ctab[static_cast<int64_t>(k) * d + j] = static_cast<float>(n32);
     for (int f = d; f < dpad; ++f) ct[static_cast<int64_t>(j) * dpad + f] = 0.f;
+    if (ctab) ctab[static_cast<int64_t>(k) * d + j] = static_cast<float>(n32);
     cn64[j] = n64;
     cn32[j] = static_cast<float>(n32);
     cnorm = sqrt(n32);
@@ -694,7 +758,7 @@ __global__ void derive_tables_kernel(int k, int d, int dpad, const double* c64, 
     double cmax = 0.0, cnmax = 0.0;
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
         double cnorm, cnv;
-        derive_cluster(j, k, d, dpad, c64, cn64, ct, cn32, ctab, cnorm, cnv);
+        derive_cluster(j, k, d, dpad, c64 + static_cast<int64_t>(j) * d, cn64, ct, cn32, ctab, cnorm, cnv);
         cmax = fmax(cmax, cnorm);
         cnmax = fmax(cnmax, cnv);
     }
@@ -707,35 +771,68 @@ __global__ void derive_tables_kernel(int k, int d, int dpad, const double* c64, 
 }
 
 // One CTA: rank-order fold, centroid update, inertia, displacement, tables.
-__global__ void kmeans_update_kernel(int k, int d, int dpad, int world, const double* gathered,
+// Stage 1 (thread per stat): fold the ranks in order 0..p-1 from the zero
+// identity (allreduce(plus_vec), cluster.cpp:123) and form the new centroid
+// (cluster.cpp:125-133) into shared memory.  Stage 2 (thread per cluster):
+// the reference's sequential per-cluster loops (displacement, norms).
+constexpr int UPD_MAX_KD = 8192;
+__global__ void __launch_bounds__(256) kmeans_update_kernel(int k, int d, int dpad, int world, const double* gathered,
                                      double* c64, double* cn64, float* ct, float* cn32, float* ctab, float* bounds,
                                      const double* sx2, double* trace, double* disp, int* flags,
                                      int iter, double tol) {
     if (flags[0]) return;
-    __shared__ double sh[256];
-    const int S = k * d + k;
+    __shared__ double sh[32];
+    extern __shared__ double upd[];  // [KD] folded sums, [KD] old centroids, [k] folded counts
+    const int S = k * d + k, KD = k * d;
+    const bool staged = KD <= UPD_MAX_KD;
+    if (staged) {
+        // allreduce(plus_vec) from the zero identity in rank order (cluster.cpp:123)
+        for (int e = threadIdx.x; e < S; e += blockDim.x) {
+            double v = 0.0;
+            for (int r = 0; r < world; ++r) v += gathered[static_cast<int64_t>(r) * S + e];
+            upd[e < KD ? e : KD + e] = v;
+            if (e < KD) upd[KD + e] = c64[e];
+        }
+        __syncthreads();
+    }
     double inertia_part = 0.0, dmax = 0.0, cmax = 0.0, cnmax = 0.0;
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        // allreduce(plus_vec) from the zero identity in rank order
-        double count = 0.0;
-        for (int r = 0; r < world; ++r) count += gathered[static_cast<int64_t>(r) * S + k * d + j];
-        double dot = 0.0, dsq = 0.0;
-        for (int f = 0; f < d; ++f) {
-            double s = 0.0;
-            for (int r = 0; r < world; ++r) s += gathered[static_cast<int64_t>(r) * S + j * d + f];
-            const double old = c64[static_cast<int64_t>(j) * d + f];
-            dot += old * s;
-            const double nxt = count > 0.0 ? s / count : old;
-            const double diff = nxt - old;
-            dsq = add_rn(dsq, mul_rn(diff, diff));  // cluster.cpp:142-146 order
-            c64[static_cast<int64_t>(j) * d + f] = nxt;
+        double count = 0.0, dot = 0.0, dsq = 0.0, n64 = 0.0, n32 = 0.0;
+        if (staged) {
+            count = upd[2 * KD + j];
+        } else {
+            for (int r = 0; r < world; ++r) count += gathered[static_cast<int64_t>(r) * S + KD + j];
         }
-        inertia_part += count * cn64[j] - 2.0 * dot;  // uses the old |c_j|^2
+        const double cn_old = cn64[j];
+        for (int f = 0; f < d; ++f) {
+            const int e = j * d + f;
+            double s = 0.0, old;
+            if (staged) {
+                s = upd[e];
+                old = upd[KD + e];
+            } else {
+                for (int r = 0; r < world; ++r) s += gathered[static_cast<int64_t>(r) * S + e];
+                old = c64[e];
+            }
+            dot += old * s;
+            const double nxt = count > 0.0 ? s / count : old;  // cluster.cpp:125-133
+            const double diff = nxt - old;
+            dsq = add_rn(dsq, mul_rn(diff, diff));              // cluster.cpp:142-146 order
+            c64[e] = nxt;
+            n64 = add_rn(n64, mul_rn(nxt, nxt));                // row_norms order
+            const float c32 = static_cast<float>(nxt);
+            ct[static_cast<int64_t>(j) * dpad + f] = -2.f * c32;
+            if (ctab) ctab[e] = -2.f * c32;
+            n32 += static_cast<double>(c32) * static_cast<double>(c32);
+        }
+        for (int f = d; f < dpad; ++f) ct[static_cast<int64_t>(j) * dpad + f] = 0.f;
+        if (ctab) ctab[KD + j] = static_cast<float>(n32);
+        cn64[j] = n64;
+        cn32[j] = static_cast<float>(n32);
+        inertia_part += count * cn_old - 2.0 * dot;  // uses the old |c_j|^2
         dmax = fmax(dmax, __dsqrt_rn(dsq));
-        double cnorm, cnv;
-        derive_cluster(j, k, d, dpad, c64, cn64, ct, cn32, ctab, cnorm, cnv);
-        cmax = fmax(cmax, cnorm);
-        cnmax = fmax(cnmax, cnv);
+        cmax = fmax(cmax, sqrt(n32));
+        cnmax = fmax(cnmax, static_cast<double>(static_cast<float>(n32)));
     }
     const double inertia = block_sum(inertia_part, sh);
     dmax = block_max(dmax, sh);
@@ -749,6 +846,18 @@ __global__ void kmeans_update_kernel(int k, int d, int dpad, int world, const do
         bounds[0] = static_cast<float>(cmax) * (1.f + 0x1.0p-20f);
         bounds[1] = static_cast<float>(cnmax) * (1.f + 0x1.0p-20f);
     }
+}
+
+static size_t update_smem(int k, int d) {
+    const size_t kd = static_cast<size_t>(k) * d;
+    const size_t bytes = kd <= UPD_MAX_KD ? (2 * kd + k) * sizeof(double) : 0;
+    static bool attr = false;
+    if (!attr) {
+        DNDC_CUDA(cudaFuncSetAttribute(kmeans_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>((2 * UPD_MAX_KD + 1024) * sizeof(double))));
+        attr = true;
+    }
+    return bytes;
 }
 
 // Validation pass (cluster.cpp:88-89) fused with sum |x|^2.
@@ -776,17 +885,22 @@ __global__ void validate_kernel(const T* __restrict__ x, int64_t count, double* 
     }
 }
 
-__global__ void validate_final_kernel(const double* pre, int G, double* sx2) {
-    if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(256) validate_final_kernel(const double* pre, int G, double* sx2) {
+    __shared__ double sh[32];
     double s = 0.0, bad = 0.0, mx = 0.0;
-    for (int g = 0; g < G; ++g) {
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
         s += pre[3 * g];
         bad += pre[3 * g + 1];
         mx = fmax(mx, pre[3 * g + 2]);
     }
-    sx2[0] = s;
-    sx2[1] = bad;
-    sx2[3] = mx;
+    s = block_sum(s, sh);
+    bad = block_sum(bad, sh);
+    mx = block_max(mx, sh);
+    if (threadIdx.x == 0) {
+        sx2[0] = s;
+        sx2[1] = bad;
+        sx2[3] = mx;
+    }
 }
 
 // gather_rows (cluster.cpp:27-42): rows owned by this rank into a zero-filled
@@ -934,7 +1048,7 @@ struct Assigner {
             sp.labels = labels;
             sp.refined = b.refined;
             sp.done = use_done ? b.flags : nullptr;
-            sfn<<<sgrid, KM_THREADS, ssmem, st>>>(sp);
+            sfn<<<sgrid, KS_THREADS, ssmem, st>>>(sp);
         } else {
             const AssignParams ap = assign_params<T>(b, x, n, d, k, gen.stages, accumulate, labels, use_done);
             gen.fn<<<gen.grid, KM_THREADS, gen.smem, st>>>(ap);
@@ -968,9 +1082,9 @@ static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n) {
             DNDC_CUDA(cudaFuncSetAttribute(A.sfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(A.ssmem)));
             int per_sm = 1;
-            DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, A.sfn, KM_THREADS, A.ssmem));
+            DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, A.sfn, KS_THREADS, A.ssmem));
             per_sm = std::max(per_sm, 1);
-            const int64_t tiles = std::max<int64_t>(ceil_div(n, KM_TILE), 1);
+            const int64_t tiles = std::max<int64_t>(ceil_div(n, KS_TILE), 1);
             A.sgrid = static_cast<int>(std::min<int64_t>(tiles, static_cast<int64_t>(ctx->num_sms) * per_sm));
             return A;
         }
@@ -1031,7 +1145,7 @@ static void scan_input(dndc_ctx* ctx, const KmBuffers& b, const T* x, int64_t co
     const int G = static_cast<int>(std::min<int64_t>(std::max<int64_t>(ceil_div(count, 256 * 8), 1), 4096));
     validate_kernel<T><<<G, 256, 0, s>>>(x, count, b.pre);
     DNDC_LAUNCHED(ctx);
-    validate_final_kernel<<<1, 32, 0, s>>>(b.pre, G, b.sx2);
+    validate_final_kernel<<<1, 256, 0, s>>>(b.pre, G, b.sx2);
     DNDC_LAUNCHED(ctx);
 }
 
@@ -1095,9 +1209,9 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
         kmeans_reset_kernel<<<1, 1, 0, st>>>(b.flags, b.refined);
         for (int it = 0; it < max_iter; ++it) {
             A.launch(b, x_local, n_local, m, k, true, nullptr, true, st);
-            reduce_partials_kernel<<<(S + 255) / 256, 256, 0, st>>>(b.partials, A.grid(), S, b.stats, b.flags);
+            reduce_partials_kernel<<<S, 256, 0, st>>>(b.partials, A.grid(), S, b.stats, b.flags);
             if (ctx->world > 1) allgather_f64(ctx, b.stats, b.gathered, S, st);
-            kmeans_update_kernel<<<1, 256, 0, st>>>(k, m, dpad_of(m), ctx->world,
+            kmeans_update_kernel<<<1, 256, update_smem(k, m), st>>>(k, m, dpad_of(m), ctx->world,
                                                    ctx->world > 1 ? b.gathered : b.stats, b.c64, b.cn64,
                                                    b.ct, b.cn32, b.ctab, b.bounds, b.sx2, b.trace, b.disp, b.flags,
                                                    it, tol);
