@@ -1,0 +1,108 @@
+"""Multi-GPU parity check (one process per GPU; run under torchrun).
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 tools/dist_check.py
+
+Every rank holds its chunk_map shard; results are compared on rank 0 against
+the oracle simulating the same world size (the reference's rank-order folds).
+Prints one line per check and exits non-zero on any failure.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2007_13552_b200.api as dnd  # noqa: E402
+from oracle.bind import Oracle  # noqa: E402
+
+
+def rel_dev(a, ref):
+    a = np.asarray(a, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.max(np.abs(a - ref) / np.maximum(1.0, np.abs(ref)))) if a.size else 0.0
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    rank, p = dist.get_rank(), dist.get_world_size()
+    comm = dnd.Communicator.from_torch_distributed(local)
+    O = Oracle()
+    ok = True
+
+    def report(name, good, detail=""):
+        nonlocal ok
+        ok = ok and good
+        if rank == 0:
+            print(f"[{'PASS' if good else 'FAIL'}] p={p} {name} {detail}", flush=True)
+
+    # generator: shard content independent of p
+    n, m = 10_007, 18
+    x = dnd.random_uniform((n, m), 0, 42, comm)
+    full = dnd.gather(x)
+    report("random_uniform shards", np.array_equal(full.view(np.uint32), O.uniform_f32(n, m, 42).view(np.uint32)))
+
+    # ring cdist: world-1 exchanges, rank-independent values
+    y = dnd.random_uniform((1001, 7), 0, 43, comm)
+    before = comm.counters()["sendrecvs"]
+    d = dnd.gather(dnd.cdist(y))
+    sr = comm.counters()["sendrecvs"] - before
+    ref = O.cdist(O.uniform_f32(1001, 7, 43).astype(np.float64), p)
+    report("cdist ring", rel_dev(d, ref) <= 1e-5 and np.all(np.diag(d) == 0) and sr == p - 1,
+           f"dev={rel_dev(d, ref):.2e} sendrecvs={sr}")
+    # ring over split y (BASELINE config 2 form)
+    yy = dnd.random_uniform((777, 7), 0, 44, comm)
+    dxy = dnd.gather(dnd.cdist_xy(y, yy))
+    refxy = O.cdist_xy(O.uniform_f32(1001, 7, 43).astype(np.float64), O.uniform_f32(777, 7, 44).astype(np.float64))
+    report("cdist_xy ring (split y)", rel_dev(dxy, refxy) <= 1e-5, f"dev={rel_dev(dxy, refxy):.2e}")
+    # f64 ring is bit-exact
+    y64 = dnd.random_uniform((300, 5), 0, 45, comm, dtype=torch.float64)
+    d64 = dnd.gather(dnd.cdist(y64))
+    report("cdist f64 ring bit-exact", np.array_equal(d64, O.cdist(O.uniform_f64(300, 5, 45), p)))
+
+    # k-means: cfg1 shape at 200k rows, 10 iterations, vs the oracle at the same p
+    n2 = 200_000
+    xk = dnd.random_uniform((n2, 18), 0, 42, comm)
+    model = dnd.kmeans_fit(xk, 8, 10, 0.0, 42)
+    c_ref, t_ref, _ = O.kmeans_fit(O.uniform_f32(n2, 18, 42).astype(np.float64), 8, 10, 0.0, 42, p)
+    report("kmeans_fit 200k x 18", rel_dev(model.centroids, c_ref) <= 1e-5 and rel_dev(model.inertia_trace, t_ref) <= 1e-5,
+           f"centroids dev={rel_dev(model.centroids, c_ref):.2e} trace dev={rel_dev(model.inertia_trace, t_ref):.2e}")
+    # identical bits on every rank (rank-order fold on every GPU)
+    allc = [None] * p
+    dist.all_gather_object(allc, model.centroids)
+    report("kmeans replicated bit-identical", all(np.array_equal(allc[0], c) for c in allc))
+    # generic kernel shape + tol
+    xs = dnd.random_uniform((5000, 5), 0, 9, comm)
+    m2 = dnd.kmeans_fit(xs, 6, 50, 1e-4, 3)
+    c2, t2, it2 = O.kmeans_fit(O.uniform_f32(5000, 5, 9).astype(np.float64), 6, 50, 1e-4, 3, p)
+    report("kmeans_fit tol (generic kernel)", m2.iterations_run == it2 and rel_dev(m2.centroids, c2) <= 1e-5,
+           f"iters {m2.iterations_run} vs {it2}")
+    # predict
+    lab = dnd.gather(dnd.kmeans_predict(model, xk))
+    report("kmeans_predict", np.array_equal(lab, O.kmeans_predict(O.uniform_f32(n2, 18, 42).astype(np.float64),
+                                                                   model.centroids)))
+    # moments
+    st = dnd.moments_axis0(x)
+    mean_ref, var_ref = O.moments_axis0(O.uniform_f32(n, m, 42).astype(np.float64), p)
+    report("moments axis0", st.count == n and rel_dev(st.mean, mean_ref) <= 1e-12 and rel_dev(st.m2 / n, var_ref) <= 1e-12)
+    # k-means++ (per-rank block layout)
+    kp = dnd.kmeanspp_indices(xk, 8, 5)
+    report("kmeanspp", np.array_equal(kp, O.kmeanspp_indices(O.uniform_f32(n2, 18, 42), 8, 5, p)), str(kp.tolist()))
+    # empty shards: p > n
+    tiny = dnd.from_global(np.array([0.0, 0.1, 10.0], np.float32), (3, 1), 0, comm)
+    mt = dnd.kmeans_fit(tiny, 2, 4, 0.0, 7)
+    lo, hi = sorted(mt.centroids[:, 0])
+    report("kmeans more ranks than rows", abs(hi - 10.0) <= 1e-12 and abs(lo - (np.float32(0.1) / 2)) <= 1e-7)
+
+    dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
