@@ -34,9 +34,11 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace dndc {
 
@@ -162,6 +164,35 @@ __device__ __noinline__ int ref_argmin_regs(const float (&xv)[D], const double* 
         for (int f = 0; f < D; ++f) g = add_rn(g, mul_rn(static_cast<double>(xv[f]), c[f]));
         const double dj = ref_distance(xn, cn64[j], g);
         if (j == 0 || dj < bd) {
+            bd = dj;
+            best = j;
+        }
+    }
+    return best;
+}
+
+// Exact reference decision restricted to a candidate set (bit j of `cand`):
+// every cluster outside it is provably farther (its fp32 score exceeds the
+// best by more than the error bound), so the lowest-index minimiser over the
+// candidates, visited in ascending order with strict <, is the reference's
+// assign_local choice (cluster.cpp:44-56).
+template <int D>
+__device__ __noinline__ int ref_argmin_cand(const float (&xv)[D], uint64_t cand, const double* __restrict__ c64,
+                                            const double* __restrict__ cn64) {
+    double xn = 0.0;
+#pragma unroll
+    for (int f = 0; f < D; ++f) xn = add_rn(xn, mul_rn(static_cast<double>(xv[f]), static_cast<double>(xv[f])));
+    int best = -1;
+    double bd = 0.0;
+    while (cand) {
+        const int j = __ffsll(static_cast<long long>(cand)) - 1;
+        cand &= cand - 1;
+        const double* c = c64 + static_cast<int64_t>(j) * D;
+        double g = 0.0;
+#pragma unroll
+        for (int f = 0; f < D; ++f) g = add_rn(g, mul_rn(static_cast<double>(xv[f]), c[f]));
+        const double dj = ref_distance(xn, cn64[j], g);
+        if (best < 0 || dj < bd) {
             bd = dj;
             best = j;
         }
@@ -476,7 +507,7 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
     constexpr int JW = (K + W - 1) / W;       // clusters owned per warp
     if (p.done && *p.done) return;
 
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     float* tiles = reinterpret_cast<float*>(smem_raw);                 // S x TILE x D
     float* sorted = tiles + S * TILE * D;                              // TILE x D
     int* cnt = reinterpret_cast<int*>(sorted + TILE * D);              // VW x K
@@ -636,29 +667,32 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
             if (j >= K) break;
             const int r0 = __shfl_sync(FULL, start, j);
             const int r1 = r0 + __shfl_sync(FULL, total, j);
-            float2 part = make_float2(0.f, 0.f);
+            // f64 accumulation straight from the fp32 rows: the run sums carry
+            // no fp32 rounding, so the centroids track the reference's to ~1e-16
+            // and near-tie flips of its trajectory stay ~1e6x rarer
+            double2 part = make_double2(0.0, 0.0);
             if (g < G) {
                 const float* src = sorted + 2 * q;
 #pragma unroll 4
                 for (int r = r0 + g; r < r1; r += G) {
                     const float2 v = *reinterpret_cast<const float2*>(src + r * D);
-                    part.x += v.x;
-                    part.y += v.y;
+                    part.x += static_cast<double>(v.x);
+                    part.y += static_cast<double>(v.y);
                 }
             }
             // tree over the G groups; a source beyond the last group contributes nothing
 #pragma unroll
             for (int o = 1; o < G; o <<= 1) {
-                const float vx = __shfl_down_sync(FULL, part.x, o * L);
-                const float vy = __shfl_down_sync(FULL, part.y, o * L);
+                const double vx = __shfl_down_sync(FULL, part.x, o * L);
+                const double vy = __shfl_down_sync(FULL, part.y, o * L);
                 if (g + o < G) {
                     part.x += vx;
                     part.y += vy;
                 }
             }
             // lanes of group 0 own features 2q, 2q+1 of cluster j (f64, registers)
-            wsum[jj].x += static_cast<double>(part.x);
-            wsum[jj].y += static_cast<double>(part.y);
+            wsum[jj].x += part.x;
+            wsum[jj].y += part.y;
         }
     }
     if (refined) atomicAdd(p.refined, refined);
@@ -678,6 +712,8 @@ static size_t small_smem() {
     return static_cast<size_t>(KS_STAGES + 1) * KS_TILE * D * 4 +
            static_cast<size_t>((KS_VW * K + 1) & ~1) * 4 + KS_STAGES * 8;
 }
+
+#include "kmeans_tc.cuh"
 
 // Per-stat sum over the CTA partials: one block per stat, a fixed strided
 // split over 256 threads and a fixed tree (deterministic for a given grid).
@@ -1025,16 +1061,33 @@ static AssignParams assign_params(const KmBuffers& b, const T* x, int64_t n, int
 template <typename T>
 struct Assigner {
     bool small = false;
+    bool tc = false;
+    void (*tfn)(CUtensorMap, TcParams) = nullptr;
+    CUtensorMap tmap{};
+    size_t tsmem = 0;
+    int tthreads = 0;
     AssignLaunch<T> gen{};
     void (*sfn)(SmallParams) = nullptr;
     size_t ssmem = 0;
     int sgrid = 0, slot = 0;
 
-    int grid() const { return small ? sgrid : gen.grid; }
+    int grid() const { return (small || tc) ? sgrid : gen.grid; }
 
     void launch(const KmBuffers& b, const T* x, int64_t n, int d, int k, bool accumulate, int32_t* labels,
                 bool use_done, cudaStream_t st) const {
-        if (small) {
+        if (tc) {
+            TcParams tp{};
+            tp.n = n;
+            tp.c64 = b.c64;
+            tp.cn64 = b.cn64;
+            tp.ctab = b.ctab;
+            tp.bounds = b.bounds;
+            tp.partials = accumulate ? b.partials : nullptr;
+            tp.labels = labels;
+            tp.refined = b.refined;
+            tp.done = use_done ? b.flags : nullptr;
+            tfn<<<sgrid, tthreads, tsmem, st>>>(tmap, tp);
+        } else if (small) {
             DNDC_CUDA(cudaMemcpyToSymbolAsync(c_km_table, b.ctab, sizeof(float) * (k * d + k),
                                               sizeof(float) * KS_TABLE * slot, cudaMemcpyDeviceToDevice, st));
             SmallParams sp{};
@@ -1068,10 +1121,56 @@ static bool pick_small(void (*&fn)(SmallParams), size_t& smem, int slot) {
     return true;
 }
 
+template <int D, int K, int P>
+static void pick_tc(Assigner<float>& A) {
+    const char* w = std::getenv("DNDC_TC_WGS");
+    if (w && w[0] == '1') {
+        A.tfn = kmeans_tc_kernel<D, K, P, 1>;
+        A.tsmem = TcCfg<D, K, P, 1>::SMEM;
+        A.tthreads = TcCfg<D, K, P, 1>::THREADS;
+    } else {
+        A.tfn = kmeans_tc_kernel<D, K, P, 2>;
+        A.tsmem = TcCfg<D, K, P, 2>::SMEM;
+        A.tthreads = TcCfg<D, K, P, 2>::THREADS;
+    }
+}
+
+// DNDC_KMEANS_KERNEL=tc|small|generic overrides the automatic choice (tests, A/B timing).
+static const char* kernel_override() {
+    const char* v = std::getenv("DNDC_KMEANS_KERNEL");
+    return v ? v : "";
+}
+
 template <typename T>
-static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n) {
+static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n, const T* x) {
     Assigner<T> A;
+    const std::string force = kernel_override();
     if constexpr (sizeof(T) == 4) {
+        int P = 0;
+        if (force != "small" && force != "generic" && reinterpret_cast<uintptr_t>(x) % 16 == 0 && n > 0) {
+            if (d == 18 && k == 8 && n % 2 == 0) { pick_tc<18, 8, 2>(A); P = 2; }
+            else if (d == 32 && k == 8 && n % 2 == 0) { pick_tc<32, 8, 2>(A); P = 2; }
+            else if (d == 64 && k == 64) { pick_tc<64, 64, 1>(A); P = 1; }
+        }
+        if (P > 0) {
+            A.tc = true;
+            A.tmap = make_tmap_2d_f32(x, static_cast<uint64_t>(n / P), static_cast<uint64_t>(P * d),
+                                      static_cast<uint64_t>(P * d * 4), 4, 128);
+            DNDC_CUDA(cudaFuncSetAttribute(A.tfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(A.tsmem)));
+            int per_sm = 1;
+            DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, A.tfn, A.tthreads, A.tsmem));
+            per_sm = std::max(1, std::min(per_sm, 2));
+            const int64_t tiles = std::max<int64_t>(ceil_div(n / P, 128), 1);
+            A.sgrid = static_cast<int>(std::min<int64_t>(tiles, static_cast<int64_t>(ctx->num_sms) * per_sm));
+            return A;
+        }
+    }
+    if constexpr (sizeof(T) == 4) {
+        if (force == "generic") {
+            A.gen = plan_assign<T>(ctx, k, d, n);
+            return A;
+        }
         const int slot = ctx->km_slot % KS_SLOTS;
         bool ok = false;
         if (d == 18 && k == 8) ok = pick_small<18, 8>(A.sfn, A.ssmem, slot);
@@ -1092,6 +1191,7 @@ static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n) {
     A.gen = plan_assign<T>(ctx, k, d, n);
     return A;
 }
+
 
 static void validate_k(int64_t n, int k, const char* who) {
     if (k < 1) value_error(std::string(who) + ": k must be positive, got " + std::to_string(k));
@@ -1168,7 +1268,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
                     std::to_string(ext[ctx->rank]));
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
-    const Assigner<T> A = plan<T>(ctx, k, m, n_local);
+    const Assigner<T> A = plan<T>(ctx, k, m, n_local, x_local);
     const KmBuffers b = buffers(ctx, k, m, max_iter, A.grid());
     const int S = k * m + k;
 
@@ -1279,7 +1379,7 @@ static void kmeans_predict(dndc_ctx* ctx, const T* x, int64_t n, int64_t m64, co
     if (k < 1) value_error("kmeans_predict: k must be positive");
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
-    const Assigner<T> A = plan<T>(ctx, k, m, n);
+    const Assigner<T> A = plan<T>(ctx, k, m, n, x);
     const KmBuffers b = buffers(ctx, k, m, 1, A.grid());
     double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * k * m));
     std::memcpy(h, cent_host, sizeof(double) * k * m);
@@ -1287,7 +1387,7 @@ static void kmeans_predict(dndc_ctx* ctx, const T* x, int64_t n, int64_t m64, co
     DNDC_CUDA(cudaMemsetAsync(b.refined, 0, sizeof(unsigned long long), s));
     derive_tables(ctx, b, k, m);
     if (n > 0) {
-        if (A.small) scan_input<T>(ctx, b, x, n * m, s);
+        if (A.small || A.tc) scan_input<T>(ctx, b, x, n * m, s);
         A.launch(b, x, n, m, k, false, labels, false, s);
         DNDC_LAUNCHED(ctx);
     }
@@ -1319,7 +1419,7 @@ static void time_assign(dndc_ctx* ctx, const float* x, int64_t n, int64_t m64, i
                         double* bytes) {
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
-    const Assigner<float> A = plan<float>(ctx, k, m, n);
+    const Assigner<float> A = plan<float>(ctx, k, m, n, x);
     const bool fresh = ctx->slots.find("km_c64") == ctx->slots.end();
     const KmBuffers b = buffers(ctx, k, m, 1, A.grid());
     if (fresh) {

@@ -1,0 +1,445 @@
+// kmeans_tc.cuh -- tcgen05 assign/accumulate kernel (included by kmeans.cu
+// inside namespace dndc; needs ref_argmin_cand, FULL and ceil_div from there).
+//
+// The K*D score FMAs per row run on the 5th-gen tensor cores:
+//   * X is streamed by TMA 2-D tile loads as P rows per MMA row ("packed
+//     rows": X viewed as [n/P x P*D]; D = 18 rows pair up into 36 columns with
+//     a 144-byte pitch), box {4 columns, 128 packed rows} = the SWIZZLE_NONE
+//     K-major canonical layout of tc.cuh.  3-stage ring, one producer thread.
+//   * scores[packed row][h*K + j] = x_h . (-2 c_j) with a block-diagonal
+//     centroid operand (N = P*K), 3xTF32: the tensor core truncates fp32
+//     inputs to tf32 (pinned by tests/test_gpu_tc.py), so hi = the raw TMA
+//     tile and the epilogue only writes lo = x - trunc(x);
+//     hi.Bhi + hi.Blo + lo.Bhi accumulate in TMEM (fp32).
+//   * Two epilogue warpgroups take alternating tiles (thread = packed row =
+//     TMEM lane), so one warpgroup's CUDA-core work overlaps the other's MMA.
+//     Per tile: split, score readback (tcgen05.ld), top-2 against a rigorous
+//     per-row error bound, exact f64 re-decision over the candidate clusters
+//     only, then the counting sort by label into the (now free) lo buffer and
+//     warp-per-cluster f64 run sums -- as kmeans_small_kernel.
+//   * tf32 MN-major operands are not supported (zeros; tests/test_gpu_tc.py),
+//     so the one-hot accumulation stays on the CUDA cores.
+
+struct TcParams {
+    int64_t n;            // rows (a multiple of P)
+    const double* c64;
+    const double* cn64;
+    const float* ctab;    // [K*D] -2 c (fp32), [K] |c|^2 (fp32)
+    const float* bounds;  // [0] max |c_j|, [1] max |c_j|^2
+    double* partials;     // null: predict only
+    int32_t* labels;
+    unsigned long long* refined;
+    const int* done;
+};
+
+__host__ __device__ constexpr int tc_pow2_cols(int c) {
+    return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
+}
+
+template <int D, int K, int P, int WG_ = 2>
+struct TcCfg {
+    static constexpr int KC = ((P * D + 7) / 8) * 8;  // MMA K (tf32 steps of 8)
+    static constexpr int NCH = KC / 4;                // 16-byte column chunks
+    static constexpr int NS = P * K;                  // MMA N: score slots
+    static constexpr int PR = 128;                    // packed rows per tile (MMA M)
+    static constexpr int TROWS = PR * P;              // data rows per tile
+    static constexpr int S = 3;                       // TMA stages
+    static constexpr int WGS = WG_;                   // epilogue warpgroups
+    static constexpr int EPI = 128 * WGS;
+    static constexpr int THREADS = EPI + 32;          // + the producer / MMA warp
+    static constexpr int TILE_BYTES = NCH * PR * 16;
+    static constexpr int SORT_BYTES = TROWS * D * 4;
+    static constexpr int WORK_BYTES = TILE_BYTES > SORT_BYTES ? TILE_BYTES : SORT_BYTES;  // lo, then sorted rows
+    static constexpr int B_BYTES = NCH * NS * 16;
+    static constexpr int VW = 4 * P;                  // 32-row groups per tile
+    static constexpr int TMEM_COLS = tc_pow2_cols(WGS * NS);
+    static constexpr int OFF_TILE = 0;
+    static constexpr int OFF_WORK = OFF_TILE + S * TILE_BYTES;
+    static constexpr int OFF_BHI = OFF_WORK + WGS * WORK_BYTES;
+    static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
+    static constexpr int OFF_CN = OFF_BLO + B_BYTES;
+    static constexpr int OFF_CNT = OFF_CN + ((K * 4 + 15) / 16) * 16;
+    static constexpr int OFF_BAR = OFF_CNT + WGS * ((VW * K * 4 + 15) / 16) * 16;
+    static constexpr int NBARS = 2 * S + 3 * WGS;
+    static constexpr int OFF_TMEM = OFF_BAR + NBARS * 8;
+    static constexpr int SMEM = OFF_TMEM + 16;
+    static_assert(NS % 16 == 0 && NS <= 256, "MMA N (P*K) must be a multiple of 16, <= 256");
+    static_assert(D % 2 == 0 && D <= 64 && K <= 64, "tc kernel shape");
+    static_assert(WGS * K * D * 8 <= WGS * WORK_BYTES, "final combine scratch");
+};
+
+template <int D, int K, int P, int WG_>
+__global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
+    kmeans_tc_kernel(const __grid_constant__ CUtensorMap map, TcParams p) {
+    using C = TcCfg<D, K, P, WG_>;
+    constexpr int NCH = C::NCH, NS = C::NS, PR = C::PR, S = C::S, KD = K * D, VW = C::VW, WGS = C::WGS;
+    constexpr int L = D / 2;                // phase-2 lanes per row (float2 each)
+    constexpr int G = 32 / L;               // rows summed in parallel per warp
+    constexpr int JW = (K + 3) / 4;         // clusters owned per epilogue warp
+    constexpr int KL = (K + 31) / 32;       // clusters per lane in the scans
+    if (p.done && *p.done) return;
+
+    extern __shared__ __align__(1024) unsigned char smem[];
+    float* tiles = reinterpret_cast<float*>(smem + C::OFF_TILE);
+    float* bhi = reinterpret_cast<float*>(smem + C::OFF_BHI);
+    float* blo = reinterpret_cast<float*>(smem + C::OFF_BLO);
+    float* cn = reinterpret_cast<float*>(smem + C::OFF_CN);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+    uint64_t* full = bars;              // [S] TMA landed
+    uint64_t* empty = bars + S;         // [S] stage free
+    uint64_t* loready = bars + 2 * S;   // [WGS] lo split written
+    uint64_t* dfull = loready + WGS;    // [WGS] scores ready
+    uint64_t* dempty = dfull + WGS;     // [WGS] scores read
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool accumulate = p.partials != nullptr;
+    constexpr int CTRL = C::EPI / 32;  // control warp index
+
+    if (warp == CTRL) {
+        tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+        if (lane == 0) {
+            for (int s = 0; s < S; ++s) {
+                tc::mbar_init(&full[s], 1);
+                tc::mbar_init(&empty[s], 1);
+            }
+            for (int w = 0; w < WGS; ++w) {
+                tc::mbar_init(&loready[w], 1);
+                tc::mbar_init(&dfull[w], 1);
+                tc::mbar_init(&dempty[w], 128);
+            }
+            tc::mbar_fence_init();
+            tc::tma_prefetch_desc(&map);
+        }
+    } else {
+        // block-diagonal centroid operand, split into tf32 hi / lo, K-major chunks
+        for (int e = tid; e < NS * C::KC; e += C::EPI) {
+            const int n = e / C::KC, c = e % C::KC;
+            const int h = n / K, j = n % K;
+            const int f = c - h * D;
+            const float v = (f >= 0 && f < D) ? p.ctab[j * D + f] : 0.f;
+            const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+            const int off = (c / 4) * (NS * 4) + n * 4 + (c % 4);
+            bhi[off] = hi;
+            blo[off] = v - hi;
+        }
+        for (int j = tid; j < K; j += C::EPI) cn[j] = p.ctab[KD + j];
+        tc::fence_async_smem();
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int64_t npacked = p.n / P;
+    const int64_t ntiles = ceil_div(npacked, PR);
+    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    if (warp == CTRL) {
+        // ------------------------------------------------ TMA + MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_tf32(128, NS, 0, 0);
+            int64_t issued = 0;
+            for (int64_t it = 0; it < my_tiles; ++it) {
+                while (issued < my_tiles && issued < it + S) {
+                    const int st = static_cast<int>(issued % S);
+                    if (issued >= S) tc::mbar_wait(&empty[st], static_cast<uint32_t>((issued / S - 1) & 1));
+                    const int prow = static_cast<int>((blockIdx.x + issued * gridDim.x) * PR);
+                    tc::mbar_expect_tx(&full[st], C::TILE_BYTES);
+                    float* dst = tiles + st * (C::TILE_BYTES / 4);
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) tc::tma_load_2d(dst + c * PR * 4, &map, &full[st], c * 4, prow);
+                    ++issued;
+                }
+                const int st = static_cast<int>(it % S), w = static_cast<int>(it % WGS);
+                const int64_t use = it / WGS;  // this warpgroup's use index
+                tc::mbar_wait(&loready[w], static_cast<uint32_t>(use & 1));
+                if (use >= 1) tc::mbar_wait(&dempty[w], static_cast<uint32_t>((use - 1) & 1));
+                tc::tc_fence_after();
+                const uint32_t a0 = tc::smem_u32(tiles + st * (C::TILE_BYTES / 4));
+                const uint32_t l0 = tc::smem_u32(smem + C::OFF_WORK + w * C::WORK_BYTES);
+                const uint32_t bh0 = tc::smem_u32(bhi), bl0 = tc::smem_u32(blo);
+                const uint32_t dt = tmem + w * NS;
+#pragma unroll
+                for (int ks = 0; ks < C::KC / 8; ++ks) {
+                    const uint64_t ahi = tc::smem_desc(a0 + ks * 2 * PR * 16, PR * 16, 128);
+                    const uint64_t alo = tc::smem_desc(l0 + ks * 2 * PR * 16, PR * 16, 128);
+                    const uint64_t bh = tc::smem_desc(bh0 + ks * 2 * NS * 16, NS * 16, 128);
+                    const uint64_t bl = tc::smem_desc(bl0 + ks * 2 * NS * 16, NS * 16, 128);
+                    tc::mma_tf32(dt, ahi, bh, idesc, ks > 0);
+                    tc::mma_tf32(dt, ahi, bl, idesc, 1);
+                    tc::mma_tf32(dt, alo, bh, idesc, 1);
+                }
+                tc::mma_commit(&dfull[w]);
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue warpgroups
+        const int wg = warp / 4, wq = warp % 4, t = tid % 128;  // t = packed row = TMEM lane
+        float* work = reinterpret_cast<float*>(smem + C::OFF_WORK + wg * C::WORK_BYTES);
+        int* cnt = reinterpret_cast<int*>(smem + C::OFF_CNT + wg * ((VW * K * 4 + 15) / 16) * 16);
+        const uint32_t bar_id = 1 + wg;
+        const float cmax = p.bounds[0], cnmax = p.bounds[1];
+        constexpr float ERR = 4.f * (static_cast<float>(3 * C::KC) * 0x1.0p-24f + 3.f * 0x1.0p-20f);
+        long long count_acc[KL];
+#pragma unroll
+        for (int u = 0; u < KL; ++u) count_acc[u] = 0;
+        unsigned long long refined = 0;
+        const int g = lane / L, q = lane % L;
+        double2 wsum[JW];
+#pragma unroll
+        for (int jj = 0; jj < JW; ++jj) wsum[jj] = make_double2(0.0, 0.0);
+
+        for (int64_t it = wg; it < my_tiles; it += WGS) {
+            const int st = static_cast<int>(it % S);
+            const int64_t use = it / WGS;
+            const int64_t prow0 = (blockIdx.x + it * gridDim.x) * PR;
+            const float* xt = tiles + st * (C::TILE_BYTES / 4);
+            tc::mbar_wait(&full[st], static_cast<uint32_t>((it / S) & 1));
+
+            // split: lo = x - trunc_tf32(x); the raw row stays in registers
+            float4 xr[NCH];
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                const float4 v = *reinterpret_cast<const float4*>(xt + c * PR * 4 + t * 4);
+                xr[c] = v;
+                float4 l;
+                l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                *reinterpret_cast<float4*>(work + c * PR * 4 + t * 4) = l;
+            }
+            tc::fence_async_smem();
+            tc::named_sync(bar_id, 128);
+            if (t == 0) tc::mbar_arrive(&loready[wg]);
+
+            auto xval = [&](int c) {
+                const float4 v4 = xr[c / 4];
+                return (c % 4 == 0) ? v4.x : (c % 4 == 1) ? v4.y : (c % 4 == 2) ? v4.z : v4.w;
+            };
+            // per-row |x|^2 for the error bound (fp32; only scales the bound)
+            float xx[P];
+#pragma unroll
+            for (int h = 0; h < P; ++h) {
+                xx[h] = 0.f;
+#pragma unroll
+                for (int f = 0; f < D; ++f) xx[h] = fmaf(xval(h * D + f), xval(h * D + f), xx[h]);
+            }
+
+            // scores: running top-2 over 16-column TMEM chunks
+            tc::mbar_wait(&dfull[wg], static_cast<uint32_t>(use & 1));
+            tc::tc_fence_after();
+            const uint32_t trow = tmem + (static_cast<uint32_t>(wq * 32) << 16) + wg * NS;
+            float b1[P], b2[P];
+            int i1[P];
+#pragma unroll
+            for (int h = 0; h < P; ++h) {
+                b1[h] = FLT_MAX;
+                b2[h] = FLT_MAX;
+                i1[h] = 0;
+            }
+#pragma unroll
+            for (int q16 = 0; q16 < NS / 16; ++q16) {
+                float v[16];
+                tc::tmem_ld16(trow + q16 * 16, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int slot = q16 * 16 + i, h = slot / K, j = slot % K;
+                    const float s = cn[j] + v[i];
+                    const bool lt = s < b1[h];
+                    b2[h] = fminf(b2[h], fmaxf(b1[h], s));
+                    b1[h] = fminf(b1[h], s);
+                    i1[h] = lt ? j : i1[h];
+                }
+            }
+            int label[P];
+            bool flag[P];
+            float tau[P];
+            bool any_flag = false;
+#pragma unroll
+            for (int h = 0; h < P; ++h) {
+                const int64_t row = (prow0 + t) * P + h;
+                label[h] = row < p.n ? i1[h] : K;  // rows past the end sort last
+                tau[h] = ERR * (cnmax + 2.f * sqrtf(xx[h]) * cmax);
+                flag[h] = row < p.n && K > 1 && !(b2[h] - b1[h] > tau[h]);
+                any_flag |= flag[h];
+            }
+            // near-ties: candidate clusters (score within tau of the best) from a
+            // second, warp-uniform TMEM pass (tcgen05.ld is .sync.aligned), then
+            // the exact f64 decision over the candidates only
+            if (__any_sync(FULL, any_flag)) {
+                uint64_t cand[P];
+#pragma unroll
+                for (int h = 0; h < P; ++h) cand[h] = 0;
+#pragma unroll
+                for (int q16 = 0; q16 < NS / 16; ++q16) {
+                    float v[16];
+                    tc::tmem_ld16(trow + q16 * 16, v);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int slot = q16 * 16 + i, h = slot / K, j = slot % K;
+                        if (cn[j] + v[i] <= b1[h] + tau[h]) cand[h] |= 1ull << j;
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < P; ++h) {
+                    if (flag[h]) {
+                        float xv[D];
+#pragma unroll
+                        for (int f = 0; f < D; ++f) xv[f] = xval(h * D + f);
+                        label[h] = ref_argmin_cand<D>(xv, cand[h], p.c64, p.cn64);
+                        ++refined;
+                    }
+                }
+            }
+            if (p.labels) {
+#pragma unroll
+                for (int h = 0; h < P; ++h) {
+                    const int64_t row = (prow0 + t) * P + h;
+                    if (row < p.n) p.labels[row] = label[h];
+                }
+            }
+            tc::tc_fence_before();
+            tc::mbar_arrive(&dempty[wg]);
+            if (t == 0) tc::mbar_arrive(&empty[st]);  // the tile is in registers; its MMAs completed
+            if (!accumulate) continue;
+
+            // ---------------- counting sort of the tile by label (groups vw = h*4 + wq)
+            unsigned mine[P];
+            int rank[P];
+            for (int e = lane; e < P * K; e += 32) cnt[((e / K) * 4 + wq) * K + (e % K)] = 0;
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < P; ++h) {
+                mine[h] = __match_any_sync(FULL, label[h]);
+                rank[h] = __popc(mine[h] & ((1u << lane) - 1u));
+                if (rank[h] == 0 && label[h] < K) cnt[(h * 4 + wq) * K + label[h]] = __popc(mine[h]);
+            }
+            tc::named_sync(bar_id, 128);
+            int total[KL], before[KL][P], start[KL];
+#pragma unroll
+            for (int u = 0; u < KL; ++u) {
+                const int j = lane + 32 * u;
+                total[u] = 0;
+#pragma unroll
+                for (int h = 0; h < P; ++h) before[u][h] = 0;
+                if (j < K) {
+#pragma unroll
+                    for (int v = 0; v < VW; ++v) {
+                        const int c = cnt[v * K + j];
+                        total[u] += c;
+#pragma unroll
+                        for (int h = 0; h < P; ++h) before[u][h] += v < h * 4 + wq ? c : 0;
+                    }
+                }
+            }
+            {
+                int carry = 0;
+#pragma unroll
+                for (int u = 0; u < KL; ++u) {
+                    int incl = total[u];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int v = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    start[u] = carry + incl - total[u];
+                    carry += __shfl_sync(FULL, incl, 31);
+                    if (wq == 0) count_acc[u] += total[u];
+                }
+            }
+            // scatter rows into label order (features from registers) -- the lo
+            // buffer is free once the scores are in (its MMAs completed)
+#pragma unroll
+            for (int h = 0; h < P; ++h) {
+                const int lb = label[h] < K ? label[h] : 0;
+                int base = 0;
+#pragma unroll
+                for (int u = 0; u < KL; ++u) {
+                    const int v = __shfl_sync(FULL, start[u] + before[u][h], lb % 32);
+                    if (lb / 32 == u) base = v;
+                }
+                const int pos = base + rank[h];
+                if (label[h] < K) {
+#pragma unroll
+                    for (int f = 0; f < D; f += 2)
+                        *reinterpret_cast<float2*>(work + pos * D + f) = make_float2(xval(h * D + f), xval(h * D + f + 1));
+                }
+            }
+            tc::named_sync(bar_id, 128);
+
+            // warp wq sums the sorted runs of clusters wq, wq+4, ... (f64 from the fp32 rows)
+#pragma unroll
+            for (int jj = 0; jj < JW; ++jj) {
+                const int j = wq + jj * 4;
+                if (j >= K) break;
+                const int r0 = __shfl_sync(FULL, start[j / 32], j % 32);
+                const int r1 = r0 + __shfl_sync(FULL, total[j / 32], j % 32);
+                double2 part = make_double2(0.0, 0.0);
+                if (g < G) {
+                    const float* src = work + 2 * q;
+#pragma unroll 4
+                    for (int r = r0 + g; r < r1; r += G) {
+                        const float2 v = *reinterpret_cast<const float2*>(src + r * D);
+                        part.x += static_cast<double>(v.x);
+                        part.y += static_cast<double>(v.y);
+                    }
+                }
+#pragma unroll
+                for (int o = 1; o < G; o <<= 1) {
+                    const double vx = __shfl_down_sync(FULL, part.x, o * L);
+                    const double vy = __shfl_down_sync(FULL, part.y, o * L);
+                    if (g + o < G) {
+                        part.x += vx;
+                        part.y += vy;
+                    }
+                }
+                wsum[jj].x += part.x;
+                wsum[jj].y += part.y;
+            }
+            // the next tile's split rewrites `work` (lo): all warps must be done reading it
+            tc::named_sync(bar_id, 128);
+        }
+        if (refined) atomicAdd(p.refined, refined);
+        if (accumulate) {
+            // combine the warpgroups in a fixed order: wg 1 parks its sums, wg 0 adds
+            double* park = reinterpret_cast<double*>(smem + C::OFF_WORK);
+            tc::named_sync(3, C::EPI);  // every warpgroup is past its last tile
+            if (wg == 1) {
+#pragma unroll
+                for (int jj = 0; jj < JW; ++jj) {
+                    const int j = wq + jj * 4;
+                    if (j < K && g == 0 && q < L) *reinterpret_cast<double2*>(park + j * D + 2 * q) = wsum[jj];
+                }
+                if (wq == 0)
+#pragma unroll
+                    for (int u = 0; u < KL; ++u)
+                        if (lane + 32 * u < K) park[KD + lane + 32 * u] = static_cast<double>(count_acc[u]);
+            }
+            tc::named_sync(3, C::EPI);
+            if (wg == 0) {
+                double* out = p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K);
+#pragma unroll
+                for (int jj = 0; jj < JW; ++jj) {
+                    const int j = wq + jj * 4;
+                    if (j < K && g == 0 && q < L) {
+                        const double2 o = WGS > 1 ? *reinterpret_cast<const double2*>(park + j * D + 2 * q)
+                                                  : make_double2(0.0, 0.0);
+                        *reinterpret_cast<double2*>(out + j * D + 2 * q) =
+                            make_double2(wsum[jj].x + o.x, wsum[jj].y + o.y);
+                    }
+                }
+                if (wq == 0)
+#pragma unroll
+                    for (int u = 0; u < KL; ++u)
+                        if (lane + 32 * u < K)
+                            out[KD + lane + 32 * u] =
+                                static_cast<double>(count_acc[u]) + (WGS > 1 ? park[KD + lane + 32 * u] : 0.0);
+            }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == CTRL) tc::tmem_dealloc(tmem, C::TMEM_COLS);
+}

@@ -160,3 +160,21 @@ def test_cfg1_full_size_matches_reference(comm, golden):
             assert rel_dev(model.inertia_trace, golden["cfg1_trace"]) <= 1e-5
             print(f"cfg1: centroid rel dev {rel_dev(model.centroids, golden[key]):.3e}, "
                   f"refined rows in last fit {model.refined_rows}")
+
+
+@pytest.mark.parametrize("n,m,k", [(5000, 18, 8), (3000, 32, 8), (2048, 64, 64), (70_000, 18, 8)])
+def test_kernel_variants_agree(comm, oracle, n, m, k, monkeypatch):
+    """tcgen05 (tc), CUDA-core specialised (small) and generic kernels: identical
+    labels and the reference's centroids (within fp32 partial-sum rounding)."""
+    xh = oracle.uniform_f32(n, m, 11)
+    x = dnd.from_global(xh, (n, m), 0, comm)
+    c_ref, t_ref, _ = oracle.kmeans_fit(xh.astype(np.float64), k, 6, 0.0, 3)
+    got = {}
+    for kind in ("tc", "small", "generic"):
+        monkeypatch.setenv("DNDC_KMEANS_KERNEL", kind)
+        model = dnd.kmeans_fit(x, k, 6, 0.0, 3)
+        got[kind] = model
+        assert rel_dev(model.centroids, c_ref) <= 1e-6, kind
+        assert rel_dev(model.inertia_trace, t_ref) <= 1e-6, kind
+        labels = dnd.gather(dnd.kmeans_predict(model, x))
+        assert np.array_equal(labels, oracle.kmeans_predict(xh.astype(np.float64), model.centroids)), kind
