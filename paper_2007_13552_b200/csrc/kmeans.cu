@@ -1147,7 +1147,11 @@ static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n, const T* x) {
     const std::string force = kernel_override();
     if constexpr (sizeof(T) == 4) {
         int P = 0;
-        if (force != "small" && force != "generic" && reinterpret_cast<uintptr_t>(x) % 16 == 0 && n > 0) {
+        // tensor cores where the K*D FMAs dominate (measured: cfg3 k=64, d=64 runs
+        // 2x the FFMA kernel); for k=8 the CUDA-core kernel is faster (its epilogue
+        // is cheaper than the split + TMEM readback), so tc there only on request
+        const bool want_tc = force == "tc" || (force.empty() && k * d >= 1024);
+        if (want_tc && reinterpret_cast<uintptr_t>(x) % 16 == 0 && n > 0) {
             if (d == 18 && k == 8 && n % 2 == 0) { pick_tc<18, 8, 2>(A); P = 2; }
             else if (d == 32 && k == 8 && n % 2 == 0) { pick_tc<32, 8, 2>(A); P = 2; }
             else if (d == 64 && k == 64) { pick_tc<64, 64, 1>(A); P = 1; }
