@@ -69,37 +69,42 @@ namespace ffma {
 constexpr int BM = 128, BN = 128, BK = 32, THREADS = 256;
 }
 
-template <bool VEC>
-__global__ void __launch_bounds__(ffma::THREADS)
-    cdist_tile_f32_kernel(const float* __restrict__ x, const float* __restrict__ xn, int64_t nx,
-                          const float* __restrict__ y, const float* __restrict__ yn, int64_t ny,
-                          int m, float* __restrict__ out, int64_t ld, int64_t col_off,
-                          int64_t diag_offset, int64_t row_block0) {
+// Loads a BK-deep slab of a 128-row operand tile into smem transposed
+// ([kk][row], conflict-free stores).  FULL: every row is in bounds.
+template <bool FULL>
+__device__ __forceinline__ void load_slab(float (*dst)[ffma::BM], const float* __restrict__ src, int64_t rows_left,
+                                          int m, int k0, int kc) {
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < ffma::BM * kc; idx += ffma::THREADS) {
+        const int r = idx & (ffma::BM - 1), kk = idx >> 7;
+        dst[kk][r] = (FULL || r < rows_left) ? __ldg(src + static_cast<int64_t>(r) * m + k0 + kk) : 0.f;
+    }
+}
+
+// One 128x128 output tile; FULL = interior tile (no bounds checks), DIAG =
+// the tile meets the self block's diagonal.
+template <bool VEC, bool FULL, bool DIAG>
+__device__ __forceinline__ void cdist_tile_body(const float* __restrict__ x, const float* __restrict__ xn,
+                                                int64_t nx, const float* __restrict__ y,
+                                                const float* __restrict__ yn, int64_t ny, int m,
+                                                float* __restrict__ out, int64_t ld, int64_t row0, int64_t col0,
+                                                int64_t diag_offset, float (*xs)[ffma::BM], float (*ys)[ffma::BN]) {
     using namespace ffma;
-    __shared__ __align__(16) float xs[BK][BM];
-    __shared__ __align__(16) float ys[BK][BN];
     const int tid = threadIdx.x;
     const int tx = tid & 15, ty = tid >> 4;
-    const int64_t row0 = (row_block0 + blockIdx.y) * BM;
-    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * BN;
-
     float acc[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-
+    const float* xb = x + row0 * m;
+    const float* yb = y + col0 * m;
     for (int k0 = 0; k0 < m; k0 += BK) {
         const int kc = min(BK, m - k0);
-        // r fastest: conflict-free transposed smem stores; the global reads of
-        // a 128 x kc slab stay within a few L1 lines per row.
-        for (int idx = tid; idx < BM * kc; idx += THREADS) {
-            const int r = idx % BM, kk = idx / BM;
-            const int64_t gr = row0 + r, gc = col0 + r;
-            xs[kk][r] = gr < nx ? __ldg(x + gr * m + k0 + kk) : 0.f;
-            ys[kk][r] = gc < ny ? __ldg(y + gc * m + k0 + kk) : 0.f;
-        }
+        load_slab<FULL>(xs, xb, nx - row0, m, k0, kc);
+        load_slab<FULL>(ys, yb, ny - col0, m, k0, kc);
         __syncthreads();
+#pragma unroll 2
         for (int kk = 0; kk < kc; ++kk) {
             const float4 a0 = *reinterpret_cast<const float4*>(&xs[kk][ty * 4]);
             const float4 a1 = *reinterpret_cast<const float4*>(&xs[kk][64 + ty * 4]);
@@ -114,37 +119,61 @@ __global__ void __launch_bounds__(ffma::THREADS)
         }
         __syncthreads();
     }
-
     float ynv[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const int64_t gj = col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
-        ynv[j] = gj < ny ? __ldg(yn + gj) : 0.f;
+        const int cj = j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4;
+        ynv[j] = (FULL || col0 + cj < ny) ? __ldg(yn + col0 + cj) : 0.f;
     }
+    float* obase = out + row0 * ld + col0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int64_t gi = row0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
-        if (gi >= nx) continue;
-        const float xni = __ldg(xn + gi);
-        float* orow = out + gi * ld + col_off;
+        const int ri = i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4;
+        if (!FULL && row0 + ri >= nx) continue;
+        const float xni = __ldg(xn + row0 + ri);
+        float* orow = obase + static_cast<int64_t>(ri) * ld;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int64_t c = col0 + h * 64 + tx * 4;
+            const int c = h * 64 + tx * 4;
             float v[4];
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-                const float s = fmaxf(fmaf(-2.f, acc[i][h * 4 + jj], xni + ynv[h * 4 + jj]), 0.f);
-                v[jj] = (diag_offset >= 0 && c + jj == gi + diag_offset) ? 0.f : sqrt_approx(s);
+                const float sq = fmaxf(fmaf(-2.f, acc[i][h * 4 + jj], xni + ynv[h * 4 + jj]), 0.f);
+                v[jj] = sqrt_approx(sq);
+                if (DIAG && col0 + c + jj == row0 + ri + diag_offset) v[jj] = 0.f;
             }
-            if (VEC && c + 3 < ny) {
+            if (VEC && (FULL || col0 + c + 3 < ny)) {
                 st_stream4(orow + c, v[0], v[1], v[2], v[3]);
             } else {
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj)
-                    if (c + jj < ny) st_stream(orow + c + jj, v[jj]);
+                    if (FULL || col0 + c + jj < ny) st_stream(orow + c + jj, v[jj]);
             }
         }
     }
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(ffma::THREADS)
+    cdist_tile_f32_kernel(const float* __restrict__ x, const float* __restrict__ xn, int64_t nx,
+                          const float* __restrict__ y, const float* __restrict__ yn, int64_t ny,
+                          int m, float* __restrict__ out, int64_t ld, int64_t col_off,
+                          int64_t diag_offset, int64_t row_block0) {
+    using namespace ffma;
+    __shared__ __align__(16) float xs[BK][BM];
+    __shared__ __align__(16) float ys[BK][BN];
+    const int64_t row0 = (row_block0 + blockIdx.y) * BM;
+    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * BN;
+    const bool full = row0 + BM <= nx && col0 + BN <= ny;
+    // does column j == row i + diag_offset occur inside this tile?
+    const bool diag = diag_offset >= 0 && col0 < row0 + diag_offset + BM && row0 + diag_offset < col0 + BN;
+    float* o = out + col_off;
+    if (full && !diag)
+        cdist_tile_body<VEC, true, false>(x, xn, nx, y, yn, ny, m, o, ld, row0, col0, diag_offset, xs, ys);
+    else if (diag)
+        cdist_tile_body<VEC, false, true>(x, xn, nx, y, yn, ny, m, o, ld, row0, col0, diag_offset, xs, ys);
+    else
+        cdist_tile_body<VEC, false, false>(x, xn, nx, y, yn, ny, m, o, ld, row0, col0, diag_offset, xs, ys);
 }
 
 // ------------------------------------------------------- f64 exact tile

@@ -40,7 +40,41 @@ __device__ __forceinline__ double warp_butterfly(double v) {
     return v;
 }
 
-// One warp per 2048-row block of the local shard.
+// D2 of one row against the newest pick: sequential over features in f64,
+// product rounded before the add (the oracle's order).  M > 0: compile-time
+// width (all loads issued up front, float4 when aligned); M == 0: runtime.
+template <int M>
+__device__ __forceinline__ double kpp_row(const float* __restrict__ xr, const float* c, int m) {
+    if constexpr (M > 0) {
+        float v[M];
+        if constexpr (M % 4 == 0) {
+#pragma unroll
+            for (int f = 0; f < M; f += 4) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(xr + f));
+                v[f] = q.x;
+                v[f + 1] = q.y;
+                v[f + 2] = q.z;
+                v[f + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int f = 0; f < M; ++f) v[f] = __ldg(xr + f);
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int f = 0; f < M; ++f) {
+            const double dd = sub_rn(static_cast<double>(v[f]), static_cast<double>(c[f]));
+            acc = add_rn(acc, mul_rn(dd, dd));
+        }
+        return acc;
+    } else {
+        return kpp_dist2(xr, c, m);
+    }
+}
+
+// One warp per 2048-row block of the local shard; lane l owns rows l, l+32, ...
+// (the summation order of the definition), two rows in flight per lane.
+template <int M>
 __global__ void kpp_update_kernel(const float* __restrict__ x, int64_t n, int m,
                                   const float* __restrict__ crow, double* __restrict__ d2, int first,
                                   double* __restrict__ S, int64_t nblocks) {
@@ -53,15 +87,21 @@ __global__ void kpp_update_kernel(const float* __restrict__ x, int64_t n, int m,
     const int64_t lo = b * KPP_BLOCK;
     const int64_t hi = min(n, lo + KPP_BLOCK);
     double acc = 0.0;
-    for (int64_t i = lo + lane; i < hi; i += 32) {
-        const double dist = kpp_dist2(x + i * m, c_sh, m);
-        double v = dist;
+    for (int64_t i = lo + lane; i < hi; i += 64) {
+        const int64_t i2 = i + 32;
+        const double da = kpp_row<M>(x + i * m, c_sh, m);
+        const double db = i2 < hi ? kpp_row<M>(x + i2 * m, c_sh, m) : 0.0;
+        double va = da, vb = db;
         if (!first) {
-            const double old = d2[i];
-            v = dist < old ? dist : old;
+            va = da < d2[i] ? da : d2[i];
+            if (i2 < hi) vb = db < d2[i2] ? db : d2[i2];
         }
-        d2[i] = v;
-        acc = add_rn(acc, v);
+        d2[i] = va;
+        acc = add_rn(acc, va);
+        if (i2 < hi) {
+            d2[i2] = vb;
+            acc = add_rn(acc, vb);
+        }
     }
     acc = warp_butterfly(acc);
     if (lane == 0) S[b] = acc;
@@ -245,8 +285,14 @@ static void kmeanspp(dndc_ctx* ctx, const float* x, int64_t n_local, int64_t n_g
     const int wpb = 8;
     for (int j = 1; j < k; ++j) {
         if (nblocks > 0) {
-            kpp_update_kernel<<<static_cast<unsigned>(ceil_div(nblocks, wpb)), 32 * wpb, sizeof(float) * m, s>>>(
-                x, n_local, m, crow, d2, j == 1, S, nblocks);
+            const unsigned g = static_cast<unsigned>(ceil_div(nblocks, wpb));
+            const size_t sm = sizeof(float) * m;
+            const bool a16 = reinterpret_cast<uintptr_t>(x) % 16 == 0;
+            if (m == 32 && a16) kpp_update_kernel<32><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+            else if (m == 64 && a16) kpp_update_kernel<64><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+            else if (m == 16 && a16) kpp_update_kernel<16><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+            else if (m == 18) kpp_update_kernel<18><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+            else kpp_update_kernel<0><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
             DNDC_LAUNCHED(ctx);
             kpp_group_kernel<<<static_cast<unsigned>(ceil_div(ngroups, wpb)), 32 * wpb, 0, s>>>(S, nblocks, T,
                                                                                                ngroups);

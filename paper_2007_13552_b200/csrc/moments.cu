@@ -57,12 +57,32 @@ __global__ void __launch_bounds__(MO_THREADS)
             while (i < r1) {
                 const double K = static_cast<double>(x[i * m + c]);
                 double s1 = 0.0, s2 = 0.0;
-                int cnt = 0;
-                for (; cnt < MO_KC && i < r1; ++cnt, i += lanes) {
-                    const double v = static_cast<double>(x[i * m + c]) - K;
-                    s1 += v;
-                    s2 = fma(v, v, s2);
+                const int64_t left = (r1 - i + lanes - 1) / lanes;  // rows this thread still owns
+                int cnt;
+                if (left >= MO_KC) {
+                    // full chunk: batches of 8 independent loads in flight per thread
+#pragma unroll
+                    for (int b = 0; b < MO_KC; b += 8) {
+                        T v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) v[u] = x[(i + static_cast<int64_t>(b + u) * lanes) * m + c];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const double d = static_cast<double>(v[u]) - K;
+                            s1 += d;
+                            s2 = fma(d, d, s2);
+                        }
+                    }
+                    cnt = MO_KC;
+                } else {
+                    cnt = static_cast<int>(left);
+                    for (int u = 0; u < cnt; ++u) {
+                        const double d = static_cast<double>(x[(i + static_cast<int64_t>(u) * lanes) * m + c]) - K;
+                        s1 += d;
+                        s2 = fma(d, d, s2);
+                    }
                 }
+                i += static_cast<int64_t>(cnt) * lanes;
                 const double nc = static_cast<double>(cnt);
                 Moment ch;
                 ch.n = nc;
