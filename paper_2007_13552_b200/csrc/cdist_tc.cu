@@ -1,15 +1,317 @@
-// cdist_tc.cu -- tcgen05 3xTF32 distance tile for large feature counts
-// (BASELINE config 4, d = 1024).  Placeholder dispatch until the UMMA kernel
-// lands: nothing is eligible, the FFMA tile in cdist.cu serves every shape.
+// cdist_tc.cu -- tcgen05 3xTF32 distance tiles for large feature counts
+// (BASELINE config 4: 100k x 1024 vs 100k x 1024; north_star (3): tensor cores
+// "only when the feature dimension makes it a real dense contraction").
+//
+// Reference: distance_block / matmul_local (pairwise.cpp:22-33,
+// ndarray.hpp:400-418), place_chunk (tile.hpp:90-107).
+//
+// Persistent CTAs, one per SM, 10 warps:
+//   warp 0      TMA producer: 32-column K chunks of a 128-row X tile and a
+//               256-row Y tile, SWIZZLE_128B K-major, 2-stage ring.
+//   warp 1      TMEM allocator + MMA issuer: per K=8 step three
+//               tcgen05.mma.kind::tf32 (M=128, N=256): hi.hi + hi.lo + lo.hi into
+//               a 128x256 fp32 TMEM accumulator (double-buffered: 512 columns).
+//   warps 2-5   split: lo = x - trunc_tf32(x) for both tiles of each stage (the
+//               tensor core truncates fp32 operands to tf32 -- pinned by
+//               tests/test_gpu_tc.py -- so the raw tile is the hi operand).
+//   warps 6-9   epilogue: tcgen05.ld of each accumulator row, then
+//               d = sqrt(max(xn + yn - 2g, 0)) with streaming stores into the
+//               ld-wide row block at col_off (+ the self block's zero diagonal).
+// The row norms come from the SAME tensor-core path (a diagonal-tile pass), so a
+// row's dot product with itself equals its norm bit for bit and duplicate rows
+// cancel to exactly 0, as in the reference.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace dndc {
 
-bool cdist_tc_eligible(int64_t, int64_t, int64_t) { return false; }
+namespace cdtc {
+constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2;
+constexpr int A_BYTES = BM * BK * 4;   // 16 KB
+constexpr int B_BYTES = BN * BK * 4;   // 32 KB
+constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // raw + lo
+constexpr int OFF_BAR = STAGES * STAGE_BYTES;
+constexpr int NBARS = 3 * STAGES + 4;
+constexpr int SMEM = OFF_BAR + NBARS * 8 + 16 + 1024;  // + alignment slack
+constexpr int THREADS = 320;
+constexpr int TMEM_COLS = 512;
+constexpr int GROUP = 16;  // rasterisation: GROUP x GROUP tile super-blocks
+}  // namespace cdtc
 
-void cdist_tile_tc_f32(dndc_ctx*, const float*, const float*, int64_t, const float*, const float*,
-                       int64_t, int64_t, float*, int64_t, int64_t, int64_t, cudaStream_t) {
-    throw Error(DNDC_EINTERNAL, "cdist_tc: tcgen05 path not built");
+struct CdtcParams {
+    int64_t nx, ny;
+    int m;
+    const float* xn;   // norms (null in NORM mode)
+    const float* yn;
+    float* out;        // distances (DIST) or norms (NORM)
+    int64_t ld, col_off, diag_offset;
+    bool vec;
+};
+
+__device__ __forceinline__ void cdtc_tile_of(int64_t t, int64_t nrb, int64_t ncb, int64_t& rb, int64_t& cb) {
+    using namespace cdtc;
+    const int64_t per_group = static_cast<int64_t>(GROUP) * ncb;  // GROUP row blocks x all column blocks
+    const int64_t g = t / per_group, r = t % per_group;
+    const int64_t rows_in_group = min(static_cast<int64_t>(GROUP), nrb - g * GROUP);
+    rb = g * GROUP + r % rows_in_group;
+    cb = r / rows_in_group;
+}
+
+template <bool NORM>
+__global__ void __launch_bounds__(cdtc::THREADS, 1)
+    cdist_tc_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant__ CUtensorMap mapy, CdtcParams p) {
+    using namespace cdtc;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* full = bars;                 // [STAGES] TMA landed
+    uint64_t* split = bars + STAGES;       // [STAGES] lo written
+    uint64_t* empty = bars + 2 * STAGES;   // [STAGES] MMAs done with the stage
+    uint64_t* tfull = bars + 3 * STAGES;   // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;          // [2] accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBARS);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nrb = ceil_div(p.nx, BM);
+    const int64_t ncb = NORM ? 1 : ceil_div(p.ny, BN);
+    const int64_t ntiles = nrb * ncb;
+    const int kchunks = (p.m + BK - 1) / BK;
+
+    if (warp == 1) {
+        tc::tmem_alloc(tmem_slot, TMEM_COLS);
+        if (lane == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                tc::mbar_init(&full[s], 1);
+                tc::mbar_init(&split[s], 1);
+                tc::mbar_init(&empty[s], 1);
+            }
+            for (int b = 0; b < 2; ++b) {
+                tc::mbar_init(&tfull[b], 1);
+                tc::mbar_init(&tempty[b], 1);
+            }
+            tc::mbar_fence_init();
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    auto stage_ptr = [&](int s) { return smem + s * STAGE_BYTES; };  // A, B, Alo, Blo
+
+    if (warp == 0) {
+        // ------------------------------------------------------- producer
+        if (lane == 0) {
+            tc::tma_prefetch_desc(&mapx);
+            tc::tma_prefetch_desc(&mapy);
+            int64_t g = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int64_t rb, cb;
+                if (NORM) { rb = t; cb = 0; } else cdtc_tile_of(t, nrb, ncb, rb, cb);
+                const int row0 = static_cast<int>(rb * BM);
+                const int col0 = NORM ? row0 : static_cast<int>(cb * BN);
+                for (int kc = 0; kc < kchunks; ++kc, ++g) {
+                    const int s = static_cast<int>(g % STAGES);
+                    if (g >= STAGES) tc::mbar_wait(&empty[s], static_cast<uint32_t>((g / STAGES - 1) & 1));
+                    unsigned char* st = stage_ptr(s);
+                    tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+                    tc::tma_load_2d(st, &mapx, &full[s], kc * BK, row0);
+                    tc::tma_load_2d(st + A_BYTES, &mapy, &full[s], kc * BK, col0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_tf32(BM, BN, 0, 0);
+            int64_t g = 0, tcount = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+                const int b = static_cast<int>(tcount & 1);
+                if (tcount >= 2) tc::mbar_wait(&tempty[b], static_cast<uint32_t>((tcount / 2 - 1) & 1));
+                const uint32_t dt = tmem + b * BN;
+                for (int kc = 0; kc < kchunks; ++kc, ++g) {
+                    const int s = static_cast<int>(g % STAGES);
+                    tc::mbar_wait(&split[s], static_cast<uint32_t>((g / STAGES) & 1));
+                    tc::tc_fence_after();
+                    const uint32_t a = tc::smem_u32(stage_ptr(s));
+                    const uint32_t bsm = a + A_BYTES, alo = a + A_BYTES + B_BYTES, blo = alo + A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < BK / 8; ++k) {
+                        const uint32_t ko = k * 32;  // bytes along K inside the 128-byte swizzle atom
+                        const uint64_t dah = tc::smem_desc(a + ko, 16, 1024, 2);
+                        const uint64_t dal = tc::smem_desc(alo + ko, 16, 1024, 2);
+                        const uint64_t dbh = tc::smem_desc(bsm + ko, 16, 1024, 2);
+                        const uint64_t dbl = tc::smem_desc(blo + ko, 16, 1024, 2);
+                        tc::mma_tf32(dt, dah, dbh, idesc, (kc > 0 || k > 0) ? 1u : 0u);
+                        tc::mma_tf32(dt, dah, dbl, idesc, 1);
+                        tc::mma_tf32(dt, dal, dbh, idesc, 1);
+                    }
+                    tc::mma_commit(&empty[s]);
+                }
+                tc::mma_commit(&tfull[b]);
+            }
+        }
+    } else if (warp < 6) {
+        // ------------------------------------------------------- split warps
+        const int st = threadIdx.x - 64;  // 0..127
+        int64_t g = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int kc = 0; kc < kchunks; ++kc, ++g) {
+                const int s = static_cast<int>(g % STAGES);
+                tc::mbar_wait(&full[s], static_cast<uint32_t>((g / STAGES) & 1));
+                const float4* src = reinterpret_cast<const float4*>(stage_ptr(s));
+                float4* dst = reinterpret_cast<float4*>(stage_ptr(s) + A_BYTES + B_BYTES);
+                constexpr int N4 = (A_BYTES + B_BYTES) / 16;
+#pragma unroll 4
+                for (int i = st; i < N4; i += 128) {
+                    const float4 v = src[i];
+                    float4 l;
+                    l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    dst[i] = l;
+                }
+                tc::fence_async_smem();
+                tc::named_sync(1, 128);
+                if (st == 0) tc::mbar_arrive(&split[s]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------- epilogue warps
+        const int q = warp & 3;             // TMEM lane quarter of this warp
+        const int r = q * 32 + lane;        // accumulator row = TMEM lane
+        int64_t tcount = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+            int64_t rb, cb;
+            if (NORM) { rb = t; cb = 0; } else cdtc_tile_of(t, nrb, ncb, rb, cb);
+            const int64_t row0 = rb * BM, col0 = NORM ? row0 : cb * BN;
+            const int b = static_cast<int>(tcount & 1);
+            tc::mbar_wait(&tfull[b], static_cast<uint32_t>((tcount / 2) & 1));
+            tc::tc_fence_after();
+            const int64_t gi = row0 + r;
+            const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * BN;
+            if (NORM) {
+                // the diagonal of the (X-block, X-block) tile: column r of row r
+                float v[16];
+#pragma unroll 1
+                for (int c16 = 0; c16 < BM / 16; ++c16) {
+                    tc::tmem_ld16(trow + c16 * 16, v);
+                    if (c16 == r / 16 && gi < p.nx) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (i == r % 16) p.out[gi] = v[i];
+                    }
+                }
+            } else {
+                const float xni = gi < p.nx ? __ldg(p.xn + gi) : 0.f;
+                float* orow = p.out + gi * p.ld + p.col_off + col0;
+                const bool full_cols = col0 + BN <= p.ny;
+#pragma unroll 1
+                for (int c16 = 0; c16 < BN / 16; ++c16) {
+                    float v[16];
+                    tc::tmem_ld16(trow + c16 * 16, v);
+                    if (gi >= p.nx) continue;
+                    const int64_t c0 = col0 + c16 * 16;
+                    float d[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float ynj = (c0 + i < p.ny) ? __ldg(p.yn + c0 + i) : 0.f;
+                        const float sq = fmaxf(fmaf(-2.f, v[i], xni + ynj), 0.f);
+                        d[i] = sqrt_approx(sq);
+                        if (p.diag_offset >= 0 && c0 + i == gi + p.diag_offset) d[i] = 0.f;
+                    }
+                    float* o = orow + c16 * 16;
+                    if (p.vec && full_cols) {
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4) st_stream4(o + i, d[i], d[i + 1], d[i + 2], d[i + 3]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (c0 + i < p.ny) st_stream(o + i, d[i]);
+                    }
+                }
+            }
+            tc::tc_fence_before();
+            tc::named_sync(2, 128);
+            if (r == 0) tc::mbar_arrive(&tempty[b]);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// ------------------------------------------------------------------ host
+static int tc_min_m() {
+    const char* v = std::getenv("DNDC_CDIST_TC_MIN_M");
+    return v ? std::atoi(v) : 256;
+}
+
+bool cdist_tc_eligible(int64_t nx, int64_t ny, int64_t m) {
+    return m >= tc_min_m() && m % 4 == 0 && nx >= 128 && ny >= 128;
+}
+
+// Padded view for TMA: row pitch must be a multiple of 16 bytes.
+static const float* tma_view(dndc_ctx* ctx, const char* slot, const float* src, int64_t rows, int64_t m,
+                             cudaStream_t s) {
+    if (m % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) return src;
+    throw Error(DNDC_EINTERNAL, "cdist_tc: unaligned operand");
+}
+
+void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, int64_t nx, const float* y,
+                       const float* yn_unused, int64_t ny, int64_t m, float* out, int64_t ld_out, int64_t col_off,
+                       int64_t diag_offset, cudaStream_t stream) {
+    using namespace cdtc;
+    (void)xn_unused;
+    (void)yn_unused;
+    const float* xa = tma_view(ctx, "cdtc_x", x, nx, m, stream);
+    const float* ya = tma_view(ctx, "cdtc_y", y, ny, m, stream);
+    static bool attr = false;
+    if (!attr) {
+        DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        attr = true;
+    }
+    // norms through the same tensor-core path (diagonal tiles)
+    float* xn = static_cast<float*>(ctx->slot("cdtc_xn", sizeof(float) * std::max<int64_t>(nx, 1)));
+    float* yn = static_cast<float*>(ctx->slot("cdtc_yn", sizeof(float) * std::max<int64_t>(ny, 1)));
+    auto norms = [&](const float* a, int64_t rows, float* dst) {
+        const CUtensorMap ma = make_tmap_2d_f32(a, rows, m, m * 4, BK, BM, true);
+        const CUtensorMap mb = make_tmap_2d_f32(a, rows, m, m * 4, BK, BN, true);
+        CdtcParams np{};
+        np.nx = rows;
+        np.ny = rows;
+        np.m = static_cast<int>(m);
+        np.out = dst;
+        const int grid = static_cast<int>(std::min<int64_t>(ceil_div(rows, BM), ctx->num_sms));
+        cdist_tc_kernel<true><<<grid, THREADS, SMEM, stream>>>(ma, mb, np);
+        DNDC_LAUNCHED(ctx);
+    };
+    norms(xa, nx, xn);
+    if (ya == xa && ny == nx) DNDC_CUDA(cudaMemcpyAsync(yn, xn, sizeof(float) * nx, cudaMemcpyDeviceToDevice, stream));
+    else norms(ya, ny, yn);
+
+    const CUtensorMap mx = make_tmap_2d_f32(xa, nx, m, m * 4, BK, BM, true);
+    const CUtensorMap my = make_tmap_2d_f32(ya, ny, m, m * 4, BK, BN, true);
+    CdtcParams pp{};
+    pp.nx = nx;
+    pp.ny = ny;
+    pp.m = static_cast<int>(m);
+    pp.xn = xn;
+    pp.yn = yn;
+    pp.out = out;
+    pp.ld = ld_out;
+    pp.col_off = col_off;
+    pp.diag_offset = diag_offset;
+    pp.vec = (ld_out % 4 == 0) && (col_off % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    const int64_t tiles = ceil_div(nx, BM) * ceil_div(ny, BN);
+    const int grid = static_cast<int>(std::min<int64_t>(tiles, ctx->num_sms));
+    cdist_tc_kernel<false><<<grid, THREADS, SMEM, stream>>>(mx, my, pp);
+    DNDC_LAUNCHED(ctx);
 }
 
 }  // namespace dndc

