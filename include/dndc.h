@@ -165,6 +165,13 @@ int dndc_kmeans_last_refined(const dndc_ctx* ctx, int64_t* rows_refined);
 int dndc_kmeans_time_assign_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m, int k, int reps,
                                 double* ms_per_launch, double* algorithmic_bytes);
 
+/* Measurement hook: with timing enabled, kmeans_fit records a CUDA event pair
+ * around every assign/accumulate launch inside its graph; last_assign_ms then
+ * returns the summed kernel time of the last fit and the launches it covers
+ * (iterations that ran).  For bench.py's roofline; off by default. */
+int dndc_kmeans_assign_timing(dndc_ctx* ctx, int enable);
+int dndc_kmeans_last_assign_ms(const dndc_ctx* ctx, double* total_ms, int* launches);
+
 /* -------------------------------------------------- A13-A14: moments */
 /* local_moments_axis + combine + mean_axis/var_axis along split axis 0
  * (moments.cpp:33-52, :69-114, :126-140), collective.  Outputs (host, f64):

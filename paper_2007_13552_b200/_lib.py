@@ -11,7 +11,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdndc.so")
+# DNDC_LIB_PATH: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("DNDC_LIB_PATH") or os.path.join(HERE, "libdndc.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "dndc.h")
 
 DNDC_OK, DNDC_EVALUE, DNDC_ETRANSPORT, DNDC_ECUDA, DNDC_EINTERNAL = 0, 1, 2, 3, 4
@@ -65,6 +66,8 @@ _SIGS = {
     "dndc_kmeans_predict_f32": [_P, _P, _i64, _i64, _P, _i32, _P],
     "dndc_kmeans_predict_f64": [_P, _P, _i64, _i64, _P, _i32, _P],
     "dndc_kmeans_last_refined": [_P, C.POINTER(_i64)],
+    "dndc_kmeans_assign_timing": [_P, _i32],
+    "dndc_kmeans_last_assign_ms": [_P, _P, _P],
     "dndc_kmeans_time_assign_f32": [_P, _P, _i64, _i64, _i32, _i32, _P, _P],
     "dndc_moments_axis0_f32": [_P, _P, _i64, _i64, _P, _P, _P],
     "dndc_moments_axis0_f64": [_P, _P, _i64, _i64, _P, _P, _P],

@@ -50,10 +50,22 @@ constexpr unsigned FULL = 0xffffffffu;
 struct KMeansState {
     cudaGraphExec_t exec = nullptr;
     std::string key;
+    // dndc_kmeans_assign_timing: event pairs recorded around every assign
+    // launch inside the fit graph (external event nodes)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;
+    double assign_ms = 0.0;
+    int assign_launches = 0;
 };
+
+static void free_events(KMeansState* st) {
+    for (cudaEvent_t e : st->ev) cudaEventDestroy(e);
+    st->ev.clear();
+}
 
 void destroy_kmeans_state(KMeansState* st) {
     if (!st) return;
+    free_events(st);
     if (st->exec) cudaGraphExecDestroy(st->exec);
     delete st;
 }
@@ -75,6 +87,7 @@ struct KmBuffers {
     double* pre;       // validation partials
     float* ctab;       // K*D + K constant-bank layout of the fp32 table
     unsigned long long* refined;
+    double* running;   // S running sums/counts of the delta iterations
 };
 
 static int dpad_of(int m) { return (m + 3) / 4 * 4; }
@@ -446,6 +459,8 @@ struct SmallParams {
     const double* xabs;   // max |x_e| of the shard
     double* partials;     // null: predict only
     int32_t* labels;
+    const int8_t* prev;   // delta mode: last iteration's labels (partials = sum deltas)
+    int8_t* lab8;         // this iteration's labels (fit), or null
     unsigned long long* refined;
     const int* done;
 };
@@ -485,6 +500,29 @@ __device__ __forceinline__ void bulk_load(float* dst, const float* src, uint32_t
             : "memory");
 }
 
+// Same, plus a second byte segment (the tile's previous labels) on the same barrier.
+__device__ __forceinline__ void bulk_load2(float* dst, const float* src, uint32_t bytes, int8_t* dst2,
+                                           const int8_t* src2, uint32_t bytes2, uint64_t* bar) {
+    const uint32_t body = bytes & ~15u, body2 = bytes2 & ~15u;
+    for (uint32_t b = body; b < bytes; b += 4) dst[b / 4] = src[b / 4];
+    for (uint32_t b = body2; b < bytes2; ++b) dst2[b] = src2[b];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(body + body2)
+                 : "memory");
+    if (body)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(dst)),
+            "l"(src), "r"(body), "r"(smem_u32(bar))
+            : "memory");
+    if (body2)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(dst2)),
+            "l"(src2), "r"(body2), "r"(smem_u32(bar))
+            : "memory");
+}
+
 // CTA shape of the small kernel: 128 threads (4 warps), each thread deciding
 // KS_R rows per tile (KS_R * 128-row tiles): the constant-bank operands, the
 // per-tile scan and the per-cluster loops are amortised over more rows while
@@ -493,8 +531,16 @@ constexpr int KS_THREADS = 128;
 constexpr int KS_WARPS = KS_THREADS / 32;
 constexpr int KS_R = 2;
 constexpr int KS_TILE = KS_THREADS * KS_R;
+#ifdef KS_STAGES_OVR
+constexpr int KS_STAGES = KS_STAGES_OVR;
+#else
 constexpr int KS_STAGES = 2;
+#endif
+#ifdef KS_MIN_CTAS_OVR
+constexpr int KS_MIN_CTAS = KS_MIN_CTAS_OVR;
+#else
 constexpr int KS_MIN_CTAS = 4;
+#endif
 constexpr int KS_VW = KS_WARPS * KS_R;  // 32-row groups per tile
 
 template <int D, int K, int SLOT>
@@ -509,19 +555,34 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* tiles = reinterpret_cast<float*>(smem_raw);                 // S x TILE x D
-    float* sorted = tiles + S * TILE * D;                              // TILE x D
-    int* cnt = reinterpret_cast<int*>(sorted + TILE * D);              // VW x K
-    uint64_t* bars = reinterpret_cast<uint64_t*>(cnt + ((VW * K + 1) & ~1));
+    int8_t* labs = reinterpret_cast<int8_t*>(tiles + S * TILE * D);    // S x TILE previous labels (delta)
+    double* wacc = reinterpret_cast<double*>(labs + S * TILE);         // W x 2 x K x D (delta mode)
+    int* cnt = reinterpret_cast<int*>(wacc + W * 2 * KD);              // VW x K
+    unsigned* consumed = reinterpret_cast<unsigned*>(cnt + VW * K);    // S (delta mode)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(consumed + ((VW * K + S + 1) & ~1) - VW * K);
 
     const float* CT = c_km_table + SLOT * KS_TABLE;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const float tau = 4.f * static_cast<float>(D + 3) * 0x1.0p-24f *
                       (p.bounds[1] + 2.f * sqrtf(static_cast<float>(D)) * static_cast<float>(*p.xabs) * p.bounds[0]);
+#ifdef KS_EXP_NOREFINE
+    const float tau_used = 0.f;  // timing experiment only
+#else
+    const float tau_used = tau;
+#endif
+#ifdef KS_EXP_NOPHASE2
+    const bool accumulate = false;  // timing experiment only
+#else
     const bool accumulate = p.partials != nullptr;
+#endif
+    const bool delta = accumulate && p.prev != nullptr;
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (delta)
+        for (int e = tid; e < W * 2 * KD; e += KS_THREADS) wacc[e] = 0.0;
+    if (tid < S) consumed[tid] = 0u;
     __syncthreads();
 
     const int64_t ntiles = ceil_div(p.n, TILE);
@@ -529,11 +590,18 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
     auto issue = [&](int64_t it) {
         const int64_t tile = blockIdx.x + it * gridDim.x;
         const int64_t rows = min(static_cast<int64_t>(TILE), p.n - tile * TILE);
-        bulk_load(tiles + (it % S) * TILE * D, p.x + tile * TILE * D, static_cast<uint32_t>(rows * D * 4),
-                  &bars[it % S]);
+        if (delta)
+            bulk_load2(tiles + (it % S) * TILE * D, p.x + tile * TILE * D, static_cast<uint32_t>(rows * D * 4),
+                       labs + (it % S) * TILE, p.prev + tile * TILE, static_cast<uint32_t>(rows), &bars[it % S]);
+        else
+            bulk_load(tiles + (it % S) * TILE * D, p.x + tile * TILE * D, static_cast<uint32_t>(rows * D * 4),
+                      &bars[it % S]);
     };
+    // full mode refills stage (it-1)%S mid-tile (S-1 tiles ahead); delta mode
+    // refills the stage it just finished at the end of the tile (S tiles ahead)
+    const int ahead = delta ? S : S - 1;
     if (tid == 0)
-        for (int s = 0; s < S - 1 && s < my_tiles; ++s) issue(s);
+        for (int s = 0; s < ahead && s < my_tiles; ++s) issue(s);
 
     long long count_acc = 0;  // lane j < K of warp 0: rows of cluster j
     unsigned long long refined = 0;
@@ -542,23 +610,30 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
 #pragma unroll
     for (int jj = 0; jj < JW; ++jj) wsum[jj] = make_double2(0.0, 0.0);
 
+    int cnt_delta = 0;  // delta mode, lane j < K: net rows gained by cluster j
     for (int64_t it = 0; it < my_tiles; ++it) {
         const int64_t row0 = (blockIdx.x + it * gridDim.x) * TILE;
         const float* xt = tiles + (it % S) * TILE * D;
         mbar_wait(&bars[it % S], static_cast<uint32_t>((it / S) & 1));
+        int prevl[R];
+        if (delta) {
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                const int row = tid + h * KS_THREADS;
+                prevl[h] = row0 + row < p.n ? static_cast<int>(labs[(it % S) * TILE + row]) : -1;
+            }
+        }
 
         // ---------------- phase 1: rows tid + h * 128 (h < R), lane = row
-        float xv[R][D];
+        // scores in feature pairs: one FFMA2 per two features, the centroid
+        // pair broadcast from uniform registers (constant bank)
+        float2 xv[R][L];
         int label[R];
 #pragma unroll
         for (int h = 0; h < R; ++h) {
             const int row = tid + h * KS_THREADS;
 #pragma unroll
-            for (int f = 0; f < D; f += 2) {
-                const float2 v = *reinterpret_cast<const float2*>(xt + row * D + f);
-                xv[h][f] = v.x;
-                xv[h][f + 1] = v.y;
-            }
+            for (int f = 0; f < L; ++f) xv[h][f] = *reinterpret_cast<const float2*>(xt + row * D + 2 * f);
         }
         {
             float b1[R], b2[R];
@@ -569,24 +644,34 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
                 b2[h] = FLT_MAX;
                 i1[h] = 0;
             }
+            // JG clusters x R rows of independent FFMA2 chains at a time
+            constexpr int JG = K % 4 == 0 ? 4 : 1;
 #pragma unroll
-            for (int j = 0; j < K; ++j) {
-                float sc[R];
+            for (int j0 = 0; j0 < K; j0 += JG) {
+                float2 sp[JG][R];
 #pragma unroll
-                for (int h = 0; h < R; ++h) sc[h] = CT[KD + j];
+                for (int u = 0; u < JG; ++u)
 #pragma unroll
-                for (int f = 0; f < D; ++f) {
-                    const float c = CT[j * D + f];
+                    for (int h = 0; h < R; ++h) sp[u][h] = make_float2(CT[KD + j0 + u], 0.f);
 #pragma unroll
-                    for (int h = 0; h < R; ++h) sc[h] = fmaf(xv[h][f], c, sc[h]);
+                for (int f = 0; f < L; ++f) {
+#pragma unroll
+                    for (int u = 0; u < JG; ++u) {
+                        const float2 c = make_float2(CT[(j0 + u) * D + 2 * f], CT[(j0 + u) * D + 2 * f + 1]);
+#pragma unroll
+                        for (int h = 0; h < R; ++h) sp[u][h] = ffma2(xv[h][f], c, sp[u][h]);
+                    }
                 }
 #pragma unroll
-                for (int h = 0; h < R; ++h) {
-                    const bool lt = sc[h] < b1[h];
-                    b2[h] = fminf(b2[h], fmaxf(b1[h], sc[h]));
-                    b1[h] = fminf(b1[h], sc[h]);
-                    i1[h] = lt ? j : i1[h];
-                }
+                for (int u = 0; u < JG; ++u)
+#pragma unroll
+                    for (int h = 0; h < R; ++h) {
+                        const float sc = sp[u][h].x + sp[u][h].y;
+                        const bool lt = sc < b1[h];
+                        b2[h] = fminf(b2[h], fmaxf(b1[h], sc));
+                        b1[h] = fminf(b1[h], sc);
+                        i1[h] = lt ? j0 + u : i1[h];
+                    }
             }
 #pragma unroll
             for (int h = 0; h < R; ++h) {
@@ -594,13 +679,65 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
                 label[h] = K;  // rows past the end sort last
                 if (row0 + row < p.n) {
                     label[h] = i1[h];
-                    if (K > 1 && !(b2[h] - b1[h] > tau)) {
+                    if (K > 1 && !(b2[h] - b1[h] > tau_used)) {
                         label[h] = ref_argmin<float>(xt + row * D, D, p.c64, p.cn64, K);
                         ++refined;
                     }
                     if (p.labels) p.labels[row0 + row] = label[h];
+                    if (p.lab8) p.lab8[row0 + row] = static_cast<int8_t>(label[h]);
                 }
             }
+        }
+        if (delta) {
+            // ---------------- phase 2 (delta mode): only rows whose label changed
+            // since the last iteration move their x from the old cluster's sums
+            // to the new one's; two rows per step (one per half-warp, each with
+            // its own f64 accumulator copy), in row order -- deterministic.
+            const int half = lane >> 4, hq = lane & 15;
+            double* acc = wacc + (warp * 2 + half) * KD;
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                unsigned mask = __ballot_sync(FULL, label[h] < K && label[h] != prevl[h]);
+                while (mask) {
+                    const int bA = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const int bB = mask ? __ffs(mask) - 1 : bA;
+                    const bool hasB = mask != 0u;
+                    mask &= mask - 1;
+                    const int nA = __shfl_sync(FULL, label[h], bA), oA = __shfl_sync(FULL, prevl[h], bA);
+                    const int nB = __shfl_sync(FULL, label[h], bB), oB = __shfl_sync(FULL, prevl[h], bB);
+                    if (lane < K)
+                        cnt_delta += (lane == nA) - (lane == oA) + (hasB ? (lane == nB) - (lane == oB) : 0);
+                    const int b = half ? bB : bA, nl = half ? nB : nA, ol = half ? oB : oA;
+                    if (hq < L && (half == 0 || hasB)) {
+                        const float2 v =
+                            *reinterpret_cast<const float2*>(xt + (h * KS_THREADS + warp * 32 + b) * D + 2 * hq);
+                        const double vx = static_cast<double>(v.x), vy = static_cast<double>(v.y);
+                        double2* an = reinterpret_cast<double2*>(acc + nl * D + 2 * hq);
+                        double2 t = *an;
+                        t.x += vx;
+                        t.y += vy;
+                        *an = t;
+                        if (ol >= 0) {
+                            double2* ao = reinterpret_cast<double2*>(acc + ol * D + 2 * hq);
+                            double2 u = *ao;
+                            u.x -= vx;
+                            u.y -= vy;
+                            *ao = u;
+                        }
+                    }
+                }
+            }
+            // the last warp done with this stage refills it (no CTA barrier)
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned done = atomicAdd(&consumed[it % S], 1u);
+                if (done == W - 1) {
+                    consumed[it % S] = 0u;
+                    if (it + S < my_tiles) issue(it + S);
+                }
+            }
+            continue;
         }
         if (!accumulate) {
             __syncthreads();  // every warp is done with the previous tile's stage
@@ -648,14 +785,15 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
         start -= total;
         if (warp == 0 && lane < K) count_acc += total;
 
-        // ---------------- phase 2b: scatter rows into label order
+        // ---------------- phase 2b: scatter rows into label order, in place:
+        // every row of this stage is in registers (barrier above)
+        float* sorted = const_cast<float*>(xt);
 #pragma unroll
         for (int h = 0; h < R; ++h) {
             const int pos = __shfl_sync(FULL, start + before[h], label[h] < K ? label[h] : 0) + rank[h];
             if (label[h] < K) {
 #pragma unroll
-                for (int f = 0; f < D; f += 2)
-                    *reinterpret_cast<float2*>(sorted + pos * D + f) = make_float2(xv[h][f], xv[h][f + 1]);
+                for (int f = 0; f < L; ++f) *reinterpret_cast<float2*>(sorted + pos * D + 2 * f) = xv[h][f];
             }
         }
         __syncthreads();
@@ -670,15 +808,26 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
             // f64 accumulation straight from the fp32 rows: the run sums carry
             // no fp32 rounding, so the centroids track the reference's to ~1e-16
             // and near-tie flips of its trajectory stay ~1e6x rarer
-            double2 part = make_double2(0.0, 0.0);
+            double2 part = make_double2(0.0, 0.0), part2 = make_double2(0.0, 0.0);
             if (g < G) {
                 const float* src = sorted + 2 * q;
-#pragma unroll 4
-                for (int r = r0 + g; r < r1; r += G) {
+                int r = r0 + g;
+#pragma unroll 2
+                for (; r + G < r1; r += 2 * G) {  // two independent f64 chains
+                    const float2 v = *reinterpret_cast<const float2*>(src + r * D);
+                    const float2 u = *reinterpret_cast<const float2*>(src + (r + G) * D);
+                    part.x += static_cast<double>(v.x);
+                    part.y += static_cast<double>(v.y);
+                    part2.x += static_cast<double>(u.x);
+                    part2.y += static_cast<double>(u.y);
+                }
+                if (r < r1) {
                     const float2 v = *reinterpret_cast<const float2*>(src + r * D);
                     part.x += static_cast<double>(v.x);
                     part.y += static_cast<double>(v.y);
                 }
+                part.x += part2.x;
+                part.y += part2.y;
             }
             // tree over the G groups; a source beyond the last group contributes nothing
 #pragma unroll
@@ -699,6 +848,23 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
     if (!accumulate) return;
     const int Sst = KD + K;
     double* out = p.partials + static_cast<int64_t>(blockIdx.x) * Sst;
+    if (delta) {
+        if (lane < K) cnt[warp * K + lane] = cnt_delta;
+        __syncthreads();
+        for (int e = tid; e < KD; e += KS_THREADS) {
+            double v = 0.0;
+#pragma unroll
+            for (int c = 0; c < 2 * W; ++c) v += wacc[c * KD + e];
+            out[e] = v;
+        }
+        if (tid < K) {
+            int c = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) c += cnt[w * K + tid];
+            out[KD + tid] = static_cast<double>(c);
+        }
+        return;
+    }
 #pragma unroll
     for (int jj = 0; jj < JW; ++jj) {
         const int j = warp + jj * W;
@@ -709,8 +875,8 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
 
 template <int D, int K>
 static size_t small_smem() {
-    return static_cast<size_t>(KS_STAGES + 1) * KS_TILE * D * 4 +
-           static_cast<size_t>((KS_VW * K + 1) & ~1) * 4 + KS_STAGES * 8;
+    return static_cast<size_t>(KS_STAGES) * KS_TILE * (D * 4 + 1) + static_cast<size_t>(KS_WARPS) * 2 * K * D * 8 +
+           static_cast<size_t>((KS_VW * K + KS_STAGES + 1) & ~1) * 4 + KS_STAGES * 8;
 }
 
 #include "kmeans_tc.cuh"
@@ -813,7 +979,7 @@ __global__ void derive_tables_kernel(int k, int d, int dpad, const double* c64, 
 // the reference's sequential per-cluster loops (displacement, norms).
 constexpr int UPD_MAX_KD = 8192;
 __global__ void __launch_bounds__(256) kmeans_update_kernel(int k, int d, int dpad, int world, const double* gathered,
-                                     double* c64, double* cn64, float* ct, float* cn32, float* ctab, float* bounds,
+                                     double* running, int accum, double* c64, double* cn64, float* ct, float* cn32, float* ctab, float* bounds,
                                      const double* sx2, double* trace, double* disp, int* flags,
                                      int iter, double tol) {
     if (flags[0]) return;
@@ -826,6 +992,12 @@ __global__ void __launch_bounds__(256) kmeans_update_kernel(int k, int d, int dp
         for (int e = threadIdx.x; e < S; e += blockDim.x) {
             double v = 0.0;
             for (int r = 0; r < world; ++r) v += gathered[static_cast<int64_t>(r) * S + e];
+            // delta iterations (small kernel): the stats are changes since the
+            // last iteration, added to the running per-cluster sums and counts
+            if (running) {
+                if (accum) v += running[e];
+                running[e] = v;
+            }
             upd[e < KD ? e : KD + e] = v;
             if (e < KD) upd[KD + e] = c64[e];
         }
@@ -976,6 +1148,7 @@ static KmBuffers buffers(dndc_ctx* ctx, int k, int m, int max_iter, int G) {
     b.pre = static_cast<double*>(ctx->slot("km_pre", sizeof(double) * 3 * 4096));
     b.ctab = static_cast<float*>(ctx->slot("km_ctab", sizeof(float) * (k * m + k)));
     b.refined = static_cast<unsigned long long*>(ctx->slot("km_refined", sizeof(unsigned long long)));
+    b.running = static_cast<double*>(ctx->slot("km_running", sizeof(double) * S));
     return b;
 }
 
@@ -1074,7 +1247,7 @@ struct Assigner {
     int grid() const { return (small || tc) ? sgrid : gen.grid; }
 
     void launch(const KmBuffers& b, const T* x, int64_t n, int d, int k, bool accumulate, int32_t* labels,
-                bool use_done, cudaStream_t st) const {
+                bool use_done, cudaStream_t st, const int8_t* prev = nullptr, int8_t* lab8 = nullptr) const {
         if (tc) {
             TcParams tp{};
             tp.n = n;
@@ -1099,6 +1272,8 @@ struct Assigner {
             sp.xabs = b.sx2 + 3;
             sp.partials = accumulate ? b.partials : nullptr;
             sp.labels = labels;
+            sp.prev = prev;
+            sp.lab8 = lab8;
             sp.refined = b.refined;
             sp.done = use_done ? b.flags : nullptr;
             sfn<<<sgrid, KS_THREADS, ssmem, st>>>(sp);
@@ -1309,23 +1484,37 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     derive_tables(ctx, b, k, m);
 
     // ---- the Lloyd loop, one graph per (shape, buffers, max_iter, tol)
+    // small kernel: iteration 0 accumulates full sums and records int8 labels;
+    // later iterations accumulate only the rows whose label changed (deltas)
+    int8_t* lab8 = A.small ? static_cast<int8_t*>(ctx->slot("km_lab8", std::max<int64_t>(n_local, 1))) : nullptr;
+    if (!ctx->km) ctx->km = new KMeansState();
+    KMeansState* km = ctx->km;
+    if (km->timing && km->ev.size() < 2 * static_cast<size_t>(max_iter)) {
+        free_events(km);
+        km->ev.resize(2 * static_cast<size_t>(max_iter));
+        for (auto& e : km->ev) DNDC_CUDA(cudaEventCreate(&e));
+        km->key.clear();
+    }
     auto record = [&](cudaStream_t st) {
         kmeans_reset_kernel<<<1, 1, 0, st>>>(b.flags, b.refined);
         for (int it = 0; it < max_iter; ++it) {
-            A.launch(b, x_local, n_local, m, k, true, nullptr, true, st);
+            const bool delta = A.small && it > 0;
+            if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[2 * it], st, cudaEventRecordExternal));
+            A.launch(b, x_local, n_local, m, k, true, nullptr, true, st, delta ? lab8 : nullptr, lab8);
+            if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[2 * it + 1], st, cudaEventRecordExternal));
             reduce_partials_kernel<<<S, 256, 0, st>>>(b.partials, A.grid(), S, b.stats, b.flags);
             if (ctx->world > 1) allgather_f64(ctx, b.stats, b.gathered, S, st);
             kmeans_update_kernel<<<1, 256, update_smem(k, m), st>>>(k, m, dpad_of(m), ctx->world,
-                                                   ctx->world > 1 ? b.gathered : b.stats, b.c64, b.cn64,
+                                                   ctx->world > 1 ? b.gathered : b.stats,
+                                                   A.small ? b.running : nullptr, delta ? 1 : 0, b.c64, b.cn64,
                                                    b.ct, b.cn32, b.ctab, b.bounds, b.sx2, b.trace, b.disp, b.flags,
                                                    it, tol);
         }
     };
-    if (!ctx->km) ctx->km = new KMeansState();
     cudaStream_t gs = ctx->own_stream;
     char keybuf[256];
-    std::snprintf(keybuf, sizeof(keybuf), "%p/%lld/%d/%d/%d/%.17g/%p/%d/%d", (const void*)x_local,
-                  (long long)n_local, m, k, max_iter, tol, (void*)s, A.grid(), ctx->world);
+    std::snprintf(keybuf, sizeof(keybuf), "%p/%lld/%d/%d/%d/%.17g/%p/%d/%d/%d", (const void*)x_local,
+                  (long long)n_local, m, k, max_iter, tol, (void*)s, A.grid(), ctx->world, km->timing ? 1 : 0);
     const std::string key = std::string(sizeof(T) == 4 ? "f32/" : "f64/") + keybuf;
     if (ctx->km->key != key || !ctx->km->exec) {
         if (ctx->km->exec) {
@@ -1373,6 +1562,17 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     const int iters = flags[1];
     std::memcpy(trace_host, h + sizeof(double) * k * m, sizeof(double) * max_iter);
     *iters_host = iters;
+    if (km->timing) {
+        // iterations past convergence return at once; only the ones that ran count
+        double tot = 0.0;
+        for (int it = 0; it < iters; ++it) {
+            float t = 0.f;
+            DNDC_CUDA(cudaEventElapsedTime(&t, km->ev[2 * it], km->ev[2 * it + 1]));
+            tot += t;
+        }
+        km->assign_ms = tot;
+        km->assign_launches = iters;
+    }
     ctx->last_refined = static_cast<int64_t>(
         *reinterpret_cast<const unsigned long long*>(h + sizeof(double) * (k * m + max_iter) + 16));
 }
@@ -1506,6 +1706,20 @@ int dndc_kmeans_predict_f64(dndc_ctx* ctx, const double* x, int64_t n, int64_t m
 int dndc_kmeans_time_assign_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m, int k, int reps,
                                 double* ms_per_launch, double* algorithmic_bytes) {
     return guard([&] { dndc::time_assign(ctx, x, n, m, k, reps, ms_per_launch, algorithmic_bytes); });
+}
+
+int dndc_kmeans_assign_timing(dndc_ctx* ctx, int enable) {
+    return guard([&] {
+        if (!ctx->km) ctx->km = new dndc::KMeansState();
+        if (ctx->km->timing != (enable != 0)) ctx->km->key.clear();  // re-record the graph
+        ctx->km->timing = enable != 0;
+    });
+}
+
+int dndc_kmeans_last_assign_ms(const dndc_ctx* ctx, double* total_ms, int* launches) {
+    *total_ms = ctx->km ? ctx->km->assign_ms : 0.0;
+    *launches = ctx->km ? ctx->km->assign_launches : 0;
+    return DNDC_OK;
 }
 
 int dndc_kmeans_last_refined(const dndc_ctx* ctx, int64_t* rows_refined) {

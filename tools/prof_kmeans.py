@@ -9,7 +9,8 @@ comm = dnd.Communicator(0)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 5_000_000
 m = int(sys.argv[2]) if len(sys.argv) > 2 else 18
 k = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+iters = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 x = dnd.random_uniform((n, m), 0, 42, comm)
-model = dnd.kmeans_fit(x, k, 3, 0.0, 42)
+model = dnd.kmeans_fit(x, k, iters, 0.0, 42)
 torch.cuda.synchronize()
 print("inertia", model.inertia_trace)
