@@ -11,6 +11,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # the compute API loads libdndc.so on first use and raises if it is absent
-    from . import api
+    import importlib
 
-    return getattr(api, name)
+    api = importlib.import_module(__name__ + ".api")
+    return api if name == "api" else getattr(api, name)

@@ -527,9 +527,17 @@ __device__ __forceinline__ void bulk_load2(float* dst, const float* src, uint32_
 // KS_R rows per tile (KS_R * 128-row tiles): the constant-bank operands, the
 // per-tile scan and the per-cluster loops are amortised over more rows while
 // the per-tile barriers stay cheap (4 warps).
+#ifdef KS_THREADS_OVR
+constexpr int KS_THREADS = KS_THREADS_OVR;
+#else
 constexpr int KS_THREADS = 128;
+#endif
 constexpr int KS_WARPS = KS_THREADS / 32;
+#ifdef KS_R_OVR
+constexpr int KS_R = KS_R_OVR;
+#else
 constexpr int KS_R = 2;
+#endif
 constexpr int KS_TILE = KS_THREADS * KS_R;
 #ifdef KS_STAGES_OVR
 constexpr int KS_STAGES = KS_STAGES_OVR;
@@ -542,6 +550,49 @@ constexpr int KS_MIN_CTAS = KS_MIN_CTAS_OVR;
 constexpr int KS_MIN_CTAS = 4;
 #endif
 constexpr int KS_VW = KS_WARPS * KS_R;  // 32-row groups per tile
+
+// fp32 top-2 of R rows held in registers as feature pairs: one FFMA2 per two
+// features with the centroid pair broadcast from the constant bank (uniform
+// registers), JG clusters x R rows of independent chains at a time.
+template <int D, int K, int R>
+__device__ __forceinline__ void small_top2(const float2 (&xv)[R][D / 2], const float* CT, float (&b1)[R],
+                                           float (&b2)[R], int (&i1)[R]) {
+    constexpr int L = D / 2, KD = K * D;
+    constexpr int JG = K % 4 == 0 ? 4 : 1;
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        b1[h] = FLT_MAX;
+        b2[h] = FLT_MAX;
+        i1[h] = 0;
+    }
+#pragma unroll
+    for (int j0 = 0; j0 < K; j0 += JG) {
+        float2 sp[JG][R];
+#pragma unroll
+        for (int u = 0; u < JG; ++u)
+#pragma unroll
+            for (int h = 0; h < R; ++h) sp[u][h] = make_float2(CT[KD + j0 + u], 0.f);
+#pragma unroll
+        for (int f = 0; f < L; ++f) {
+#pragma unroll
+            for (int u = 0; u < JG; ++u) {
+                const float2 c = make_float2(CT[(j0 + u) * D + 2 * f], CT[(j0 + u) * D + 2 * f + 1]);
+#pragma unroll
+                for (int h = 0; h < R; ++h) sp[u][h] = ffma2(xv[h][f], c, sp[u][h]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < JG; ++u)
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                const float sc = sp[u][h].x + sp[u][h].y;
+                const bool lt = sc < b1[h];
+                b2[h] = fminf(b2[h], fmaxf(b1[h], sc));
+                b1[h] = fminf(b1[h], sc);
+                i1[h] = lt ? j0 + u : i1[h];
+            }
+    }
+}
 
 template <int D, int K, int SLOT>
 __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(SmallParams p) {
@@ -556,8 +607,10 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* tiles = reinterpret_cast<float*>(smem_raw);                 // S x TILE x D
     int8_t* labs = reinterpret_cast<int8_t*>(tiles + S * TILE * D);    // S x TILE previous labels (delta)
-    double* wacc = reinterpret_cast<double*>(labs + S * TILE);         // W x 2 x K x D (delta mode)
-    int* cnt = reinterpret_cast<int*>(wacc + W * 2 * KD);              // VW x K
+    double* wacc = reinterpret_cast<double*>(labs + S * TILE);         // W x K x D sums of changes (delta)
+    float* scr = reinterpret_cast<float*>(wacc + W * KD);              // W x 32 x D changed rows (delta)
+    int* scl = reinterpret_cast<int*>(scr + W * 32 * D);               // W x 32 x 2 their new/old labels
+    int* cnt = reinterpret_cast<int*>(scl + W * 64);                   // VW x K
     unsigned* consumed = reinterpret_cast<unsigned*>(cnt + VW * K);    // S (delta mode)
     uint64_t* bars = reinterpret_cast<uint64_t*>(consumed + ((VW * K + S + 1) & ~1) - VW * K);
 
@@ -581,7 +634,7 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (delta)
-        for (int e = tid; e < W * 2 * KD; e += KS_THREADS) wacc[e] = 0.0;
+        for (int e = tid; e < W * KD; e += KS_THREADS) wacc[e] = 0.0;
     if (tid < S) consumed[tid] = 0u;
     __syncthreads();
 
@@ -598,7 +651,7 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
                       &bars[it % S]);
     };
     // full mode refills stage (it-1)%S mid-tile (S-1 tiles ahead); delta mode
-    // refills the stage it just finished at the end of the tile (S tiles ahead)
+    // refills a stage as soon as every warp has its rows in registers (S ahead)
     const int ahead = delta ? S : S - 1;
     if (tid == 0)
         for (int s = 0; s < ahead && s < my_tiles; ++s) issue(s);
@@ -615,13 +668,92 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
         const int64_t row0 = (blockIdx.x + it * gridDim.x) * TILE;
         const float* xt = tiles + (it % S) * TILE * D;
         mbar_wait(&bars[it % S], static_cast<uint32_t>((it / S) & 1));
-        int prevl[R];
         if (delta) {
+            // ---------------- delta mode: rows to registers, then the stage is
+            // handed back at once (the last warp to finish reading refills it),
+            // so two tiles per CTA stay in flight while this one is scored
+            float2 xv[R][L];
+            int prevl[R], label[R];
 #pragma unroll
             for (int h = 0; h < R; ++h) {
                 const int row = tid + h * KS_THREADS;
+#pragma unroll
+                for (int f = 0; f < L; ++f) xv[h][f] = *reinterpret_cast<const float2*>(xt + row * D + 2 * f);
                 prevl[h] = row0 + row < p.n ? static_cast<int>(labs[(it % S) * TILE + row]) : -1;
             }
+            __threadfence_block();
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned done = atomicAdd(&consumed[it % S], 1u);
+                if (done == W - 1) {
+                    consumed[it % S] = 0u;
+                    if (it + S < my_tiles) issue(it + S);
+                }
+            }
+            {
+                float b1[R], b2[R];
+                int i1[R];
+#ifdef KS_EXP_NOSCORE
+#pragma unroll
+                for (int h = 0; h < R; ++h) {  // timing experiment only: stream, no scores
+                    float a = 0.f;
+#pragma unroll
+                    for (int f = 0; f < L; ++f) a += xv[h][f].x + xv[h][f].y;
+                    b1[h] = a;
+                    b2[h] = a + 1e30f;
+                    i1[h] = prevl[h] < 0 ? 0 : prevl[h];
+                }
+#else
+                small_top2<D, K, R>(xv, CT, b1, b2, i1);
+#endif
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                    const int64_t gr = row0 + tid + h * KS_THREADS;
+                    label[h] = K;
+                    if (gr < p.n) {
+                        label[h] = i1[h];
+                        if (K > 1 && !(b2[h] - b1[h] > tau_used)) {
+                            // the stage may be refilled already: the row from global (L2)
+                            label[h] = ref_argmin<float>(p.x + gr * D, D, p.c64, p.cn64, K);
+                            ++refined;
+                        }
+                        if (p.lab8) p.lab8[gr] = static_cast<int8_t>(label[h]);
+                    }
+                }
+            }
+            // changed rows: compacted into the warp's scratch, then moved from
+            // the old cluster's sums to the new one's, lane = feature, in row
+            // order (deterministic)
+            float* wscr = scr + warp * 32 * D;
+            int* wscl = scl + warp * 64;
+            double* acc = wacc + warp * KD;
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                const bool ch = label[h] < K && label[h] != prevl[h];
+                const unsigned mask = __ballot_sync(FULL, ch);
+                if (mask == 0u) continue;
+                if (ch) {
+                    const int pos = __popc(mask & ((1u << lane) - 1u));
+#pragma unroll
+                    for (int f = 0; f < L; ++f) *reinterpret_cast<float2*>(wscr + pos * D + 2 * f) = xv[h][f];
+                    wscl[2 * pos] = label[h];
+                    wscl[2 * pos + 1] = prevl[h];
+                }
+                __syncwarp();
+                const int nch = __popc(mask);
+                for (int c = 0; c < nch; ++c) {
+                    const int nl = wscl[2 * c], ol = wscl[2 * c + 1];
+                    if (lane < K) cnt_delta += (lane == nl) - (lane == ol);
+#pragma unroll
+                    for (int f = lane; f < D; f += 32) {
+                        const double v = static_cast<double>(wscr[c * D + f]);
+                        acc[nl * D + f] += v;
+                        if (ol >= 0) acc[ol * D + f] -= v;
+                    }
+                }
+                __syncwarp();
+            }
+            continue;
         }
 
         // ---------------- phase 1: rows tid + h * 128 (h < R), lane = row
@@ -638,41 +770,7 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
         {
             float b1[R], b2[R];
             int i1[R];
-#pragma unroll
-            for (int h = 0; h < R; ++h) {
-                b1[h] = FLT_MAX;
-                b2[h] = FLT_MAX;
-                i1[h] = 0;
-            }
-            // JG clusters x R rows of independent FFMA2 chains at a time
-            constexpr int JG = K % 4 == 0 ? 4 : 1;
-#pragma unroll
-            for (int j0 = 0; j0 < K; j0 += JG) {
-                float2 sp[JG][R];
-#pragma unroll
-                for (int u = 0; u < JG; ++u)
-#pragma unroll
-                    for (int h = 0; h < R; ++h) sp[u][h] = make_float2(CT[KD + j0 + u], 0.f);
-#pragma unroll
-                for (int f = 0; f < L; ++f) {
-#pragma unroll
-                    for (int u = 0; u < JG; ++u) {
-                        const float2 c = make_float2(CT[(j0 + u) * D + 2 * f], CT[(j0 + u) * D + 2 * f + 1]);
-#pragma unroll
-                        for (int h = 0; h < R; ++h) sp[u][h] = ffma2(xv[h][f], c, sp[u][h]);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < JG; ++u)
-#pragma unroll
-                    for (int h = 0; h < R; ++h) {
-                        const float sc = sp[u][h].x + sp[u][h].y;
-                        const bool lt = sc < b1[h];
-                        b2[h] = fminf(b2[h], fmaxf(b1[h], sc));
-                        b1[h] = fminf(b1[h], sc);
-                        i1[h] = lt ? j0 + u : i1[h];
-                    }
-            }
+            small_top2<D, K, R>(xv, CT, b1, b2, i1);
 #pragma unroll
             for (int h = 0; h < R; ++h) {
                 const int row = tid + h * KS_THREADS;
@@ -687,57 +785,6 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
                     if (p.lab8) p.lab8[row0 + row] = static_cast<int8_t>(label[h]);
                 }
             }
-        }
-        if (delta) {
-            // ---------------- phase 2 (delta mode): only rows whose label changed
-            // since the last iteration move their x from the old cluster's sums
-            // to the new one's; two rows per step (one per half-warp, each with
-            // its own f64 accumulator copy), in row order -- deterministic.
-            const int half = lane >> 4, hq = lane & 15;
-            double* acc = wacc + (warp * 2 + half) * KD;
-#pragma unroll
-            for (int h = 0; h < R; ++h) {
-                unsigned mask = __ballot_sync(FULL, label[h] < K && label[h] != prevl[h]);
-                while (mask) {
-                    const int bA = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    const int bB = mask ? __ffs(mask) - 1 : bA;
-                    const bool hasB = mask != 0u;
-                    mask &= mask - 1;
-                    const int nA = __shfl_sync(FULL, label[h], bA), oA = __shfl_sync(FULL, prevl[h], bA);
-                    const int nB = __shfl_sync(FULL, label[h], bB), oB = __shfl_sync(FULL, prevl[h], bB);
-                    if (lane < K)
-                        cnt_delta += (lane == nA) - (lane == oA) + (hasB ? (lane == nB) - (lane == oB) : 0);
-                    const int b = half ? bB : bA, nl = half ? nB : nA, ol = half ? oB : oA;
-                    if (hq < L && (half == 0 || hasB)) {
-                        const float2 v =
-                            *reinterpret_cast<const float2*>(xt + (h * KS_THREADS + warp * 32 + b) * D + 2 * hq);
-                        const double vx = static_cast<double>(v.x), vy = static_cast<double>(v.y);
-                        double2* an = reinterpret_cast<double2*>(acc + nl * D + 2 * hq);
-                        double2 t = *an;
-                        t.x += vx;
-                        t.y += vy;
-                        *an = t;
-                        if (ol >= 0) {
-                            double2* ao = reinterpret_cast<double2*>(acc + ol * D + 2 * hq);
-                            double2 u = *ao;
-                            u.x -= vx;
-                            u.y -= vy;
-                            *ao = u;
-                        }
-                    }
-                }
-            }
-            // the last warp done with this stage refills it (no CTA barrier)
-            __syncwarp();
-            if (lane == 0) {
-                const unsigned done = atomicAdd(&consumed[it % S], 1u);
-                if (done == W - 1) {
-                    consumed[it % S] = 0u;
-                    if (it + S < my_tiles) issue(it + S);
-                }
-            }
-            continue;
         }
         if (!accumulate) {
             __syncthreads();  // every warp is done with the previous tile's stage
@@ -854,7 +901,7 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
         for (int e = tid; e < KD; e += KS_THREADS) {
             double v = 0.0;
 #pragma unroll
-            for (int c = 0; c < 2 * W; ++c) v += wacc[c * KD + e];
+            for (int c = 0; c < W; ++c) v += wacc[c * KD + e];
             out[e] = v;
         }
         if (tid < K) {
@@ -875,29 +922,25 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
 
 template <int D, int K>
 static size_t small_smem() {
-    return static_cast<size_t>(KS_STAGES) * KS_TILE * (D * 4 + 1) + static_cast<size_t>(KS_WARPS) * 2 * K * D * 8 +
+    return static_cast<size_t>(KS_STAGES) * KS_TILE * (D * 4 + 1) + static_cast<size_t>(KS_WARPS) * K * D * 8 +
+           static_cast<size_t>(KS_WARPS) * 32 * (D * 4 + 8) +
            static_cast<size_t>((KS_VW * K + KS_STAGES + 1) & ~1) * 4 + KS_STAGES * 8;
 }
 
 #include "kmeans_tc.cuh"
 
-// Per-stat sum over the CTA partials: one block per stat, a fixed strided
-// split over 256 threads and a fixed tree (deterministic for a given grid).
+// Per-stat sum over the CTA partials: one warp per stat, lanes stride over the
+// CTAs, then a fixed xor-butterfly (deterministic for a given grid).
 __global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __restrict__ partials, int G, int S,
                                                               double* __restrict__ stats, const int* done) {
     if (done && *done) return;
-    __shared__ double sh[256];
-    const int e = blockIdx.x;
+    const int e = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (e >= S) return;
     double v = 0.0;
-    for (int g = threadIdx.x; g < G; g += 256) v += partials[static_cast<int64_t>(g) * S + e];
-    sh[threadIdx.x] = v;
-    __syncthreads();
+    for (int g = lane; g < G; g += 32) v += partials[static_cast<int64_t>(g) * S + e];
 #pragma unroll
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) stats[e] = sh[0];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) stats[e] = v;
 }
 
 // Deterministic block reductions: a fixed xor-butterfly inside each warp, then
@@ -984,7 +1027,7 @@ __global__ void __launch_bounds__(256) kmeans_update_kernel(int k, int d, int dp
                                      int iter, double tol) {
     if (flags[0]) return;
     __shared__ double sh[32];
-    extern __shared__ double upd[];  // [KD] folded sums, [KD] old centroids, [k] folded counts
+    extern __shared__ double upd[];  // [KD] folded sums, [KD] old centroids, [k] folded counts, [KD] new
     const int S = k * d + k, KD = k * d;
     const bool staged = KD <= UPD_MAX_KD;
     if (staged) {
@@ -1002,26 +1045,56 @@ __global__ void __launch_bounds__(256) kmeans_update_kernel(int k, int d, int dp
             if (e < KD) upd[KD + e] = c64[e];
         }
         __syncthreads();
+        // element-parallel: new centroid (cluster.cpp:125-133, empty keeps the
+        // old one) and its fp32 tables; the order-dependent sums follow per cluster
+        double* nxt_s = upd + 2 * KD + k;
+        for (int e = threadIdx.x; e < KD; e += blockDim.x) {
+            const int j = e / d, f = e % d;
+            const double count = upd[2 * KD + j], s = upd[e], old = upd[KD + e];
+            const double nxt = count > 0.0 ? s / count : old;
+            nxt_s[e] = nxt;
+            c64[e] = nxt;
+            const float c32 = static_cast<float>(nxt);
+            ct[static_cast<int64_t>(j) * dpad + f] = -2.f * c32;
+            if (ctab) ctab[e] = -2.f * c32;
+        }
+        for (int e = threadIdx.x; e < k * (dpad - d); e += blockDim.x)
+            ct[static_cast<int64_t>(e / (dpad - d)) * dpad + d + e % (dpad - d)] = 0.f;
+        __syncthreads();
     }
     double inertia_part = 0.0, dmax = 0.0, cmax = 0.0, cnmax = 0.0;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        double count = 0.0, dot = 0.0, dsq = 0.0, n64 = 0.0, n32 = 0.0;
-        if (staged) {
-            count = upd[2 * KD + j];
-        } else {
-            for (int r = 0; r < world; ++r) count += gathered[static_cast<int64_t>(r) * S + KD + j];
+    for (int j = threadIdx.x; j < k && staged; j += blockDim.x) {
+        const double count = upd[2 * KD + j], cn_old = cn64[j];
+        const double* nxt_s = upd + 2 * KD + k;
+        double dot = 0.0, dsq = 0.0, n64 = 0.0, n32 = 0.0;
+        for (int f = 0; f < d; ++f) {
+            const int e = j * d + f;
+            const double s = upd[e], old = upd[KD + e], nxt = nxt_s[e];
+            dot += old * s;
+            const double diff = nxt - old;
+            dsq = add_rn(dsq, mul_rn(diff, diff));  // cluster.cpp:142-146 order
+            n64 = add_rn(n64, mul_rn(nxt, nxt));    // row_norms order
+            const float c32 = static_cast<float>(nxt);
+            n32 += static_cast<double>(c32) * static_cast<double>(c32);
         }
+        if (ctab) ctab[KD + j] = static_cast<float>(n32);
+        cn64[j] = n64;
+        cn32[j] = static_cast<float>(n32);
+        inertia_part += count * cn_old - 2.0 * dot;  // uses the old |c_j|^2
+        dmax = fmax(dmax, __dsqrt_rn(dsq));
+        cmax = fmax(cmax, sqrt(n32));
+        cnmax = fmax(cnmax, static_cast<double>(static_cast<float>(n32)));
+    }
+    // large k*d: the same, straight from global memory (no running sums)
+    for (int j = threadIdx.x; j < k && !staged; j += blockDim.x) {
+        double count = 0.0, dot = 0.0, dsq = 0.0, n64 = 0.0, n32 = 0.0;
+        for (int r = 0; r < world; ++r) count += gathered[static_cast<int64_t>(r) * S + KD + j];
         const double cn_old = cn64[j];
         for (int f = 0; f < d; ++f) {
             const int e = j * d + f;
-            double s = 0.0, old;
-            if (staged) {
-                s = upd[e];
-                old = upd[KD + e];
-            } else {
-                for (int r = 0; r < world; ++r) s += gathered[static_cast<int64_t>(r) * S + e];
-                old = c64[e];
-            }
+            double s = 0.0;
+            for (int r = 0; r < world; ++r) s += gathered[static_cast<int64_t>(r) * S + e];
+            const double old = c64[e];
             dot += old * s;
             const double nxt = count > 0.0 ? s / count : old;  // cluster.cpp:125-133
             const double diff = nxt - old;
@@ -1058,11 +1131,11 @@ __global__ void __launch_bounds__(256) kmeans_update_kernel(int k, int d, int dp
 
 static size_t update_smem(int k, int d) {
     const size_t kd = static_cast<size_t>(k) * d;
-    const size_t bytes = kd <= UPD_MAX_KD ? (2 * kd + k) * sizeof(double) : 0;
+    const size_t bytes = kd <= UPD_MAX_KD ? (3 * kd + k) * sizeof(double) : 0;
     static bool attr = false;
     if (!attr) {
         DNDC_CUDA(cudaFuncSetAttribute(kmeans_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>((2 * UPD_MAX_KD + 1024) * sizeof(double))));
+                                       static_cast<int>((3 * UPD_MAX_KD + 1024) * sizeof(double))));
         attr = true;
     }
     return bytes;
@@ -1502,7 +1575,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
             if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[2 * it], st, cudaEventRecordExternal));
             A.launch(b, x_local, n_local, m, k, true, nullptr, true, st, delta ? lab8 : nullptr, lab8);
             if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[2 * it + 1], st, cudaEventRecordExternal));
-            reduce_partials_kernel<<<S, 256, 0, st>>>(b.partials, A.grid(), S, b.stats, b.flags);
+            reduce_partials_kernel<<<(S + 7) / 8, 256, 0, st>>>(b.partials, A.grid(), S, b.stats, b.flags);
             if (ctx->world > 1) allgather_f64(ctx, b.stats, b.gathered, S, st);
             kmeans_update_kernel<<<1, 256, update_smem(k, m), st>>>(k, m, dpad_of(m), ctx->world,
                                                    ctx->world > 1 ? b.gathered : b.stats,
@@ -1543,7 +1616,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     DNDC_CUDA(cudaGraphLaunch(ctx->km->exec, gs));
     DNDC_CUDA(cudaEventRecord(ctx->ev_b, gs));
     DNDC_CUDA(cudaStreamWaitEvent(s, ctx->ev_b, 0));
-    ctx->launches += 1 + 3ull * max_iter + (A.small ? max_iter : 0);  // + table copies
+    ctx->launches += 1 + 3ull * max_iter;  // reset + (assign, reduce, update) per iteration
     if (ctx->world > 1) ctx->counters.allgathers += max_iter;
 
     // ---- results
