@@ -61,6 +61,10 @@ int dndc_create(int device, int rank, int world, const void* unique_id, dndc_ctx
 int dndc_destroy(dndc_ctx* ctx);
 int dndc_set_stream(dndc_ctx* ctx, void* cuda_stream);
 int dndc_rank(const dndc_ctx* ctx);
+/* How the k-means stats exchange travels for world > 1: "nvlink peer exchange"
+ * (stats stored by the fused kernel straight into every peer over NVLink,
+ * CUDA IPC mappings) or why it fell back to the NCCL allgather path. */
+const char* dndc_transport_status(const dndc_ctx* ctx);
 int dndc_world(const dndc_ctx* ctx);
 int dndc_synchronize(dndc_ctx* ctx);
 int dndc_get_counters(const dndc_ctx* ctx, dndc_counters* out);

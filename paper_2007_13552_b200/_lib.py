@@ -44,6 +44,7 @@ _SIGS = {
     "dndc_set_stream": [_P, _P],
     "dndc_rank": [_P],
     "dndc_world": [_P],
+    "dndc_transport_status": [_P],
     "dndc_synchronize": [_P],
     "dndc_get_counters": [_P, C.POINTER(Counters)],
     "dndc_launch_count": [_P],
@@ -73,7 +74,7 @@ _SIGS = {
     "dndc_moments_axis0_f64": [_P, _P, _i64, _i64, _P, _P, _P],
     "dndc_kmeanspp_indices_f32": [_P, _P, _i64, _i64, _i64, _i32, _u64, _P],
 }
-_RESTYPE = {"dndc_last_error": C.c_char_p, "dndc_launch_count": C.c_uint64}
+_RESTYPE = {"dndc_last_error": C.c_char_p, "dndc_launch_count": C.c_uint64, "dndc_transport_status": C.c_char_p}
 
 
 def header_symbols() -> list[str]:

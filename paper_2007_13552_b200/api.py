@@ -98,6 +98,11 @@ class Communicator:
         return {n: getattr(c, n) for n, _ in c._fields_}
 
     @property
+    def transport(self) -> str:
+        """How the k-means stats exchange travels (NVLink peer stores or NCCL)."""
+        return lib().dndc_transport_status(self._h).decode()
+
+    @property
     def launches(self) -> int:
         return int(lib().dndc_launch_count(self._h))
 

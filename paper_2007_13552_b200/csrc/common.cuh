@@ -92,7 +92,31 @@ struct dndc_ctx {
     void* host_staging(size_t bytes);
 
     dndc::KMeansState* km = nullptr;
+
+    // NVLink peer exchange (world > 1): a small region per rank, mapped into
+    // every other rank through CUDA IPC (runtime.cu setup_peer_exchange); the
+    // fused k-means kernel writes its stats straight into every peer's region.
+    bool p2p = false;
+    std::string p2p_status = "world == 1";
+    void* xchg = nullptr;              // own region (cudaMalloc)
+    std::vector<void*> peer_bases;     // every rank's region as mapped here (own = xchg)
+    void** peer_bases_dev = nullptr;   // the same table in device memory
 };
+
+namespace dndc {
+// Layout of one rank's exchange region: [2 slots][world][XCHG_STATS] f64
+// receive buffers, then [world] u64 arrival flags, then one u64 epoch.
+constexpr int XCHG_STATS = 4096;
+inline size_t xchg_bytes(int world) {
+    return sizeof(double) * 2 * world * XCHG_STATS + sizeof(unsigned long long) * (world + 1);
+}
+__host__ __device__ inline double* xchg_recv(void* base, int slot, int world, int r) {
+    return static_cast<double*>(base) + (static_cast<size_t>(slot) * world + r) * XCHG_STATS;
+}
+__host__ __device__ inline unsigned long long* xchg_flags(void* base, int world) {
+    return reinterpret_cast<unsigned long long*>(static_cast<double*>(base) + 2 * static_cast<size_t>(world) * XCHG_STATS);
+}
+}  // namespace dndc
 
 namespace dndc {
 

@@ -56,6 +56,7 @@ struct KMeansState {
     std::vector<cudaEvent_t> ev;
     double assign_ms = 0.0;
     int assign_launches = 0;
+    std::vector<double> per_launch_ms;
 };
 
 static void free_events(KMeansState* st) {
@@ -88,6 +89,8 @@ struct KmBuffers {
     float* ctab;       // K*D + K constant-bank layout of the fp32 table
     unsigned long long* refined;
     double* running;   // S running sums/counts of the delta iterations
+    unsigned long long* acc64;  // fused tail: fixed-point stats accumulator
+    unsigned* counters;  // [0] fused-tail arrival ticket, [1] tile counter
 };
 
 static int dpad_of(int m) { return (m + 3) / 4 * 4; }
@@ -450,6 +453,45 @@ constexpr int KS_SLOTS = 4;
 constexpr int KS_TABLE = 1152;  // floats per slot (K*D + K)
 __constant__ float c_km_table[KS_SLOTS * KS_TABLE];
 
+struct UpdArgs {
+    int k, d, dpad, world;
+    const double* gathered;  // world per-rank stats, folded here in rank order
+    int64_t gstride;         // doubles between two ranks' stats in `gathered`
+    double* running;         // delta iterations: running sums/counts (or null)
+    int accum;               // 1: gathered holds changes, added to running
+    double *c64, *cn64;
+    float *ct, *cn32, *ctab, *bounds;
+    const double* sx2;
+    double *trace, *disp;
+    int* flags;
+    int iter;
+    double tol;
+    // where the update reads running / c64 / cn64 / sx2 (the fused tail points
+    // these at shared-memory copies it prefetched; otherwise the arrays above)
+    const double *rd_running, *rd_c64, *rd_cn64, *rd_sx2;
+};
+
+__device__ void update_body(const UpdArgs& a, double* upd, double* sh);
+
+// Fused tail of the small kernel (world == 1, or NVLink peer exchange): every
+// CTA adds its partial stats into one fixed-point int64 accumulator (integer
+// adds are associative: the result does not depend on arrival order); the
+// last CTA to arrive converts them back to f64, stores the rank's stats into
+// every rank's exchange region, waits for every rank's arrival flag and runs
+// the update -- the whole Lloyd iteration in one launch.
+struct FuseArgs {
+    int on;
+    unsigned long long* acc64;  // [S] fixed-point sums, zero between launches
+    const double* xabs;   // max |x_e| of the shard (sets the fixed-point scale)
+    int64_t n;            // rows of the shard
+    unsigned* counters;   // [1] arrival ticket, zero between launches
+    double* stats;        // [S] this rank's stats
+    void* const* peers;   // [world] exchange regions (world > 1)
+    int rank;
+    unsigned* tile_ctr;   // reset with the tickets
+    UpdArgs upd;
+};
+
 struct SmallParams {
     const float* x;
     int64_t n;
@@ -463,6 +505,8 @@ struct SmallParams {
     int8_t* lab8;         // this iteration's labels (fit), or null
     unsigned long long* refined;
     const int* done;
+    unsigned* tile_ctr;   // delta mode: dynamic tile scheduling (zero at launch)
+    FuseArgs fu;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -551,6 +595,138 @@ constexpr int KS_MIN_CTAS = 4;
 #endif
 constexpr int KS_VW = KS_WARPS * KS_R;  // 32-row groups per tile
 
+#ifdef KS_TAIL_TRACE
+__device__ unsigned long long g_tail_trace[16];
+__device__ unsigned long long g_cta_trace[2 * 2048];
+__device__ __forceinline__ void cta_mark(int i) {
+    if (threadIdx.x == 0 && blockIdx.x < 2048) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        g_cta_trace[2 * blockIdx.x + i] = t;
+    }
+}
+__device__ __forceinline__ void tail_mark(int i) {
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        g_tail_trace[i] = t;
+    }
+}
+#else
+__device__ __forceinline__ void tail_mark(int) {}
+__device__ __forceinline__ void cta_mark(int) {}
+#endif
+
+// One CTA-wide arrival ticket; true in every thread of the last CTA to arrive.
+__device__ __forceinline__ bool last_arrival(unsigned* ctr, unsigned total, int* s_flag) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *s_flag = atomicAdd(ctr, 1u) == total - 1u;
+    __syncthreads();
+    const bool last = *s_flag != 0;
+    if (last) __threadfence();
+    return last;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Called by every thread of every CTA once its partial row is written.
+// `work` is >= (3 k d + k + 40) doubles of shared memory no longer in use.
+__device__ void fused_tail(const FuseArgs& f, const double* part, int S, int KD, double* work) {
+    const int G = gridDim.x;
+    int* s_flag = reinterpret_cast<int*>(work);
+    unsigned long long* s_epoch = reinterpret_cast<unsigned long long*>(work + 1);
+    double* sh = work + 8;
+    double* upd = work + 40;
+    if (blockIdx.x == 0) tail_mark(0);
+    cta_mark(1);
+    // sums: f64 partial -> int64 at 2^-(61 - e) with n max|x| < 2^e: exact to
+    // ~1e-18 of the largest possible sum, so the total matches an f64
+    // accumulation to its own rounding level
+    int e2 = 0;
+    frexp(static_cast<double>(f.n) * *f.xabs + 1.0, &e2);
+    const int shift = 61 - e2;
+    // what the update will read, fetched now so only the last CTA's final
+    // loads stay on the critical path
+    const int k = S - KD;
+    double* pre = work + 1536;  // running[S] | c64[KD] | cn64[k] | sx2[4] | stats[S]
+    for (int e = threadIdx.x; e < S; e += blockDim.x) {
+        if (f.upd.running) pre[e] = f.upd.running[e];
+        if (e < KD) pre[S + e] = f.upd.c64[e];
+        if (e < k) pre[S + KD + e] = f.upd.cn64[e];
+        if (e < 4) pre[S + KD + k + e] = f.upd.sx2[e];
+    }
+    double* stats_s = pre + S + KD + k + 4;
+    __syncthreads();  // `part` complete
+    for (int e = threadIdx.x; e < S; e += blockDim.x) {
+        const double v = part[e];
+        const long long q = e < KD ? llrint(ldexp(v, shift)) : llrint(v);
+        if (q != 0) atomicAdd(f.acc64 + e, static_cast<unsigned long long>(q));
+    }
+    if (!last_arrival(f.counters, G, s_flag)) return;
+    tail_mark(1);
+    if (threadIdx.x == 0) {
+        f.counters[0] = 0u;  // every ticket is in
+        if (f.tile_ctr) *f.tile_ctr = 0u;
+    }
+    const int world = f.upd.world;
+    unsigned long long epoch = 0;
+    int slot = 0;
+    if (world > 1) {
+        if (threadIdx.x == 0) {
+            unsigned long long* ep = xchg_flags(f.peers[f.rank], world) + world;
+            *s_epoch = *ep + 1;
+            *ep = *s_epoch;
+        }
+        __syncthreads();
+        epoch = *s_epoch;
+        slot = static_cast<int>(epoch & 1);
+    }
+    for (int e = threadIdx.x; e < S; e += blockDim.x) {
+        const long long q = static_cast<long long>(atomicExch(f.acc64 + e, 0ull));  // read + reset
+        const double v = e < KD ? ldexp(static_cast<double>(q), -shift) : static_cast<double>(q);
+        f.stats[e] = v;
+        stats_s[e] = v;
+        for (int r = 0; r < world && world > 1; ++r) xchg_recv(f.peers[r], slot, world, f.rank)[e] = v;  // NVLink
+    }
+    tail_mark(2);
+    UpdArgs a = f.upd;
+    a.gathered = stats_s;
+    a.gstride = S;
+    a.rd_running = pre;
+    a.rd_c64 = pre + S;
+    a.rd_cn64 = pre + S + KD;
+    a.rd_sx2 = pre + S + KD + k;
+    __syncthreads();  // stats_s complete
+    if (world > 1) {
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x < world) {
+            st_release_sys(xchg_flags(f.peers[threadIdx.x], world) + f.rank, epoch);
+            const unsigned long long* mine = xchg_flags(f.peers[f.rank], world) + threadIdx.x;
+            const long long t0 = clock64();
+            while (ld_acquire_sys(mine) < epoch) {
+                __nanosleep(64);
+                if (clock64() - t0 > 40000000000ll) __trap();  // a peer never arrived (~20 s)
+            }
+        }
+        __syncthreads();
+        __threadfence();
+        a.gathered = xchg_recv(f.peers[f.rank], slot, world, 0);
+        a.gstride = XCHG_STATS;
+    }
+    tail_mark(3);
+    update_body(a, upd, sh);
+    tail_mark(4);
+}
+
 // fp32 top-2 of R rows held in registers as feature pairs: one FFMA2 per two
 // features with the centroid pair broadcast from the constant bank (uniform
 // registers), JG clusters x R rows of independent chains at a time.
@@ -612,7 +788,8 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
     int* scl = reinterpret_cast<int*>(scr + W * 32 * D);               // W x 32 x 2 their new/old labels
     int* cnt = reinterpret_cast<int*>(scl + W * 64);                   // VW x K
     unsigned* consumed = reinterpret_cast<unsigned*>(cnt + VW * K);    // S (delta mode)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(consumed + ((VW * K + S + 1) & ~1) - VW * K);
+    int* stage_tile = reinterpret_cast<int*>(consumed + S);             // S (dynamic schedule)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(cnt + ((VW * K + 2 * S + 1) & ~1));
 
     const float* CT = c_km_table + SLOT * KS_TABLE;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -629,6 +806,8 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
     const bool accumulate = p.partials != nullptr;
 #endif
     const bool delta = accumulate && p.prev != nullptr;
+    if (p.fu.on && blockIdx.x == 0) tail_mark(5);
+    if (p.fu.on) cta_mark(0);
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -650,11 +829,35 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
             bulk_load(tiles + (it % S) * TILE * D, p.x + tile * TILE * D, static_cast<uint32_t>(rows * D * 4),
                       &bars[it % S]);
     };
+    // delta mode with a tile counter: tiles handed out dynamically (a CTA that
+    // runs ahead takes more), so every CTA finishes within about one tile
+    const bool dyn = accumulate && p.tile_ctr != nullptr;
+    auto grab = [&](int s) {
+        const unsigned t = atomicAdd(p.tile_ctr, 1u);
+        if (t < ntiles) {
+            const int64_t rows = min(static_cast<int64_t>(TILE), p.n - static_cast<int64_t>(t) * TILE);
+            stage_tile[s] = static_cast<int>(t);
+            if (delta)
+                bulk_load2(tiles + s * TILE * D, p.x + static_cast<int64_t>(t) * TILE * D,
+                           static_cast<uint32_t>(rows * D * 4), labs + s * TILE,
+                           p.prev + static_cast<int64_t>(t) * TILE, static_cast<uint32_t>(rows), &bars[s]);
+            else
+                bulk_load(tiles + s * TILE * D, p.x + static_cast<int64_t>(t) * TILE * D,
+                          static_cast<uint32_t>(rows * D * 4), &bars[s]);
+        } else {
+            stage_tile[s] = -1;
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
+        }
+    };
     // full mode refills stage (it-1)%S mid-tile (S-1 tiles ahead); delta mode
     // refills a stage as soon as every warp has its rows in registers (S ahead)
     const int ahead = delta ? S : S - 1;
-    if (tid == 0)
-        for (int s = 0; s < ahead && s < my_tiles; ++s) issue(s);
+    if (tid == 0) {
+        if (dyn)
+            for (int s = 0; s < ahead; ++s) grab(s);
+        else
+            for (int s = 0; s < ahead && s < my_tiles; ++s) issue(s);
+    }
 
     long long count_acc = 0;  // lane j < K of warp 0: rows of cluster j
     unsigned long long refined = 0;
@@ -664,10 +867,12 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
     for (int jj = 0; jj < JW; ++jj) wsum[jj] = make_double2(0.0, 0.0);
 
     int cnt_delta = 0;  // delta mode, lane j < K: net rows gained by cluster j
-    for (int64_t it = 0; it < my_tiles; ++it) {
-        const int64_t row0 = (blockIdx.x + it * gridDim.x) * TILE;
+    for (int64_t it = 0; dyn || it < my_tiles; ++it) {
         const float* xt = tiles + (it % S) * TILE * D;
         mbar_wait(&bars[it % S], static_cast<uint32_t>((it / S) & 1));
+        const int64_t tile_id = dyn ? static_cast<int64_t>(stage_tile[it % S]) : blockIdx.x + it * gridDim.x;
+        if (tile_id < 0) break;
+        const int64_t row0 = tile_id * TILE;
         if (delta) {
             // ---------------- delta mode: rows to registers, then the stage is
             // handed back at once (the last warp to finish reading refills it),
@@ -687,7 +892,10 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
                 const unsigned done = atomicAdd(&consumed[it % S], 1u);
                 if (done == W - 1) {
                     consumed[it % S] = 0u;
-                    if (it + S < my_tiles) issue(it + S);
+                    if (dyn)
+                        grab(static_cast<int>(it % S));
+                    else if (it + S < my_tiles)
+                        issue(it + S);
                 }
             }
             {
@@ -807,7 +1015,12 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
             if (rank[h] == 0 && label[h] < K) cnt[(h * W + warp) * K + label[h]] = __popc(mine[h]);
         }
         __syncthreads();  // counts visible; every warp is done with the previous tile
-        if (tid == 0 && it + S - 1 < my_tiles) issue(it + S - 1);
+        if (tid == 0) {
+            if (dyn)
+                grab(static_cast<int>((it + S - 1) % S));
+            else if (it + S - 1 < my_tiles)
+                issue(it + S - 1);
+        }
 
         // lane j: start of cluster j in the sorted tile and the offsets of this
         // warp's groups inside it
@@ -894,7 +1107,10 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
     if (refined) atomicAdd(p.refined, refined);
     if (!accumulate) return;
     const int Sst = KD + K;
-    double* out = p.partials + static_cast<int64_t>(blockIdx.x) * Sst;
+    // fused: the CTA's partial row stays in shared memory (past the tail's
+    // scratch); otherwise it goes to the partials array for the reduce kernel
+    double* out = p.fu.on ? reinterpret_cast<double*>(tiles) + 1024 : p.partials + static_cast<int64_t>(blockIdx.x) * Sst;
+    if (p.fu.on) __syncthreads();  // the last tile's rows in `tiles` are consumed
     if (delta) {
         if (lane < K) cnt[warp * K + lane] = cnt_delta;
         __syncthreads();
@@ -910,21 +1126,22 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
             for (int w = 0; w < W; ++w) c += cnt[w * K + tid];
             out[KD + tid] = static_cast<double>(c);
         }
-        return;
-    }
+    } else {
 #pragma unroll
-    for (int jj = 0; jj < JW; ++jj) {
-        const int j = warp + jj * W;
-        if (j < K && g == 0 && q < L) *reinterpret_cast<double2*>(out + j * D + 2 * q) = wsum[jj];
+        for (int jj = 0; jj < JW; ++jj) {
+            const int j = warp + jj * W;
+            if (j < K && g == 0 && q < L) *reinterpret_cast<double2*>(out + j * D + 2 * q) = wsum[jj];
+        }
+        if (warp == 0 && lane < K) out[KD + lane] = static_cast<double>(count_acc);
     }
-    if (warp == 0 && lane < K) out[KD + lane] = static_cast<double>(count_acc);
+    if (p.fu.on) fused_tail(p.fu, out, Sst, KD, reinterpret_cast<double*>(tiles));
 }
 
 template <int D, int K>
 static size_t small_smem() {
     return static_cast<size_t>(KS_STAGES) * KS_TILE * (D * 4 + 1) + static_cast<size_t>(KS_WARPS) * K * D * 8 +
            static_cast<size_t>(KS_WARPS) * 32 * (D * 4 + 8) +
-           static_cast<size_t>((KS_VW * K + KS_STAGES + 1) & ~1) * 4 + KS_STAGES * 8;
+           static_cast<size_t>((KS_VW * K + 2 * KS_STAGES + 1) & ~1) * 4 + KS_STAGES * 8;
 }
 
 #include "kmeans_tc.cuh"
@@ -1021,30 +1238,35 @@ __global__ void derive_tables_kernel(int k, int d, int dpad, const double* c64, 
 // (cluster.cpp:125-133) into shared memory.  Stage 2 (thread per cluster):
 // the reference's sequential per-cluster loops (displacement, norms).
 constexpr int UPD_MAX_KD = 8192;
-__global__ void __launch_bounds__(256) kmeans_update_kernel(int k, int d, int dpad, int world, const double* gathered,
-                                     double* running, int accum, double* c64, double* cn64, float* ct, float* cn32, float* ctab, float* bounds,
-                                     const double* sx2, double* trace, double* disp, int* flags,
-                                     int iter, double tol) {
-    if (flags[0]) return;
-    __shared__ double sh[32];
-    extern __shared__ double upd[];  // [KD] folded sums, [KD] old centroids, [k] folded counts, [KD] new
+
+// The update step, executed by one CTA (any blockDim): `upd` is shared memory
+// of (3 k d + k) doubles (k d <= UPD_MAX_KD), `sh` 32 doubles.
+__device__ void update_body(const UpdArgs& a, double* upd, double* sh) {
+    const int k = a.k, d = a.d, dpad = a.dpad, world = a.world, accum = a.accum, iter = a.iter;
+    const double* gathered = a.gathered;
+    double *running = a.running, *c64 = a.c64, *cn64 = a.cn64, *trace = a.trace, *disp = a.disp;
+    float *ct = a.ct, *cn32 = a.cn32, *ctab = a.ctab, *bounds = a.bounds;
+    const double* sx2 = a.sx2;
+    int* flags = a.flags;
+    const double tol = a.tol;
     const int S = k * d + k, KD = k * d;
     const bool staged = KD <= UPD_MAX_KD;
     if (staged) {
         // allreduce(plus_vec) from the zero identity in rank order (cluster.cpp:123)
         for (int e = threadIdx.x; e < S; e += blockDim.x) {
             double v = 0.0;
-            for (int r = 0; r < world; ++r) v += gathered[static_cast<int64_t>(r) * S + e];
+            for (int r = 0; r < world; ++r) v += gathered[static_cast<int64_t>(r) * a.gstride + e];
             // delta iterations (small kernel): the stats are changes since the
             // last iteration, added to the running per-cluster sums and counts
             if (running) {
-                if (accum) v += running[e];
+                if (accum) v += a.rd_running[e];
                 running[e] = v;
             }
             upd[e < KD ? e : KD + e] = v;
-            if (e < KD) upd[KD + e] = c64[e];
+            if (e < KD) upd[KD + e] = a.rd_c64[e];
         }
         __syncthreads();
+        tail_mark(6);
         // element-parallel: new centroid (cluster.cpp:125-133, empty keeps the
         // old one) and its fp32 tables; the order-dependent sums follow per cluster
         double* nxt_s = upd + 2 * KD + k;
@@ -1061,10 +1283,11 @@ __global__ void __launch_bounds__(256) kmeans_update_kernel(int k, int d, int dp
         for (int e = threadIdx.x; e < k * (dpad - d); e += blockDim.x)
             ct[static_cast<int64_t>(e / (dpad - d)) * dpad + d + e % (dpad - d)] = 0.f;
         __syncthreads();
+        tail_mark(7);
     }
     double inertia_part = 0.0, dmax = 0.0, cmax = 0.0, cnmax = 0.0;
     for (int j = threadIdx.x; j < k && staged; j += blockDim.x) {
-        const double count = upd[2 * KD + j], cn_old = cn64[j];
+        const double count = upd[2 * KD + j], cn_old = a.rd_cn64[j];
         const double* nxt_s = upd + 2 * KD + k;
         double dot = 0.0, dsq = 0.0, n64 = 0.0, n32 = 0.0;
         for (int f = 0; f < d; ++f) {
@@ -1088,12 +1311,12 @@ __global__ void __launch_bounds__(256) kmeans_update_kernel(int k, int d, int dp
     // large k*d: the same, straight from global memory (no running sums)
     for (int j = threadIdx.x; j < k && !staged; j += blockDim.x) {
         double count = 0.0, dot = 0.0, dsq = 0.0, n64 = 0.0, n32 = 0.0;
-        for (int r = 0; r < world; ++r) count += gathered[static_cast<int64_t>(r) * S + KD + j];
+        for (int r = 0; r < world; ++r) count += gathered[static_cast<int64_t>(r) * a.gstride + KD + j];
         const double cn_old = cn64[j];
         for (int f = 0; f < d; ++f) {
             const int e = j * d + f;
             double s = 0.0;
-            for (int r = 0; r < world; ++r) s += gathered[static_cast<int64_t>(r) * S + e];
+            for (int r = 0; r < world; ++r) s += gathered[static_cast<int64_t>(r) * a.gstride + e];
             const double old = c64[e];
             dot += old * s;
             const double nxt = count > 0.0 ? s / count : old;  // cluster.cpp:125-133
@@ -1115,18 +1338,44 @@ __global__ void __launch_bounds__(256) kmeans_update_kernel(int k, int d, int dp
         cmax = fmax(cmax, sqrt(n32));
         cnmax = fmax(cnmax, static_cast<double>(static_cast<float>(n32)));
     }
-    const double inertia = block_sum(inertia_part, sh);
-    dmax = block_max(dmax, sh);
-    cmax = block_max(cmax, sh);
-    cnmax = block_max(cnmax, sh);
+    tail_mark(8);
+    // one combined block reduction (fixed order: xor-butterfly, then warps in order)
+    const double sx2_total = threadIdx.x == 0 ? a.rd_sx2[2] : 0.0;
+    inertia_part = warp_sum(inertia_part);
+    dmax = warp_max(dmax);
+    cmax = warp_max(cmax);
+    cnmax = warp_max(cnmax);
+    const int nw = (blockDim.x + 31) / 32;
+    if ((threadIdx.x & 31) == 0) {
+        const int w = threadIdx.x / 32;
+        sh[4 * w] = inertia_part;
+        sh[4 * w + 1] = dmax;
+        sh[4 * w + 2] = cmax;
+        sh[4 * w + 3] = cnmax;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        trace[iter] = sx2[2] + inertia;
+        double inertia = 0.0;
+        for (int w = 0; w < nw; ++w) {
+            inertia += sh[4 * w];
+            dmax = fmax(dmax, sh[4 * w + 1]);
+            cmax = fmax(cmax, sh[4 * w + 2]);
+            cnmax = fmax(cnmax, sh[4 * w + 3]);
+        }
+        trace[iter] = sx2_total + inertia;
         disp[iter] = dmax;
         flags[1] = iter + 1;
         if (dmax < tol) flags[0] = 1;
         bounds[0] = static_cast<float>(cmax) * (1.f + 0x1.0p-20f);
         bounds[1] = static_cast<float>(cnmax) * (1.f + 0x1.0p-20f);
     }
+}
+
+__global__ void __launch_bounds__(256) kmeans_update_kernel(UpdArgs a) {
+    if (a.flags[0]) return;
+    __shared__ double sh[32];
+    extern __shared__ double upd[];  // [KD] folded sums, [KD] old centroids, [k] folded counts, [KD] new
+    update_body(a, upd, sh);
 }
 
 static size_t update_smem(int k, int d) {
@@ -1196,7 +1445,14 @@ __global__ void gather_rows_kernel(const T* __restrict__ x, int64_t lo, int64_t 
     }
 }
 
-__global__ void kmeans_reset_kernel(int* flags, unsigned long long* refined) {
+__global__ void zero_u32_kernel(unsigned* p, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0u;
+}
+
+__global__ void kmeans_reset_kernel(int* flags, unsigned long long* refined, unsigned* counters, int ncounters,
+                                    unsigned long long* acc64, int S) {
+    for (int i = 0; i < ncounters; ++i) counters[i] = 0u;
+    for (int i = 0; i < S; ++i) acc64[i] = 0ull;
     flags[0] = 0;
     flags[1] = 0;
     *refined = 0ull;
@@ -1222,6 +1478,8 @@ static KmBuffers buffers(dndc_ctx* ctx, int k, int m, int max_iter, int G) {
     b.ctab = static_cast<float*>(ctx->slot("km_ctab", sizeof(float) * (k * m + k)));
     b.refined = static_cast<unsigned long long*>(ctx->slot("km_refined", sizeof(unsigned long long)));
     b.running = static_cast<double*>(ctx->slot("km_running", sizeof(double) * S));
+    b.acc64 = static_cast<unsigned long long*>(ctx->slot("km_acc64", sizeof(unsigned long long) * S));
+    b.counters = static_cast<unsigned*>(ctx->slot("km_counters", sizeof(unsigned) * 2));
     return b;
 }
 
@@ -1320,7 +1578,8 @@ struct Assigner {
     int grid() const { return (small || tc) ? sgrid : gen.grid; }
 
     void launch(const KmBuffers& b, const T* x, int64_t n, int d, int k, bool accumulate, int32_t* labels,
-                bool use_done, cudaStream_t st, const int8_t* prev = nullptr, int8_t* lab8 = nullptr) const {
+                bool use_done, cudaStream_t st, const int8_t* prev = nullptr, int8_t* lab8 = nullptr,
+                const FuseArgs* fu = nullptr, unsigned* tile_ctr = nullptr) const {
         if (tc) {
             TcParams tp{};
             tp.n = n;
@@ -1347,6 +1606,8 @@ struct Assigner {
             sp.labels = labels;
             sp.prev = prev;
             sp.lab8 = lab8;
+            if (fu) sp.fu = *fu;
+            sp.tile_ctr = tile_ctr;
             sp.refined = b.refined;
             sp.done = use_done ? b.flags : nullptr;
             sfn<<<sgrid, KS_THREADS, ssmem, st>>>(sp);
@@ -1507,6 +1768,36 @@ static void derive_tables(dndc_ctx* ctx, const KmBuffers& b, int k, int m) {
     DNDC_LAUNCHED(ctx);
 }
 
+static UpdArgs upd_args(const KmBuffers& b, int k, int m, int world, const double* gathered, double* running,
+                        bool delta, int it, double tol) {
+    UpdArgs a{};
+    a.k = k;
+    a.d = m;
+    a.dpad = dpad_of(m);
+    a.world = world;
+    a.gathered = gathered;
+    a.gstride = static_cast<int64_t>(k) * m + k;
+    a.running = running;
+    a.accum = delta ? 1 : 0;
+    a.c64 = b.c64;
+    a.cn64 = b.cn64;
+    a.ct = b.ct;
+    a.cn32 = b.cn32;
+    a.ctab = b.ctab;
+    a.bounds = b.bounds;
+    a.sx2 = b.sx2;
+    a.trace = b.trace;
+    a.disp = b.disp;
+    a.flags = b.flags;
+    a.iter = it;
+    a.tol = tol;
+    a.rd_running = running;
+    a.rd_c64 = b.c64;
+    a.rd_cn64 = b.cn64;
+    a.rd_sx2 = b.sx2;
+    return a;
+}
+
 template <typename T>
 static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t n_global, int64_t m64,
                        int k, int max_iter, double tol, uint64_t seed, const double* init_host,
@@ -1557,8 +1848,8 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     derive_tables(ctx, b, k, m);
 
     // ---- the Lloyd loop, one graph per (shape, buffers, max_iter, tol)
-    // small kernel: iteration 0 accumulates full sums and records int8 labels;
-    // later iterations accumulate only the rows whose label changed (deltas)
+    // small kernel: every iteration records int8 labels; the first ones
+    // accumulate full sums, later ones only the rows whose label changed
     int8_t* lab8 = A.small ? static_cast<int8_t*>(ctx->slot("km_lab8", std::max<int64_t>(n_local, 1))) : nullptr;
     if (!ctx->km) ctx->km = new KMeansState();
     KMeansState* km = ctx->km;
@@ -1568,26 +1859,48 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
         for (auto& e : km->ev) DNDC_CUDA(cudaEventCreate(&e));
         km->key.clear();
     }
+    // one launch per iteration (fused tail) on one GPU or with the NVLink
+    // peer exchange; otherwise assign -> reduce -> NCCL allgather -> update
+    const bool fuse = A.small && (ctx->world == 1 || ctx->p2p) && !std::getenv("DNDC_NO_FUSE");
+    const int ncounters = 2;
+    unsigned* tile_ctr = b.counters + 1;
     auto record = [&](cudaStream_t st) {
-        kmeans_reset_kernel<<<1, 1, 0, st>>>(b.flags, b.refined);
+        kmeans_reset_kernel<<<1, 1, 0, st>>>(b.flags, b.refined, b.counters, ncounters, b.acc64, S);
         for (int it = 0; it < max_iter; ++it) {
-            const bool delta = A.small && it > 0;
+            // iterations 0 and 1 accumulate every row (after the first update most
+            // labels still move); from iteration 2 on only the rows that changed
+            const bool delta = A.small && it > 1;
+            FuseArgs fa{};
+            if (fuse) {
+                fa.on = 1;
+                fa.acc64 = b.acc64;
+                fa.xabs = b.sx2 + 3;
+                fa.n = n_local;
+                fa.counters = b.counters;
+                fa.stats = b.stats;
+                fa.peers = ctx->world > 1 ? ctx->peer_bases_dev : nullptr;
+                fa.rank = ctx->rank;
+                fa.tile_ctr = tile_ctr;
+                fa.upd = upd_args(b, k, m, ctx->world, nullptr, b.running, delta, it, tol);
+            }
             if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[2 * it], st, cudaEventRecordExternal));
-            A.launch(b, x_local, n_local, m, k, true, nullptr, true, st, delta ? lab8 : nullptr, lab8);
+            if (A.small && !fuse) zero_u32_kernel<<<1, 32, 0, st>>>(tile_ctr, 1);
+            A.launch(b, x_local, n_local, m, k, true, nullptr, true, st, delta ? lab8 : nullptr, lab8,
+                     fuse ? &fa : nullptr, A.small ? tile_ctr : nullptr);
             if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[2 * it + 1], st, cudaEventRecordExternal));
+            if (fuse) continue;
             reduce_partials_kernel<<<(S + 7) / 8, 256, 0, st>>>(b.partials, A.grid(), S, b.stats, b.flags);
             if (ctx->world > 1) allgather_f64(ctx, b.stats, b.gathered, S, st);
-            kmeans_update_kernel<<<1, 256, update_smem(k, m), st>>>(k, m, dpad_of(m), ctx->world,
-                                                   ctx->world > 1 ? b.gathered : b.stats,
-                                                   A.small ? b.running : nullptr, delta ? 1 : 0, b.c64, b.cn64,
-                                                   b.ct, b.cn32, b.ctab, b.bounds, b.sx2, b.trace, b.disp, b.flags,
-                                                   it, tol);
+            const UpdArgs ua = upd_args(b, k, m, ctx->world, ctx->world > 1 ? b.gathered : b.stats,
+                                        A.small ? b.running : nullptr, delta, it, tol);
+            kmeans_update_kernel<<<1, 256, update_smem(k, m), st>>>(ua);
         }
     };
     cudaStream_t gs = ctx->own_stream;
     char keybuf[256];
-    std::snprintf(keybuf, sizeof(keybuf), "%p/%lld/%d/%d/%d/%.17g/%p/%d/%d/%d", (const void*)x_local,
-                  (long long)n_local, m, k, max_iter, tol, (void*)s, A.grid(), ctx->world, km->timing ? 1 : 0);
+    std::snprintf(keybuf, sizeof(keybuf), "%p/%lld/%d/%d/%d/%.17g/%p/%d/%d/%d/%d", (const void*)x_local,
+                  (long long)n_local, m, k, max_iter, tol, (void*)s, A.grid(), ctx->world, km->timing ? 1 : 0,
+                  fuse ? 1 : 0);
     const std::string key = std::string(sizeof(T) == 4 ? "f32/" : "f64/") + keybuf;
     if (ctx->km->key != key || !ctx->km->exec) {
         if (ctx->km->exec) {
@@ -1616,7 +1929,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     DNDC_CUDA(cudaGraphLaunch(ctx->km->exec, gs));
     DNDC_CUDA(cudaEventRecord(ctx->ev_b, gs));
     DNDC_CUDA(cudaStreamWaitEvent(s, ctx->ev_b, 0));
-    ctx->launches += 1 + 3ull * max_iter;  // reset + (assign, reduce, update) per iteration
+    ctx->launches += 1 + (fuse ? 1ull : 3ull) * max_iter;  // reset + (assign[, reduce, update]) per iteration
     if (ctx->world > 1) ctx->counters.allgathers += max_iter;
 
     // ---- results
@@ -1638,10 +1951,12 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     if (km->timing) {
         // iterations past convergence return at once; only the ones that ran count
         double tot = 0.0;
+        km->per_launch_ms.assign(iters, 0.0);
         for (int it = 0; it < iters; ++it) {
             float t = 0.f;
             DNDC_CUDA(cudaEventElapsedTime(&t, km->ev[2 * it], km->ev[2 * it + 1]));
             tot += t;
+            km->per_launch_ms[it] = t;
         }
         km->assign_ms = tot;
         km->assign_launches = iters;
@@ -1781,12 +2096,27 @@ int dndc_kmeans_time_assign_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_
     return guard([&] { dndc::time_assign(ctx, x, n, m, k, reps, ms_per_launch, algorithmic_bytes); });
 }
 
+#ifdef KS_TAIL_TRACE
+int dndc_internal_tail_trace(unsigned long long* out16) {
+    return guard([&] { DNDC_CUDA(cudaMemcpyFromSymbol(out16, dndc::g_tail_trace, 16 * sizeof(unsigned long long))); });
+}
+int dndc_internal_cta_trace(unsigned long long* out4096) {
+    return guard([&] { DNDC_CUDA(cudaMemcpyFromSymbol(out4096, dndc::g_cta_trace, 4096 * sizeof(unsigned long long))); });
+}
+#endif
+
 int dndc_kmeans_assign_timing(dndc_ctx* ctx, int enable) {
     return guard([&] {
         if (!ctx->km) ctx->km = new dndc::KMeansState();
         if (ctx->km->timing != (enable != 0)) ctx->km->key.clear();  // re-record the graph
         ctx->km->timing = enable != 0;
     });
+}
+
+int dndc_internal_assign_times(const dndc_ctx* ctx, double* out, int cap) {
+    const int n = ctx->km ? static_cast<int>(ctx->km->per_launch_ms.size()) : 0;
+    for (int i = 0; i < n && i < cap; ++i) out[i] = ctx->km->per_launch_ms[i];
+    return n;
 }
 
 int dndc_kmeans_last_assign_ms(const dndc_ctx* ctx, double* total_ms, int* launches) {

@@ -9,6 +9,7 @@
 //     every rank holds bit-identical results (never NCCL's ring order);
 //   - sendrecv is a grouped ncclSend/ncclRecv pair (transport.hpp:122-129);
 //   - TransportCounters are kept per rank (transport.hpp:19-27).
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -55,6 +56,73 @@ void allreduce_sum_f64(dndc_ctx* ctx, double* buf, size_t count, cudaStream_t st
     // cluster.cpp:27-42), so the sum is exact whatever NCCL's order.
     DNDC_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, ctx->comm, stream));
     ctx->counters.allreduces++;
+}
+
+// Maps every rank's exchange region into every rank (CUDA IPC handles
+// allgathered over NCCL).  Any failure leaves ctx->p2p false and the k-means
+// stats exchange on the NCCL allgather path; DNDC_P2P=0 forces that path.
+static void setup_peer_exchange(dndc_ctx* ctx) {
+    const char* env = std::getenv("DNDC_P2P");
+    if (env && env[0] == '0') {
+        ctx->p2p_status = "disabled by DNDC_P2P=0";
+        return;
+    }
+    const int W = ctx->world;
+    cudaStream_t s = ctx->own_stream;
+    DNDC_CUDA(cudaMalloc(&ctx->xchg, xchg_bytes(W)));
+    DNDC_CUDA(cudaMemsetAsync(ctx->xchg, 0, xchg_bytes(W), s));
+    cudaIpcMemHandle_t mine;
+    DNDC_CUDA(cudaIpcGetMemHandle(&mine, ctx->xchg));
+    char* dh = nullptr;
+    DNDC_CUDA(cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * W));
+    DNDC_CUDA(cudaMemcpyAsync(dh + sizeof(cudaIpcMemHandle_t) * ctx->rank, &mine, sizeof(mine),
+                              cudaMemcpyHostToDevice, s));
+    // the allgather also orders every rank's zeroing before any peer write
+    DNDC_NCCL(ncclAllGather(dh + sizeof(cudaIpcMemHandle_t) * ctx->rank, dh, sizeof(cudaIpcMemHandle_t), ncclChar,
+                            ctx->comm, s));
+    std::vector<cudaIpcMemHandle_t> all(W);
+    DNDC_CUDA(cudaMemcpyAsync(all.data(), dh, sizeof(cudaIpcMemHandle_t) * W, cudaMemcpyDeviceToHost, s));
+    DNDC_CUDA(cudaStreamSynchronize(s));
+    cudaFree(dh);
+    ctx->peer_bases.assign(W, nullptr);
+    bool ok = true;
+    std::string why;
+    for (int r = 0; r < W; ++r) {
+        if (r == ctx->rank) {
+            ctx->peer_bases[r] = ctx->xchg;
+            continue;
+        }
+        void* p = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+            why = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+            break;
+        }
+        ctx->peer_bases[r] = p;
+    }
+    // every rank must agree on the path: AND of the local outcomes
+    int* flag = nullptr;
+    DNDC_CUDA(cudaMalloc(&flag, sizeof(int)));
+    const int v = ok ? 1 : 0;
+    DNDC_CUDA(cudaMemcpyAsync(flag, &v, sizeof(int), cudaMemcpyHostToDevice, s));
+    DNDC_NCCL(ncclAllReduce(flag, flag, 1, ncclInt32, ncclMin, ctx->comm, s));
+    int all_ok = 0;
+    DNDC_CUDA(cudaMemcpyAsync(&all_ok, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DNDC_CUDA(cudaStreamSynchronize(s));
+    cudaFree(flag);
+    if (!all_ok) {
+        for (int r = 0; r < W; ++r)
+            if (r != ctx->rank && ctx->peer_bases[r]) cudaIpcCloseMemHandle(ctx->peer_bases[r]);
+        ctx->peer_bases.clear();
+        ctx->p2p_status = ok ? "a peer could not map the exchange regions" : why;
+        return;
+    }
+    DNDC_CUDA(cudaMalloc(&ctx->peer_bases_dev, sizeof(void*) * W));
+    DNDC_CUDA(cudaMemcpy(ctx->peer_bases_dev, ctx->peer_bases.data(), sizeof(void*) * W, cudaMemcpyHostToDevice));
+    ctx->p2p = true;
+    ctx->p2p_status = "nvlink peer exchange";
 }
 
 }  // namespace dndc
@@ -131,6 +199,7 @@ int dndc_create(int device, int rank, int world, const void* unique_id, dndc_ctx
             ncclUniqueId id;
             std::memcpy(&id, unique_id, sizeof(id));
             DNDC_NCCL(ncclCommInitRank(&ctx->comm, world, id, rank));
+            dndc::setup_peer_exchange(ctx.get());
         }
         *out = ctx.release();
     });
@@ -144,6 +213,10 @@ int dndc_destroy(dndc_ctx* ctx) {
         dndc::destroy_kmeans_state(ctx->km);
         for (auto& kv : ctx->slots) cudaFree(kv.second.first);
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        for (int r = 0; r < static_cast<int>(ctx->peer_bases.size()); ++r)
+            if (r != ctx->rank && ctx->peer_bases[r]) cudaIpcCloseMemHandle(ctx->peer_bases[r]);
+        if (ctx->peer_bases_dev) cudaFree(ctx->peer_bases_dev);
+        if (ctx->xchg) cudaFree(ctx->xchg);
         if (ctx->comm) ncclCommDestroy(ctx->comm);
         cudaEventDestroy(ctx->ev_a);
         cudaEventDestroy(ctx->ev_b);
@@ -161,6 +234,8 @@ int dndc_set_stream(dndc_ctx* ctx, void* cuda_stream) {
 }
 
 int dndc_rank(const dndc_ctx* ctx) { return ctx->rank; }
+
+const char* dndc_transport_status(const dndc_ctx* ctx) { return ctx->p2p_status.c_str(); }
 int dndc_world(const dndc_ctx* ctx) { return ctx->world; }
 
 int dndc_synchronize(dndc_ctx* ctx) {

@@ -26,9 +26,14 @@ _lib.check(L.dndc_kmeans_assign_timing(comm.handle, 1))
 mod = dnd.kmeans_fit(x, k, 20, 0.0, 42)
 tot, nl = C.c_double(), C.c_int()
 _lib.check(L.dndc_kmeans_last_assign_ms(comm.handle, C.byref(tot), C.byref(nl)))
+per = (C.c_double * 64)()
+L.dndc_internal_assign_times.restype = C.c_int
+npl = L.dndc_internal_assign_times(comm.handle, per, 64)
+per_s = " ".join(f"{per[i]*1e3:.0f}" for i in range(npl))
 _lib.check(L.dndc_kmeans_assign_timing(comm.handle, 0))
 g = np.load("tests/golden/reference_golden.npz")
 rel = float(np.max(np.abs(mod.centroids - g["cfg1_centroids"]) / np.maximum(1, np.abs(g["cfg1_centroids"]))))
+print("per-launch us:", per_s)
 print(f"full-mode assign {ms.value*1e3:6.1f} us | in-fit assign avg {tot.value/nl.value*1e3:6.1f} us ({by.value/(tot.value/nl.value)/1e6:5.0f} GB/s) | iters/s {100/(s.elapsed_time(e)/1e3):7.0f} | rel {rel:.1e} refined {mod.refined_rows}")
 '''
 libs = sys.argv[1:] or sorted(glob.glob(os.path.join(ROOT, "variants", "*.so")))
