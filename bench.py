@@ -302,6 +302,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config(world), "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
             "cpu_baseline": cpu, "clocks": clk, "refined_rows_last_fit": model.refined_rows,
+            "stats_exchange": comm.transport if world > 1 else "single GPU (fused in-kernel update)",
             "final_inertia": model.inertia_trace[-1],
         }))
     if dist:

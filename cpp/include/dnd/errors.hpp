@@ -1,0 +1,40 @@
+// dnd/errors.hpp -- B200 drop-in for proj/include/dnd/errors.hpp: the same
+// exception types, raised from the C-ABI status codes of include/dndc.h.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+
+#include "dndc.h"
+
+namespace dnd {
+
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+/// Invalid shapes/arguments (errors.hpp:14-18 of the reference).
+struct ValueError : Error {
+    using Error::Error;
+};
+/// Collective/transport failures (errors.hpp:21-25): NCCL or the NVLink exchange.
+struct TransportError : Error {
+    using Error::Error;
+};
+/// A CUDA failure inside libdndc (no reference counterpart: the CPU path has none).
+struct DeviceError : Error {
+    using Error::Error;
+};
+
+namespace detail {
+inline void check(int rc) {
+    if (rc == DNDC_OK) return;
+    const std::string msg = dndc_last_error();
+    switch (rc) {
+        case DNDC_EVALUE: throw ValueError(msg);
+        case DNDC_ETRANSPORT: throw TransportError(msg);
+        case DNDC_ECUDA: throw DeviceError(msg);
+        default: throw Error(msg);
+    }
+}
+}  // namespace detail
+}  // namespace dnd

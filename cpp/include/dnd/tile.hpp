@@ -1,0 +1,28 @@
+// dnd/tile.hpp -- host tiles (proj/include/dnd/tile.hpp:16-40): what the
+// reference keeps per rank; here a host staging type next to the HBM shard.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace dnd {
+
+using index_t = std::int64_t;
+
+namespace detail {
+inline index_t product(const std::vector<index_t>& v) {
+    index_t p = 1;
+    for (index_t e : v) p *= e;
+    return p;
+}
+}  // namespace detail
+
+template <typename T>
+struct Tile {
+    std::vector<index_t> extents;
+    std::vector<T> data;
+    int ndim() const { return static_cast<int>(extents.size()); }
+    index_t numel() const { return detail::product(extents); }
+};
+
+}  // namespace dnd

@@ -1,0 +1,206 @@
+// C++ drop-in tests: the reference's own test cases (proj/tests/test_pairwise.cpp,
+// test_cluster.cpp, test_moments.cpp, test_chunking.cpp) written against the
+// B200 dnd API, run with one rank per visible GPU (up to 2).
+//
+//     make -C cpp test && cpp/build/test_dnd
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "dnd/dnd.hpp"
+
+using dnd::Communicator;
+using dnd::index_t;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                              \
+    do {                                                                         \
+        if (cond) {                                                              \
+            ++g_pass;                                                            \
+        } else {                                                                 \
+            ++g_fail;                                                            \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+        }                                                                        \
+    } while (0)
+#define CHECK_THROWS_AS(expr, type)          \
+    do {                                     \
+        bool thrown = false;                 \
+        try {                                \
+            (void)(expr);                    \
+        } catch (const type&) {              \
+            thrown = true;                   \
+        }                                    \
+        CHECK(thrown&& #expr " throws " #type); \
+    } while (0)
+
+static bool close_rel(double a, double b, double tol) { return std::abs(a - b) <= tol * std::max(1.0, std::abs(b)); }
+
+// naive_cdist (oracles.hpp:61-73): the reference formula, f64, no FMA
+static std::vector<double> naive_cdist(const std::vector<double>& x, index_t n, const std::vector<double>& y,
+                                       index_t ny, index_t m) {
+    std::vector<double> nx(n), nyv(ny), out(n * ny);
+    auto sq = [&](const std::vector<double>& a, index_t i) {
+        volatile double acc = 0.0;
+        for (index_t f = 0; f < m; ++f) {
+            volatile double p = a[i * m + f] * a[i * m + f];
+            acc = acc + p;
+        }
+        return static_cast<double>(acc);
+    };
+    for (index_t i = 0; i < n; ++i) nx[i] = sq(x, i);
+    for (index_t j = 0; j < ny; ++j) nyv[j] = sq(y, j);
+    for (index_t i = 0; i < n; ++i)
+        for (index_t j = 0; j < ny; ++j) {
+            volatile double g = 0.0;
+            for (index_t f = 0; f < m; ++f) {
+                volatile double p = x[i * m + f] * y[j * m + f];
+                g = g + p;
+            }
+            volatile double s = nx[i] + nyv[j];
+            volatile double t = 2.0 * g;
+            const double d = s - t;
+            out[i * ny + j] = std::sqrt(d > 0.0 ? d : 0.0);
+        }
+    return out;
+}
+
+static void each_world(const std::function<void(const Communicator&)>& body) {
+    int ndev = 0;
+    dnd::detail::check(dndc_device_count(&ndev));
+    for (int p = 1; p <= std::min(ndev, 2); ++p) dnd::run_world(p, body);
+}
+
+int main() {
+    // chunking (test_chunking.cpp:10-14)
+    {
+        const auto m = dnd::chunk_map(5, 3);
+        CHECK((m.extents == std::vector<index_t>{2, 2, 1}));
+        CHECK((m.offsets == std::vector<index_t>{0, 2, 4}));
+    }
+    each_world([](const Communicator& comm) {
+        // (0,0),(3,4) -> [[0,5],[5,0]] exactly (test_pairwise.cpp:23-28)
+        auto x64 = dnd::from_global<double>({0, 0, 3, 4}, {2, 2}, 0, comm);
+        CHECK((dnd::gather(dnd::cdist(x64)) == std::vector<double>{0, 5, 5, 0}));
+        auto x32 = dnd::from_global<float>({0, 0, 3, 4}, {2, 2}, 0, comm);
+        CHECK((dnd::gather(dnd::cdist(x32)) == std::vector<float>{0, 5, 5, 0}));
+
+        // repeated rows -> 0 (test_pairwise.cpp:16-21)
+        std::vector<double> rep;
+        for (int i = 0; i < 5; ++i) rep.insert(rep.end(), {1.0, 2.0, 3.0});
+        const auto d_rep = dnd::gather(dnd::cdist(dnd::from_global<double>(rep, {5, 3}, 0, comm)));
+        CHECK(std::all_of(d_rep.begin(), d_rep.end(), [](double v) { return v == 0.0; }));
+
+        // cdist f64 bit-exact against the naive oracle; cdist_xy too
+        const index_t n = 37, ny = 11, m = 6;
+        auto xa = dnd::random_uniform<double>({n, m}, 0, 7, comm);
+        auto ya = dnd::random_uniform<double>({ny, m}, std::nullopt, 8, comm);
+        const auto xh = dnd::gather(xa), yh = dnd::gather(ya);
+        CHECK(dnd::gather(dnd::cdist(xa)) == naive_cdist(xh, n, xh, n, m));
+        CHECK(dnd::gather(dnd::cdist_xy(xa, ya)) == naive_cdist(xh, n, yh, ny, m));
+        const auto c0 = comm.counters();
+        dnd::cdist_xy(xa, ya);
+        CHECK(comm.counters().sendrecvs == c0.sendrecvs);  // communication-free (test_pairwise.cpp:146-166)
+
+        // fp32 within the parity gate (1e-5 rel)
+        auto xf = dnd::random_uniform<float>({n, m}, 0, 7, comm);
+        const auto df = dnd::gather(dnd::cdist(xf));
+        const auto ref = naive_cdist(xh, n, xh, n, m);  // same values: random_uniform<float> == f32(f64)
+        double dev = 0.0;
+        const auto xfh = dnd::gather(xf);
+        const auto ref32 = naive_cdist(std::vector<double>(xfh.begin(), xfh.end()), n,
+                                       std::vector<double>(xfh.begin(), xfh.end()), n, m);
+        for (std::size_t i = 0; i < df.size(); ++i)
+            dev = std::max(dev, std::abs(df[i] - ref32[i]) / std::max(1.0, std::abs(ref32[i])));
+        CHECK(dev <= 1e-5);
+        (void)ref;
+
+        // distance to a zero row = sqrt(|x|^2) (test_pairwise.cpp:116-133)
+        dnd::Tile<double> a{{2, 3}, {1, 2, 2, 0, 3, 4}};
+        dnd::Tile<double> z{{1, 3}, {0, 0, 0}};
+        const auto blk = dnd::detail::distance_block(a, dnd::detail::row_norms(a), z, dnd::detail::row_norms(z));
+        CHECK(blk.data[0] == 3.0 && blk.data[1] == 5.0);
+
+        // predict (test_cluster.cpp:221-241)
+        dnd::KMeansModel model;
+        model.k = 3;
+        model.n_features = 2;
+        model.centroids = {0, 0, 5, 5, 9, 0};
+        auto xp = dnd::from_global<double>({0, 0, 5, 5, 9, 0}, {3, 2}, 0, comm);
+        CHECK((dnd::gather(dnd::kmeans_predict(model, xp)) == std::vector<std::int32_t>{0, 1, 2}));
+        dnd::KMeansModel tie;
+        tie.k = 2;
+        tie.n_features = 1;
+        tie.centroids = {0.0, 2.0};
+        auto xt = dnd::from_global<double>({1.0, 1.0}, {2, 1}, 0, comm);
+        CHECK((dnd::gather(dnd::kmeans_predict(tie, xt)) == std::vector<std::int32_t>{0, 0}));
+
+        // k = 1 -> the global mean (test_cluster.cpp:119-132)
+        auto xk = dnd::random_uniform<double>({101, 4}, 0, 3, comm);
+        const auto xkh = dnd::gather(xk);
+        const auto m1 = dnd::kmeans_fit(xk, 1, 3, 0.0, 5);
+        for (int f = 0; f < 4; ++f) {
+            double s = 0.0;
+            for (int i = 0; i < 101; ++i) s += xkh[i * 4 + f];
+            CHECK(close_rel(m1.centroids[f], s / 101.0, 1e-12));
+        }
+
+        // two clouds -> their exact means (test_cluster.cpp:83-117)
+        std::vector<float> cl;
+        for (int i = 0; i < 40; ++i) cl.insert(cl.end(), {0.0f + 0.01f * (i % 7), 0.0f + 0.02f * (i % 5)});
+        for (int i = 0; i < 40; ++i) cl.insert(cl.end(), {10.0f + 0.01f * (i % 3), 10.0f + 0.03f * (i % 4)});
+        auto xc = dnd::from_global<float>(cl, {80, 2}, 0, comm);
+        const auto mc = dnd::kmeans_fit(xc, 2, 10, 0.0, 1);
+        double mean_a[2] = {0, 0}, mean_b[2] = {0, 0};
+        for (int i = 0; i < 40; ++i)
+            for (int f = 0; f < 2; ++f) {
+                mean_a[f] += static_cast<double>(cl[i * 2 + f]) / 40.0;
+                mean_b[f] += static_cast<double>(cl[(40 + i) * 2 + f]) / 40.0;
+            }
+        const bool a_first = mc.centroids[0] < 5.0;
+        const double* ca = a_first ? &mc.centroids[0] : &mc.centroids[2];
+        const double* cb = a_first ? &mc.centroids[2] : &mc.centroids[0];
+        if (!close_rel(ca[0], mean_a[0], 1e-12))
+            std::fprintf(stderr, "p=%d clouds: %.17g %.17g | %.17g %.17g vs %.17g %.17g | %.17g %.17g (iters %d)\n",
+                         comm.size(), mc.centroids[0], mc.centroids[1], mc.centroids[2], mc.centroids[3], mean_a[0],
+                         mean_a[1], mean_b[0], mean_b[1], mc.iterations_run);
+        CHECK(close_rel(ca[0], mean_a[0], 1e-12) && close_rel(ca[1], mean_a[1], 1e-12));
+        CHECK(close_rel(cb[0], mean_b[0], 1e-12) && close_rel(cb[1], mean_b[1], 1e-12));
+        for (std::size_t i = 1; i < mc.inertia_trace.size(); ++i)
+            CHECK(mc.inertia_trace[i] <= mc.inertia_trace[i - 1] * (1 + 1e-12));
+
+        // validation (test_cluster.cpp:285-300)
+        auto xv = dnd::from_global<double>({1, 2, 3, 4}, {2, 2}, 0, comm);
+        CHECK_THROWS_AS(dnd::kmeans_fit(xv, 3, 5, 0.0, 1), dnd::ValueError);
+        CHECK_THROWS_AS(dnd::kmeans_fit(xv, 1, 0, 0.0, 1), dnd::ValueError);
+        auto xnan = dnd::from_global<double>({1, NAN, 3, 4}, {2, 2}, 0, comm);
+        CHECK_THROWS_AS(dnd::kmeans_fit(xnan, 1, 2, 0.0, 1), dnd::ValueError);
+        auto v1 = dnd::from_global<double>({1, 2, 3}, {3}, 0, comm);
+        CHECK_THROWS_AS(dnd::cdist(v1), dnd::ValueError);
+
+        // moments: [1,2,3,4] -> mean 2.5, var 1.25 / 5/3 (test_moments.cpp:46-56, :182-192)
+        auto mv = dnd::from_global<double>({1, 2, 3, 4}, {4, 1}, 0, comm);
+        CHECK(dnd::mean(mv) == 2.5);
+        CHECK(close_rel(dnd::var(mv), 1.25, 1e-15));
+        CHECK(close_rel(dnd::var(mv, 1), 5.0 / 3.0, 1e-15));
+        CHECK(close_rel(dnd::gather(dnd::var_axis(mv, 0, 1))[0], 5.0 / 3.0, 1e-15));
+        // the 1e8 offset (test_moments.cpp:160-180): single pass stays accurate
+        std::vector<double> off;
+        for (int i = 0; i < 1000; ++i) off.push_back(1e8 + (i % 10));
+        auto xo = dnd::from_global<double>(off, {1000, 1}, 0, comm);
+        CHECK(close_rel(dnd::var(xo), 8.25, 1e-9));
+        // combine with the identity returns the operand exactly
+        auto st = dnd::local_moments(dnd::Tile<double>{{3}, {1, 5, 9}});
+        const auto st2 = dnd::combine(st, dnd::MomentState::identity(1));
+        CHECK(st2.count == st.count && st2.mean == st.mean && st2.m2 == st.m2);
+        // random_uniform is split- and rank-count independent (A1)
+        auto r1 = dnd::random_uniform<float>({53, 5}, 0, 42, comm);
+        auto r2 = dnd::random_uniform<float>({53, 5}, std::nullopt, 42, comm);
+        CHECK(dnd::gather(r1) == dnd::gather(r2));
+    });
+    std::printf("test_dnd: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail ? 1 : 0;
+}

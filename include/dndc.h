@@ -75,6 +75,31 @@ uint64_t dndc_launch_count(const dndc_ctx* ctx);
 /* chunk_map (chunking.cpp:9-30), host only. */
 int dndc_chunk_map(int64_t n, int world, int64_t* offsets_host, int64_t* extents_host);
 
+/* ---------------------------------------------- device memory and copies */
+/* What a host layer needs to own device tiles without CUDA headers (the C++
+ * drop-in in cpp/include/dnd keeps DndArray shards in HBM through these).
+ * Copies are synchronous with respect to the handle's stream. */
+#define DNDC_COPY_H2D 1
+#define DNDC_COPY_D2H 2
+#define DNDC_COPY_D2D 3
+int dndc_device_count(int* out);
+/* Communicator::barrier (transport.hpp:150-153), collective. */
+int dndc_barrier(dndc_ctx* ctx);
+int dndc_alloc(dndc_ctx* ctx, size_t bytes, void** out);
+int dndc_free(dndc_ctx* ctx, void* p);
+int dndc_memcpy(dndc_ctx* ctx, void* dst, const void* src, size_t bytes, int kind);
+
+/* gather of a split=0 array (ndarray.hpp:389-393 via resplit :354-368),
+ * collective: every rank's device rows (row_bytes each) concatenated in rank
+ * order into out_host; *total_rows receives the global row count. */
+int dndc_allgather_rows(dndc_ctx* ctx, const void* local, int64_t rows, int64_t row_bytes, void* out_host,
+                        int64_t* total_rows);
+
+/* Communicator::allreduce(plus) (transport.hpp:136-148, A15), collective, in
+ * place on a device buffer: sum over ranks folded in rank order 0..p-1 from
+ * the zero identity, bit-identical on every rank. */
+int dndc_allreduce_f64(dndc_ctx* ctx, double* buf, int64_t count);
+
 /* ------------------------------------------------------- A1: generator */
 /* random_uniform<float>/<double> (ndarray.hpp:154-169, common.hpp:14-27): the
  * rows x m block starting at global row row0, bit-identical to the reference. */
@@ -157,6 +182,15 @@ int dndc_kmeans_predict_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m,
                             const double* centroids_host, int k, int32_t* labels);
 int dndc_kmeans_predict_f64(dndc_ctx* ctx, const double* x, int64_t n, int64_t m,
                             const double* centroids_host, int k, int32_t* labels);
+
+/* One Lloyd assignment/accumulation step on this rank's rows (cluster.cpp:
+ * 108-122, A8/A9) against given centroids (k x m f64, host): the LOCAL
+ * (not reduced) stats, k*m sums then k counts, then the local inertia
+ * (sum of squared distances of the rows to their centroid), k*m + k + 1
+ * doubles on the host; labels (device int32, n) when non-NULL.
+ * Communication-free: reduce with dndc_allreduce_f64 for the global step. */
+int dndc_kmeans_step_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m, const double* centroids_host,
+                         int k, double* stats_host, int32_t* labels);
 
 /* Statistics of the most recent kmeans_fit/predict on this context: rows whose
  * fp32 top-2 gap fell inside the error bound and were re-decided in f64. */

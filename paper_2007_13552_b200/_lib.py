@@ -49,6 +49,14 @@ _SIGS = {
     "dndc_get_counters": [_P, C.POINTER(Counters)],
     "dndc_launch_count": [_P],
     "dndc_chunk_map": [_i64, _i32, _P, _P],
+    "dndc_device_count": [_P],
+    "dndc_barrier": [_P],
+    "dndc_alloc": [_P, C.c_size_t, _P],
+    "dndc_free": [_P, _P],
+    "dndc_memcpy": [_P, _P, _P, C.c_size_t, _i32],
+    "dndc_allgather_rows": [_P, _P, _i64, _i64, _P, _P],
+    "dndc_allreduce_f64": [_P, _P, _i64],
+    "dndc_kmeans_step_f32": [_P, _P, _i64, _i64, _P, _i32, _P, _P],
     "dndc_fill_uniform_f32": [_P, _u64, _i64, _i64, _i64, _P],
     "dndc_fill_uniform_f64": [_P, _u64, _i64, _i64, _i64, _P],
     "dndc_row_norms_f32": [_P, _P, _i64, _i64, _P],

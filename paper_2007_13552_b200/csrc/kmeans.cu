@@ -406,14 +406,16 @@ __global__ void __launch_bounds__(KM_THREADS) kmeans_assign_kernel(AssignParams 
                     for (int fb = 0; fb < d; fb += 32) {
                         const int f = fb + lane;
                         if (f < d) {
-                            T part = T(0);
+                            // f64 from the first term: fp32 run sums would put
+                            // ~1e-7 relative error into the centroids
+                            double part = 0.0;
                             unsigned mm = mask;
                             while (mm) {
                                 const int r = __ffs(mm) - 1;
                                 mm &= mm - 1;
-                                part += xt[(c * 32 + r) * srow + f];
+                                part += static_cast<double>(xt[(c * 32 + r) * srow + f]);
                             }
-                            acc[j * d + f] += static_cast<double>(part);
+                            acc[j * d + f] += part;
                         }
                     }
                 }
@@ -1989,6 +1991,48 @@ static void kmeans_predict(dndc_ctx* ctx, const T* x, int64_t n, int64_t m64, co
     ctx->last_refined = static_cast<int64_t>(*hr);
 }
 
+// One assignment/accumulation pass against given centroids: local stats and
+// local inertia (sum |x|^2 + sum_j n_j |c_j|^2 - 2 c_j . S_j, the fit's form).
+static void kmeans_step(dndc_ctx* ctx, const float* x, int64_t n, int64_t m64, const double* cent_host, int k,
+                        double* stats_host, int32_t* labels) {
+    if (k < 1) value_error("kmeans_step: k must be positive");
+    if (n < 0 || m64 < 1) value_error("kmeans_step: bad extents");
+    const int m = static_cast<int>(m64);
+    cudaStream_t s = ctx->stream;
+    const Assigner<float> A = plan<float>(ctx, k, m, n, x);
+    const KmBuffers b = buffers(ctx, k, m, 1, A.grid());
+    const int S = k * m + k;
+    double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * std::max(k * m, S + 4)));
+    std::memcpy(h, cent_host, sizeof(double) * k * m);
+    DNDC_CUDA(cudaMemcpyAsync(b.c64, h, sizeof(double) * k * m, cudaMemcpyHostToDevice, s));
+    DNDC_CUDA(cudaMemsetAsync(b.refined, 0, sizeof(unsigned long long), s));
+    DNDC_CUDA(cudaMemsetAsync(b.stats, 0, sizeof(double) * S, s));
+    DNDC_CUDA(cudaMemsetAsync(b.sx2, 0, sizeof(double) * 4, s));
+    derive_tables(ctx, b, k, m);
+    if (n > 0) {
+        scan_input<float>(ctx, b, x, n * m, s);
+        A.launch(b, x, n, m, k, true, labels, false, s);
+        DNDC_LAUNCHED(ctx);
+        reduce_partials_kernel<<<(S + 7) / 8, 256, 0, s>>>(b.partials, A.grid(), S, b.stats, nullptr);
+        DNDC_LAUNCHED(ctx);
+    }
+    DNDC_CUDA(cudaMemcpyAsync(h, b.stats, sizeof(double) * S, cudaMemcpyDeviceToHost, s));
+    DNDC_CUDA(cudaMemcpyAsync(h + S, b.sx2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    DNDC_CUDA(cudaStreamSynchronize(s));
+    double inertia = h[S];
+    for (int j = 0; j < k; ++j) {
+        double cn = 0.0, dot = 0.0;
+        for (int f = 0; f < m; ++f) {
+            const double c = cent_host[static_cast<int64_t>(j) * m + f];
+            cn += c * c;
+            dot += c * h[j * m + f];
+        }
+        inertia += h[k * m + j] * cn - 2.0 * dot;
+    }
+    std::memcpy(stats_host, h, sizeof(double) * S);
+    stats_host[S] = inertia;
+}
+
 template <typename T>
 static void init_centroids_api(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t n_global,
                                int64_t m, int k, uint64_t seed, double* out_host) {
@@ -2089,6 +2133,11 @@ int dndc_kmeans_predict_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m,
 int dndc_kmeans_predict_f64(dndc_ctx* ctx, const double* x, int64_t n, int64_t m,
                             const double* centroids_host, int k, int32_t* labels) {
     return guard([&] { dndc::kmeans_predict<double>(ctx, x, n, m, centroids_host, k, labels); });
+}
+
+int dndc_kmeans_step_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m, const double* centroids_host,
+                         int k, double* stats_host, int32_t* labels) {
+    return guard([&] { dndc::kmeans_step(ctx, x, n, m, centroids_host, k, stats_host, labels); });
 }
 
 int dndc_kmeans_time_assign_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m, int k, int reps,

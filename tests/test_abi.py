@@ -2,6 +2,7 @@
 every declared symbol, and its host-only entry points behave like the
 reference functions they replace."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -70,3 +71,17 @@ def test_product_package_never_uses_the_oracle():
         assert not bad.search(f.read_text()), f
     deps = subprocess.run(["ldd", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "oracle" not in deps and "dndref" not in deps
+
+
+def test_cpp_dropin_compiles_against_the_c_abi():
+    """cpp/include/dnd (the reference's C++ API names) builds over include/dndc.h
+    and links libdndc.so only -- no CUDA headers on the host side."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run(["make", "-C", os.path.join(root, "cpp")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert os.path.exists(os.path.join(root, "cpp", "build", "test_dnd"))
+    for h in ("ndarray.hpp", "pairwise.hpp", "cluster.hpp", "moments.hpp", "transport.hpp", "chunking.hpp"):
+        src = open(os.path.join(root, "cpp", "include", "dnd", h)).read()
+        assert "cuda_runtime" not in src and "#include <cuda" not in src

@@ -178,3 +178,38 @@ def test_kernel_variants_agree(comm, oracle, n, m, k, monkeypatch):
         assert rel_dev(model.inertia_trace, t_ref) <= 1e-6, kind
         labels = dnd.gather(dnd.kmeans_predict(model, x))
         assert np.array_equal(labels, oracle.kmeans_predict(xh.astype(np.float64), model.centroids)), kind
+
+
+def test_kmeans_step_c_abi(comm, oracle):
+    # dndc_kmeans_step_f32: one assign/accumulate pass, local stats
+    import ctypes as C
+
+    from paper_2007_13552_b200 import _lib
+
+    n, m, k = 5003, 18, 8
+    xh = oracle.uniform_f32(n, m, 11)
+    x = dnd.from_global(xh, (n, m), 0, comm)
+    cents = np.ascontiguousarray(oracle.uniform_f64(k, m, 12))
+    stats = np.zeros(k * m + k + 1)
+    labels = torch.empty(n, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().dndc_kmeans_step_f32(comm.handle, x.tile.data_ptr(), n, m, cents.ctypes.data, k,
+                                              stats.ctypes.data, labels.data_ptr()))
+    lab = labels.cpu().numpy()
+    x64 = xh.astype(np.float64)
+    assert np.array_equal(lab, oracle.kmeans_predict(x64, cents))
+    for j in range(k):
+        sel = x64[lab == j]
+        assert stats[k * m + j] == len(sel)
+        assert rel_dev(stats[j * m:(j + 1) * m], sel.sum(0)) <= 1e-12
+    d2 = ((x64[:, None, :] - cents[None]) ** 2).sum(-1)
+    assert abs(stats[-1] - d2[np.arange(n), lab].sum()) <= 1e-9 * d2.min(1).sum()
+
+
+def test_allreduce_f64_single_rank_identity(comm):
+    import ctypes as C
+
+    from paper_2007_13552_b200 import _lib
+
+    buf = torch.arange(7, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().dndc_allreduce_f64(comm.handle, buf.data_ptr(), 7))
+    assert torch.equal(buf.cpu(), torch.arange(7, dtype=torch.float64))

@@ -33,6 +33,8 @@ def main():
     comm = dnd.Communicator.from_torch_distributed(local)
     O = Oracle()
     ok = True
+    if rank == 0:
+        print(f"transport: {comm.transport}", flush=True)
 
     def report(name, good, detail=""):
         nonlocal ok
