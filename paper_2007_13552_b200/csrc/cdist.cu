@@ -81,44 +81,39 @@ __device__ __forceinline__ void load_slab(float (*dst)[ffma::BM], const float* _
     }
 }
 
-// One 128x128 output tile; FULL = interior tile (no bounds checks), DIAG =
-// the tile meets the self block's diagonal.
-template <bool VEC, bool FULL, bool DIAG>
-__device__ __forceinline__ void cdist_tile_body(const float* __restrict__ x, const float* __restrict__ xn,
-                                                int64_t nx, const float* __restrict__ y,
-                                                const float* __restrict__ yn, int64_t ny, int m,
-                                                float* __restrict__ out, int64_t ld, int64_t row0, int64_t col0,
-                                                int64_t diag_offset, float (*xs)[ffma::BM], float (*ys)[ffma::BN]) {
-    using namespace ffma;
-    const int tid = threadIdx.x;
-    const int tx = tid & 15, ty = tid >> 4;
-    float acc[8][8];
+// acc[i][jp] (column pairs) += x-slab . y-slab over kc features: one FFMA2 with
+// x_i broadcast per two outputs.
+__device__ __forceinline__ void tile_mainloop(float2 (&acc)[8][4], const float (*xs)[ffma::BM],
+                                              const float (*ys)[ffma::BN], int kc) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-    const float* xb = x + row0 * m;
-    const float* yb = y + col0 * m;
-    for (int k0 = 0; k0 < m; k0 += BK) {
-        const int kc = min(BK, m - k0);
-        load_slab<FULL>(xs, xb, nx - row0, m, k0, kc);
-        load_slab<FULL>(ys, yb, ny - col0, m, k0, kc);
-        __syncthreads();
+        for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
 #pragma unroll 2
-        for (int kk = 0; kk < kc; ++kk) {
-            const float4 a0 = *reinterpret_cast<const float4*>(&xs[kk][ty * 4]);
-            const float4 a1 = *reinterpret_cast<const float4*>(&xs[kk][64 + ty * 4]);
-            const float4 b0 = *reinterpret_cast<const float4*>(&ys[kk][tx * 4]);
-            const float4 b1 = *reinterpret_cast<const float4*>(&ys[kk][64 + tx * 4]);
-            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    for (int kk = 0; kk < kc; ++kk) {
+        const float4 a0 = *reinterpret_cast<const float4*>(&xs[kk][ty * 4]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&xs[kk][64 + ty * 4]);
+        const float4 b0 = *reinterpret_cast<const float4*>(&ys[kk][tx * 4]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&ys[kk][64 + tx * 4]);
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                             make_float2(b1.z, b1.w)};
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-        }
-        __syncthreads();
+            for (int j = 0; j < 4; ++j) acc[i][j] = ffma2(make_float2(a[i], a[i]), b[j], acc[i][j]);
     }
+}
+
+// d = sqrt(max(xn_i + yn_j - 2 g_ij, 0)) for the thread's 8x8 outputs, streaming
+// stores; FULL = interior tile (no bounds checks), DIAG = the tile meets the
+// self block's diagonal (entries j == i + diag_offset written as 0).
+template <bool VEC, bool FULL, bool DIAG>
+__device__ __forceinline__ void tile_epilogue(const float2 (&acc)[8][4], const float* __restrict__ xn, int64_t nx,
+                                              const float* __restrict__ yn, int64_t ny, float* __restrict__ out,
+                                              int64_t ld, int64_t row0, int64_t col0, int64_t diag_offset) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     float ynv[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -137,10 +132,17 @@ __device__ __forceinline__ void cdist_tile_body(const float* __restrict__ x, con
             const int c = h * 64 + tx * 4;
             float v[4];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const float sq = fmaxf(fmaf(-2.f, acc[i][h * 4 + jj], xni + ynv[h * 4 + jj]), 0.f);
-                v[jj] = sqrt_approx(sq);
-                if (DIAG && col0 + c + jj == row0 + ri + diag_offset) v[jj] = 0.f;
+            for (int jp = 0; jp < 2; ++jp) {
+                const float2 base =
+                    fadd2(make_float2(xni, xni), make_float2(ynv[h * 4 + 2 * jp], ynv[h * 4 + 2 * jp + 1]));
+                const float2 sq = ffma2(make_float2(-2.f, -2.f), acc[i][h * 2 + jp], base);
+                v[2 * jp] = sqrt_approx(fmaxf(sq.x, 0.f));
+                v[2 * jp + 1] = sqrt_approx(fmaxf(sq.y, 0.f));
+            }
+            if (DIAG) {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                    if (col0 + c + jj == row0 + ri + diag_offset) v[jj] = 0.f;
             }
             if (VEC && (FULL || col0 + c + 3 < ny)) {
                 st_stream4(orow + c, v[0], v[1], v[2], v[3]);
@@ -151,6 +153,51 @@ __device__ __forceinline__ void cdist_tile_body(const float* __restrict__ x, con
             }
         }
     }
+}
+
+// One 128x128 output tile (any m: K slabs of BK through shared memory).
+template <bool VEC, bool FULL, bool DIAG>
+__device__ __forceinline__ void cdist_tile_body(const float* __restrict__ x, const float* __restrict__ xn,
+                                                int64_t nx, const float* __restrict__ y,
+                                                const float* __restrict__ yn, int64_t ny, int m,
+                                                float* __restrict__ out, int64_t ld, int64_t row0, int64_t col0,
+                                                int64_t diag_offset, float (*xs)[ffma::BM], float (*ys)[ffma::BN]) {
+    using namespace ffma;
+    float2 acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    const float* xb = x + row0 * m;
+    const float* yb = y + col0 * m;
+    for (int k0 = 0; k0 < m; k0 += BK) {
+        const int kc = min(BK, m - k0);
+        load_slab<FULL>(xs, xb, nx - row0, m, k0, kc);
+        load_slab<FULL>(ys, yb, ny - col0, m, k0, kc);
+        __syncthreads();
+        if (k0 == 0) {
+            tile_mainloop(acc, xs, ys, kc);
+        } else {
+            // continue the same fma chain across slabs (the norms use one chain)
+            const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll 2
+            for (int kk = 0; kk < kc; ++kk) {
+                const float4 a0 = *reinterpret_cast<const float4*>(&xs[kk][ty * 4]);
+                const float4 a1 = *reinterpret_cast<const float4*>(&xs[kk][64 + ty * 4]);
+                const float4 b0 = *reinterpret_cast<const float4*>(&ys[kk][tx * 4]);
+                const float4 b1 = *reinterpret_cast<const float4*>(&ys[kk][64 + tx * 4]);
+                const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                     make_float2(b1.z, b1.w)};
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = ffma2(make_float2(a[i], a[i]), b[j], acc[i][j]);
+            }
+        }
+        __syncthreads();
+    }
+    tile_epilogue<VEC, FULL, DIAG>(acc, xn, nx, yn, ny, out, ld, row0, col0, diag_offset);
 }
 
 template <bool VEC>
@@ -174,6 +221,72 @@ __global__ void __launch_bounds__(ffma::THREADS)
         cdist_tile_body<VEC, false, true>(x, xn, nx, y, yn, ny, m, o, ld, row0, col0, diag_offset, xs, ys);
     else
         cdist_tile_body<VEC, false, false>(x, xn, nx, y, yn, ny, m, o, ld, row0, col0, diag_offset, xs, ys);
+}
+
+// ------------------------------------------------ f32 persistent row panels
+// For m <= 32 (one K slab; BASELINE cfg2 has m = 18) the one-shot tile kernel
+// spends its time loading operands it never reuses.  Here a CTA keeps a
+// 128-row X slab in shared memory and sweeps PANEL_TILES column tiles of Y,
+// prefetching the next Y slab with cp.async while it computes and stores the
+// current tile: the output stream (the roofline) never waits on operand loads.
+constexpr int PANEL_TILES = 16;
+
+__device__ __forceinline__ void issue_slab_async(float (*dst)[ffma::BM], const float* __restrict__ src, int64_t row0,
+                                                 int64_t n, int m) {
+    for (int idx = threadIdx.x; idx < ffma::BM * m; idx += ffma::THREADS) {
+        const int r = idx & (ffma::BM - 1), kk = idx >> 7;
+        const bool in = row0 + r < n;
+        const float* g = in ? src + (row0 + r) * m + kk : src;
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&dst[kk][r]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(g), "r"(in ? 4 : 0) : "memory");
+    }
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(ffma::THREADS, 2)
+    cdist_panel_f32_kernel(const float* __restrict__ x, const float* __restrict__ xn, int64_t nx,
+                           const float* __restrict__ y, const float* __restrict__ yn, int64_t ny, int m,
+                           float* __restrict__ out, int64_t ld, int64_t col_off, int64_t diag_offset) {
+    using namespace ffma;
+    extern __shared__ __align__(16) float panel_smem[];
+    float(*xs)[BM] = reinterpret_cast<float(*)[BM]>(panel_smem);
+    // (no pointer array: indexing one with a runtime value makes the compiler
+    // fall back to generic loads)
+    auto ys = [&](int b) { return reinterpret_cast<float(*)[BN]>(panel_smem + BK * BM + b * BK * BN); };
+    const int64_t nrb = ceil_div(nx, BM), ncb = ceil_div(ny, BN);
+    const int64_t per_row = ceil_div(ncb, PANEL_TILES), units = nrb * per_row;
+    float* o = out + col_off;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int64_t rb = u / per_row, ct0 = (u % per_row) * PANEL_TILES;
+        const int64_t ct1 = min(ct0 + PANEL_TILES, ncb), row0 = rb * BM;
+        __syncthreads();  // the previous unit's readers are done with xs / ys
+        issue_slab_async(xs, x, row0, nx, m);
+        issue_slab_async(ys(0), y, ct0 * BN, ny, m);
+        cp_async_commit();
+        for (int64_t ct = ct0; ct < ct1; ++ct) {
+            const int buf = static_cast<int>((ct - ct0) & 1);
+            if (ct + 1 < ct1) {
+                issue_slab_async(ys(buf ^ 1), y, (ct + 1) * BN, ny, m);
+                cp_async_commit();
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            float2 acc[8][4];
+            tile_mainloop(acc, xs, ys(buf), m);
+            __syncthreads();  // ys[buf] is refilled at the top of the next tile
+            const int64_t col0 = ct * BN;
+            const bool full = row0 + BM <= nx && col0 + BN <= ny;
+            const bool diag = diag_offset >= 0 && col0 < row0 + diag_offset + BM && row0 + diag_offset < col0 + BN;
+            if (full && !diag)
+                tile_epilogue<VEC, true, false>(acc, xn, nx, yn, ny, o, ld, row0, col0, diag_offset);
+            else if (diag)
+                tile_epilogue<VEC, false, true>(acc, xn, nx, yn, ny, o, ld, row0, col0, diag_offset);
+            else
+                tile_epilogue<VEC, false, false>(acc, xn, nx, yn, ny, o, ld, row0, col0, diag_offset);
+        }
+    }
 }
 
 // ------------------------------------------------------- f64 exact tile
@@ -243,6 +356,19 @@ void cdist_tile(dndc_ctx* ctx, const T* x, const T* xn, int64_t nx, const T* y, 
         }
         const bool vec = (ld_out % 4 == 0) && (col_off % 4 == 0) &&
                          (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+        if (m <= ffma::BK) {
+            const int64_t units = ceil_div(nx, ffma::BM) * ceil_div(ceil_div(ny, ffma::BN), PANEL_TILES);
+            const int grid = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(ctx->num_sms) * 2));
+            const size_t smem = sizeof(float) * 3 * ffma::BK * ffma::BM;
+            if (vec)
+                cdist_panel_f32_kernel<true><<<grid, ffma::THREADS, smem, stream>>>(
+                    x, xn, nx, y, yn, ny, static_cast<int>(m), out, ld_out, col_off, diag_offset);
+            else
+                cdist_panel_f32_kernel<false><<<grid, ffma::THREADS, smem, stream>>>(
+                    x, xn, nx, y, yn, ny, static_cast<int>(m), out, ld_out, col_off, diag_offset);
+            DNDC_LAUNCHED(ctx);
+            return;
+        }
         const int64_t row_blocks = ceil_div(nx, ffma::BM);
         const unsigned gx = static_cast<unsigned>(ceil_div(ny, ffma::BN));
         for (int64_t rb = 0; rb < row_blocks; rb += 65535) {
