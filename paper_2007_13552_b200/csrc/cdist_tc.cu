@@ -33,10 +33,14 @@ constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2;
 constexpr int A_BYTES = BM * BK * 4;   // 16 KB
 constexpr int B_BYTES = BN * BK * 4;   // 32 KB
 constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // raw + lo
-constexpr int OFF_BAR = STAGES * STAGE_BYTES;
+constexpr int EPI_WARPS = 8;                            // 2 per TMEM lane quarter
+constexpr int STG_BOX = 16 * 32 * 4;                    // one store box: 32 rows x 16 cols (SWIZZLE_64B)
+constexpr int STG_BYTES = 2 * STG_BOX;                  // per epilogue warp: double-buffered
+constexpr int OFF_STG = STAGES * STAGE_BYTES;
+constexpr int OFF_BAR = OFF_STG + EPI_WARPS * STG_BYTES;
 constexpr int NBARS = 3 * STAGES + 4;
 constexpr int SMEM = OFF_BAR + NBARS * 8 + 16 + 1024;  // + alignment slack
-constexpr int THREADS = 320;
+constexpr int THREADS = (6 + EPI_WARPS) * 32;
 constexpr int TMEM_COLS = 512;
 constexpr int GROUP = 16;  // rasterisation: GROUP x GROUP tile super-blocks
 }  // namespace cdtc
@@ -60,10 +64,15 @@ __device__ __forceinline__ void cdtc_tile_of(int64_t t, int64_t nrb, int64_t ncb
     cb = r / rows_in_group;
 }
 
-template <bool NORM>
+// MODE 0: row norms (diagonal tiles); 1: distances with direct stores (any
+// alignment); 2: distances staged in swizzled shared memory and written by TMA
+// bulk stores (32x32 boxes, out-of-range rows/columns clipped by the unit).
+template <int MODE>
 __global__ void __launch_bounds__(cdtc::THREADS, 1)
-    cdist_tc_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant__ CUtensorMap mapy, CdtcParams p) {
+    cdist_tc_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant__ CUtensorMap mapy,
+                    const __grid_constant__ CUtensorMap mapo, CdtcParams p) {
     using namespace cdtc;
+    constexpr bool NORM = MODE == 0;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -180,8 +189,79 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 if (st == 0) tc::mbar_arrive(&split[s]);
             }
         }
-    } else {
-        // ------------------------------------------------------- epilogue warps
+    } else if (MODE == 2) {
+        // ------------------------------------------------------- epilogue (TMA stores)
+        // warp e: TMEM lanes of quarter (warp % 4), columns [128 h, 128 h + 128)
+        const int e = warp - 6, q = warp & 3, half = e >> 2;
+        const int r = q * 32 + lane;
+        unsigned char* stg = smem + OFF_STG + e * STG_BYTES;  // 2 boxes, 512-aligned (SWIZZLE_64B atoms)
+        int64_t tcount = 0, nbox = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+            int64_t rb, cb;
+            cdtc_tile_of(t, nrb, ncb, rb, cb);
+            const int64_t row0 = rb * BM, col0 = cb * BN;
+            const int b = static_cast<int>(tcount & 1);
+            tc::mbar_wait(&tfull[b], static_cast<uint32_t>((tcount / 2) & 1));
+            tc::tc_fence_after();
+            const int64_t gi = row0 + r;
+            const float xni = gi < p.nx ? __ldg(p.xn + gi) : 0.f;
+            const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * BN;
+            const bool diag = p.diag_offset >= 0 && col0 < row0 + p.diag_offset + BM &&
+                              row0 + p.diag_offset < col0 + BN;
+#pragma unroll 1
+            for (int cc = 0; cc < 8; ++cc, ++nbox) {
+                const int c0 = half * 128 + cc * 16;
+                float v[16];
+                tc::tmem_ld16(trow + c0, v);
+                const int64_t gc = col0 + c0;
+                float d[16];
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    float4 yv = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (gc + j + 3 < p.ny) {
+                        yv = __ldg(reinterpret_cast<const float4*>(p.yn + gc + j));
+                    } else {
+                        if (gc + j < p.ny) yv.x = __ldg(p.yn + gc + j);
+                        if (gc + j + 1 < p.ny) yv.y = __ldg(p.yn + gc + j + 1);
+                        if (gc + j + 2 < p.ny) yv.z = __ldg(p.yn + gc + j + 2);
+                    }
+                    const float2 b0 = fadd2(make_float2(xni, xni), make_float2(yv.x, yv.y));
+                    const float2 b1 = fadd2(make_float2(xni, xni), make_float2(yv.z, yv.w));
+                    const float2 s0 = ffma2(make_float2(-2.f, -2.f), make_float2(v[j], v[j + 1]), b0);
+                    const float2 s1 = ffma2(make_float2(-2.f, -2.f), make_float2(v[j + 2], v[j + 3]), b1);
+                    d[j] = sqrt_approx(fmaxf(s0.x, 0.f));
+                    d[j + 1] = sqrt_approx(fmaxf(s0.y, 0.f));
+                    d[j + 2] = sqrt_approx(fmaxf(s1.x, 0.f));
+                    d[j + 3] = sqrt_approx(fmaxf(s1.y, 0.f));
+                }
+                if (diag) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (gc + j == gi + p.diag_offset) d[j] = 0.f;
+                }
+                // buffer nbox & 1: its previous box (two stores ago) has been read
+                unsigned char* box = stg + (nbox & 1) * STG_BOX;
+                if (lane == 0) tc::bulk_wait_read1();
+                __syncwarp();
+                // SWIZZLE_64B: 16-byte chunk j of row `lane` sits at chunk j ^ ((lane >> 1) & 3)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    *reinterpret_cast<float4*>(box + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                        make_float4(d[4 * j], d[4 * j + 1], d[4 * j + 2], d[4 * j + 3]);
+                tc::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tc::tma_store_2d(&mapo, box, static_cast<int>(gc), static_cast<int>(row0 + q * 32));
+                    tc::bulk_commit();
+                }
+            }
+            tc::tc_fence_before();
+            tc::named_sync(2, 32 * EPI_WARPS);
+            if (e == 0 && lane == 0) tc::mbar_arrive(&tempty[b]);
+        }
+        if (lane == 0) tc::bulk_wait0();
+    } else if (warp < 10) {
+        // ------------------------------------------------------- epilogue warps (MODE 0 / 1)
         const int q = warp & 3;             // TMEM lane quarter of this warp
         const int r = q * 32 + lane;        // accumulator row = TMEM lane
         int64_t tcount = 0;
@@ -252,14 +332,24 @@ static int tc_min_m() {
 }
 
 bool cdist_tc_eligible(int64_t nx, int64_t ny, int64_t m) {
-    return m >= tc_min_m() && m % 4 == 0 && nx >= 128 && ny >= 128;
+    return m >= tc_min_m() && nx >= 128 && ny >= 128;
 }
 
 // Padded view for TMA: row pitch must be a multiple of 16 bytes.
-static const float* tma_view(dndc_ctx* ctx, const char* slot, const float* src, int64_t rows, int64_t m,
-                             cudaStream_t s) {
-    if (m % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) return src;
-    throw Error(DNDC_EINTERNAL, "cdist_tc: unaligned operand");
+// (m = 18 rows are 72 B apart: a pitched copy with 16-byte-multiple pitch; the
+// pad columns are never read -- the tensor map has m columns, TMA zero-fills)
+struct TmaView {
+    const float* p;
+    int64_t pitch;  // elements
+};
+static TmaView tma_view(dndc_ctx* ctx, const char* slot, const float* src, int64_t rows, int64_t m, cudaStream_t s) {
+    if (m % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) return {src, m};
+    const int64_t pitch = (m + 3) / 4 * 4;
+    float* dst = static_cast<float*>(ctx->slot(slot, sizeof(float) * std::max<int64_t>(rows, 1) * pitch));
+    if (rows > 0)
+        DNDC_CUDA(cudaMemcpy2DAsync(dst, pitch * sizeof(float), src, m * sizeof(float), m * sizeof(float), rows,
+                                    cudaMemcpyDeviceToDevice, s));
+    return {dst, pitch};
 }
 
 void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, int64_t nx, const float* y,
@@ -268,35 +358,38 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     using namespace cdtc;
     (void)xn_unused;
     (void)yn_unused;
-    const float* xa = tma_view(ctx, "cdtc_x", x, nx, m, stream);
-    const float* ya = tma_view(ctx, "cdtc_y", y, ny, m, stream);
+    const TmaView xv = tma_view(ctx, "cdtc_x", x, nx, m, stream);
+    const TmaView yv = (y == x && ny == nx) ? xv : tma_view(ctx, "cdtc_y", y, ny, m, stream);
+    const float* xa = xv.p;
+    const float* ya = yv.p;
     static bool attr = false;
     if (!attr) {
-        DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-        DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
         attr = true;
     }
     // norms through the same tensor-core path (diagonal tiles)
     float* xn = static_cast<float*>(ctx->slot("cdtc_xn", sizeof(float) * std::max<int64_t>(nx, 1)));
     float* yn = static_cast<float*>(ctx->slot("cdtc_yn", sizeof(float) * std::max<int64_t>(ny, 1)));
-    auto norms = [&](const float* a, int64_t rows, float* dst) {
-        const CUtensorMap ma = make_tmap_2d_f32(a, rows, m, m * 4, BK, BM, true);
-        const CUtensorMap mb = make_tmap_2d_f32(a, rows, m, m * 4, BK, BN, true);
+    auto norms = [&](const float* a, int64_t pitch, int64_t rows, float* dst) {
+        const CUtensorMap ma = make_tmap_2d_f32(a, rows, m, pitch * 4, BK, BM, true);
+        const CUtensorMap mb = make_tmap_2d_f32(a, rows, m, pitch * 4, BK, BN, true);
         CdtcParams np{};
         np.nx = rows;
         np.ny = rows;
         np.m = static_cast<int>(m);
         np.out = dst;
         const int grid = static_cast<int>(std::min<int64_t>(ceil_div(rows, BM), ctx->num_sms));
-        cdist_tc_kernel<true><<<grid, THREADS, SMEM, stream>>>(ma, mb, np);
+        cdist_tc_kernel<0><<<grid, THREADS, SMEM, stream>>>(ma, mb, ma, np);
         DNDC_LAUNCHED(ctx);
     };
-    norms(xa, nx, xn);
+    norms(xa, xv.pitch, nx, xn);
     if (ya == xa && ny == nx) DNDC_CUDA(cudaMemcpyAsync(yn, xn, sizeof(float) * nx, cudaMemcpyDeviceToDevice, stream));
-    else norms(ya, ny, yn);
+    else norms(ya, yv.pitch, ny, yn);
 
-    const CUtensorMap mx = make_tmap_2d_f32(xa, nx, m, m * 4, BK, BM, true);
-    const CUtensorMap my = make_tmap_2d_f32(ya, ny, m, m * 4, BK, BN, true);
+    const CUtensorMap mx = make_tmap_2d_f32(xa, nx, m, xv.pitch * 4, BK, BM, true);
+    const CUtensorMap my = make_tmap_2d_f32(ya, ny, m, yv.pitch * 4, BK, BN, true);
     CdtcParams pp{};
     pp.nx = nx;
     pp.ny = ny;
@@ -310,7 +403,14 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     pp.vec = (ld_out % 4 == 0) && (col_off % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
     const int64_t tiles = ceil_div(nx, BM) * ceil_div(ny, BN);
     const int grid = static_cast<int>(std::min<int64_t>(tiles, ctx->num_sms));
-    cdist_tc_kernel<false><<<grid, THREADS, SMEM, stream>>>(mx, my, pp);
+    float* obase = out + col_off;
+    if (pp.vec && (ld_out * 4) % 16 == 0 && ny >= 16) {
+        // TMA stores: the window [nx x ny] of the ld-wide output at col_off
+        const CUtensorMap mo = make_tmap_2d_f32_swz(obase, nx, ny, ld_out * 4, 16, 32, 64);
+        cdist_tc_kernel<2><<<grid, THREADS, SMEM, stream>>>(mx, my, mo, pp);
+    } else {
+        cdist_tc_kernel<1><<<grid, THREADS, SMEM, stream>>>(mx, my, mx, pp);
+    }
     DNDC_LAUNCHED(ctx);
 }
 

@@ -115,6 +115,11 @@ __global__ void __launch_bounds__(128) tc_probe_kernel(int mode, const float* a,
 
 CUtensorMap make_tmap_2d_f32(const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_bytes, uint32_t box_cols,
                              uint32_t box_rows, bool swizzle128) {
+    return make_tmap_2d_f32_swz(base, rows, cols, pitch_bytes, box_cols, box_rows, swizzle128 ? 128 : 0);
+}
+
+CUtensorMap make_tmap_2d_f32_swz(const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_bytes,
+                                 uint32_t box_cols, uint32_t box_rows, int swizzle_bytes) {
     using encode_t = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -133,7 +138,9 @@ CUtensorMap make_tmap_2d_f32(const void* base, uint64_t rows, uint64_t cols, uin
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                              swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                              : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                    : CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(DNDC_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return map;
