@@ -242,8 +242,11 @@ __device__ __forceinline__ void issue_slab_async(float (*dst)[ffma::BM], const f
     }
 }
 
+#ifndef CDIST_PANEL_CTAS
+#define CDIST_PANEL_CTAS 2
+#endif
 template <bool VEC>
-__global__ void __launch_bounds__(ffma::THREADS, 2)
+__global__ void __launch_bounds__(ffma::THREADS, CDIST_PANEL_CTAS)
     cdist_panel_f32_kernel(const float* __restrict__ x, const float* __restrict__ xn, int64_t nx,
                            const float* __restrict__ y, const float* __restrict__ yn, int64_t ny, int m,
                            float* __restrict__ out, int64_t ld, int64_t col_off, int64_t diag_offset) {
@@ -358,7 +361,7 @@ void cdist_tile(dndc_ctx* ctx, const T* x, const T* xn, int64_t nx, const T* y, 
                          (reinterpret_cast<uintptr_t>(out) % 16 == 0);
         if (m <= ffma::BK) {
             const int64_t units = ceil_div(nx, ffma::BM) * ceil_div(ceil_div(ny, ffma::BN), PANEL_TILES);
-            const int grid = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(ctx->num_sms) * 2));
+            const int grid = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(ctx->num_sms) * CDIST_PANEL_CTAS));
             const size_t smem = sizeof(float) * 3 * ffma::BK * ffma::BM;
             if (vec)
                 cdist_panel_f32_kernel<true><<<grid, ffma::THREADS, smem, stream>>>(

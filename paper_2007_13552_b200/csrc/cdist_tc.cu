@@ -208,13 +208,8 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
             const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * BN;
             const bool diag = p.diag_offset >= 0 && col0 < row0 + p.diag_offset + BM &&
                               row0 + p.diag_offset < col0 + BN;
-#pragma unroll 1
-            for (int cc = 0; cc < 8; ++cc, ++nbox) {
-                const int c0 = half * 128 + cc * 16;
-                float v[16];
-                tc::tmem_ld16(trow + c0, v);
-                const int64_t gc = col0 + c0;
-                float d[16];
+            // column norms of a 16-column chunk, fetched one chunk ahead
+            auto load_yn = [&](int64_t gc, float4 (&y4)[4]) {
 #pragma unroll
                 for (int j = 0; j < 16; j += 4) {
                     float4 yv = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -225,6 +220,25 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                         if (gc + j + 1 < p.ny) yv.y = __ldg(p.yn + gc + j + 1);
                         if (gc + j + 2 < p.ny) yv.z = __ldg(p.yn + gc + j + 2);
                     }
+                    y4[j / 4] = yv;
+                }
+            };
+            float4 ynext[4];
+            load_yn(col0 + half * 128, ynext);
+#pragma unroll 1
+            for (int cc = 0; cc < 8; ++cc, ++nbox) {
+                const int c0 = half * 128 + cc * 16;
+                float v[16];
+                tc::tmem_ld16(trow + c0, v);
+                const int64_t gc = col0 + c0;
+                float4 ycur[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) ycur[u] = ynext[u];
+                if (cc + 1 < 8) load_yn(gc + 16, ynext);
+                float d[16];
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    const float4 yv = ycur[j / 4];
                     const float2 b0 = fadd2(make_float2(xni, xni), make_float2(yv.x, yv.y));
                     const float2 b1 = fadd2(make_float2(xni, xni), make_float2(yv.z, yv.w));
                     const float2 s0 = ffma2(make_float2(-2.f, -2.f), make_float2(v[j], v[j + 1]), b0);
