@@ -1931,7 +1931,8 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     DNDC_CUDA(cudaGraphLaunch(ctx->km->exec, gs));
     DNDC_CUDA(cudaEventRecord(ctx->ev_b, gs));
     DNDC_CUDA(cudaStreamWaitEvent(s, ctx->ev_b, 0));
-    ctx->launches += 1 + (fuse ? 1ull : 3ull) * max_iter;  // reset + (assign[, reduce, update]) per iteration
+    // reset + per iteration: assign (fused) | [tile reset,] assign, reduce, update
+    ctx->launches += 1 + (fuse ? 1ull : A.small ? 4ull : 3ull) * max_iter;
     if (ctx->world > 1) ctx->counters.allgathers += max_iter;
 
     // ---- results
