@@ -1392,24 +1392,50 @@ static size_t update_smem(int k, int d) {
     return bytes;
 }
 
-// Validation pass (cluster.cpp:88-89) fused with sum |x|^2.
+// Validation pass (cluster.cpp:88-89) fused with sum |x|^2 and max |x|.  fp32
+// input streams as float4 (two independent f64 sums; x*x is exact in f64).
 template <typename T>
-__global__ void validate_kernel(const T* __restrict__ x, int64_t count, double* out) {
+__global__ void __launch_bounds__(256) validate_kernel(const T* __restrict__ x, int64_t count, double* out) {
     __shared__ double sh[256];
-    double s = 0.0, bad = 0.0, mx = 0.0;
+    double s = 0.0, s2 = 0.0, bad = 0.0;
+    float mxf = 0.f;
+    double mx = 0.0;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += stride) {
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int64_t tail0 = 0;
+    if constexpr (sizeof(T) == 4) {
+        if (reinterpret_cast<uintptr_t>(x) % 16 == 0) {
+            const float4* x4 = reinterpret_cast<const float4*>(x);
+            const int64_t n4 = count / 4;
+            for (int64_t i = t0; i < n4; i += stride) {
+                const float4 v = __ldg(x4 + i);
+                const float a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if ((__float_as_uint(a[u]) & 0x7f800000u) == 0x7f800000u) {
+                        bad += 1.0;
+                    } else {
+                        const double d = static_cast<double>(a[u]);
+                        if (u & 1) s2 = fma(d, d, s2); else s = fma(d, d, s);
+                        mxf = fmaxf(mxf, fabsf(a[u]));
+                    }
+                }
+            }
+            tail0 = n4 * 4;
+        }
+    }
+    for (int64_t e = tail0 + t0; e < count; e += stride) {
         const double v = static_cast<double>(x[e]);
         if (!isfinite(v)) {
             bad += 1.0;
         } else {
-            s += v * v;
+            s = fma(v, v, s);
             mx = fmax(mx, fabs(v));
         }
     }
-    s = block_sum(s, sh);
+    s = block_sum(s + s2, sh);
     bad = block_sum(bad, sh);
-    mx = block_max(mx, sh);
+    mx = block_max(fmax(mx, static_cast<double>(mxf)), sh);
     if (threadIdx.x == 0) {
         out[3 * blockIdx.x] = s;
         out[3 * blockIdx.x + 1] = bad;
@@ -1757,7 +1783,9 @@ static void init_centroids(dndc_ctx* ctx, const KmBuffers& b, const T* x_local, 
 // validation pass: sum x^2, non-finite count and max |x| of the shard -> b.sx2[0, 1, 3]
 template <typename T>
 static void scan_input(dndc_ctx* ctx, const KmBuffers& b, const T* x, int64_t count, cudaStream_t s) {
-    const int G = static_cast<int>(std::min<int64_t>(std::max<int64_t>(ceil_div(count, 256 * 8), 1), 4096));
+    // enough CTAs for ~32 KB in flight per SM, each thread >= 8 float4
+    const int G = static_cast<int>(std::min<int64_t>(std::max<int64_t>(ceil_div(count, 256 * 32), 1),
+                                                     static_cast<int64_t>(ctx->num_sms) * 8));
     validate_kernel<T><<<G, 256, 0, s>>>(x, count, b.pre);
     DNDC_LAUNCHED(ctx);
     validate_final_kernel<<<1, 256, 0, s>>>(b.pre, G, b.sx2);
