@@ -5,18 +5,20 @@
 // Reference: distance_block / matmul_local (pairwise.cpp:22-33,
 // ndarray.hpp:400-418), place_chunk (tile.hpp:90-107).
 //
-// Persistent CTAs, one per SM, 10 warps:
+// Persistent CTAs, one per SM, 14 warps (2-5 idle):
 //   warp 0      TMA producer: 32-column K chunks of a 128-row X tile and a
 //               256-row Y tile, SWIZZLE_128B K-major, 2-stage ring.
 //   warp 1      TMEM allocator + MMA issuer: per K=8 step three
 //               tcgen05.mma.kind::tf32 (M=128, N=256): hi.hi + hi.lo + lo.hi into
 //               a 128x256 fp32 TMEM accumulator (double-buffered: 512 columns).
-//   warps 2-5   split: lo = x - trunc_tf32(x) for both tiles of each stage (the
-//               tensor core truncates fp32 operands to tf32 -- pinned by
-//               tests/test_gpu_tc.py -- so the raw tile is the hi operand).
-//   warps 6-9   epilogue: tcgen05.ld of each accumulator row, then
-//               d = sqrt(max(xn + yn - 2g, 0)) with streaming stores into the
-//               ld-wide row block at col_off (+ the self block's zero diagonal).
+//   (lo = x - trunc_tf32(x) is made once per operand by split_lo_kernel and
+//    loaded by TMA next to the raw tile, which is the hi operand: the tensor
+//    core truncates fp32 to tf32 -- pinned by tests/test_gpu_tc.py.  Splitting
+//    in shared memory per tile cost as much smem bandwidth as the MMAs.)
+//   warps 6-13  epilogue: tcgen05.ld of each accumulator row, then
+//               d = sqrt(max(xn + yn - 2g, 0)) into swizzled smem boxes written
+//               by TMA bulk stores (+ the self block's zero diagonal); rows
+//               whose window is not 16-byte aligned use direct stores (warps 6-9).
 // The row norms come from the SAME tensor-core path (a diagonal-tile pass), so a
 // row's dot product with itself equals its norm bit for bit and duplicate rows
 // cancel to exactly 0, as in the reference.
@@ -70,6 +72,7 @@ __device__ __forceinline__ void cdtc_tile_of(int64_t t, int64_t nrb, int64_t ncb
 template <int MODE>
 __global__ void __launch_bounds__(cdtc::THREADS, 1)
     cdist_tc_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant__ CUtensorMap mapy,
+                    const __grid_constant__ CUtensorMap mapxl, const __grid_constant__ CUtensorMap mapyl,
                     const __grid_constant__ CUtensorMap mapo, CdtcParams p) {
     using namespace cdtc;
     constexpr bool NORM = MODE == 0;
@@ -126,9 +129,13 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                     const int s = static_cast<int>(g % STAGES);
                     if (g >= STAGES) tc::mbar_wait(&empty[s], static_cast<uint32_t>((g / STAGES - 1) & 1));
                     unsigned char* st = stage_ptr(s);
-                    tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+                    // hi = the raw tile (the tensor core truncates to tf32), lo from
+                    // the pre-split copies: no generic-proxy pass over the stage
+                    tc::mbar_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
                     tc::tma_load_2d(st, &mapx, &full[s], kc * BK, row0);
                     tc::tma_load_2d(st + A_BYTES, &mapy, &full[s], kc * BK, col0);
+                    tc::tma_load_2d(st + A_BYTES + B_BYTES, &mapxl, &full[s], kc * BK, row0);
+                    tc::tma_load_2d(st + 2 * A_BYTES + B_BYTES, &mapyl, &full[s], kc * BK, col0);
                 }
             }
         }
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 const uint32_t dt = tmem + b * BN;
                 for (int kc = 0; kc < kchunks; ++kc, ++g) {
                     const int s = static_cast<int>(g % STAGES);
-                    tc::mbar_wait(&split[s], static_cast<uint32_t>((g / STAGES) & 1));
+                    tc::mbar_wait(&full[s], static_cast<uint32_t>((g / STAGES) & 1));
                     tc::tc_fence_after();
                     const uint32_t a = tc::smem_u32(stage_ptr(s));
                     const uint32_t bsm = a + A_BYTES, alo = a + A_BYTES + B_BYTES, blo = alo + A_BYTES;
@@ -164,31 +171,8 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
             }
         }
     } else if (warp < 6) {
-        // ------------------------------------------------------- split warps
-        const int st = threadIdx.x - 64;  // 0..127
-        int64_t g = 0;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            for (int kc = 0; kc < kchunks; ++kc, ++g) {
-                const int s = static_cast<int>(g % STAGES);
-                tc::mbar_wait(&full[s], static_cast<uint32_t>((g / STAGES) & 1));
-                const float4* src = reinterpret_cast<const float4*>(stage_ptr(s));
-                float4* dst = reinterpret_cast<float4*>(stage_ptr(s) + A_BYTES + B_BYTES);
-                constexpr int N4 = (A_BYTES + B_BYTES) / 16;
-#pragma unroll 4
-                for (int i = st; i < N4; i += 128) {
-                    const float4 v = src[i];
-                    float4 l;
-                    l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                    l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                    l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                    l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                    dst[i] = l;
-                }
-                tc::fence_async_smem();
-                tc::named_sync(1, 128);
-                if (st == 0) tc::mbar_arrive(&split[s]);
-            }
-        }
+        // (warps 2-5 split lo = x - trunc_tf32(x) in an earlier version; the lo
+        // operands now arrive pre-split by TMA -- see split_lo_kernel)
     } else if (MODE == 2) {
         // ------------------------------------------------------- epilogue (TMA stores)
         // warp e: TMEM lanes of quarter (warp % 4), columns [128 h, 128 h + 128)
@@ -366,6 +350,34 @@ static TmaView tma_view(dndc_ctx* ctx, const char* slot, const float* src, int64
     return {dst, pitch};
 }
 
+// lo = x - trunc_tf32(x) over a pitched fp32 matrix (pad columns included;
+// the tensor maps never read them): the 3xTF32 low operand, made once per
+// operand instead of per tile inside the kernel.
+__global__ void split_lo_kernel(const float4* __restrict__ src, int64_t count4, float4* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count4;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const float4 v = __ldg(src + i);
+        float4 l;
+        l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+        l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+        l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+        l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+        dst[i] = l;
+    }
+}
+
+static TmaView lo_view(dndc_ctx* ctx, const char* slot, TmaView v, int64_t rows, cudaStream_t s) {
+    float* dst = static_cast<float*>(ctx->slot(slot, sizeof(float) * std::max<int64_t>(rows, 1) * v.pitch));
+    const int64_t count4 = rows * v.pitch / 4;
+    if (count4 > 0) {
+        const int grid = static_cast<int>(std::min<int64_t>(ceil_div(count4, 256), ctx->num_sms * 8));
+        split_lo_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(v.p), count4,
+                                             reinterpret_cast<float4*>(dst));
+        DNDC_LAUNCHED(ctx);
+    }
+    return {dst, v.pitch};
+}
+
 void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, int64_t nx, const float* y,
                        const float* yn_unused, int64_t ny, int64_t m, float* out, int64_t ld_out, int64_t col_off,
                        int64_t diag_offset, cudaStream_t stream) {
@@ -376,6 +388,8 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     const TmaView yv = (y == x && ny == nx) ? xv : tma_view(ctx, "cdtc_y", y, ny, m, stream);
     const float* xa = xv.p;
     const float* ya = yv.p;
+    const TmaView xl = lo_view(ctx, "cdtc_xlo", xv, nx, stream);
+    const TmaView yl = (ya == xa && ny == nx) ? xl : lo_view(ctx, "cdtc_ylo", yv, ny, stream);
     static bool attr = false;
     if (!attr) {
         DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -386,24 +400,28 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     // norms through the same tensor-core path (diagonal tiles)
     float* xn = static_cast<float*>(ctx->slot("cdtc_xn", sizeof(float) * std::max<int64_t>(nx, 1)));
     float* yn = static_cast<float*>(ctx->slot("cdtc_yn", sizeof(float) * std::max<int64_t>(ny, 1)));
-    auto norms = [&](const float* a, int64_t pitch, int64_t rows, float* dst) {
+    auto norms = [&](const float* a, const float* al, int64_t pitch, int64_t rows, float* dst) {
         const CUtensorMap ma = make_tmap_2d_f32(a, rows, m, pitch * 4, BK, BM, true);
         const CUtensorMap mb = make_tmap_2d_f32(a, rows, m, pitch * 4, BK, BN, true);
+        const CUtensorMap mal = make_tmap_2d_f32(al, rows, m, pitch * 4, BK, BM, true);
+        const CUtensorMap mbl = make_tmap_2d_f32(al, rows, m, pitch * 4, BK, BN, true);
         CdtcParams np{};
         np.nx = rows;
         np.ny = rows;
         np.m = static_cast<int>(m);
         np.out = dst;
         const int grid = static_cast<int>(std::min<int64_t>(ceil_div(rows, BM), ctx->num_sms));
-        cdist_tc_kernel<0><<<grid, THREADS, SMEM, stream>>>(ma, mb, ma, np);
+        cdist_tc_kernel<0><<<grid, THREADS, SMEM, stream>>>(ma, mb, mal, mbl, ma, np);
         DNDC_LAUNCHED(ctx);
     };
-    norms(xa, xv.pitch, nx, xn);
+    norms(xa, xl.p, xv.pitch, nx, xn);
     if (ya == xa && ny == nx) DNDC_CUDA(cudaMemcpyAsync(yn, xn, sizeof(float) * nx, cudaMemcpyDeviceToDevice, stream));
-    else norms(ya, yv.pitch, ny, yn);
+    else norms(ya, yl.p, yv.pitch, ny, yn);
 
     const CUtensorMap mx = make_tmap_2d_f32(xa, nx, m, xv.pitch * 4, BK, BM, true);
     const CUtensorMap my = make_tmap_2d_f32(ya, ny, m, yv.pitch * 4, BK, BN, true);
+    const CUtensorMap mxl = make_tmap_2d_f32(xl.p, nx, m, xl.pitch * 4, BK, BM, true);
+    const CUtensorMap myl = make_tmap_2d_f32(yl.p, ny, m, yl.pitch * 4, BK, BN, true);
     CdtcParams pp{};
     pp.nx = nx;
     pp.ny = ny;
@@ -421,9 +439,9 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     if (pp.vec && (ld_out * 4) % 16 == 0 && ny >= 16) {
         // TMA stores: the window [nx x ny] of the ld-wide output at col_off
         const CUtensorMap mo = make_tmap_2d_f32_swz(obase, nx, ny, ld_out * 4, 16, 32, 64);
-        cdist_tc_kernel<2><<<grid, THREADS, SMEM, stream>>>(mx, my, mo, pp);
+        cdist_tc_kernel<2><<<grid, THREADS, SMEM, stream>>>(mx, my, mxl, myl, mo, pp);
     } else {
-        cdist_tc_kernel<1><<<grid, THREADS, SMEM, stream>>>(mx, my, mx, pp);
+        cdist_tc_kernel<1><<<grid, THREADS, SMEM, stream>>>(mx, my, mxl, myl, mx, pp);
     }
     DNDC_LAUNCHED(ctx);
 }
