@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cdist", action="store_true", help="skip the secondary cdist (config 2) measurement")
     return ap.parse_args()
 
 
@@ -292,6 +293,41 @@ def run_ours(args):
             "iteration_us": iter_us,
             "iteration_frac_of_hbm_floor": (byt / (peak * 1e9)) / (iter_us * 1e-6)}
 
+    # ---- secondary metric of BASELINE.json: cdist GB/s on config 2 (X, Y
+    # 200k x 18 fp32 split over the ranks, Y's shards travelling the ring);
+    # bytes = output written + inputs read, time = max over ranks
+    cdist = None
+    if not args.no_cdist:
+        del x, xe, dev_x, host_x
+        torch.cuda.empty_cache()
+        n2, m2 = 200_000, 18
+        xa = dnd.random_uniform((n2, m2), 0, 42, comm)
+        ya = dnd.random_uniform((n2, m2), 0, 43, comm)
+        d = dnd.cdist_xy(xa, ya)  # warm (allocates the output shard)
+        barrier()
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        reps = 3
+        c0.record(stream)
+        for _ in range(reps):
+            d = dnd.cdist_xy(xa, ya)
+        c1.record(stream)
+        barrier()
+        tc_ms = c0.elapsed_time(c1) / reps
+        if dist:
+            t = torch.tensor([tc_ms], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tc_ms = float(t.item())
+        byt = 4.0 * n2 * n2 + 4.0 * 2 * n2 * m2
+        gbs = byt / (tc_ms * 1e-3) / 1e9
+        cdist = {"metric": "cdist GB/s (config 2: X, Y 200k x 18 fp32, split=0, Y shards on the ring)",
+                 "value": gbs, "unit": "GB/s", "ms_per_call": tc_ms, "bytes_per_call": byt,
+                 "roofline": {"bound": "hbm (output write)", "achieved": gbs, "peak": peak * world,
+                              "frac": gbs / (peak * world), "unit": "GB/s",
+                              "kernel": "cdist_panel_f32_kernel (FFMA2, persistent row panels)"}}
+        del d, xa, ya
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline()
@@ -303,6 +339,7 @@ def run_ours(args):
             "config": config(world), "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
             "cpu_baseline": cpu, "clocks": clk, "refined_rows_last_fit": model.refined_rows,
             "stats_exchange": comm.transport if world > 1 else "single GPU (fused in-kernel update)",
+            "cdist_cfg2": cdist,
             "final_inertia": model.inertia_trace[-1],
         }))
     if dist:

@@ -11,7 +11,7 @@ timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=
 timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc=$?" >> $OUT/bench_ref.err
 if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_bench.csv \
-      python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
+      python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-cdist > $OUT/ncu_launch.log 2>&1
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:kmeans_small -s 12 -c 1 \
       -o $OUT/prof_assign python tools/prof_kmeans.py 5000000 18 8 20 > $OUT/ncu_full.log 2>&1
 fi
