@@ -35,19 +35,24 @@ constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2;
 constexpr int A_BYTES = BM * BK * 4;   // 16 KB
 constexpr int B_BYTES = BN * BK * 4;   // 32 KB
 constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // raw + lo
-constexpr int EPI_WARPS = 8;                            // 2 per TMEM lane quarter
+constexpr int EPI_MAX = 12;                             // epilogue warps: 8 (2 stages) or 12 (1 stage)
 constexpr int STG_BOX = 16 * 32 * 4;                    // one store box: 32 rows x 16 cols (SWIZZLE_64B)
 constexpr int STG_BYTES = 2 * STG_BOX;                  // per epilogue warp: double-buffered
-constexpr int OFF_STG = STAGES * STAGE_BYTES;
-constexpr int OFF_BAR = OFF_STG + EPI_WARPS * STG_BYTES;
 constexpr int NBARS = 3 * STAGES + 4;
-constexpr int SMEM = OFF_BAR + NBARS * 8 + 16 + 1024;  // + alignment slack
-constexpr int THREADS = (6 + EPI_WARPS) * 32;
+constexpr int THREADS = (2 + EPI_MAX) * 32;
+// shared-memory layout for `nst` stages and `epi` TMA-store epilogue warps
+__host__ __device__ constexpr int off_stg(int nst) { return nst * STAGE_BYTES; }
+__host__ __device__ constexpr int off_bar(int nst, int epi) { return off_stg(nst) + epi * STG_BYTES; }
+__host__ __device__ constexpr int smem_bytes(int nst, int epi) { return off_bar(nst, epi) + NBARS * 8 + 16 + 1024; }
+constexpr int SMEM = smem_bytes(2, 8);  // the largest configuration
+static_assert(smem_bytes(1, 12) <= SMEM, "smem layouts");
 constexpr int TMEM_COLS = 512;
 constexpr int GROUP = 16;  // rasterisation: GROUP x GROUP tile super-blocks
 }  // namespace cdtc
 
 struct CdtcParams {
+    int nst;          // TMA stages (1 when a tile is one K chunk: the MMAs are short)
+    int epi;          // TMA-store epilogue warps (MODE 2): 8 = warps 6-13, 12 = warps 2-13
     int64_t nx, ny;
     int m;
     const float* xn;   // norms (null in NORM mode)
@@ -78,7 +83,9 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
     constexpr bool NORM = MODE == 0;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    const int nst = p.nst, epi = MODE == 2 ? p.epi : 8;
+    const int STG = nst;  // stages in use
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off_bar(nst, epi));
     uint64_t* full = bars;                 // [STAGES] TMA landed
     uint64_t* split = bars + STAGES;       // [STAGES] lo written
     uint64_t* empty = bars + 2 * STAGES;   // [STAGES] MMAs done with the stage
@@ -126,8 +133,8 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 const int row0 = static_cast<int>(rb * BM);
                 const int col0 = NORM ? row0 : static_cast<int>(cb * BN);
                 for (int kc = 0; kc < kchunks; ++kc, ++g) {
-                    const int s = static_cast<int>(g % STAGES);
-                    if (g >= STAGES) tc::mbar_wait(&empty[s], static_cast<uint32_t>((g / STAGES - 1) & 1));
+                    const int s = static_cast<int>(g % STG);
+                    if (g >= STG) tc::mbar_wait(&empty[s], static_cast<uint32_t>((g / STG - 1) & 1));
                     unsigned char* st = stage_ptr(s);
                     // hi = the raw tile (the tensor core truncates to tf32), lo from
                     // the pre-split copies: no generic-proxy pass over the stage
@@ -149,8 +156,8 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 if (tcount >= 2) tc::mbar_wait(&tempty[b], static_cast<uint32_t>((tcount / 2 - 1) & 1));
                 const uint32_t dt = tmem + b * BN;
                 for (int kc = 0; kc < kchunks; ++kc, ++g) {
-                    const int s = static_cast<int>(g % STAGES);
-                    tc::mbar_wait(&full[s], static_cast<uint32_t>((g / STAGES) & 1));
+                    const int s = static_cast<int>(g % STG);
+                    tc::mbar_wait(&full[s], static_cast<uint32_t>((g / STG) & 1));
                     tc::tc_fence_after();
                     const uint32_t a = tc::smem_u32(stage_ptr(s));
                     const uint32_t bsm = a + A_BYTES, alo = a + A_BYTES + B_BYTES, blo = alo + A_BYTES;
@@ -170,15 +177,14 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 tc::mma_commit(&tfull[b]);
             }
         }
-    } else if (warp < 6) {
-        // (warps 2-5 split lo = x - trunc_tf32(x) in an earlier version; the lo
-        // operands now arrive pre-split by TMA -- see split_lo_kernel)
-    } else if (MODE == 2) {
+    } else if (MODE == 2 && warp >= 14 - epi) {
         // ------------------------------------------------------- epilogue (TMA stores)
         // warp e: TMEM lanes of quarter (warp % 4), columns [128 h, 128 h + 128)
-        const int e = warp - 6, q = warp & 3, half = e >> 2;
+        // warp e of `epi`: TMEM lanes of quarter (warp % 4); the quarter's 16
+        // column chunks of 16 go round-robin over its epi/4 warps
+        const int e = warp - (14 - epi), q = warp & 3, sub = e >> 2, nsub = epi >> 2;
         const int r = q * 32 + lane;
-        unsigned char* stg = smem + OFF_STG + e * STG_BYTES;  // 2 boxes, 512-aligned (SWIZZLE_64B atoms)
+        unsigned char* stg = smem + off_stg(nst) + e * STG_BYTES;  // 2 boxes, 512-aligned (SWIZZLE_64B atoms)
         int64_t tcount = 0, nbox = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
             int64_t rb, cb;
@@ -208,17 +214,17 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 }
             };
             float4 ynext[4];
-            load_yn(col0 + half * 128, ynext);
+            load_yn(col0 + sub * 16, ynext);
 #pragma unroll 1
-            for (int cc = 0; cc < 8; ++cc, ++nbox) {
-                const int c0 = half * 128 + cc * 16;
+            for (int cc = sub; cc < 16; cc += nsub, ++nbox) {
+                const int c0 = cc * 16;
                 float v[16];
                 tc::tmem_ld16(trow + c0, v);
                 const int64_t gc = col0 + c0;
                 float4 ycur[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) ycur[u] = ynext[u];
-                if (cc + 1 < 8) load_yn(gc + 16, ynext);
+                if (cc + nsub < 16) load_yn(gc + 16 * nsub, ynext);
                 float d[16];
 #pragma unroll
                 for (int j = 0; j < 16; j += 4) {
@@ -254,11 +260,11 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 }
             }
             tc::tc_fence_before();
-            tc::named_sync(2, 32 * EPI_WARPS);
+            tc::named_sync(2, 32 * epi);
             if (e == 0 && lane == 0) tc::mbar_arrive(&tempty[b]);
         }
         if (lane == 0) tc::bulk_wait0();
-    } else if (warp < 10) {
+    } else if (MODE != 2 && warp >= 6 && warp < 10) {
         // ------------------------------------------------------- epilogue warps (MODE 0 / 1)
         const int q = warp & 3;             // TMEM lane quarter of this warp
         const int r = q * 32 + lane;        // accumulator row = TMEM lane
@@ -409,6 +415,8 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
         np.nx = rows;
         np.ny = rows;
         np.m = static_cast<int>(m);
+        np.nst = m <= BK ? 1 : 2;
+        np.epi = 8;
         np.out = dst;
         const int grid = static_cast<int>(std::min<int64_t>(ceil_div(rows, BM), ctx->num_sms));
         cdist_tc_kernel<0><<<grid, THREADS, SMEM, stream>>>(ma, mb, mal, mbl, ma, np);
@@ -433,6 +441,10 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     pp.col_off = col_off;
     pp.diag_offset = diag_offset;
     pp.vec = (ld_out % 4 == 0) && (col_off % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    // one K chunk per tile: one stage keeps the MMAs fed and frees room for 12
+    // epilogue warps (the epilogue is then the long pole)
+    pp.nst = m <= BK ? 1 : 2;
+    pp.epi = pp.nst == 1 ? 12 : 8;
     const int64_t tiles = ceil_div(nx, BM) * ceil_div(ny, BN);
     const int grid = static_cast<int>(std::min<int64_t>(tiles, ctx->num_sms));
     float* obase = out + col_off;
