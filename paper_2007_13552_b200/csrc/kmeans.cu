@@ -600,6 +600,14 @@ constexpr int KS_VW = KS_WARPS * KS_R;  // 32-row groups per tile
 #ifdef KS_TAIL_TRACE
 __device__ unsigned long long g_tail_trace[16];
 __device__ unsigned long long g_cta_trace[2 * 2048];
+__device__ unsigned long long g_iter_trace[2 * 64];  // per iteration: CTA 0 start, update done
+__device__ __forceinline__ void iter_mark(int it, int i) {
+    if (threadIdx.x == 0 && it < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        g_iter_trace[2 * it + i] = t;
+    }
+}
 __device__ __forceinline__ void cta_mark(int i) {
     if (threadIdx.x == 0 && blockIdx.x < 2048) {
         unsigned long long t;
@@ -617,6 +625,7 @@ __device__ __forceinline__ void tail_mark(int i) {
 #else
 __device__ __forceinline__ void tail_mark(int) {}
 __device__ __forceinline__ void cta_mark(int) {}
+__device__ __forceinline__ void iter_mark(int, int) {}
 #endif
 
 // One CTA-wide arrival ticket; true in every thread of the last CTA to arrive.
@@ -727,6 +736,7 @@ __device__ void fused_tail(const FuseArgs& f, const double* part, int S, int KD,
     tail_mark(3);
     update_body(a, upd, sh);
     tail_mark(4);
+    iter_mark(f.upd.iter, 1);
 }
 
 // fp32 top-2 of R rows held in registers as feature pairs: one FFMA2 per two
@@ -808,7 +818,10 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
     const bool accumulate = p.partials != nullptr;
 #endif
     const bool delta = accumulate && p.prev != nullptr;
-    if (p.fu.on && blockIdx.x == 0) tail_mark(5);
+    if (p.fu.on && blockIdx.x == 0) {
+        tail_mark(5);
+        iter_mark(p.fu.upd.iter, 0);
+    }
     if (p.fu.on) cta_mark(0);
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -2177,6 +2190,9 @@ int dndc_kmeans_time_assign_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_
 #ifdef KS_TAIL_TRACE
 int dndc_internal_tail_trace(unsigned long long* out16) {
     return guard([&] { DNDC_CUDA(cudaMemcpyFromSymbol(out16, dndc::g_tail_trace, 16 * sizeof(unsigned long long))); });
+}
+int dndc_internal_iter_trace(unsigned long long* out128) {
+    return guard([&] { DNDC_CUDA(cudaMemcpyFromSymbol(out128, dndc::g_iter_trace, 128 * sizeof(unsigned long long))); });
 }
 int dndc_internal_cta_trace(unsigned long long* out4096) {
     return guard([&] { DNDC_CUDA(cudaMemcpyFromSymbol(out4096, dndc::g_cta_trace, 4096 * sizeof(unsigned long long))); });

@@ -35,3 +35,9 @@ print(f"{G} CTAs: start spread {st.max():.1f} us; finish min {en.min():.1f} p10 
 sm = np.arange(G) % 148
 late = np.argsort(en)[-8:]
 print("latest CTAs (id, finish us):", [(int(i), round(float(en[i]), 1)) for i in late])
+
+it = (C.c_ulonglong * 128)()
+_lib.check(_lib.lib().dndc_internal_iter_trace(it))
+v = np.array(it[:], dtype=np.int64).reshape(64, 2)[:20]
+print("per iteration (us): kernel start->update done | gap to the next kernel's start")
+print(" ".join(f"{(v[i,1]-v[i,0])/1e3:.0f}|{(v[i+1,0]-v[i,1])/1e3:.1f}" for i in range(19)))
