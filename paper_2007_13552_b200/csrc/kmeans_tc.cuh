@@ -43,7 +43,7 @@ struct TcCfg {
     static constexpr int NS = P * K;                  // MMA N: score slots
     static constexpr int PR = 128;                    // packed rows per tile (MMA M)
     static constexpr int TROWS = PR * P;              // data rows per tile
-    static constexpr int S = 3;                       // TMA stages
+    static constexpr int S = K * D >= 4096 ? 2 : 3;  // TMA stages (2 leaves room for the sums)
     static constexpr int WGS = WG_;                   // epilogue warpgroups
     static constexpr int EPI = 128 * WGS;
     static constexpr int THREADS = EPI + 32;          // + the producer / MMA warp
@@ -59,13 +59,16 @@ struct TcCfg {
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
     static constexpr int OFF_CN = OFF_BLO + B_BYTES;
     static constexpr int OFF_CNT = OFF_CN + ((K * 4 + 15) / 16) * 16;
-    static constexpr int OFF_BAR = OFF_CNT + WGS * ((VW * K * 4 + 15) / 16) * 16;
+    // per-warpgroup f64 cluster sums (each warp owns clusters wq, wq+4, ...)
+    static constexpr int OFF_ACC = OFF_CNT + WGS * ((VW * K * 4 + 15) / 16) * 16;
+    static constexpr int OFF_BAR = OFF_ACC + WGS * K * D * 8;
     static constexpr int NBARS = 2 * S + 3 * WGS;
     static constexpr int OFF_TMEM = OFF_BAR + NBARS * 8;
     static constexpr int SMEM = OFF_TMEM + 16;
     static_assert(NS % 16 == 0 && NS <= 256, "MMA N (P*K) must be a multiple of 16, <= 256");
     static_assert(D % 2 == 0 && D <= 64 && K <= 64, "tc kernel shape");
     static_assert(WGS * K * D * 8 <= WGS * WORK_BYTES, "final combine scratch");
+    static_assert(OFF_TMEM + 16 <= 232448, "shared memory");
 };
 
 template <int D, int K, int P, int WG_>
@@ -186,9 +189,9 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
         for (int u = 0; u < KL; ++u) count_acc[u] = 0;
         unsigned long long refined = 0;
         const int g = lane / L, q = lane % L;
-        double2 wsum[JW];
-#pragma unroll
-        for (int jj = 0; jj < JW; ++jj) wsum[jj] = make_double2(0.0, 0.0);
+        // cluster sums in shared memory (registers would spill at K = 64)
+        double* acc = reinterpret_cast<double*>(smem + C::OFF_ACC) + wg * KD;
+        for (int e = t; e < KD; e += 128) acc[e] = 0.0;
 
         for (int64_t it = wg; it < my_tiles; it += WGS) {
             const int st = static_cast<int>(it % S);
@@ -395,47 +398,44 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                         part.y += vy;
                     }
                 }
-                wsum[jj].x += part.x;
-                wsum[jj].y += part.y;
+                if (g == 0 && q < L) {
+                    double2* a = reinterpret_cast<double2*>(acc + j * D + 2 * q);
+                    double2 v = *a;
+                    v.x += part.x;
+                    v.y += part.y;
+                    *a = v;
+                }
             }
             // the next tile's split rewrites `work` (lo): all warps must be done reading it
             tc::named_sync(bar_id, 128);
         }
         if (refined) atomicAdd(p.refined, refined);
         if (accumulate) {
-            // combine the warpgroups in a fixed order: wg 1 parks its sums, wg 0 adds
+            // combine the warpgroups in a fixed order (wg 0 + wg 1): sums from
+            // shared memory, counts parked by wg 1
             double* park = reinterpret_cast<double*>(smem + C::OFF_WORK);
             tc::named_sync(3, C::EPI);  // every warpgroup is past its last tile
-            if (wg == 1) {
+            if (wg == 1 && wq == 0) {
 #pragma unroll
-                for (int jj = 0; jj < JW; ++jj) {
-                    const int j = wq + jj * 4;
-                    if (j < K && g == 0 && q < L) *reinterpret_cast<double2*>(park + j * D + 2 * q) = wsum[jj];
-                }
-                if (wq == 0)
-#pragma unroll
-                    for (int u = 0; u < KL; ++u)
-                        if (lane + 32 * u < K) park[KD + lane + 32 * u] = static_cast<double>(count_acc[u]);
+                for (int u = 0; u < KL; ++u)
+                    if (lane + 32 * u < K) park[lane + 32 * u] = static_cast<double>(count_acc[u]);
             }
             tc::named_sync(3, C::EPI);
             if (wg == 0) {
                 double* out = p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K);
+                const double* acc0 = reinterpret_cast<const double*>(smem + C::OFF_ACC);
+                for (int e = t; e < KD; e += 128) {
+                    double v = acc0[e];
 #pragma unroll
-                for (int jj = 0; jj < JW; ++jj) {
-                    const int j = wq + jj * 4;
-                    if (j < K && g == 0 && q < L) {
-                        const double2 o = WGS > 1 ? *reinterpret_cast<const double2*>(park + j * D + 2 * q)
-                                                  : make_double2(0.0, 0.0);
-                        *reinterpret_cast<double2*>(out + j * D + 2 * q) =
-                            make_double2(wsum[jj].x + o.x, wsum[jj].y + o.y);
-                    }
+                    for (int w = 1; w < WGS; ++w) v += acc0[w * KD + e];
+                    out[e] = v;
                 }
                 if (wq == 0)
 #pragma unroll
                     for (int u = 0; u < KL; ++u)
                         if (lane + 32 * u < K)
                             out[KD + lane + 32 * u] =
-                                static_cast<double>(count_acc[u]) + (WGS > 1 ? park[KD + lane + 32 * u] : 0.0);
+                                static_cast<double>(count_acc[u]) + (WGS > 1 ? park[lane + 32 * u] : 0.0);
             }
         }
     }
