@@ -219,7 +219,7 @@ def cdist_cfg2(dnd, _lib, comm, stream, barrier, dist, local, world, peak):
             "value": gbs, "unit": "GB/s", "ms_per_call": tc_ms, "bytes_per_call": byt, "n_gpus": world,
             "roofline": {"bound": "hbm (output write)", "achieved": gbs, "peak": peak * world,
                          "frac": gbs / (peak * world), "unit": "GB/s",
-                         "kernel": "cdist_panel_f32_kernel (FFMA2, persistent row panels)"}}
+                         "kernel": "cdist_tc_kernel<2,32> (tcgen05 3xTF32, TMA bulk-store epilogue)"}}
 
 
 def run_ours(args):

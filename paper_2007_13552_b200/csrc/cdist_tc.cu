@@ -36,16 +36,19 @@ constexpr int A_BYTES = BM * BK * 4;   // 16 KB
 constexpr int B_BYTES = BN * BK * 4;   // 32 KB
 constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // raw + lo
 constexpr int EPI_MAX = 12;                             // epilogue warps: 8 (2 stages) or 12 (1 stage)
-constexpr int STG_BOX = 16 * 32 * 4;                    // one store box: 32 rows x 16 cols (SWIZZLE_64B)
-constexpr int STG_BYTES = 2 * STG_BOX;                  // per epilogue warp: double-buffered
+// store boxes: 32 rows x BC columns (BC = 16: SWIZZLE_64B, 32: SWIZZLE_128B),
+// double-buffered per epilogue warp
+__host__ __device__ constexpr int stg_bytes(int bc) { return 2 * bc * 32 * 4; }
 constexpr int NBARS = 3 * STAGES + 4;
 constexpr int THREADS = (2 + EPI_MAX) * 32;
 // shared-memory layout for `nst` stages and `epi` TMA-store epilogue warps
 __host__ __device__ constexpr int off_stg(int nst) { return nst * STAGE_BYTES; }
-__host__ __device__ constexpr int off_bar(int nst, int epi) { return off_stg(nst) + epi * STG_BYTES; }
-__host__ __device__ constexpr int smem_bytes(int nst, int epi) { return off_bar(nst, epi) + NBARS * 8 + 16 + 1024; }
-constexpr int SMEM = smem_bytes(2, 8);  // the largest configuration
-static_assert(smem_bytes(1, 12) <= SMEM, "smem layouts");
+__host__ __device__ constexpr int off_bar(int nst, int epi, int bc) { return off_stg(nst) + epi * stg_bytes(bc); }
+__host__ __device__ constexpr int smem_bytes(int nst, int epi, int bc) {
+    return off_bar(nst, epi, bc) + NBARS * 8 + 16 + 1024;
+}
+constexpr int SMEM = smem_bytes(2, 8, 16);  // the largest configuration
+static_assert(smem_bytes(1, 12, 32) <= SMEM, "smem layouts");
 constexpr int TMEM_COLS = 512;
 constexpr int GROUP = 16;  // rasterisation: GROUP x GROUP tile super-blocks
 }  // namespace cdtc
@@ -74,7 +77,7 @@ __device__ __forceinline__ void cdtc_tile_of(int64_t t, int64_t nrb, int64_t ncb
 // MODE 0: row norms (diagonal tiles); 1: distances with direct stores (any
 // alignment); 2: distances staged in swizzled shared memory and written by TMA
 // bulk stores (32x32 boxes, out-of-range rows/columns clipped by the unit).
-template <int MODE>
+template <int MODE, int BC = 16>
 __global__ void __launch_bounds__(cdtc::THREADS, 1)
     cdist_tc_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant__ CUtensorMap mapy,
                     const __grid_constant__ CUtensorMap mapxl, const __grid_constant__ CUtensorMap mapyl,
@@ -85,7 +88,7 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int nst = p.nst, epi = MODE == 2 ? p.epi : 8;
     const int STG = nst;  // stages in use
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off_bar(nst, epi));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off_bar(nst, epi, BC));
     uint64_t* full = bars;                 // [STAGES] TMA landed
     uint64_t* split = bars + STAGES;       // [STAGES] lo written
     uint64_t* empty = bars + 2 * STAGES;   // [STAGES] MMAs done with the stage
@@ -179,12 +182,12 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
         }
     } else if (MODE == 2 && warp >= 14 - epi) {
         // ------------------------------------------------------- epilogue (TMA stores)
-        // warp e: TMEM lanes of quarter (warp % 4), columns [128 h, 128 h + 128)
-        // warp e of `epi`: TMEM lanes of quarter (warp % 4); the quarter's 16
-        // column chunks of 16 go round-robin over its epi/4 warps
+        // warp e of `epi`: TMEM lanes of quarter (warp % 4); the quarter's
+        // 256/BC column chunks go round-robin over its epi/4 warps
+        constexpr int NCH = BN / BC, BOX = BC * 32 * 4;
         const int e = warp - (14 - epi), q = warp & 3, sub = e >> 2, nsub = epi >> 2;
         const int r = q * 32 + lane;
-        unsigned char* stg = smem + off_stg(nst) + e * STG_BYTES;  // 2 boxes, 512-aligned (SWIZZLE_64B atoms)
+        unsigned char* stg = smem + off_stg(nst) + e * stg_bytes(BC);  // 2 boxes, swizzle-atom aligned
         int64_t tcount = 0, nbox = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
             int64_t rb, cb;
@@ -198,10 +201,10 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
             const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * BN;
             const bool diag = p.diag_offset >= 0 && col0 < row0 + p.diag_offset + BM &&
                               row0 + p.diag_offset < col0 + BN;
-            // column norms of a 16-column chunk, fetched one chunk ahead
-            auto load_yn = [&](int64_t gc, float4 (&y4)[4]) {
+            // column norms of a chunk, fetched one chunk ahead
+            auto load_yn = [&](int64_t gc, float4 (&y4)[BC / 4]) {
 #pragma unroll
-                for (int j = 0; j < 16; j += 4) {
+                for (int j = 0; j < BC; j += 4) {
                     float4 yv = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (gc + j + 3 < p.ny) {
                         yv = __ldg(reinterpret_cast<const float4*>(p.yn + gc + j));
@@ -213,21 +216,22 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                     y4[j / 4] = yv;
                 }
             };
-            float4 ynext[4];
-            load_yn(col0 + sub * 16, ynext);
+            float4 ynext[BC / 4];
+            load_yn(col0 + sub * BC, ynext);
 #pragma unroll 1
-            for (int cc = sub; cc < 16; cc += nsub, ++nbox) {
-                const int c0 = cc * 16;
-                float v[16];
-                tc::tmem_ld16(trow + c0, v);
+            for (int cc = sub; cc < NCH; cc += nsub, ++nbox) {
+                const int c0 = cc * BC;
+                float v[BC];
+#pragma unroll
+                for (int h = 0; h < BC / 16; ++h) tc::tmem_ld16(trow + c0 + 16 * h, *reinterpret_cast<float(*)[16]>(v + 16 * h));
                 const int64_t gc = col0 + c0;
-                float4 ycur[4];
+                float4 ycur[BC / 4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) ycur[u] = ynext[u];
-                if (cc + nsub < 16) load_yn(gc + 16 * nsub, ynext);
-                float d[16];
+                for (int u = 0; u < BC / 4; ++u) ycur[u] = ynext[u];
+                if (cc + nsub < NCH) load_yn(gc + BC * nsub, ynext);
+                float d[BC];
 #pragma unroll
-                for (int j = 0; j < 16; j += 4) {
+                for (int j = 0; j < BC; j += 4) {
                     const float4 yv = ycur[j / 4];
                     const float2 b0 = fadd2(make_float2(xni, xni), make_float2(yv.x, yv.y));
                     const float2 b1 = fadd2(make_float2(xni, xni), make_float2(yv.z, yv.w));
@@ -240,18 +244,21 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 }
                 if (diag) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
+                    for (int j = 0; j < BC; ++j)
                         if (gc + j == gi + p.diag_offset) d[j] = 0.f;
                 }
                 // buffer nbox & 1: its previous box (two stores ago) has been read
-                unsigned char* box = stg + (nbox & 1) * STG_BOX;
+                unsigned char* box = stg + (nbox & 1) * BOX;
                 if (lane == 0) tc::bulk_wait_read1();
                 __syncwarp();
-                // SWIZZLE_64B: 16-byte chunk j of row `lane` sits at chunk j ^ ((lane >> 1) & 3)
+                // 16-byte chunk j of row `lane` sits at chunk j ^ (the row's swizzle
+                // phase): SWIZZLE_64B (lane >> 1) & 3, SWIZZLE_128B lane & 7
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    *reinterpret_cast<float4*>(box + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                for (int j = 0; j < BC / 4; ++j) {
+                    const int phys = BC == 16 ? (j ^ ((lane >> 1) & 3)) : (j ^ (lane & 7));
+                    *reinterpret_cast<float4*>(box + lane * (BC * 4) + (phys << 4)) =
                         make_float4(d[4 * j], d[4 * j + 1], d[4 * j + 2], d[4 * j + 3]);
+                }
                 tc::fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
@@ -330,13 +337,21 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
 }
 
 // ------------------------------------------------------------------ host
+constexpr int BK_SMALL = 32;  // one K chunk (cdtc::BK)
+
 static int tc_min_m() {
     const char* v = std::getenv("DNDC_CDIST_TC_MIN_M");
     return v ? std::atoi(v) : 256;
 }
 
+// d >= 256: a real dense contraction (tensor-pipe bound).  d <= 32 on large
+// blocks: one K chunk per tile, the output stream dominates and the
+// tensor-core epilogue (12 warps, TMA bulk stores) writes it faster than the
+// FFMA tile kernel (cfg2: 44.4 vs 48.7 ms).  DNDC_CDIST_TC_MIN_M overrides.
 bool cdist_tc_eligible(int64_t nx, int64_t ny, int64_t m) {
-    return m >= tc_min_m() && nx >= 128 && ny >= 128;
+    if (nx < 128 || ny < 128) return false;
+    if (std::getenv("DNDC_CDIST_TC_MIN_M")) return m >= tc_min_m();
+    return m >= 256 || (m <= BK_SMALL && nx * ny >= (int64_t{1} << 26));
 }
 
 // Padded view for TMA: row pitch must be a multiple of 16 bytes.
@@ -400,7 +415,8 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     if (!attr) {
         DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
         DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-        DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
         attr = true;
     }
     // norms through the same tensor-core path (diagonal tiles)
@@ -450,8 +466,14 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     float* obase = out + col_off;
     if (pp.vec && (ld_out * 4) % 16 == 0 && ny >= 16) {
         // TMA stores: the window [nx x ny] of the ld-wide output at col_off
-        const CUtensorMap mo = make_tmap_2d_f32_swz(obase, nx, ny, ld_out * 4, 16, 32, 64);
-        cdist_tc_kernel<2><<<grid, THREADS, SMEM, stream>>>(mx, my, mxl, myl, mo, pp);
+        if (pp.nst == 1 && ny >= 32) {
+            // 128-byte box rows: half the TMA store transactions of 16-column boxes
+            const CUtensorMap mo = make_tmap_2d_f32_swz(obase, nx, ny, ld_out * 4, 32, 32, 128);
+            cdist_tc_kernel<2, 32><<<grid, THREADS, SMEM, stream>>>(mx, my, mxl, myl, mo, pp);
+        } else {
+            const CUtensorMap mo = make_tmap_2d_f32_swz(obase, nx, ny, ld_out * 4, 16, 32, 64);
+            cdist_tc_kernel<2, 16><<<grid, THREADS, SMEM, stream>>>(mx, my, mxl, myl, mo, pp);
+        }
     } else {
         cdist_tc_kernel<1><<<grid, THREADS, SMEM, stream>>>(mx, my, mxl, myl, mx, pp);
     }

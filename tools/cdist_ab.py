@@ -33,7 +33,7 @@ dev = float(np.max(np.abs(got - ref) / np.maximum(1, np.abs(ref))))
 print(f"{t*1e3:.1f} ms  {4.0*n*n/t/1e9:.0f} GB/s  rel dev {dev:.2e}")
 '''
 import glob
-runs = [("ffma panel", {}), ("tcgen05 3xTF32", {"DNDC_CDIST_TC_MIN_M": "1"})]
+runs = [("default", {}), ("ffma panel", {"DNDC_CDIST_TC_MIN_M": "100000"}), ("tcgen05 3xTF32", {"DNDC_CDIST_TC_MIN_M": "1"})]
 runs += [(os.path.basename(v), {"DNDC_LIB_PATH": v}) for v in sorted(glob.glob(os.path.join(ROOT, "variants", "*.so")))]
 for label, env in runs:
     r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, env=dict(os.environ, **env), capture_output=True,
