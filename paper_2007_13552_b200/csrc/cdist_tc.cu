@@ -112,7 +112,9 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
             }
             for (int b = 0; b < 2; ++b) {
                 tc::mbar_init(&tfull[b], 1);
-                tc::mbar_init(&tempty[b], 1);
+                // MODE 2: every epilogue warp arrives on its own (no CTA-wide
+                // named barrier per tile); otherwise one arrival after a barrier
+                tc::mbar_init(&tempty[b], MODE == 2 ? epi : 1);
             }
             tc::mbar_fence_init();
         }
@@ -267,8 +269,8 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 }
             }
             tc::tc_fence_before();
-            tc::named_sync(2, 32 * epi);
-            if (e == 0 && lane == 0) tc::mbar_arrive(&tempty[b]);
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[b]);
         }
         if (lane == 0) tc::bulk_wait0();
     } else if (MODE != 2 && warp >= 6 && warp < 10) {
