@@ -596,6 +596,10 @@ constexpr int KS_MIN_CTAS = KS_MIN_CTAS_OVR;
 constexpr int KS_MIN_CTAS = 4;
 #endif
 constexpr int KS_VW = KS_WARPS * KS_R;  // 32-row groups per tile
+constexpr int KS_SCR = 8;               // changed rows staged per warp and batch (delta mode)
+#ifndef KS_DONLY_CTAS
+#define KS_DONLY_CTAS 4
+#endif
 
 #ifdef KS_TAIL_TRACE
 __device__ unsigned long long g_tail_trace[16];
@@ -782,8 +786,8 @@ __device__ __forceinline__ void small_top2(const float2 (&xv)[R][D / 2], const f
     }
 }
 
-template <int D, int K, int SLOT>
-__global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(SmallParams p) {
+template <int D, int K, int SLOT, bool DONLY = false>
+__global__ void __launch_bounds__(KS_THREADS, DONLY ? KS_DONLY_CTAS : KS_MIN_CTAS) kmeans_small_kernel(SmallParams p) {
     static_assert(D % 2 == 0 && D <= 64 && K <= 32, "small kernel shape");
     constexpr int TILE = KS_TILE, S = KS_STAGES, W = KS_WARPS, R = KS_R, VW = KS_VW;
     constexpr int L = D / 2;                  // lanes per row in phase 2 (float2 each)
@@ -796,9 +800,9 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
     float* tiles = reinterpret_cast<float*>(smem_raw);                 // S x TILE x D
     int8_t* labs = reinterpret_cast<int8_t*>(tiles + S * TILE * D);    // S x TILE previous labels (delta)
     double* wacc = reinterpret_cast<double*>(labs + S * TILE);         // W x K x D sums of changes (delta)
-    float* scr = reinterpret_cast<float*>(wacc + W * KD);              // W x 32 x D changed rows (delta)
-    int* scl = reinterpret_cast<int*>(scr + W * 32 * D);               // W x 32 x 2 their new/old labels
-    int* cnt = reinterpret_cast<int*>(scl + W * 64);                   // VW x K
+    float* scr = reinterpret_cast<float*>(wacc + W * KD);              // W x KS_SCR x D changed rows (delta)
+    int* scl = reinterpret_cast<int*>(scr + W * KS_SCR * D);           // W x KS_SCR x 2 their new/old labels
+    int* cnt = reinterpret_cast<int*>(scl + W * 2 * KS_SCR);           // VW x K
     unsigned* consumed = reinterpret_cast<unsigned*>(cnt + VW * K);    // S (delta mode)
     int* stage_tile = reinterpret_cast<int*>(consumed + S);             // S (dynamic schedule)
     uint64_t* bars = reinterpret_cast<uint64_t*>(cnt + ((VW * K + 2 * S + 1) & ~1));
@@ -815,9 +819,9 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
 #ifdef KS_EXP_NOPHASE2
     const bool accumulate = false;  // timing experiment only
 #else
-    const bool accumulate = p.partials != nullptr;
+    const bool accumulate = DONLY || p.partials != nullptr;
 #endif
-    const bool delta = accumulate && p.prev != nullptr;
+    const bool delta = DONLY || (accumulate && p.prev != nullptr);
     if (p.fu.on && blockIdx.x == 0) {
         tail_mark(5);
         iter_mark(p.fu.upd.iter, 0);
@@ -947,34 +951,47 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
             // changed rows: compacted into the warp's scratch, then moved from
             // the old cluster's sums to the new one's, lane = feature, in row
             // order (deterministic)
-            float* wscr = scr + warp * 32 * D;
-            int* wscl = scl + warp * 64;
+            float* wscr = scr + warp * KS_SCR * D;
+            int* wscl = scl + warp * 2 * KS_SCR;
             double* acc = wacc + warp * KD;
 #pragma unroll
             for (int h = 0; h < R; ++h) {
                 const bool ch = label[h] < K && label[h] != prevl[h];
-                const unsigned mask = __ballot_sync(FULL, ch);
-                if (mask == 0u) continue;
-                if (ch) {
-                    const int pos = __popc(mask & ((1u << lane) - 1u));
+                unsigned mask = __ballot_sync(FULL, ch);
+                while (mask) {
+                    // a batch of at most KS_SCR changed rows (the lowest set bits)
+                    unsigned batch = mask;
+                    if (__popc(batch) > KS_SCR) {
+                        batch = 0u;
+                        unsigned rest = mask;
 #pragma unroll
-                    for (int f = 0; f < L; ++f) *reinterpret_cast<float2*>(wscr + pos * D + 2 * f) = xv[h][f];
-                    wscl[2 * pos] = label[h];
-                    wscl[2 * pos + 1] = prevl[h];
-                }
-                __syncwarp();
-                const int nch = __popc(mask);
-                for (int c = 0; c < nch; ++c) {
-                    const int nl = wscl[2 * c], ol = wscl[2 * c + 1];
-                    if (lane < K) cnt_delta += (lane == nl) - (lane == ol);
-#pragma unroll
-                    for (int f = lane; f < D; f += 32) {
-                        const double v = static_cast<double>(wscr[c * D + f]);
-                        acc[nl * D + f] += v;
-                        if (ol >= 0) acc[ol * D + f] -= v;
+                        for (int i = 0; i < KS_SCR; ++i) {
+                            batch |= rest & (0u - rest);
+                            rest &= rest - 1u;
+                        }
                     }
+                    mask &= ~batch;
+                    if ((batch >> lane) & 1u) {
+                        const int pos = __popc(batch & ((1u << lane) - 1u));
+#pragma unroll
+                        for (int f = 0; f < L; ++f) *reinterpret_cast<float2*>(wscr + pos * D + 2 * f) = xv[h][f];
+                        wscl[2 * pos] = label[h];
+                        wscl[2 * pos + 1] = prevl[h];
+                    }
+                    __syncwarp();
+                    const int nch = __popc(batch);
+                    for (int c = 0; c < nch; ++c) {
+                        const int nl = wscl[2 * c], ol = wscl[2 * c + 1];
+                        if (lane < K) cnt_delta += (lane == nl) - (lane == ol);
+#pragma unroll
+                        for (int f = lane; f < D; f += 32) {
+                            const double v = static_cast<double>(wscr[c * D + f]);
+                            acc[nl * D + f] += v;
+                            if (ol >= 0) acc[ol * D + f] -= v;
+                        }
+                    }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
             continue;
         }
@@ -1155,7 +1172,7 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MIN_CTAS) kmeans_small_kernel(S
 template <int D, int K>
 static size_t small_smem() {
     return static_cast<size_t>(KS_STAGES) * KS_TILE * (D * 4 + 1) + static_cast<size_t>(KS_WARPS) * K * D * 8 +
-           static_cast<size_t>(KS_WARPS) * 32 * (D * 4 + 8) +
+           static_cast<size_t>(KS_WARPS) * KS_SCR * (D * 4 + 8) +
            static_cast<size_t>((KS_VW * K + 2 * KS_STAGES + 1) & ~1) * 4 + KS_STAGES * 8;
 }
 
@@ -1613,10 +1630,14 @@ struct Assigner {
     int tthreads = 0;
     AssignLaunch<T> gen{};
     void (*sfn)(SmallParams) = nullptr;
+    void (*dfn)(SmallParams) = nullptr;  // delta-only instantiation (fewer registers, more CTAs)
     size_t ssmem = 0;
-    int sgrid = 0, slot = 0;
+    int sgrid = 0, dgrid = 0, slot = 0;
 
     int grid() const { return (small || tc) ? sgrid : gen.grid; }
+    // the grid of a launch (delta iterations run the delta-only kernel)
+    int grid_for(bool delta) const { return (small && delta && dfn) ? dgrid : grid(); }
+    int max_grid() const { return std::max(grid(), small ? dgrid : 0); }
 
     void launch(const KmBuffers& b, const T* x, int64_t n, int d, int k, bool accumulate, int32_t* labels,
                 bool use_done, cudaStream_t st, const int8_t* prev = nullptr, int8_t* lab8 = nullptr,
@@ -1651,7 +1672,10 @@ struct Assigner {
             sp.tile_ctr = tile_ctr;
             sp.refined = b.refined;
             sp.done = use_done ? b.flags : nullptr;
-            sfn<<<sgrid, KS_THREADS, ssmem, st>>>(sp);
+            if (prev && dfn)
+                dfn<<<dgrid, KS_THREADS, ssmem, st>>>(sp);
+            else
+                sfn<<<sgrid, KS_THREADS, ssmem, st>>>(sp);
         } else {
             const AssignParams ap = assign_params<T>(b, x, n, d, k, gen.stages, accumulate, labels, use_done);
             gen.fn<<<gen.grid, KM_THREADS, gen.smem, st>>>(ap);
@@ -1660,12 +1684,12 @@ struct Assigner {
 };
 
 template <int D, int K>
-static bool pick_small(void (*&fn)(SmallParams), size_t& smem, int slot) {
+static bool pick_small(void (*&fn)(SmallParams), void (*&dfn)(SmallParams), size_t& smem, int slot) {
     switch (slot) {
-        case 0: fn = kmeans_small_kernel<D, K, 0>; break;
-        case 1: fn = kmeans_small_kernel<D, K, 1>; break;
-        case 2: fn = kmeans_small_kernel<D, K, 2>; break;
-        default: fn = kmeans_small_kernel<D, K, 3>; break;
+        case 0: fn = kmeans_small_kernel<D, K, 0>; dfn = kmeans_small_kernel<D, K, 0, true>; break;
+        case 1: fn = kmeans_small_kernel<D, K, 1>; dfn = kmeans_small_kernel<D, K, 1, true>; break;
+        case 2: fn = kmeans_small_kernel<D, K, 2>; dfn = kmeans_small_kernel<D, K, 2, true>; break;
+        default: fn = kmeans_small_kernel<D, K, 3>; dfn = kmeans_small_kernel<D, K, 3, true>; break;
     }
     smem = small_smem<D, K>();
     return true;
@@ -1727,8 +1751,8 @@ static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n, const T* x) {
         }
         const int slot = ctx->km_slot % KS_SLOTS;
         bool ok = false;
-        if (d == 18 && k == 8) ok = pick_small<18, 8>(A.sfn, A.ssmem, slot);
-        else if (d == 32 && k == 8) ok = pick_small<32, 8>(A.sfn, A.ssmem, slot);
+        if (d == 18 && k == 8) ok = pick_small<18, 8>(A.sfn, A.dfn, A.ssmem, slot);
+        else if (d == 32 && k == 8) ok = pick_small<32, 8>(A.sfn, A.dfn, A.ssmem, slot);
         if (ok) {
             A.small = true;
             A.slot = slot;
@@ -1739,6 +1763,12 @@ static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n, const T* x) {
             per_sm = std::max(per_sm, 1);
             const int64_t tiles = std::max<int64_t>(ceil_div(n, KS_TILE), 1);
             A.sgrid = static_cast<int>(std::min<int64_t>(tiles, static_cast<int64_t>(ctx->num_sms) * per_sm));
+            DNDC_CUDA(cudaFuncSetAttribute(A.dfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(A.ssmem)));
+            int dper_sm = 1;
+            DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper_sm, A.dfn, KS_THREADS, A.ssmem));
+            dper_sm = std::max(dper_sm, 1);
+            A.dgrid = static_cast<int>(std::min<int64_t>(tiles, static_cast<int64_t>(ctx->num_sms) * dper_sm));
             return A;
         }
     }
@@ -1855,7 +1885,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
     const Assigner<T> A = plan<T>(ctx, k, m, n_local, x_local);
-    const KmBuffers b = buffers(ctx, k, m, max_iter, A.grid());
+    const KmBuffers b = buffers(ctx, k, m, max_iter, A.max_grid());
     const int S = k * m + k;
 
     // ---- validation + sum |x|^2 (one pass), agreed by every rank
@@ -1932,7 +1962,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
                      fuse ? &fa : nullptr, A.small ? tile_ctr : nullptr);
             if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[2 * it + 1], st, cudaEventRecordExternal));
             if (fuse) continue;
-            reduce_partials_kernel<<<(S + 7) / 8, 256, 0, st>>>(b.partials, A.grid(), S, b.stats, b.flags);
+            reduce_partials_kernel<<<(S + 7) / 8, 256, 0, st>>>(b.partials, A.grid_for(delta), S, b.stats, b.flags);
             if (ctx->world > 1) allgather_f64(ctx, b.stats, b.gathered, S, st);
             const UpdArgs ua = upd_args(b, k, m, ctx->world, ctx->world > 1 ? b.gathered : b.stats,
                                         A.small ? b.running : nullptr, delta, it, tol);
