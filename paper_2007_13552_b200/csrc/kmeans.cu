@@ -597,6 +597,9 @@ constexpr int KS_MIN_CTAS = 4;
 #endif
 constexpr int KS_VW = KS_WARPS * KS_R;  // 32-row groups per tile
 constexpr int KS_SCR = 8;               // changed rows staged per warp and batch (delta mode)
+#ifndef KS_FULL_ITERS
+#define KS_FULL_ITERS 2  // iterations that accumulate every row (labels still moving a lot)
+#endif
 #ifndef KS_DONLY_CTAS
 #define KS_DONLY_CTAS 4
 #endif
@@ -1942,7 +1945,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
         for (int it = 0; it < max_iter; ++it) {
             // iterations 0 and 1 accumulate every row (after the first update most
             // labels still move); from iteration 2 on only the rows that changed
-            const bool delta = A.small && it > 1;
+            const bool delta = A.small && it > KS_FULL_ITERS - 1;
             FuseArgs fa{};
             if (fuse) {
                 fa.on = 1;
