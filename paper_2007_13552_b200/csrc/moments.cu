@@ -105,6 +105,85 @@ __global__ void __launch_bounds__(MO_THREADS)
     }
 }
 
+// fp32, m % 4 == 0, 16-byte aligned: each thread owns 4 adjacent columns
+// (one float4 per row), so a warp streams whole 128-byte rows with 8 rows of
+// loads in flight per thread; the same shifted-chunk sums and Chan merges
+// per column as above.
+__global__ void __launch_bounds__(MO_THREADS)
+    moments_partial_v4_kernel(const float4* __restrict__ x4, int64_t n, int m4, int lanes, int64_t rows_per_cta,
+                              double* __restrict__ partials) {
+    __shared__ Moment sh[MO_THREADS][4];
+    const int m = 4 * m4;
+    const int c4 = threadIdx.x % m4, rl = threadIdx.x / m4;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_cta;
+    const int64_t r1 = min(n, r0 + rows_per_cta);
+    Moment run[4] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+    if (rl < lanes) {
+        int64_t i = r0 + rl;
+        while (i < r1) {
+            const float4 k4 = __ldg(x4 + i * m4 + c4);
+            const double K[4] = {k4.x, k4.y, k4.z, k4.w};
+            double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
+            const int64_t left = (r1 - i + lanes - 1) / lanes;
+            int cnt;
+            if (left >= MO_KC) {
+#pragma unroll
+                for (int b = 0; b < MO_KC; b += 8) {
+                    float4 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = __ldg(x4 + (i + static_cast<int64_t>(b + u) * lanes) * m4 + c4);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const double d[4] = {static_cast<double>(v[u].x) - K[0], static_cast<double>(v[u].y) - K[1],
+                                             static_cast<double>(v[u].z) - K[2], static_cast<double>(v[u].w) - K[3]};
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            s1[c] += d[c];
+                            s2[c] = fma(d[c], d[c], s2[c]);
+                        }
+                    }
+                }
+                cnt = MO_KC;
+            } else {
+                cnt = static_cast<int>(left);
+                for (int u = 0; u < cnt; ++u) {
+                    const float4 v = __ldg(x4 + (i + static_cast<int64_t>(u) * lanes) * m4 + c4);
+                    const double d[4] = {static_cast<double>(v.x) - K[0], static_cast<double>(v.y) - K[1],
+                                         static_cast<double>(v.z) - K[2], static_cast<double>(v.w) - K[3]};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        s1[c] += d[c];
+                        s2[c] = fma(d[c], d[c], s2[c]);
+                    }
+                }
+            }
+            i += static_cast<int64_t>(cnt) * lanes;
+            const double nc = static_cast<double>(cnt);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                Moment ch;
+                ch.n = nc;
+                ch.mean = K[c] + s1[c] / nc;
+                ch.m2 = fmax(s2[c] - s1[c] * s1[c] / nc, 0.0);
+                run[c] = combine1(run[c], ch);
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sh[threadIdx.x][c] = run[c];
+    __syncthreads();
+    // column 4*c4 + c: row lanes merged in order
+    for (int col = threadIdx.x; col < m; col += MO_THREADS) {
+        const int g = col / 4, c = col % 4;
+        Moment acc = sh[g][c];
+        for (int l = 1; l < lanes; ++l) acc = combine1(acc, sh[l * m4 + g][c]);
+        double* out = partials + static_cast<int64_t>(blockIdx.x) * 3 * m;
+        out[col] = acc.n;
+        out[m + col] = acc.mean;
+        out[2 * m + col] = acc.m2;
+    }
+}
+
 __global__ void moments_final_kernel(const double* __restrict__ partials, int G, int m,
                                      double* __restrict__ out) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -128,7 +207,19 @@ static void moments_axis0(dndc_ctx* ctx, const T* x, int64_t n_local, int64_t m6
     const size_t rec = 3 * static_cast<size_t>(std::max(m, 1));
     double* local = static_cast<double*>(ctx->slot("mo_local", sizeof(double) * rec));
     double* all = static_cast<double*>(ctx->slot("mo_all", sizeof(double) * rec * ctx->world));
-    if (n_local > 0 && m > 0) {
+    const bool v4 = sizeof(T) == 4 && m % 4 == 0 && m / 4 <= MO_THREADS && reinterpret_cast<uintptr_t>(x) % 16 == 0;
+    if (n_local > 0 && m > 0 && v4) {
+        const int m4 = m / 4, lanes = MO_THREADS / m4;
+        const int64_t min_rows = static_cast<int64_t>(lanes) * MO_KC * 4;
+        const int64_t G = std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, ceil_div(n_local, min_rows)));
+        const int64_t rows_per_cta = ceil_div(n_local, G);
+        double* partials = static_cast<double*>(ctx->slot("mo_partials", sizeof(double) * rec * G));
+        moments_partial_v4_kernel<<<static_cast<unsigned>(G), MO_THREADS, 0, s>>>(
+            reinterpret_cast<const float4*>(x), n_local, m4, lanes, rows_per_cta, partials);
+        DNDC_LAUNCHED(ctx);
+        moments_final_kernel<<<(m + 127) / 128, 128, 0, s>>>(partials, static_cast<int>(G), m, local);
+        DNDC_LAUNCHED(ctx);
+    } else if (n_local > 0 && m > 0) {
         const int cols = std::min(m, MO_THREADS);
         const int lanes = MO_THREADS / cols;
         // enough CTAs to fill the GPU, each with at least a few chunks per lane
