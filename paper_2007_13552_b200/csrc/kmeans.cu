@@ -1514,9 +1514,22 @@ __global__ void kmeans_reset_kernel(int* flags, unsigned long long* refined, uns
                                     unsigned long long* acc64, int S) {
     for (int i = 0; i < ncounters; ++i) counters[i] = 0u;
     for (int i = 0; i < S; ++i) acc64[i] = 0ull;
-    flags[0] = 0;
+    flags[0] = flags[2];  // invalid input (validate_fold_kernel): every iteration is skipped
     flags[1] = 0;
     *refined = 0ull;
+}
+
+// world x (sum |x|^2, non-finite count) -> sx2[2] = global sum; flags[2] =
+// any non-finite value on any rank (cluster.cpp:88-89 raises ValueError)
+__global__ void validate_fold_kernel(const double* all, int world, double* sx2, int* flags) {
+    if (threadIdx.x != 0) return;
+    double sum = 0.0, bad = 0.0;
+    for (int r = 0; r < world; ++r) {
+        sum += all[2 * r];
+        bad += all[2 * r + 1];
+    }
+    sx2[2] = sum;
+    flags[2] = bad > 0.0 ? 1 : 0;
 }
 
 // ----------------------------------------------------------------- host
@@ -1812,7 +1825,7 @@ std::vector<int64_t> init_indices(int64_t n, int k, uint64_t seed) {
 
 template <typename T>
 static void init_centroids(dndc_ctx* ctx, const KmBuffers& b, const T* x_local, int64_t lo,
-                           int64_t n_local, int m, int k, uint64_t seed, int64_t n_global) {
+                           int64_t n_local, int m, int k, uint64_t seed, int64_t n_global, bool sync = true) {
     const auto idx = init_indices(n_global, k, seed);
     int64_t* didx = static_cast<int64_t*>(ctx->slot("km_idx", sizeof(int64_t) * k));
     int64_t* hidx = static_cast<int64_t*>(ctx->host_staging(sizeof(int64_t) * k));
@@ -1823,7 +1836,8 @@ static void init_centroids(dndc_ctx* ctx, const KmBuffers& b, const T* x_local, 
     DNDC_LAUNCHED(ctx);
     allreduce_sum_f64(ctx, b.c64, static_cast<size_t>(k) * m, ctx->stream);
     // the pinned staging buffer is reused by later calls: finish the copy first
-    DNDC_CUDA(cudaStreamSynchronize(ctx->stream));
+    // (kmeans_fit orders its next use on the stream instead)
+    if (sync) DNDC_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 // validation pass: sum x^2, non-finite count and max |x| of the shard -> b.sx2[0, 1, 3]
@@ -1891,35 +1905,22 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     const KmBuffers b = buffers(ctx, k, m, max_iter, A.max_grid());
     const int S = k * m + k;
 
-    // ---- validation + sum |x|^2 (one pass), agreed by every rank
-    {
-        scan_input<T>(ctx, b, x_local, n_local * m, s);
-        double* all = b.gathered;  // scratch: world x 2
-        allgather_f64(ctx, b.sx2, all, 2, s);
-        double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * std::max(4, 2 * ctx->world)));
-        DNDC_CUDA(cudaMemcpyAsync(h, all, sizeof(double) * 2 * ctx->world, cudaMemcpyDeviceToHost, s));
-        DNDC_CUDA(cudaStreamSynchronize(s));
-        double sx2 = 0.0, bad = 0.0;
-        for (int r = 0; r < ctx->world; ++r) {
-            sx2 += h[2 * r];
-            bad += h[2 * r + 1];
-        }
-        if (bad > 0.0) value_error("kmeans_fit: input contains non-finite values");
-        h[0] = 0.0;
-        h[1] = 0.0;
-        h[2] = sx2;
-        DNDC_CUDA(cudaMemcpyAsync(b.sx2, h, sizeof(double) * 3, cudaMemcpyHostToDevice, s));
-        DNDC_CUDA(cudaStreamSynchronize(s));
-    }
+    // ---- validation + sum |x|^2 (one pass), agreed by every rank, all on the
+    // device: a non-finite value anywhere sets flags[2] (and the iterations
+    // skip); the host raises after the single synchronisation at the end
+    scan_input<T>(ctx, b, x_local, n_local * m, s);
+    allgather_f64(ctx, b.sx2, b.gathered, 2, s);  // gathered: scratch, world x 2
+    validate_fold_kernel<<<1, 32, 0, s>>>(b.gathered, ctx->world, b.sx2, b.flags);
+    DNDC_LAUNCHED(ctx);
 
-    // ---- initial centroids
+    // ---- initial centroids (no host round trip: the pinned staging buffer is
+    // next written by the results copy, which is ordered after this upload)
     if (init_host) {
         double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * k * m));
         std::memcpy(h, init_host, sizeof(double) * k * m);
         DNDC_CUDA(cudaMemcpyAsync(b.c64, h, sizeof(double) * k * m, cudaMemcpyHostToDevice, s));
-        DNDC_CUDA(cudaStreamSynchronize(s));
     } else {
-        init_centroids<T>(ctx, b, x_local, off[ctx->rank], n_local, m, k, seed, n_global);
+        init_centroids<T>(ctx, b, x_local, off[ctx->rank], n_local, m, k, seed, n_global, false);
     }
     derive_tables(ctx, b, k, m);
 
@@ -2015,13 +2016,14 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     DNDC_CUDA(cudaMemcpyAsync(h, b.c64, sizeof(double) * k * m, cudaMemcpyDeviceToHost, s));
     DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * k * m, b.trace, sizeof(double) * max_iter,
                               cudaMemcpyDeviceToHost, s));
-    DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * (k * m + max_iter), b.flags, sizeof(int) * 2,
+    DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * (k * m + max_iter), b.flags, sizeof(int) * 3,
                               cudaMemcpyDeviceToHost, s));
     DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * (k * m + max_iter) + 16, b.refined,
                               sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     DNDC_CUDA(cudaStreamSynchronize(s));
-    std::memcpy(cent_host, h, sizeof(double) * k * m);
     const int* flags = reinterpret_cast<const int*>(h + sizeof(double) * (k * m + max_iter));
+    if (flags[2]) value_error("kmeans_fit: input contains non-finite values");
+    std::memcpy(cent_host, h, sizeof(double) * k * m);
     const int iters = flags[1];
     std::memcpy(trace_host, h + sizeof(double) * k * m, sizeof(double) * max_iter);
     *iters_host = iters;

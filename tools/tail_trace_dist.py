@@ -24,7 +24,8 @@ for it in (2, 20):
     _lib.check(L.dndc_internal_tail_trace(t))
     b = t[5]
     line = (f"rank {rank} fit {it:2d}: last CTA {(t[1]-b)/1e3:6.1f} | reduced {(t[2]-b)/1e3:6.1f} | "
-            f"exchanged {(t[3]-b)/1e3:6.1f} | updated {(t[4]-b)/1e3:6.1f} us  (abs start {b % 10**9 / 1e3:.1f} us)")
+            f"exchanged {(t[3]-b)/1e3:6.1f} | updated {(t[4]-b)/1e3:6.1f} us [fold {(t[6]-t[3])/1e3:.1f} elem "
+            f"{(t[7]-t[6])/1e3:.1f} clusters {(t[8]-t[7])/1e3:.1f} final {(t[4]-t[8])/1e3:.1f}]")
     out = [None] * dist.get_world_size()
     dist.all_gather_object(out, line)
     if rank == 0:
