@@ -214,3 +214,18 @@ def test_allreduce_f64_single_rank_identity(comm):
     buf = torch.arange(7, dtype=torch.float64, device="cuda")
     _lib.check(_lib.lib().dndc_allreduce_f64(comm.handle, buf.data_ptr(), 7))
     assert torch.equal(buf.cpu(), torch.arange(7, dtype=torch.float64))
+
+
+def test_fused_fit_rejects_non_finite_then_recovers(comm, oracle):
+    # cfg1-shaped rows (the fused small kernel): a NaN raises ValueError after
+    # the device-side validation, and the next fit on the same context is clean
+    n, m, k = 20_000, 18, 8
+    xh = oracle.uniform_f32(n, m, 21)
+    bad = xh.copy()
+    bad[12345, 7] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        dnd.kmeans_fit(dnd.from_global(bad, (n, m), 0, comm), k, 5, 0.0, 3)
+    model = dnd.kmeans_fit(dnd.from_global(xh, (n, m), 0, comm), k, 5, 0.0, 3)
+    c_ref, t_ref, _ = oracle.kmeans_fit(xh.astype(np.float64), k, 5, 0.0, 3)
+    assert rel_dev(model.centroids, c_ref) <= 1e-6
+    assert model.iterations_run == 5
