@@ -85,6 +85,7 @@ struct dndc_ctx {
     // the same addresses (CUDA-graph friendly).
     std::map<std::string, std::pair<void*, size_t>> slots;
     void* slot(const std::string& name, size_t bytes);
+    uint64_t slot_gen = 0;  // bumped on every (re)allocation: captured graphs key on it
 
     // pinned host staging for small results
     void* pinned = nullptr;

@@ -48,8 +48,13 @@ constexpr int KM_TILE = 256;  // rows per tile: one per thread in phase 1
 constexpr unsigned FULL = 0xffffffffu;
 
 struct KMeansState {
-    cudaGraphExec_t exec = nullptr;
-    std::string key;
+    // instantiated fit graphs, most recent first (e.g. two alternating input
+    // buffers of a pipelined caller); keyed on shape, buffers and slot_gen
+    std::vector<std::pair<std::string, cudaGraphExec_t>> graphs;
+    void clear_graphs() {
+        for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+        graphs.clear();
+    }
     // dndc_kmeans_assign_timing: event pairs recorded around every assign
     // launch inside the fit graph (external event nodes)
     bool timing = false;
@@ -67,7 +72,7 @@ static void free_events(KMeansState* st) {
 void destroy_kmeans_state(KMeansState* st) {
     if (!st) return;
     free_events(st);
-    if (st->exec) cudaGraphExecDestroy(st->exec);
+    st->clear_graphs();
     delete st;
 }
 
@@ -1934,7 +1939,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
         free_events(km);
         km->ev.resize(2 * static_cast<size_t>(max_iter));
         for (auto& e : km->ev) DNDC_CUDA(cudaEventCreate(&e));
-        km->key.clear();
+        km->clear_graphs();
     }
     // one launch per iteration (fused tail) on one GPU or with the NVLink
     // peer exchange; otherwise assign -> reduce -> NCCL allgather -> update
@@ -1975,15 +1980,18 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     };
     cudaStream_t gs = ctx->own_stream;
     char keybuf[256];
-    std::snprintf(keybuf, sizeof(keybuf), "%p/%lld/%d/%d/%d/%.17g/%p/%d/%d/%d/%d", (const void*)x_local,
+    std::snprintf(keybuf, sizeof(keybuf), "%p/%lld/%d/%d/%d/%.17g/%p/%d/%d/%d/%d/%llu", (const void*)x_local,
                   (long long)n_local, m, k, max_iter, tol, (void*)s, A.grid(), ctx->world, km->timing ? 1 : 0,
-                  fuse ? 1 : 0);
+                  fuse ? 1 : 0, static_cast<unsigned long long>(ctx->slot_gen));
     const std::string key = std::string(sizeof(T) == 4 ? "f32/" : "f64/") + keybuf;
-    if (ctx->km->key != key || !ctx->km->exec) {
-        if (ctx->km->exec) {
-            cudaGraphExecDestroy(ctx->km->exec);
-            ctx->km->exec = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    for (size_t i = 0; i < km->graphs.size(); ++i)
+        if (km->graphs[i].first == key) {
+            exec = km->graphs[i].second;
+            std::rotate(km->graphs.begin(), km->graphs.begin() + i, km->graphs.begin() + i + 1);
+            break;
         }
+    if (!exec) {
         const uint64_t before = ctx->counters.allgathers;
         cudaGraph_t graph;
         // capture on the context's own (non-legacy) stream: the legacy default
@@ -1997,13 +2005,17 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
         }
         DNDC_CUDA(cudaStreamEndCapture(gs, &graph));
         ctx->counters.allgathers = before;  // counted per replay below
-        DNDC_CUDA(cudaGraphInstantiate(&ctx->km->exec, graph, 0));
+        DNDC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
         DNDC_CUDA(cudaGraphDestroy(graph));
-        ctx->km->key = key;
+        km->graphs.insert(km->graphs.begin(), {key, exec});
+        while (km->graphs.size() > 4) {
+            cudaGraphExecDestroy(km->graphs.back().second);
+            km->graphs.pop_back();
+        }
     }
     DNDC_CUDA(cudaEventRecord(ctx->ev_a, s));
     DNDC_CUDA(cudaStreamWaitEvent(gs, ctx->ev_a, 0));
-    DNDC_CUDA(cudaGraphLaunch(ctx->km->exec, gs));
+    DNDC_CUDA(cudaGraphLaunch(exec, gs));
     DNDC_CUDA(cudaEventRecord(ctx->ev_b, gs));
     DNDC_CUDA(cudaStreamWaitEvent(s, ctx->ev_b, 0));
     // reset + per iteration: assign (fused) | [tile reset,] assign, reduce, update
@@ -2237,7 +2249,7 @@ int dndc_internal_cta_trace(unsigned long long* out4096) {
 int dndc_kmeans_assign_timing(dndc_ctx* ctx, int enable) {
     return guard([&] {
         if (!ctx->km) ctx->km = new dndc::KMeansState();
-        if (ctx->km->timing != (enable != 0)) ctx->km->key.clear();  // re-record the graph
+        if (ctx->km->timing != (enable != 0)) ctx->km->clear_graphs();  // re-record the graphs
         ctx->km->timing = enable != 0;
     });
 }

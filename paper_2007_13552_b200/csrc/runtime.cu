@@ -139,6 +139,7 @@ void* dndc_ctx::slot(const std::string& name, size_t bytes) {
     void* p = nullptr;
     DNDC_CUDA(cudaMalloc(&p, bytes));
     slots[name] = {p, bytes};
+    ++slot_gen;
     return p;
 }
 
