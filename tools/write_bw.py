@@ -1,4 +1,4 @@
-"""Pure-write and copy bandwidth of this B200 (torch kernels, CUDA events):
+"""Pure-write, pure-read and copy bandwidth of this B200 (torch kernels, CUDA events):
 the ceiling for cdist, whose traffic is almost all output writes."""
 import json
 
@@ -10,8 +10,10 @@ b = torch.empty(n // 4, dtype=torch.float32, device="cuda")
 c = torch.empty(n // 4, dtype=torch.float32, device="cuda")
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 res = {}
+r = torch.empty(1, dtype=torch.float32, device="cuda")
 for name, fn, byt in (("write_fill", lambda: a.fill_(1.0), 4.0 * n),
-                      ("copy_rw", lambda: c.copy_(b), 2 * 4.0 * n / 4)):
+                      ("copy_rw", lambda: c.copy_(b), 2 * 4.0 * n / 4),
+                      ("read_sum", lambda: torch.sum(a), 4.0 * n)):
     fn()
     torch.cuda.synchronize()
     best = 1e9
