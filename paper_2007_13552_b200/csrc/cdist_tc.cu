@@ -38,17 +38,29 @@ constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // raw + lo
 constexpr int EPI_MAX = 12;                             // epilogue warps: 8 (2 stages) or 12 (1 stage)
 // store boxes: 32 rows x BC columns (BC = 16: SWIZZLE_64B, 32: SWIZZLE_128B),
 // double-buffered per epilogue warp
-__host__ __device__ constexpr int stg_bytes(int bc) { return 2 * bc * 32 * 4; }
+#ifndef CDTC_NBUF1
+#define CDTC_NBUF1 2  // store boxes in flight per warp in the one-stage layout
+#endif
+#ifndef CDTC_EPI1
+#define CDTC_EPI1 12
+#endif
+#ifndef CDTC_BC1
+#define CDTC_BC1 32
+#endif
+__host__ __device__ constexpr int stg_bytes(int bc, int nbuf = 2) { return nbuf * bc * 32 * 4; }
 constexpr int NBARS = 3 * STAGES + 4;
 constexpr int THREADS = (2 + EPI_MAX) * 32;
 // shared-memory layout for `nst` stages and `epi` TMA-store epilogue warps
 __host__ __device__ constexpr int off_stg(int nst) { return nst * STAGE_BYTES; }
-__host__ __device__ constexpr int off_bar(int nst, int epi, int bc) { return off_stg(nst) + epi * stg_bytes(bc); }
+__host__ __device__ constexpr int nbuf_of(int nst) { return nst == 1 ? CDTC_NBUF1 : 2; }
+__host__ __device__ constexpr int off_bar(int nst, int epi, int bc) {
+    return off_stg(nst) + epi * stg_bytes(bc, nbuf_of(nst));
+}
 __host__ __device__ constexpr int smem_bytes(int nst, int epi, int bc) {
     return off_bar(nst, epi, bc) + NBARS * 8 + 16 + 1024;
 }
 constexpr int SMEM = smem_bytes(2, 8, 16);  // the largest configuration
-static_assert(smem_bytes(1, 12, 32) <= SMEM, "smem layouts");
+static_assert(smem_bytes(1, CDTC_EPI1, CDTC_BC1) <= SMEM, "smem layouts");
 constexpr int TMEM_COLS = 512;
 constexpr int GROUP = 16;  // rasterisation: GROUP x GROUP tile super-blocks
 }  // namespace cdtc
@@ -189,7 +201,8 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
         constexpr int NCH = BN / BC, BOX = BC * 32 * 4;
         const int e = warp - (14 - epi), q = warp & 3, sub = e >> 2, nsub = epi >> 2;
         const int r = q * 32 + lane;
-        unsigned char* stg = smem + off_stg(nst) + e * stg_bytes(BC);  // 2 boxes, swizzle-atom aligned
+        const int nbuf = nbuf_of(nst);
+        unsigned char* stg = smem + off_stg(nst) + e * stg_bytes(BC, nbuf);  // nbuf boxes, swizzle-atom aligned
         int64_t tcount = 0, nbox = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
             int64_t rb, cb;
@@ -249,9 +262,14 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                     for (int j = 0; j < BC; ++j)
                         if (gc + j == gi + p.diag_offset) d[j] = 0.f;
                 }
-                // buffer nbox & 1: its previous box (two stores ago) has been read
-                unsigned char* box = stg + (nbox & 1) * BOX;
-                if (lane == 0) tc::bulk_wait_read1();
+                // buffer nbox % nbuf: its previous box (nbuf stores ago) has been read
+                unsigned char* box = stg + (nbox % nbuf) * BOX;
+                if (lane == 0) {
+                    if (nbuf == 3)
+                        asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+                    else
+                        tc::bulk_wait_read1();
+                }
                 __syncwarp();
                 // 16-byte chunk j of row `lane` sits at chunk j ^ (the row's swizzle
                 // phase): SWIZZLE_64B (lane >> 1) & 3, SWIZZLE_128B lane & 7
@@ -462,13 +480,13 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     // one K chunk per tile: one stage keeps the MMAs fed and frees room for 12
     // epilogue warps (the epilogue is then the long pole)
     pp.nst = m <= BK ? 1 : 2;
-    pp.epi = pp.nst == 1 ? 12 : 8;
+    pp.epi = pp.nst == 1 ? CDTC_EPI1 : 8;
     const int64_t tiles = ceil_div(nx, BM) * ceil_div(ny, BN);
     const int grid = static_cast<int>(std::min<int64_t>(tiles, ctx->num_sms));
     float* obase = out + col_off;
     if (pp.vec && (ld_out * 4) % 16 == 0 && ny >= 16) {
         // TMA stores: the window [nx x ny] of the ld-wide output at col_off
-        if (pp.nst == 1 && ny >= 32) {
+        if (pp.nst == 1 && ny >= 32 && CDTC_BC1 == 32) {
             // 128-byte box rows: half the TMA store transactions of 16-column boxes
             const CUtensorMap mo = make_tmap_2d_f32_swz(obase, nx, ny, ld_out * 4, 32, 32, 128);
             cdist_tc_kernel<2, 32><<<grid, THREADS, SMEM, stream>>>(mx, my, mxl, myl, mo, pp);
