@@ -1,0 +1,185 @@
+// dnd -- GPU bench / verify CLI over the C++ drop-in API.
+//
+// Mirrors the reference's tools/main.cpp subcommands `bench` and `verify`
+// (tools/bench.cpp:84-130, tools/verify.cpp:20-193) for the hot-path
+// algorithms, with the same protocol: warmup runs, then timed runs bracketed by
+// barriers with the slowest rank reported, synthetic random_uniform data.
+//
+//   dnd bench  --algo kmeans|cdist|moments --synthetic 5000000x18 [--k 8]
+//              [--iters 20] [--ranks 1] [--warmup 1] [--runs 9] [--seed 42]
+//   dnd verify --algo kmeans|cdist|moments --synthetic 20000x18 [--ranks 2] ...
+//
+// bench prints one JSON object (the reference's report keys plus GB/s);
+// verify runs the algorithm on `ranks` GPUs and on one and reports the largest
+// relative deviation |a-b|/max(1,|b|) against the gate (distances/centroids
+// 1e-5, moments 1e-12), exit status 1 when it fails.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "dnd/dnd.hpp"
+
+namespace {
+
+struct Options {
+    std::string cmd, algo = "kmeans";
+    dnd::index_t rows = 20000, cols = 18;
+    int k = 8, iters = 20, ranks = 1, warmup = 1, runs = 9;
+    std::uint64_t seed = 42;
+};
+
+[[noreturn]] void usage(const char* why) {
+    std::fprintf(stderr,
+                 "dnd: %s\nusage: dnd bench|verify --algo kmeans|cdist|moments --synthetic ROWSxCOLS [--k K] "
+                 "[--iters N] [--ranks P] [--warmup W] [--runs R] [--seed S]\n",
+                 why);
+    std::exit(2);
+}
+
+Options parse(int argc, char** argv) {
+    if (argc < 2) usage("missing subcommand");
+    Options o;
+    o.cmd = argv[1];
+    if (o.cmd != "bench" && o.cmd != "verify") usage("unknown subcommand");
+    for (int i = 2; i < argc; ++i) {
+        const std::string a = argv[i];
+        if (i + 1 >= argc) usage(("missing value for " + a).c_str());
+        const std::string v = argv[++i];
+        if (a == "--algo") o.algo = v;
+        else if (a == "--synthetic") {
+            const auto x = v.find('x');
+            if (x == std::string::npos) usage("--synthetic takes ROWSxCOLS");
+            o.rows = std::atoll(v.substr(0, x).c_str());
+            o.cols = std::atoll(v.substr(x + 1).c_str());
+        } else if (a == "--k") o.k = std::atoi(v.c_str());
+        else if (a == "--iters") o.iters = std::atoi(v.c_str());
+        else if (a == "--ranks") o.ranks = std::atoi(v.c_str());
+        else if (a == "--warmup") o.warmup = std::atoi(v.c_str());
+        else if (a == "--runs") o.runs = std::atoi(v.c_str());
+        else if (a == "--seed") o.seed = std::strtoull(v.c_str(), nullptr, 10);
+        else usage(("unknown option " + a).c_str());
+    }
+    if (o.algo != "kmeans" && o.algo != "cdist" && o.algo != "moments") usage("unknown --algo");
+    if (o.rows < 1 || o.cols < 1 || o.ranks < 1 || o.runs < 1 || o.warmup < 0) usage("bad sizes");
+    return o;
+}
+
+// one run of the algorithm; returns a scalar that depends on the result
+// (kept, like the reference's sink, so nothing is optimised away) and fills
+// `out` with the replicated result for verify
+double run_algo(const Options& o, const dnd::DndArray<float>& x, std::vector<double>* out) {
+    const dnd::Communicator& comm = x.comm();
+    if (o.algo == "kmeans") {
+        const auto model = dnd::kmeans_fit(x, o.k, o.iters, 0.0, o.seed);
+        if (out) *out = model.centroids;
+        return model.inertia_trace.back();
+    }
+    if (o.algo == "cdist") {
+        const auto d = dnd::cdist(x);
+        if (out) {
+            const auto g = dnd::gather(d);
+            out->assign(g.begin(), g.end());
+        }
+        float first = 0.f;
+        if (d.numel_local() > 1)
+            dnd::detail::check(dndc_memcpy(comm.handle(), &first, d.device_data() + 1, sizeof(float), DNDC_COPY_D2H));
+        return first;
+    }
+    const auto mu = dnd::gather(dnd::mean_axis(x, 0));
+    const auto var = dnd::gather(dnd::var_axis(x, 0));
+    if (out) {
+        *out = mu;
+        out->insert(out->end(), var.begin(), var.end());
+    }
+    return mu[0] + var[0];
+}
+
+double bytes_per_run(const Options& o) {
+    const double xb = 4.0 * o.rows * o.cols;
+    if (o.algo == "kmeans") return xb * o.iters;
+    if (o.algo == "cdist") return 4.0 * o.rows * o.rows + xb;
+    return xb;
+}
+
+int bench(const Options& o) {
+    std::vector<double> secs;
+    std::mutex mu;
+    dnd::run_world(o.ranks, [&](const dnd::Communicator& comm) {
+        const auto x = dnd::random_uniform<float>({o.rows, o.cols}, 0, o.seed, comm);
+        double sink = 0.0;
+        for (int w = 0; w < o.warmup; ++w) sink += run_algo(o, x, nullptr);
+        // slowest rank per run (bench.cpp:102-112): the ranks are threads of
+        // this process, so the max is taken under a mutex after the runs
+        std::vector<double> mine;
+        for (int r = 0; r < o.runs; ++r) {
+            comm.barrier();
+            const auto t0 = std::chrono::steady_clock::now();
+            sink += run_algo(o, x, nullptr);
+            comm.barrier();
+            mine.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        }
+        if (!std::isfinite(sink)) throw dnd::ValueError("benchmark produced non-finite results");
+        std::lock_guard<std::mutex> lock(mu);
+        if (secs.empty()) secs.assign(mine.size(), 0.0);
+        for (size_t i = 0; i < mine.size(); ++i) secs[i] = std::max(secs[i], mine[i]);
+    });
+    const auto st = dnd::local_moments(dnd::Tile<double>{{static_cast<dnd::index_t>(secs.size())}, secs});
+    std::string runs;
+    for (double t : secs) runs += (runs.empty() ? "" : ", ") + std::to_string(t);
+    const double mean = st.mean[0], sd = std::sqrt(st.m2[0] / static_cast<double>(st.count));
+    std::printf("{\"algo\": \"%s\", \"ranks\": %d, \"split\": 0, \"params\": {\"rows\": %lld, \"cols\": %lld, "
+                "\"k\": %d, \"iters\": %d, \"seed\": %llu}, \"warmup_runs\": %d, \"timed_runs\": %d, "
+                "\"mean_seconds\": %.9g, \"std_seconds\": %.9g, \"GB_per_s\": %.6g, \"device\": \"B200 (libdndc)\", "
+                "\"run_seconds\": [%s]}\n",
+                o.algo.c_str(), o.ranks, static_cast<long long>(o.rows), static_cast<long long>(o.cols), o.k, o.iters,
+                static_cast<unsigned long long>(o.seed), o.warmup, o.runs, mean, sd, bytes_per_run(o) / mean / 1e9,
+                runs.c_str());
+    return 0;
+}
+
+int verify(const Options& o) {
+    std::vector<double> dist_res, single_res;
+    std::mutex mu;
+    auto collect = [&](int ranks, std::vector<double>& dst) {
+        dnd::run_world(ranks, [&](const dnd::Communicator& comm) {
+            const auto x = dnd::random_uniform<float>({o.rows, o.cols}, 0, o.seed, comm);
+            std::vector<double> r;
+            run_algo(o, x, &r);
+            std::lock_guard<std::mutex> lock(mu);
+            if (comm.rank() == 0) dst = r;
+        });
+    };
+    collect(o.ranks, dist_res);
+    collect(1, single_res);
+    if (dist_res.size() != single_res.size()) {
+        std::printf("{\"algo\": \"%s\", \"ranks\": %d, \"pass\": false, \"error\": \"size mismatch\"}\n",
+                    o.algo.c_str(), o.ranks);
+        return 1;
+    }
+    double dev = 0.0;
+    for (size_t i = 0; i < dist_res.size(); ++i)
+        dev = std::max(dev, std::abs(dist_res[i] - single_res[i]) / std::max(1.0, std::abs(single_res[i])));
+    const double gate = o.algo == "moments" ? 1e-12 : 1e-5;  // tools/verify.cpp:20-33 + BASELINE.json
+    const bool pass = dev <= gate;
+    std::printf("{\"algo\": \"%s\", \"ranks\": %d, \"max_rel_dev\": %.3e, \"gate\": %.0e, \"pass\": %s}\n",
+                o.algo.c_str(), o.ranks, dev, gate, pass ? "true" : "false");
+    return pass ? 0 : 1;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    const Options o = parse(argc, argv);
+    try {
+        return o.cmd == "bench" ? bench(o) : verify(o);
+    } catch (const dnd::Error& e) {
+        std::fprintf(stderr, "dnd: %s\n", e.what());
+        return 1;
+    }
+}

@@ -87,6 +87,12 @@ struct dndc_ctx {
     void* slot(const std::string& name, size_t bytes);
     uint64_t slot_gen = 0;  // bumped on every (re)allocation: captured graphs key on it
 
+    // stream-ordered pool behind dndc_alloc/dndc_free (hostio.cu): arrays the
+    // host layer allocates per call (cdist outputs, results) reuse memory
+    // instead of paying cudaMalloc/cudaFree each time; trimmed on OOM
+    cudaMemPool_t pool = nullptr;
+    void trim_pool();
+
     // pinned host staging for small results
     void* pinned = nullptr;
     size_t pinned_bytes = 0;

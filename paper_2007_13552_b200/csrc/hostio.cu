@@ -47,7 +47,25 @@ int dndc_alloc(dndc_ctx* ctx, size_t bytes, void** out) {
     return guard([&] {
         DNDC_CUDA(cudaSetDevice(ctx->device));
         *out = nullptr;
-        if (bytes) DNDC_CUDA(cudaMalloc(out, bytes));
+        if (!bytes) return;
+        if (!ctx->pool) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = ctx->device;
+            DNDC_CUDA(cudaMemPoolCreate(&ctx->pool, &props));
+            uint64_t keep = UINT64_MAX;  // never release on sync: reuse across calls
+            DNDC_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        }
+        cudaError_t e = cudaMallocFromPoolAsync(out, bytes, ctx->pool, ctx->stream);
+        if (e == cudaErrorMemoryAllocation) {
+            (void)cudaGetLastError();
+            ctx->trim_pool();
+            e = cudaMallocFromPoolAsync(out, bytes, ctx->pool, ctx->stream);
+        }
+        DNDC_CUDA(e);
+        // usable from any stream and from the host layer's next call at once
+        DNDC_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
 
@@ -55,8 +73,10 @@ int dndc_free(dndc_ctx* ctx, void* p) {
     return guard([&] {
         if (!p) return;
         DNDC_CUDA(cudaSetDevice(ctx->device));
+        // ring sends may still read the array on comm_stream
+        DNDC_CUDA(cudaStreamSynchronize(ctx->comm_stream));
         DNDC_CUDA(cudaStreamSynchronize(ctx->stream));
-        DNDC_CUDA(cudaFree(p));
+        DNDC_CUDA(cudaFreeAsync(p, ctx->stream));
     });
 }
 

@@ -14,6 +14,7 @@
 // reference's allreduce(combine) fold (moments.cpp:45-47, transport.hpp:140-146).
 #include <algorithm>
 #include <cstring>
+#include <numeric>
 
 #include "common.cuh"
 
@@ -105,15 +106,22 @@ __global__ void __launch_bounds__(MO_THREADS)
     }
 }
 
-// fp32, m % 4 == 0, 16-byte aligned: each thread owns 4 adjacent columns
-// (one float4 per row), so a warp streams whole 128-byte rows with 8 rows of
-// loads in flight per thread; the same shifted-chunk sums and Chan merges
-// per column as above.
-__global__ void __launch_bounds__(MO_THREADS)
-    moments_partial_v4_kernel(const float4* __restrict__ x4, int64_t n, int m4, int lanes, int64_t rows_per_cta,
-                              double* __restrict__ partials) {
+// fp32, 16-byte aligned: the shard is read as groups of rg = 4/gcd(m, 4)
+// rows (rg*m floats, a whole number of float4s), each thread owning one
+// float4 slot of a group -- 4 fixed (row-in-group, column) positions -- so a
+// warp streams contiguous bytes with 8 groups of loads in flight per thread
+// whatever m is (m = 18: 2-row groups of 9 float4s).  The same shifted-chunk
+// sums and Chan merges per slot as above; a column's rg slots per row lane are
+// merged in (lane, row-in-group) order.  n here counts groups; the n % rg
+// leftover rows are folded in by moments_final_kernel.
+#ifndef MO_V4_MIN_CTAS
+#define MO_V4_MIN_CTAS 2
+#endif
+__global__ void __launch_bounds__(MO_THREADS, MO_V4_MIN_CTAS)
+    moments_partial_v4_kernel(const float4* __restrict__ x4, int64_t n, int m, int rg, int lanes,
+                              int64_t rows_per_cta, double* __restrict__ partials) {
     __shared__ Moment sh[MO_THREADS][4];
-    const int m = 4 * m4;
+    const int m4 = rg * m / 4;
     const int c4 = threadIdx.x % m4, rl = threadIdx.x / m4;
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_cta;
     const int64_t r1 = min(n, r0 + rows_per_cta);
@@ -172,11 +180,14 @@ __global__ void __launch_bounds__(MO_THREADS)
 #pragma unroll
     for (int c = 0; c < 4; ++c) sh[threadIdx.x][c] = run[c];
     __syncthreads();
-    // column 4*c4 + c: row lanes merged in order
+    // column col sits at group offsets r*m + col, r < rg
     for (int col = threadIdx.x; col < m; col += MO_THREADS) {
-        const int g = col / 4, c = col % 4;
-        Moment acc = sh[g][c];
-        for (int l = 1; l < lanes; ++l) acc = combine1(acc, sh[l * m4 + g][c]);
+        Moment acc{0.0, 0.0, 0.0};
+        for (int l = 0; l < lanes; ++l)
+            for (int r = 0; r < rg; ++r) {
+                const int e = r * m + col;
+                acc = combine1(acc, sh[l * m4 + e / 4][e % 4]);
+            }
         double* out = partials + static_cast<int64_t>(blockIdx.x) * 3 * m;
         out[col] = acc.n;
         out[m + col] = acc.mean;
@@ -184,15 +195,30 @@ __global__ void __launch_bounds__(MO_THREADS)
     }
 }
 
-__global__ void moments_final_kernel(const double* __restrict__ partials, int G, int m,
-                                     double* __restrict__ out) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= m) return;
+// one CTA per column: the CTA partials merged in a fixed tree (thread t folds
+// partials t, t+256, ... in order, then a pairwise tree over the threads),
+// then the tail_rows rows at `tail` (rows the grouped kernel did not cover)
+// one Welford step each
+__global__ void __launch_bounds__(MO_THREADS)
+    moments_final_kernel(const double* __restrict__ partials, int G, int m, const float* __restrict__ tail,
+                         int tail_rows, double* __restrict__ out) {
+    __shared__ Moment sh[MO_THREADS];
+    const int c = blockIdx.x;
     Moment acc{0.0, 0.0, 0.0};
-    for (int g = 0; g < G; ++g) {
+    for (int g = threadIdx.x; g < G; g += MO_THREADS) {
         const double* p = partials + static_cast<int64_t>(g) * 3 * m;
         acc = combine1(acc, Moment{p[c], p[m + c], p[2 * m + c]});
     }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int h = MO_THREADS / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) sh[threadIdx.x] = combine1(sh[threadIdx.x], sh[threadIdx.x + h]);
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    acc = sh[0];
+    for (int t = 0; t < tail_rows; ++t)
+        acc = combine1(acc, Moment{1.0, static_cast<double>(tail[static_cast<int64_t>(t) * m + c]), 0.0});
     out[c] = acc.n;
     out[m + c] = acc.mean;
     out[2 * m + c] = acc.m2;
@@ -207,17 +233,28 @@ static void moments_axis0(dndc_ctx* ctx, const T* x, int64_t n_local, int64_t m6
     const size_t rec = 3 * static_cast<size_t>(std::max(m, 1));
     double* local = static_cast<double*>(ctx->slot("mo_local", sizeof(double) * rec));
     double* all = static_cast<double*>(ctx->slot("mo_all", sizeof(double) * rec * ctx->world));
-    const bool v4 = sizeof(T) == 4 && m % 4 == 0 && m / 4 <= MO_THREADS && reinterpret_cast<uintptr_t>(x) % 16 == 0;
-    if (n_local > 0 && m > 0 && v4) {
-        const int m4 = m / 4, lanes = MO_THREADS / m4;
-        const int64_t min_rows = static_cast<int64_t>(lanes) * MO_KC * 4;
-        const int64_t G = std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, ceil_div(n_local, min_rows)));
-        const int64_t rows_per_cta = ceil_div(n_local, G);
+    const int rg = m > 0 ? 4 / std::gcd(m, 4) : 1;  // rows per float4-aligned group
+    const int64_t n_groups = n_local / rg;
+    const bool v4 = sizeof(T) == 4 && m > 0 && rg * m / 4 <= MO_THREADS && n_groups > 0 &&
+                    reinterpret_cast<uintptr_t>(x) % 16 == 0;
+    if (v4) {
+        const int m4 = rg * m / 4, lanes = MO_THREADS / m4;
+        const int64_t min_groups = static_cast<int64_t>(lanes) * MO_KC * 4;
+        // one full wave: resident CTAs per SM x SMs (a partial second wave
+        // costs up to 2x at 5M x 18), fewer when the shard is small
+        static int occ = 0;
+        if (!occ) DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, moments_partial_v4_kernel, MO_THREADS, 0));
+        const int64_t G = std::max<int64_t>(
+            1, std::min<int64_t>(static_cast<int64_t>(ctx->num_sms) * std::max(occ, 1), ceil_div(n_groups, min_groups)));
+        const int64_t groups_per_cta = ceil_div(n_groups, G);
         double* partials = static_cast<double*>(ctx->slot("mo_partials", sizeof(double) * rec * G));
         moments_partial_v4_kernel<<<static_cast<unsigned>(G), MO_THREADS, 0, s>>>(
-            reinterpret_cast<const float4*>(x), n_local, m4, lanes, rows_per_cta, partials);
+            reinterpret_cast<const float4*>(x), n_groups, m, rg, lanes, groups_per_cta, partials);
         DNDC_LAUNCHED(ctx);
-        moments_final_kernel<<<(m + 127) / 128, 128, 0, s>>>(partials, static_cast<int>(G), m, local);
+        const int tail_rows = static_cast<int>(n_local - n_groups * rg);
+        const float* tail = reinterpret_cast<const float*>(x) + n_groups * rg * static_cast<int64_t>(m);
+        moments_final_kernel<<<m, MO_THREADS, 0, s>>>(partials, static_cast<int>(G), m, tail, tail_rows,
+                                                             local);
         DNDC_LAUNCHED(ctx);
     } else if (n_local > 0 && m > 0) {
         const int cols = std::min(m, MO_THREADS);
@@ -230,7 +267,7 @@ static void moments_axis0(dndc_ctx* ctx, const T* x, int64_t n_local, int64_t m6
         moments_partial_kernel<T><<<static_cast<unsigned>(G), MO_THREADS, 0, s>>>(x, n_local, m, cols, lanes,
                                                                                 rows_per_cta, partials);
         DNDC_LAUNCHED(ctx);
-        moments_final_kernel<<<(m + 127) / 128, 128, 0, s>>>(partials, static_cast<int>(G), m, local);
+        moments_final_kernel<<<m, MO_THREADS, 0, s>>>(partials, static_cast<int>(G), m, nullptr, 0, local);
         DNDC_LAUNCHED(ctx);
     } else {
         DNDC_CUDA(cudaMemsetAsync(local, 0, sizeof(double) * rec, s));

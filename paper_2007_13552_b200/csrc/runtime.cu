@@ -137,10 +137,22 @@ void* dndc_ctx::slot(const std::string& name, size_t bytes) {
         slots.erase(it);
     }
     void* p = nullptr;
-    DNDC_CUDA(cudaMalloc(&p, bytes));
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation && pool) {  // the array pool may hold the memory
+        (void)cudaGetLastError();
+        trim_pool();
+        e = cudaMalloc(&p, bytes);
+    }
+    DNDC_CUDA(e);
     slots[name] = {p, bytes};
     ++slot_gen;
     return p;
+}
+
+void dndc_ctx::trim_pool() {
+    if (!pool) return;
+    DNDC_CUDA(cudaStreamSynchronize(stream));
+    DNDC_CUDA(cudaMemPoolTrimTo(pool, 0));
 }
 
 void* dndc_ctx::host_staging(size_t bytes) {
@@ -218,6 +230,7 @@ int dndc_destroy(dndc_ctx* ctx) {
             if (r != ctx->rank && ctx->peer_bases[r]) cudaIpcCloseMemHandle(ctx->peer_bases[r]);
         if (ctx->peer_bases_dev) cudaFree(ctx->peer_bases_dev);
         if (ctx->xchg) cudaFree(ctx->xchg);
+        if (ctx->pool) cudaMemPoolDestroy(ctx->pool);  // released once outstanding arrays are freed
         if (ctx->comm) ncclCommDestroy(ctx->comm);
         cudaEventDestroy(ctx->ev_a);
         cudaEventDestroy(ctx->ev_b);

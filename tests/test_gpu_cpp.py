@@ -1,6 +1,7 @@
 """The C++ drop-in API (cpp/include/dnd) on the GPU: the reference's own test
 cases (test_pairwise/test_cluster/test_moments/test_chunking) written against
 it, one rank per visible GPU up to 2 (cpp/tests/test_dnd.cpp)."""
+import json
 import os
 import subprocess
 
@@ -16,3 +17,32 @@ def test_cpp_dropin_reference_cases():
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr[-3000:]
     assert " 0 failed" in r.stdout
+
+
+def _dnd(*args):
+    subprocess.run(["make", "-C", os.path.join(ROOT, "cpp")], check=True, capture_output=True)
+    r = subprocess.run([os.path.join(ROOT, "cpp", "build", "dnd"), *args], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def _ranks():
+    import torch
+    return min(2, torch.cuda.device_count())
+
+
+@pytest.mark.parametrize("algo", ["kmeans", "cdist", "moments"])
+def test_cli_bench_report_shape(algo):
+    """`dnd bench` keeps the reference report keys (tools/bench.cpp:118-128)."""
+    rep = _dnd("bench", "--algo", algo, "--synthetic", "20000x18", "--runs", "3", "--ranks", str(_ranks()))
+    for key in ("algo", "ranks", "split", "params", "warmup_runs", "timed_runs", "mean_seconds", "std_seconds"):
+        assert key in rep
+    assert rep["algo"] == algo and rep["timed_runs"] == 3
+    assert rep["mean_seconds"] > 0 and rep["std_seconds"] >= 0
+
+
+@pytest.mark.parametrize("algo", ["kmeans", "cdist", "moments"])
+def test_cli_verify_distributed_vs_single(algo):
+    """`dnd verify`: P ranks against one rank within the gate (tools/verify.cpp)."""
+    rep = _dnd("verify", "--algo", algo, "--synthetic", "3000x18", "--ranks", str(_ranks()))
+    assert rep["pass"] is True, rep

@@ -47,7 +47,8 @@ def test_offset_stability(comm):
     assert abs(std - base.std()) <= 1e-6 * base.std()
 
 
-@pytest.mark.parametrize("n,m", [(1, 3), (7, 1), (33, 300), (100_003, 32), (65_536, 18)])
+@pytest.mark.parametrize("n,m", [(1, 3), (7, 1), (33, 300), (100_003, 32), (65_536, 18), (2, 18), (3, 17), (100_001, 18),
+                                 (50_003, 5), (40_001, 130), (10_007, 257), (5_003, 6), (1_000_003, 3)])
 def test_moments_shapes(comm, oracle, n, m):
     xh = oracle.uniform_f32(n, m, n + m)
     a = dnd.from_global(xh, (n, m), 0, comm)
