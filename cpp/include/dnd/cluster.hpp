@@ -33,6 +33,7 @@ std::vector<double> kmeans_init_centroids(const DndArray<T>& x, int k, std::uint
     detail::require_2d(x, "kmeans_init_centroids");
     const index_t n = x.shape()[0], m = x.shape()[1];
     if (k < 1 || k > n) throw ValueError("kmeans_init_centroids: k=" + std::to_string(k) + " out of range");
+    if (x.split() && *x.split() != 0) return kmeans_init_centroids(resplit(x, 0), k, seed);  // cluster.cpp:79
     std::vector<double> c(static_cast<std::size_t>(k * m), 0.0);
     if constexpr (std::is_same_v<T, float>) {
         index_t rows = 0;
@@ -64,9 +65,8 @@ template <typename T>
 KMeansModel kmeans_fit(const DndArray<T>& x, int k, int max_iter, double tol, std::uint64_t seed) {
     static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "kmeans_fit: float or double");
     detail::require_2d(x, "kmeans_fit");
-    if (!x.split() && x.comm().size() > 1)
-        throw ValueError("kmeans_fit: pass row shards (split=0); replicated input on several ranks is not on the "
-                         "B200 path");
+    if ((x.split() && *x.split() != 0) || (!x.split() && x.comm().size() > 1))
+        return kmeans_fit(resplit(x, 0), k, max_iter, tol, seed);  // cluster.cpp:91
     const index_t n = x.shape()[0], m = x.shape()[1];
     KMeansModel model;
     model.k = k;
@@ -91,6 +91,8 @@ KMeansModel kmeans_fit(const DndArray<T>& x, int k, int max_iter, double tol, st
 template <typename T>
 DndArray<std::int32_t> kmeans_predict(const KMeansModel& model, const DndArray<T>& x) {
     detail::require_2d(x, "kmeans_predict");
+    if (x.split() && *x.split() != 0)
+        throw ValueError("kmeans_predict: input must be split=0 or replicated");  // cluster.cpp:160-161
     if (x.shape()[1] != model.n_features)
         throw ValueError("kmeans_predict: model has " + std::to_string(model.n_features) + " features, input " +
                          std::to_string(x.shape()[1]));

@@ -80,6 +80,7 @@ inline double variance_from(const MomentState& s, std::size_t i, std::int64_t dd
 /// replicated arrays are reduced locally like the reference.
 template <typename T>
 MomentState global_state(const DndArray<T>& a, int axis) {
+    if (a.split() && *a.split() != 0) return global_state(resplit(a, 0), axis);
     if (!a.split()) {
         Tile<double> t{a.lshape(), {}};
         const Tile<T> h = a.tile();

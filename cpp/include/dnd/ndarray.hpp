@@ -7,11 +7,14 @@
 //    C-ABI, freed with the last copy); device_data() exposes it;
 //  * tile() returns a HOST copy of the shard by value (the reference returns a
 //    reference to its host tile); code that reads tile().data keeps working;
-//  * split must be 0 or none (the hot path's layouts; resplit to other axes is
-//    SURVEY.md 8(f) F1, not built);
+//  * any split axis (or none); the hot-path kernels take row shards, so
+//    cdist / kmeans_fit / moments resplit other layouts to split=0 first, as
+//    the reference does (pairwise.cpp:41, cluster.cpp:79) -- resplit runs on
+//    the GPUs (dndc_resplit: one grouped NCCL exchange);
 //  * element types with device kernels: float and double (int32 for labels).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -39,12 +42,19 @@ inline void validate_shape_split(const std::vector<index_t>& shape, std::optiona
         if (e < 0) throw ValueError("negative extent in shape " + shape_string(shape));
     if (split && (*split < 0 || *split >= static_cast<int>(shape.size())))
         throw ValueError("split axis " + std::to_string(*split) + " out of range for shape " + shape_string(shape));
-    if (split && *split != 0)
-        throw ValueError("split=" + std::to_string(*split) +
-                         ": the B200 arrays hold row shards (split=0) or replicated data (split=none)");
 }
 
-/// Rows of this rank and elements per row (product of the trailing extents).
+/// Local extents of this rank's shard (ndarray.hpp local_extents).
+inline std::vector<index_t> local_extents(const std::vector<index_t>& shape, std::optional<int> split,
+                                         const Communicator& comm) {
+    std::vector<index_t> l = shape;
+    if (split) l[static_cast<std::size_t>(*split)] = chunk_map(shape[static_cast<std::size_t>(*split)], comm.size())
+                                                         .extent(comm.rank());
+    return l;
+}
+
+/// Rows of this rank and elements per row (product of the trailing extents),
+/// for split 0 or none.
 inline void local_rows(const std::vector<index_t>& shape, std::optional<int> split, const Communicator& comm,
                        index_t& row0, index_t& rows, index_t& row_elems) {
     const index_t n = shape.empty() ? 1 : shape[0];
@@ -104,11 +114,11 @@ public:
 
     ChunkMap split_chunks() const {
         if (!split_) throw ValueError("split_chunks: array is not split");
-        return chunk_map(shape_[0], comm_.size());
+        return chunk_map(shape_[static_cast<std::size_t>(*split_)], comm_.size());
     }
 
-    /// Row offset of this rank's shard in the global array (0 when replicated).
-    index_t row_offset() const { return split_ ? split_chunks().offset(comm_.rank()) : 0; }
+    /// Row offset of this rank's shard in the global array (0 unless split=0).
+    index_t row_offset() const { return split_ == 0 ? split_chunks().offset(comm_.rank()) : 0; }
 
 private:
     std::vector<index_t> shape_;
@@ -122,14 +132,25 @@ namespace detail {
 template <typename T>
 DndArray<T> empty_like_shape(std::vector<index_t> shape, std::optional<int> split, const Communicator& comm) {
     validate_shape_split(shape, split);
-    index_t row0, rows, row_elems;
-    local_rows(shape, split, comm, row0, rows, row_elems);
-    std::vector<index_t> lshape = shape;
-    if (!lshape.empty()) lshape[0] = rows;
-    auto dev = device_alloc<T>(comm, rows * row_elems);
+    std::vector<index_t> lshape = local_extents(shape, split, comm);
+    auto dev = device_alloc<T>(comm, product(lshape));
     return DndArray<T>(std::move(shape), split, comm, std::move(lshape), std::move(dev));
 }
 }  // namespace detail
+
+/// Same global content on another split axis, or replicated (ndarray.hpp:340-386),
+/// moved between the HBM shards by dndc_resplit.
+template <typename T>
+DndArray<T> resplit(const DndArray<T>& a, std::optional<int> new_split) {
+    detail::validate_shape_split(a.shape(), new_split);
+    if (a.split() == new_split) return a;
+    auto b = detail::empty_like_shape<T>(a.shape(), new_split, a.comm());
+    if (a.numel_global() > 0)
+        detail::check(dndc_resplit(a.comm().handle(), a.device_data(), a.ndim(), a.shape().data(),
+                                   static_cast<std::int64_t>(sizeof(T)), a.split() ? *a.split() : -1,
+                                   new_split ? *new_split : -1, b.device_data()));
+    return b;
+}
 
 // ---------------------------------------------------------------- factories
 
@@ -140,6 +161,9 @@ template <typename T>
 DndArray<T> random_uniform(std::vector<index_t> shape, std::optional<int> split, std::uint64_t seed,
                            const Communicator& comm) {
     static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "random_uniform: float or double");
+    detail::validate_shape_split(shape, split);
+    if (split && *split != 0 && shape.size() > 1)  // generated as row shards, then moved
+        return resplit(random_uniform<T>(shape, 0, seed, comm), split);
     auto a = detail::empty_like_shape<T>(shape, split, comm);
     index_t row0, rows, row_elems;
     detail::local_rows(shape, split, comm, row0, rows, row_elems);
@@ -163,6 +187,22 @@ DndArray<T> from_global(const std::vector<T>& data, std::vector<index_t> shape, 
         throw ValueError("from_global: data holds " + std::to_string(data.size()) + " elements, shape " +
                          detail::shape_string(shape) + " needs " + std::to_string(detail::product(shape)));
     auto a = detail::empty_like_shape<T>(shape, split, comm);
+    if (split && *split != 0) {
+        // (outer, extent, inner) view of the split axis: copy this rank's slab
+        const std::size_t s = static_cast<std::size_t>(*split);
+        index_t outer = 1, inner = 1;
+        for (std::size_t i = 0; i < s; ++i) outer *= shape[i];
+        for (std::size_t i = s + 1; i < shape.size(); ++i) inner *= shape[i];
+        const ChunkMap map = chunk_map(shape[s], comm.size());
+        const index_t off = map.offset(comm.rank()), ext = map.extent(comm.rank());
+        std::vector<T> local(static_cast<std::size_t>(outer * ext * inner));
+        for (index_t o = 0; o < outer; ++o)
+            std::copy_n(data.begin() + (o * shape[s] + off) * inner, ext * inner, local.begin() + o * ext * inner);
+        if (!local.empty())
+            detail::check(dndc_memcpy(comm.handle(), a.device_data(), local.data(), local.size() * sizeof(T),
+                                      DNDC_COPY_H2D));
+        return a;
+    }
     index_t row0, rows, row_elems;
     detail::local_rows(shape, split, comm, row0, rows, row_elems);
     if (rows * row_elems > 0)
@@ -175,6 +215,7 @@ DndArray<T> from_global(const std::vector<T>& data, std::vector<index_t> shape, 
 template <typename T>
 std::vector<T> gather(const DndArray<T>& a) {
     if (!a.split()) return a.tile().data;
+    if (*a.split() != 0) return resplit(a, std::nullopt).tile().data;
     std::vector<T> out(static_cast<std::size_t>(a.numel_global()));
     index_t row_elems = 1;
     for (std::size_t i = 1; i < a.shape().size(); ++i) row_elems *= a.shape()[i];

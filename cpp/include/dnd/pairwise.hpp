@@ -38,6 +38,7 @@ DndArray<T> cdist(const DndArray<T>& x) {
     detail::require_2d(x, "cdist");
     const index_t n = x.shape()[0], m = x.shape()[1];
     if (n == 0) throw ValueError("cdist: empty input");
+    if (x.split() && *x.split() != 0) return cdist(resplit(x, 0));  // pairwise.cpp:41
     index_t rows = 0;
     const T* xl = detail::rank_rows(x, rows);
     auto out = detail::empty_like_shape<T>({n, n}, 0, x.comm());
@@ -60,6 +61,9 @@ DndArray<T> cdist_xy(const DndArray<T>& x, const DndArray<T>& y) {
     if (x.shape()[1] != y.shape()[1])
         throw ValueError("cdist_xy: feature counts differ (" + std::to_string(x.shape()[1]) + " vs " +
                          std::to_string(y.shape()[1]) + ")");
+    // pairwise.cpp:93-94: x to row shards; y other than row shards replicated
+    if (x.split() && *x.split() != 0) return cdist_xy(resplit(x, 0), y);
+    if (y.split() && *y.split() != 0) return cdist_xy(x, resplit(y, std::nullopt));
     const index_t n = x.shape()[0], ny = y.shape()[0], m = x.shape()[1];
     index_t rows = 0;
     const T* xl = detail::rank_rows(x, rows);

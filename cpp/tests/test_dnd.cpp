@@ -201,6 +201,61 @@ int main() {
         auto r2 = dnd::random_uniform<float>({53, 5}, std::nullopt, 42, comm);
         CHECK(dnd::gather(r1) == dnd::gather(r2));
     });
+
+    // resplit (test_ndarray.cpp:205-260, acceptance.cpp:70-89): every split
+    // transition preserves the content bitwise, lands on the requested axis,
+    // and balances the new axis per its chunk map; ranks 1..visible GPUs
+    {
+        std::vector<double> data3(5 * 7 * 3);
+        for (std::size_t i = 0; i < data3.size(); ++i) data3[i] = std::sin(0.37 * static_cast<double>(i)) * 100.0;
+        const std::vector<std::optional<int>> splits{std::nullopt, 0, 1, 2};
+        each_world([&](const Communicator& comm) {
+            for (const auto& from : splits)
+                for (const auto& to : splits) {
+                    auto a = dnd::from_global(data3, {5, 7, 3}, from, comm);
+                    auto r = dnd::resplit(a, to);
+                    CHECK(r.split() == to);
+                    CHECK(dnd::gather(r) == data3);
+                    if (to) CHECK(r.lshape()[static_cast<std::size_t>(*to)] == r.split_chunks().extent(comm.rank()));
+                }
+            auto a0 = dnd::from_global(data3, {5, 7, 3}, 0, comm);
+            CHECK(dnd::resplit(dnd::resplit(a0, 1), 0).tile().data == a0.tile().data);
+            // 2 x 4, split=1 -> none on every rank
+            const std::vector<double> mat{1, 2, 3, 4, 5, 6, 7, 8};
+            auto r = dnd::resplit(dnd::from_global(mat, {2, 4}, 1, comm), std::nullopt);
+            CHECK(!r.split() && r.lshape() == std::vector<index_t>({2, 4}) && r.tile().data == mat);
+            // f32 through the same machinery (test_ndarray.cpp:290-300)
+            std::vector<float> f(24);
+            for (int i = 0; i < 24; ++i) f[i] = static_cast<float>(i) * 0.25f;
+            CHECK(dnd::gather(dnd::resplit(dnd::from_global(f, {4, 6}, 1, comm), 0)) == f);
+            // random_uniform with split=1 equals split=0 content
+            CHECK(dnd::gather(dnd::random_uniform<float>({37, 9}, 1, 42, comm)) ==
+                  dnd::gather(dnd::random_uniform<float>({37, 9}, 0, 42, comm)));
+        });
+        // cdist of inputs with other splits (test_pairwise.cpp:47-58)
+        const index_t n = 23, m = 5;
+        std::vector<double> data(n * m);
+        for (std::size_t i = 0; i < data.size(); ++i) data[i] = std::cos(0.91 * static_cast<double>(i));
+        const auto expected = naive_cdist(data, n, data, n, m);
+        each_world([&](const Communicator& comm) {
+            for (auto split : {std::optional<int>(1), std::optional<int>()}) {
+                auto x = dnd::from_global(data, {n, m}, split, comm);
+                const auto d = dnd::gather(dnd::cdist(x));
+                double dev = 0.0;
+                for (std::size_t i = 0; i < d.size(); ++i) dev = std::max(dev, std::abs(d[i] - expected[i]));
+                CHECK(dev <= 1e-8);
+                // kmeans_fit and moments on the same layouts match split=0
+                auto x0 = dnd::from_global(data, {n, m}, 0, comm);
+                const auto ma = dnd::kmeans_fit(x, 3, 10, 0.0, 7), mb = dnd::kmeans_fit(x0, 3, 10, 0.0, 7);
+                CHECK(ma.centroids == mb.centroids && ma.iterations_run == mb.iterations_run);
+                const auto va = dnd::gather(dnd::var_axis(x, 0)), vb = dnd::gather(dnd::var_axis(x0, 0));
+                for (index_t c = 0; c < m; ++c) CHECK(close_rel(va[c], vb[c], 1e-14));
+            }
+            CHECK_THROWS_AS(dnd::kmeans_predict(dnd::kmeans_fit(dnd::from_global(data, {n, m}, 0, comm), 2, 3, 0.0, 1),
+                                                dnd::from_global(data, {n, m}, 1, comm)),
+                            dnd::ValueError);
+        });
+    }
     std::printf("test_dnd: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
 }

@@ -9,11 +9,15 @@
 //              [--iters 20] [--ranks 1] [--warmup 1] [--runs 9] [--seed 42]
 //   dnd verify --algo kmeans|cdist|moments --synthetic 20000x18 [--ranks 2] ...
 //
-// bench prints one JSON object (the reference's report keys plus GB/s);
+// bench prints one JSON object (the reference's report keys plus GB/s, the
+// fraction of p x the measured HBM copy peak, and NVML clocks);
 // verify runs the algorithm on `ranks` GPUs and on one and reports the largest
 // relative deviation |a-b|/max(1,|b|) against the gate (distances/centroids
 // 1e-5, moments 1e-12), exit status 1 when it fails.
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -21,6 +25,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dnd/dnd.hpp"
@@ -32,12 +37,13 @@ struct Options {
     dnd::index_t rows = 20000, cols = 18;
     int k = 8, iters = 20, ranks = 1, warmup = 1, runs = 9;
     std::uint64_t seed = 42;
+    double peak_gbs = 6538.9;  // MEASURED_PEAKS.json hbm_gbs (copy bandwidth)
 };
 
 [[noreturn]] void usage(const char* why) {
     std::fprintf(stderr,
                  "dnd: %s\nusage: dnd bench|verify --algo kmeans|cdist|moments --synthetic ROWSxCOLS [--k K] "
-                 "[--iters N] [--ranks P] [--warmup W] [--runs R] [--seed S]\n",
+                 "[--iters N] [--ranks P] [--warmup W] [--runs R] [--seed S] [--peak-gbs G]\n",
                  why);
     std::exit(2);
 }
@@ -63,6 +69,7 @@ Options parse(int argc, char** argv) {
         else if (a == "--warmup") o.warmup = std::atoi(v.c_str());
         else if (a == "--runs") o.runs = std::atoi(v.c_str());
         else if (a == "--seed") o.seed = std::strtoull(v.c_str(), nullptr, 10);
+        else if (a == "--peak-gbs") o.peak_gbs = std::atof(v.c_str());
         else usage(("unknown option " + a).c_str());
     }
     if (o.algo != "kmeans" && o.algo != "cdist" && o.algo != "moments") usage("unknown --algo");
@@ -100,6 +107,68 @@ double run_algo(const Options& o, const dnd::DndArray<float>& x, std::vector<dou
     return mu[0] + var[0];
 }
 
+// SM clock and throttle reasons of GPU 0 sampled every 5 ms during the timed
+// runs through NVML (dlopen'ed: the driver ships it; absent -> "clocks": null)
+class ClockSampler {
+  public:
+    ClockSampler() {
+        lib_ = dlopen("libnvidia-ml.so.1", RTLD_NOW);
+        if (!lib_) return;
+        auto init = reinterpret_cast<int (*)()>(dlsym(lib_, "nvmlInit_v2"));
+        auto get = reinterpret_cast<int (*)(unsigned, void**)>(dlsym(lib_, "nvmlDeviceGetHandleByIndex_v2"));
+        clock_ = reinterpret_cast<int (*)(void*, int, unsigned*)>(dlsym(lib_, "nvmlDeviceGetClockInfo"));
+        maxclock_ = reinterpret_cast<int (*)(void*, int, unsigned*)>(dlsym(lib_, "nvmlDeviceGetMaxClockInfo"));
+        reasons_ = reinterpret_cast<int (*)(void*, unsigned long long*)>(
+            dlsym(lib_, "nvmlDeviceGetCurrentClocksThrottleReasons"));
+        ok_ = init && get && clock_ && maxclock_ && reasons_ && init() == 0 && get(0, &dev_) == 0;
+    }
+    void start() {
+        if (!ok_) return;
+        run_ = true;
+        th_ = std::thread([this] {
+            while (run_) {
+                unsigned mhz = 0;
+                unsigned long long r = 0;
+                if (clock_(dev_, 1 /*NVML_CLOCK_SM*/, &mhz) == 0) mhz_.push_back(mhz);
+                if (reasons_(dev_, &r) == 0) seen_ |= r;
+                std::this_thread::sleep_for(std::chrono::milliseconds(5));
+            }
+        });
+    }
+    void stop() {
+        if (!th_.joinable()) return;
+        run_ = false;
+        th_.join();
+    }
+    std::string json() {
+        if (!ok_ || mhz_.empty()) return "null";
+        std::sort(mhz_.begin(), mhz_.end());
+        unsigned mx = 0;
+        maxclock_(dev_, 1, &mx);
+        static const std::pair<unsigned long long, const char*> names[] = {
+            {0x4, "sw_power_cap"}, {0x8, "hw_slowdown"}, {0x20, "sw_thermal_slowdown"},
+            {0x40, "hw_thermal_slowdown"}, {0x80, "hw_power_brake_slowdown"}};
+        std::string rs;
+        for (const auto& [bit, name] : names)
+            if (seen_ & bit) rs += std::string(rs.empty() ? "" : ", ") + "\"" + name + "\"";
+        return "{\"sm_mhz\": " + std::to_string(mhz_[mhz_.size() / 2]) + ", \"sm_max_mhz\": " + std::to_string(mx) +
+               ", \"reasons\": [" + rs + "], \"samples\": " + std::to_string(mhz_.size()) + "}";
+    }
+    ~ClockSampler() { stop(); }
+
+  private:
+    void* lib_ = nullptr;
+    void* dev_ = nullptr;
+    bool ok_ = false;
+    std::atomic<bool> run_{false};
+    std::thread th_;
+    std::vector<unsigned> mhz_;
+    unsigned long long seen_ = 0;
+    int (*clock_)(void*, int, unsigned*) = nullptr;
+    int (*maxclock_)(void*, int, unsigned*) = nullptr;
+    int (*reasons_)(void*, unsigned long long*) = nullptr;
+};
+
 double bytes_per_run(const Options& o) {
     const double xb = 4.0 * o.rows * o.cols;
     if (o.algo == "kmeans") return xb * o.iters;
@@ -110,10 +179,12 @@ double bytes_per_run(const Options& o) {
 int bench(const Options& o) {
     std::vector<double> secs;
     std::mutex mu;
+    ClockSampler clocks;
     dnd::run_world(o.ranks, [&](const dnd::Communicator& comm) {
         const auto x = dnd::random_uniform<float>({o.rows, o.cols}, 0, o.seed, comm);
         double sink = 0.0;
         for (int w = 0; w < o.warmup; ++w) sink += run_algo(o, x, nullptr);
+        if (comm.rank() == 0) clocks.start();
         // slowest rank per run (bench.cpp:102-112): the ranks are threads of
         // this process, so the max is taken under a mutex after the runs
         std::vector<double> mine;
@@ -124,6 +195,7 @@ int bench(const Options& o) {
             comm.barrier();
             mine.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
         }
+        if (comm.rank() == 0) clocks.stop();
         if (!std::isfinite(sink)) throw dnd::ValueError("benchmark produced non-finite results");
         std::lock_guard<std::mutex> lock(mu);
         if (secs.empty()) secs.assign(mine.size(), 0.0);
@@ -135,11 +207,11 @@ int bench(const Options& o) {
     const double mean = st.mean[0], sd = std::sqrt(st.m2[0] / static_cast<double>(st.count));
     std::printf("{\"algo\": \"%s\", \"ranks\": %d, \"split\": 0, \"params\": {\"rows\": %lld, \"cols\": %lld, "
                 "\"k\": %d, \"iters\": %d, \"seed\": %llu}, \"warmup_runs\": %d, \"timed_runs\": %d, "
-                "\"mean_seconds\": %.9g, \"std_seconds\": %.9g, \"GB_per_s\": %.6g, \"device\": \"B200 (libdndc)\", "
-                "\"run_seconds\": [%s]}\n",
+                "\"mean_seconds\": %.9g, \"std_seconds\": %.9g, \"GB_per_s\": %.6g, \"roofline_frac\": %.4f, "
+                "\"peak_gbs_per_gpu\": %.1f, \"clocks\": %s, \"device\": \"B200 (libdndc)\", \"run_seconds\": [%s]}\n",
                 o.algo.c_str(), o.ranks, static_cast<long long>(o.rows), static_cast<long long>(o.cols), o.k, o.iters,
                 static_cast<unsigned long long>(o.seed), o.warmup, o.runs, mean, sd, bytes_per_run(o) / mean / 1e9,
-                runs.c_str());
+                bytes_per_run(o) / mean / 1e9 / (o.peak_gbs * o.ranks), o.peak_gbs, clocks.json().c_str(), runs.c_str());
     return 0;
 }
 

@@ -95,6 +95,15 @@ int dndc_memcpy(dndc_ctx* ctx, void* dst, const void* src, size_t bytes, int kin
 int dndc_allgather_rows(dndc_ctx* ctx, const void* local, int64_t rows, int64_t row_bytes, void* out_host,
                         int64_t* total_rows);
 
+/* resplit (ndarray.hpp:340-386, F1), collective: move a row-major N-D array
+ * (ndim <= 8, elem_bytes 1/2/4/8) from src_split to dst_split (-1 = replicated)
+ * without changing its global content.  src_local / dst_local are this rank's
+ * device shards under the chunk map of the respective axis; replicated ->
+ * split slices locally, split -> anything is one grouped NCCL send/recv of the
+ * intersection blocks.  Returns after the stream has drained. */
+int dndc_resplit(dndc_ctx* ctx, const void* src_local, int ndim, const int64_t* shape, int64_t elem_bytes,
+                 int src_split, int dst_split, void* dst_local);
+
 /* Communicator::allreduce(plus) (transport.hpp:136-148, A15), collective, in
  * place on a device buffer: sum over ranks folded in rank order 0..p-1 from
  * the zero identity, bit-identical on every rank. */

@@ -55,6 +55,7 @@ _SIGS = {
     "dndc_free": [_P, _P],
     "dndc_memcpy": [_P, _P, _P, C.c_size_t, _i32],
     "dndc_allgather_rows": [_P, _P, _i64, _i64, _P, _P],
+    "dndc_resplit": [_P, _P, _i32, _P, _i64, _i32, _i32, _P],
     "dndc_allreduce_f64": [_P, _P, _i64],
     "dndc_kmeans_step_f32": [_P, _P, _i64, _i64, _P, _i32, _P, _P],
     "dndc_fill_uniform_f32": [_P, _u64, _i64, _i64, _i64, _P],

@@ -10,7 +10,7 @@ live in HBM as torch CUDA tensors, which are used only as device memory.
   ------------------------------------------  -----------------------------------
   Communicator / run_world (transport.hpp)    Communicator (one per GPU / rank)
   chunk_map (chunking.hpp:27)                 chunk_map
-  DndArray<T> (ndarray.hpp:58-91)             DndArray (split 0 or None)
+  DndArray<T> (ndarray.hpp:58-91)             DndArray (any split, resplit)
   random_uniform / from_global / gather       random_uniform / from_global / gather
   detail::row_norms / distance_block          row_norms / distance_block
   cdist / cdist_xy (pairwise.hpp:15-19)       cdist / cdist_xy
@@ -32,7 +32,7 @@ from ._lib import TransportError, check, lib
 
 __all__ = [
     "Communicator", "DndArray", "KMeansModel", "MomentState", "TransportError", "chunk_map",
-    "random_uniform", "from_global", "gather", "row_norms", "distance_block", "cdist", "cdist_xy",
+    "random_uniform", "from_global", "gather", "resplit", "row_norms", "distance_block", "cdist", "cdist_xy",
     "kmeans_init_indices", "kmeans_init_centroids", "kmeans_fit", "kmeans_predict", "mean_axis",
     "var_axis", "stddev_axis", "moments_axis0", "kmeanspp_indices",
 ]
@@ -131,7 +131,8 @@ def chunk_map(n: int, p: int) -> tuple[np.ndarray, np.ndarray]:
 
 @dataclass
 class DndArray:
-    """A 2-D (or 1-D) array split along axis 0 (or replicated, split=None)."""
+    """An N-D array split along one axis (or replicated, split=None); the
+    hot-path ops take row shards and resplit other layouts first."""
 
     shape: tuple
     split: int | None
@@ -147,23 +148,54 @@ class DndArray:
     def split_chunks(self):
         if self.split is None:
             raise ValueError("split_chunks: array is not split")
-        return chunk_map(self.shape[0], self.comm.size())
+        return chunk_map(self.shape[self.split], self.comm.size())
 
     def row_offset(self) -> int:
-        return 0 if self.split is None else int(self.split_chunks()[0][self.comm.rank()])
+        return int(self.split_chunks()[0][self.comm.rank()]) if self.split == 0 else 0
 
 
 def _check_split(shape, split):
     if any(e < 0 for e in shape):
         raise ValueError(f"negative extent in shape {tuple(shape)}")
-    if split is not None and split != 0:
-        raise ValueError("the B200 hot path supports split=0 or replicated arrays (SURVEY.md 8(f) F1)")
+    if split is not None and not 0 <= split < len(shape):
+        raise ValueError(f"split axis {split} out of range for shape {tuple(shape)}")
+
+
+def _local_shape(shape, split, comm):
+    if split is None:
+        return tuple(shape)
+    off, ext = chunk_map(shape[split], comm.size())
+    return tuple(int(ext[comm.rank()]) if d == split else e for d, e in enumerate(shape))
+
+
+def resplit(a: DndArray, new_split) -> DndArray:
+    """dnd::resplit (ndarray.hpp:340-386): same global content on another
+    split axis or replicated, moved between the HBM shards by dndc_resplit
+    (one grouped NCCL exchange of the intersection blocks)."""
+    _check_split(a.shape, new_split)
+    if a.split == new_split:
+        return a
+    tile = torch.empty(_local_shape(a.shape, new_split, a.comm), dtype=a.tile.dtype, device=a.tile.device)
+    if int(np.prod(a.shape)) > 0:
+        shp = np.asarray(a.shape, np.int64)
+        src = a.tile.contiguous()
+        check(lib().dndc_resplit(a.comm.handle, _ptr(src), len(a.shape), shp.ctypes.data, src.element_size(),
+                                 -1 if a.split is None else int(a.split), -1 if new_split is None else int(new_split),
+                                 _ptr(tile)))
+    return DndArray(a.shape, new_split, a.comm, tile)
+
+
+def _rows(x: DndArray) -> DndArray:
+    """x as row shards or replicated (pairwise.cpp:41, cluster.cpp:91)."""
+    return resplit(x, 0) if x.split not in (None, 0) else x
 
 
 def random_uniform(shape, split, seed: int, comm: Communicator, dtype=torch.float32) -> DndArray:
     """dnd::random_uniform<T> (ndarray.hpp:154-169), generated on the GPU."""
     shape = tuple(int(s) for s in shape)
     _check_split(shape, split)
+    if split not in (None, 0):  # generated as row shards, then moved
+        return resplit(random_uniform(shape, 0, seed, comm, dtype), split)
     n = shape[0]
     m = int(np.prod(shape[1:])) if len(shape) > 1 else 1
     if split is None:
@@ -189,8 +221,10 @@ def from_global(data, shape, split, comm: Communicator, dtype=None) -> DndArray:
                          f"{int(np.prod(shape))}")
     arr = arr.reshape(shape)
     if split is not None:
-        off, ext = chunk_map(shape[0], comm.size())
-        arr = arr[off[comm.rank()]: off[comm.rank()] + ext[comm.rank()]]
+        off, ext = chunk_map(shape[split], comm.size())
+        sl = [slice(None)] * len(shape)
+        sl[split] = slice(int(off[comm.rank()]), int(off[comm.rank()] + ext[comm.rank()]))
+        arr = arr[tuple(sl)]
     np_dtype = np.float64 if dtype == torch.float64 else (np.int32 if dtype == torch.int32 else np.float32)
     tile = torch.from_numpy(np.ascontiguousarray(arr, dtype=np_dtype)).to(f"cuda:{comm.device}")
     return DndArray(shape, split, comm, tile)
@@ -198,6 +232,8 @@ def from_global(data, shape, split, comm: Communicator, dtype=None) -> DndArray:
 
 def gather(a: DndArray) -> np.ndarray:
     """Full global content on every rank (dnd::gather, ndarray.hpp:389-393)."""
+    if a.split not in (None, 0):
+        a = resplit(a, None)
     local = a.tile.detach().cpu().numpy()
     if a.split is None or a.comm.size() == 1:
         return local.reshape(a.shape)
@@ -251,8 +287,8 @@ def cdist(x: DndArray) -> DndArray:
     _require_2d(x, "cdist")
     if x.shape[0] == 0:
         raise ValueError("cdist: input has no rows")
-    if x.split is None:
-        raise ValueError("cdist: replicated input; redistribute to split=0 (SURVEY.md 8(f) F1)")
+    if x.split != 0:
+        x = resplit(x, 0)  # pairwise.cpp:41
     n, m = x.shape
     out = torch.empty((x.tile.shape[0], n), dtype=x.tile.dtype, device=x.tile.device)
     check(_fn("dndc_cdist", x.tile)(x.comm.handle, _ptr(x.tile), x.tile.shape[0], n, m, _ptr(out)))
@@ -266,6 +302,9 @@ def cdist_xy(x: DndArray, y: DndArray) -> DndArray:
         raise ValueError("cdist_xy: inputs must be 2-D")
     if x.shape[1] != y.shape[1]:
         raise ValueError(f"cdist_xy: feature counts {x.shape[1]} and {y.shape[1]} do not match")
+    x = _rows(x)  # pairwise.cpp:93-94
+    if y.split not in (None, 0):
+        y = resplit(y, None)
     m = x.shape[1]
     nx_local = x.tile.shape[0] if x.split == 0 else x.shape[0]
     out = torch.empty((nx_local, y.shape[0]), dtype=x.tile.dtype, device=x.tile.device)
@@ -313,6 +352,7 @@ def _shard(x: DndArray):
 def kmeans_init_centroids(x: DndArray, k: int, seed: int) -> np.ndarray:
     """cluster.cpp:77-81 (rows replicated to every rank, f64)."""
     _require_2d(x, "kmeans_init_centroids")
+    x = _rows(x)
     comm, n_local, n_global = _shard(x)
     m = x.shape[1]
     out = np.empty((max(k, 1), m), np.float64)
@@ -328,6 +368,7 @@ def kmeans_init_centroids(x: DndArray, k: int, seed: int) -> np.ndarray:
 def kmeans_fit(x: DndArray, k: int, max_iter: int, tol: float, seed: int, init=None) -> KMeansModel:
     """Lloyd's algorithm (cluster.cpp:83-153) on the fused GPU kernels."""
     _require_2d(x, "kmeans_fit")
+    x = _rows(x)
     comm, n_local, n_global = _shard(x)
     m = x.shape[1]
     if k < 1:
@@ -354,6 +395,8 @@ def kmeans_fit(x: DndArray, k: int, max_iter: int, tol: float, seed: int, init=N
 def kmeans_predict(model: KMeansModel, x: DndArray) -> DndArray:
     """cluster.cpp:155-172 (ties to the lowest centroid index)."""
     _require_2d(x, "kmeans_predict")
+    if x.split not in (None, 0):
+        raise ValueError("kmeans_predict: input must be split=0 or replicated")  # cluster.cpp:160-161
     if x.shape[1] != model.n_features:
         raise ValueError(f"kmeans_predict: input has {x.shape[1]} features, model expects {model.n_features}")
     n_local = x.tile.shape[0]
@@ -376,6 +419,7 @@ class MomentState:
 def moments_axis0(a: DndArray) -> MomentState:
     """local_moments_axis + rank-order combine (moments.cpp:41-52)."""
     _require_2d(a, "moments")
+    a = _rows(a)
     m = a.shape[1]
     cnt = np.zeros(1, np.int64)
     mean = np.zeros(max(m, 1), np.float64)
@@ -417,6 +461,7 @@ def stddev_axis(a: DndArray, axis: int = 0, ddof: int = 0) -> DndArray:
 def kmeanspp_indices(x: DndArray, k: int, seed: int) -> np.ndarray:
     """k-means++ seeding (BASELINE config 5; definition in DESIGN.md)."""
     _require_2d(x, "kmeanspp")
+    x = _rows(x)
     if x.tile.dtype != torch.float32:
         raise ValueError("kmeanspp: float32 input required")
     comm, n_local, n_global = _shard(x)

@@ -86,3 +86,35 @@ def test_kmeanspp_duplicate_rows_fallback(comm, oracle):
     xh = np.ones((100, 4), np.float32)
     x = dnd.from_global(xh, (100, 4), 0, comm)
     assert np.array_equal(dnd.kmeanspp_indices(x, 4, 5), oracle.kmeanspp_indices(xh, 4, 5))
+
+
+@pytest.mark.parametrize("shape", [(5, 7, 3), (23, 5), (1, 1, 1), (7, 6, 5)])
+def test_resplit_all_transitions(comm, shape):
+    """resplit (ndarray.hpp:340-386; test_ndarray.cpp:233-250): every split
+    transition keeps the content bitwise and lands on the requested axis."""
+    data = np.arange(int(np.prod(shape)), dtype=np.float64) * 0.37 - 3.0
+    splits = [None] + list(range(len(shape)))
+    for src in splits:
+        for dst in splits:
+            a = dnd.from_global(data, shape, src, comm)
+            r = dnd.resplit(a, dst)
+            assert r.split == dst
+            assert np.array_equal(dnd.gather(r).ravel(), data)
+            if dst is not None:
+                assert r.tile.shape[dst] == int(r.split_chunks()[1][comm.rank()])
+
+
+def test_ops_on_other_splits(comm, oracle):
+    """cdist / kmeans_fit / moments accept split=1 and replicated inputs by
+    resplitting to row shards first (pairwise.cpp:41, cluster.cpp:91)."""
+    n, m = 257, 6
+    xh = oracle.uniform_f32(n, m, 5)
+    x0 = dnd.from_global(xh, (n, m), 0, comm)
+    for split in (1, None):
+        x = dnd.from_global(xh, (n, m), split, comm)
+        assert np.array_equal(dnd.gather(dnd.cdist(x)), dnd.gather(dnd.cdist(x0)))
+        ma, mb = dnd.kmeans_fit(x, 4, 8, 0.0, 3), dnd.kmeans_fit(x0, 4, 8, 0.0, 3)
+        assert np.array_equal(ma.centroids, mb.centroids)
+        assert close(dnd.moments_axis0(x).mean, dnd.moments_axis0(x0).mean, 1e-14)
+    with pytest.raises(ValueError):
+        dnd.kmeans_predict(dnd.kmeans_fit(x0, 2, 3, 0.0, 1), dnd.from_global(xh, (n, m), 1, comm))

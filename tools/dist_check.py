@@ -99,6 +99,18 @@ def main():
     mt = dnd.kmeans_fit(tiny, 2, 4, 0.0, 7)
     lo, hi = sorted(mt.centroids[:, 0])
     report("kmeans more ranks than rows", abs(hi - 10.0) <= 1e-12 and abs(lo - (np.float32(0.1) / 2)) <= 1e-7)
+    # resplit (ndarray.hpp:340-386): all transitions bitwise, then the ops on split=1 input
+    shape3 = (7, 6, 5)
+    d3 = np.arange(np.prod(shape3), dtype=np.float64) * 0.5 - 7.0
+    good = True
+    for src in (None, 0, 1, 2):
+        for dst in (None, 0, 1, 2):
+            r = dnd.resplit(dnd.from_global(d3, shape3, src, comm), dst)
+            good &= r.split == dst and np.array_equal(dnd.gather(r).ravel(), d3)
+    report("resplit all transitions (7,6,5)", good)
+    xs1 = dnd.resplit(xk, 1)
+    m1 = dnd.kmeans_fit(xs1, 8, 10, 0.0, 42)
+    report("kmeans_fit on split=1 input", np.array_equal(m1.centroids, model.centroids))
 
     dist.barrier()
     comm.close()
