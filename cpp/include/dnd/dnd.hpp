@@ -3,6 +3,7 @@
 
 #include "dnd/chunking.hpp"
 #include "dnd/cluster.hpp"
+#include "dnd/dataio.hpp"
 #include "dnd/errors.hpp"
 #include "dnd/moments.hpp"
 #include "dnd/ndarray.hpp"

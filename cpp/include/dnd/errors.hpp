@@ -20,6 +20,10 @@ struct ValueError : Error {
 struct TransportError : Error {
     using Error::Error;
 };
+/// Malformed containers and file I/O failures (errors.hpp:40).
+struct DataError : Error {
+    using Error::Error;
+};
 /// A CUDA failure inside libdndc (no reference counterpart: the CPU path has none).
 struct DeviceError : Error {
     using Error::Error;
@@ -33,6 +37,7 @@ inline void check(int rc) {
         case DNDC_EVALUE: throw ValueError(msg);
         case DNDC_ETRANSPORT: throw TransportError(msg);
         case DNDC_ECUDA: throw DeviceError(msg);
+        case DNDC_EDATA: throw DataError(msg);
         default: throw Error(msg);
     }
 }

@@ -3,8 +3,12 @@
 // B200 dnd API, run with one rank per visible GPU (up to 2).
 //
 //     make -C cpp test && cpp/build/test_dnd
+#include <unistd.h>
+
 #include <algorithm>
 #include <cmath>
+#include <filesystem>
+#include <fstream>
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
@@ -255,6 +259,121 @@ int main() {
                                                 dnd::from_global(data, {n, m}, 1, comm)),
                             dnd::ValueError);
         });
+    }
+
+    // DNB containers (test_dataio.cpp:26-220), loaded straight into HBM
+    {
+        namespace fs = std::filesystem;
+        const fs::path dir = fs::temp_directory_path() / ("dnd_dataio_" + std::to_string(::getpid()));
+        fs::create_directories(dir);
+        auto write_text = [&](const std::string& name, const std::string& text) {
+            std::ofstream(dir / name) << text;
+            return (dir / name).string();
+        };
+        std::vector<double> d60(60);
+        for (std::size_t i = 0; i < d60.size(); ++i) d60[i] = std::sin(1.7 * static_cast<double>(i) + 0.3);
+        const std::vector<index_t> shape{5, 4, 3};
+        const std::vector<std::optional<int>> splits{std::nullopt, 0, 1, 2};
+        each_world([&](const Communicator& comm) {
+            const auto path = (dir / ("rt" + std::to_string(comm.size()))).string();
+            for (const auto& ss : splits)
+                for (const auto& ls : splits) {
+                    dnd::dnb_save(dnd::from_global(d60, shape, ss, comm), path);
+                    auto b = dnd::dnb_load<double>(path, ls, comm);
+                    CHECK(b.shape() == shape && b.split() == ls && dnd::gather(b) == d60);
+                }
+            // f32 round trip; loading as f64 names the dtype_code
+            std::vector<float> f24(24);
+            for (int i = 0; i < 24; ++i) f24[i] = static_cast<float>(i) / 7.0f;
+            const auto fpath = (dir / ("f" + std::to_string(comm.size()))).string();
+            dnd::dnb_save(dnd::from_global(f24, {6, 4}, 0, comm), fpath);
+            CHECK(dnd::gather(dnd::dnb_load<float>(fpath, 0, comm)) == f24);
+            CHECK_THROWS_AS(dnd::dnb_load<double>(fpath, 0, comm), dnd::DataError);
+            CHECK(dnd::dnb_read_header(fpath).dtype == dnd::DnbDtype::f32);
+            // chunked loads slice like the chunk map; replicated == gathered chunks
+            const auto apath = (dir / ("a" + std::to_string(comm.size()))).string();
+            dnd::dnb_save(dnd::from_global<double>({0, 1, 2, 3, 4}, {5}, std::nullopt, comm), apath);
+            const auto part = dnd::dnb_load<double>(apath, 0, comm).tile().data;
+            const auto map = dnd::chunk_map(5, comm.size());
+            std::vector<double> want;
+            for (index_t i = map.offset(comm.rank()); i < map.end(comm.rank()); ++i) want.push_back(double(i));
+            CHECK(part == want);
+            CHECK(dnd::dnb_load<double>(apath, std::nullopt, comm).tile().data ==
+                  dnd::gather(dnd::dnb_load<double>(apath, 0, comm)));
+            // an empty array gives a header-only file
+            const auto epath = (dir / ("e" + std::to_string(comm.size()))).string();
+            dnd::dnb_save(dnd::from_global<double>({}, {0, 7}, 0, comm), epath);
+            auto e = dnd::dnb_load<double>(epath, 0, comm);
+            CHECK(e.shape() == std::vector<index_t>({0, 7}) && e.numel_local() == 0);
+            CHECK(fs::file_size(epath) == 6 + 8 * 2);
+        });
+        // header law: 6 + 8 ndim + 8 numel bytes
+        dnd::run_world(1, [&](const Communicator& comm) {
+            const std::vector<std::vector<index_t>> shapes{{3}, {2, 5}, {4, 1, 6}};
+            for (const auto& sh : shapes) {
+                const auto path = (dir / "law").string();
+                dnd::dnb_save(dnd::random_uniform<double>(sh, std::nullopt, 3, comm), path);
+                CHECK(fs::file_size(path) == 6 + 8 * sh.size() + 8 * static_cast<std::uint64_t>(dnd::detail::product(sh)));
+            }
+        });
+        // malformed containers name the field
+        const auto good = (dir / "good.dnb").string();
+        dnd::run_world(1, [&](const Communicator& comm) {
+            dnd::dnb_save(dnd::from_global<double>({0, 1, 2, 3}, {4}, std::nullopt, comm), good);
+        });
+        auto clone = [&](const std::string& name, std::size_t cut, long at, char v) {
+            std::ifstream in(good, std::ios::binary);
+            std::vector<char> bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+            bytes.resize(bytes.size() - cut);
+            if (at >= 0) bytes[static_cast<std::size_t>(at)] = v;
+            std::ofstream(dir / name, std::ios::binary).write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
+            return (dir / name).string();
+        };
+        auto throws_with = [](auto&& fn, const std::string& needle) {
+            try {
+                fn();
+            } catch (const dnd::DataError& e) {
+                return std::string(e.what()).find(needle) != std::string::npos;
+            }
+            return false;
+        };
+        CHECK(throws_with([&] { dnd::dnb_read_header(clone("magic.dnb", 0, 0, 'X')); }, "magic"));
+        CHECK(throws_with([&] { dnd::dnb_read_header(clone("dtype.dnb", 0, 4, 9)); }, "dtype_code"));
+        const auto trunc = clone("short.dnb", 8, -1, 0);
+        dnd::run_world(1, [&](const Communicator& comm) {
+            CHECK(throws_with([&] { dnd::dnb_load<double>(trunc, std::nullopt, comm); }, "truncated"));
+        });
+        CHECK_THROWS_AS(dnd::dnb_read_header((dir / "missing.dnb").string()), dnd::DataError);
+        // CSV conversion
+        const auto m_dnb = (dir / "m.dnb").string();
+        dnd::csv_to_dnb(write_text("m.csv", "1,2\n3,4\n"), m_dnb);
+        std::string text;
+        std::vector<double> expect;
+        for (int i = 0; i < 7; ++i)
+            for (int j = 0; j < 4; ++j) {
+                const double v = std::cos(0.1 * (i * 4 + j)) * 100.0 - 50.0;
+                expect.push_back(v);
+                char buf[64];
+                std::snprintf(buf, sizeof buf, "%.17g", v);
+                text += buf;
+                text += j + 1 < 4 ? "," : "\n";
+            }
+        const auto r_dnb = (dir / "r.dnb").string();
+        dnd::csv_to_dnb(write_text("r.csv", text), r_dnb);
+        const auto h_dnb = (dir / "h.dnb").string();
+        dnd::csv_to_dnb(write_text("h.csv", "a,b\n1.5,2.5\n3.5, 4.5\n"), h_dnb, dnd::DnbDtype::f32, true);
+        each_world([&](const Communicator& comm) {
+            auto a = dnd::dnb_load<double>(m_dnb, std::nullopt, comm);
+            CHECK(a.shape() == std::vector<index_t>({2, 2}) && a.tile().data == std::vector<double>({1, 2, 3, 4}));
+            CHECK(dnd::gather(dnd::dnb_load<double>(r_dnb, 0, comm)) == expect);
+            auto hf = dnd::dnb_load<float>(h_dnb, std::nullopt, comm);
+            CHECK(hf.tile().data == std::vector<float>({1.5f, 2.5f, 3.5f, 4.5f}));
+        });
+        CHECK(throws_with([&] { dnd::csv_to_dnb(write_text("rag.csv", "1,2\n3\n"), (dir / "o").string()); }, "line 2"));
+        CHECK(throws_with([&] { dnd::csv_to_dnb(write_text("gar.csv", "1,2\n3,x\n"), (dir / "o").string()); },
+                          "line 2"));
+        CHECK_THROWS_AS(dnd::csv_to_dnb(write_text("empty.csv", "\n"), (dir / "o").string()), dnd::DataError);
+        fs::remove_all(dir);
     }
     std::printf("test_dnd: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;

@@ -8,6 +8,8 @@
 //   dnd bench  --algo kmeans|cdist|moments --synthetic 5000000x18 [--k 8]
 //              [--iters 20] [--ranks 1] [--warmup 1] [--runs 9] [--seed 42]
 //   dnd verify --algo kmeans|cdist|moments --synthetic 20000x18 [--ranks 2] ...
+//   (--data FILE.dnb instead of --synthetic loads a DNB container into HBM;
+//    --algo load times that load itself, f32 containers)
 //
 // bench prints one JSON object (the reference's report keys plus GB/s, the
 // fraction of p x the measured HBM copy peak, and NVML clocks);
@@ -23,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <filesystem>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -33,7 +36,7 @@
 namespace {
 
 struct Options {
-    std::string cmd, algo = "kmeans";
+    std::string cmd, algo = "kmeans", data;  // data: DNB path (else synthetic)
     dnd::index_t rows = 20000, cols = 18;
     int k = 8, iters = 20, ranks = 1, warmup = 1, runs = 9;
     std::uint64_t seed = 42;
@@ -42,7 +45,7 @@ struct Options {
 
 [[noreturn]] void usage(const char* why) {
     std::fprintf(stderr,
-                 "dnd: %s\nusage: dnd bench|verify --algo kmeans|cdist|moments --synthetic ROWSxCOLS [--k K] "
+                 "dnd: %s\nusage: dnd bench|verify --algo kmeans|cdist|moments|load --synthetic ROWSxCOLS | --data FILE.dnb [--k K] "
                  "[--iters N] [--ranks P] [--warmup W] [--runs R] [--seed S] [--peak-gbs G]\n",
                  why);
     std::exit(2);
@@ -58,6 +61,7 @@ Options parse(int argc, char** argv) {
         if (i + 1 >= argc) usage(("missing value for " + a).c_str());
         const std::string v = argv[++i];
         if (a == "--algo") o.algo = v;
+        else if (a == "--data") o.data = v;
         else if (a == "--synthetic") {
             const auto x = v.find('x');
             if (x == std::string::npos) usage("--synthetic takes ROWSxCOLS");
@@ -72,7 +76,14 @@ Options parse(int argc, char** argv) {
         else if (a == "--peak-gbs") o.peak_gbs = std::atof(v.c_str());
         else usage(("unknown option " + a).c_str());
     }
-    if (o.algo != "kmeans" && o.algo != "cdist" && o.algo != "moments") usage("unknown --algo");
+    if (o.algo != "kmeans" && o.algo != "cdist" && o.algo != "moments" && o.algo != "load") usage("unknown --algo");
+    if (o.algo == "load" && o.data.empty()) usage("--algo load times dnb_load of --data");
+    if (!o.data.empty()) {  // shape from the container header (options.hpp:71-90)
+        const auto h = dnd::dnb_read_header(o.data);
+        if (h.extents.size() != 2) usage("--data needs a 2-D DNB container");
+        o.rows = static_cast<dnd::index_t>(h.extents[0]);
+        o.cols = static_cast<dnd::index_t>(h.extents[1]);
+    }
     if (o.rows < 1 || o.cols < 1 || o.ranks < 1 || o.runs < 1 || o.warmup < 0) usage("bad sizes");
     return o;
 }
@@ -82,6 +93,14 @@ Options parse(int argc, char** argv) {
 // `out` with the replicated result for verify
 double run_algo(const Options& o, const dnd::DndArray<float>& x, std::vector<double>* out) {
     const dnd::Communicator& comm = x.comm();
+    if (o.algo == "load") {  // the DNB container into the HBM shards (dataio.hpp:102-142)
+        const auto y = dnd::dnb_load<float>(o.data, 0, comm);
+        if (out) {
+            const auto g = dnd::gather(y);
+            out->assign(g.begin(), g.end());
+        }
+        return y.numel_local() > 0 ? 1.0 : 0.0;
+    }
     if (o.algo == "kmeans") {
         const auto model = dnd::kmeans_fit(x, o.k, o.iters, 0.0, o.seed);
         if (out) *out = model.centroids;
@@ -169,10 +188,19 @@ class ClockSampler {
     int (*reasons_)(void*, unsigned long long*) = nullptr;
 };
 
+// the input: a DNB file loaded straight into the HBM shards (f64 files are
+// narrowed to the fp32 hot path), or random_uniform<float>
+dnd::DndArray<float> make_input(const Options& o, const dnd::Communicator& comm) {
+    if (o.data.empty()) return dnd::random_uniform<float>({o.rows, o.cols}, 0, o.seed, comm);
+    if (dnd::dnb_read_header(o.data).dtype == dnd::DnbDtype::f32) return dnd::dnb_load<float>(o.data, 0, comm);
+    return dnd::astype<float>(dnd::dnb_load<double>(o.data, 0, comm));
+}
+
 double bytes_per_run(const Options& o) {
     const double xb = 4.0 * o.rows * o.cols;
     if (o.algo == "kmeans") return xb * o.iters;
     if (o.algo == "cdist") return 4.0 * o.rows * o.rows + xb;
+    if (o.algo == "load") return static_cast<double>(std::filesystem::file_size(o.data));
     return xb;
 }
 
@@ -181,7 +209,7 @@ int bench(const Options& o) {
     std::mutex mu;
     ClockSampler clocks;
     dnd::run_world(o.ranks, [&](const dnd::Communicator& comm) {
-        const auto x = dnd::random_uniform<float>({o.rows, o.cols}, 0, o.seed, comm);
+        const auto x = make_input(o, comm);
         double sink = 0.0;
         for (int w = 0; w < o.warmup; ++w) sink += run_algo(o, x, nullptr);
         if (comm.rank() == 0) clocks.start();
@@ -220,7 +248,7 @@ int verify(const Options& o) {
     std::mutex mu;
     auto collect = [&](int ranks, std::vector<double>& dst) {
         dnd::run_world(ranks, [&](const dnd::Communicator& comm) {
-            const auto x = dnd::random_uniform<float>({o.rows, o.cols}, 0, o.seed, comm);
+            const auto x = make_input(o, comm);
             std::vector<double> r;
             run_algo(o, x, &r);
             std::lock_guard<std::mutex> lock(mu);
@@ -247,8 +275,8 @@ int verify(const Options& o) {
 }  // namespace
 
 int main(int argc, char** argv) {
-    const Options o = parse(argc, argv);
     try {
+        const Options o = parse(argc, argv);
         return o.cmd == "bench" ? bench(o) : verify(o);
     } catch (const dnd::Error& e) {
         std::fprintf(stderr, "dnd: %s\n", e.what());

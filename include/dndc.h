@@ -35,6 +35,7 @@ extern "C" {
 #define DNDC_ETRANSPORT 2 /* dnd::TransportError (errors.hpp:21-25) */
 #define DNDC_ECUDA 3      /* CUDA runtime / launch failure */
 #define DNDC_EINTERNAL 4
+#define DNDC_EDATA 5      /* dnd::DataError (errors.hpp:40): file I/O and container format */
 
 #define DNDC_UNIQUE_ID_BYTES 128
 
@@ -103,6 +104,16 @@ int dndc_allgather_rows(dndc_ctx* ctx, const void* local, int64_t rows, int64_t 
  * intersection blocks.  Returns after the stream has drained. */
 int dndc_resplit(dndc_ctx* ctx, const void* src_local, int ndim, const int64_t* shape, int64_t elem_bytes,
                  int src_split, int dst_split, void* dst_local);
+
+/* DNB container I/O straight between a file and HBM (dataio.hpp:61-142, F2):
+ * the byte range [byte_offset, byte_offset + bytes) of `path` is streamed
+ * through two pinned chunks (positioned reads overlapped with the H2D copy)
+ * into dev_dst, or from dev_src into an existing file.  The DNB header itself
+ * (magic, dtype, extents) is parsed by the host layer.  Local, not
+ * collective; DNDC_EDATA on open/short-read/write failures. */
+int dndc_file_read_to_device(dndc_ctx* ctx, const char* path, uint64_t byte_offset, size_t bytes, void* dev_dst);
+int dndc_file_write_from_device(dndc_ctx* ctx, const char* path, uint64_t byte_offset, const void* dev_src,
+                                size_t bytes);
 
 /* Communicator::allreduce(plus) (transport.hpp:136-148, A15), collective, in
  * place on a device buffer: sum over ranks folded in rank order 0..p-1 from

@@ -15,12 +15,16 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DNDC_LIB_PATH") or os.path.join(HERE, "libdndc.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "dndc.h")
 
-DNDC_OK, DNDC_EVALUE, DNDC_ETRANSPORT, DNDC_ECUDA, DNDC_EINTERNAL = 0, 1, 2, 3, 4
+DNDC_OK, DNDC_EVALUE, DNDC_ETRANSPORT, DNDC_ECUDA, DNDC_EINTERNAL, DNDC_EDATA = 0, 1, 2, 3, 4, 5
 UNIQUE_ID_BYTES = 128
 
 
 class TransportError(RuntimeError):
     """dnd::TransportError (errors.hpp:21-25)."""
+
+
+class DataError(RuntimeError):
+    """dnd::DataError (errors.hpp:40): file I/O and container format."""
 
 
 class DeviceError(RuntimeError):
@@ -56,6 +60,8 @@ _SIGS = {
     "dndc_memcpy": [_P, _P, _P, C.c_size_t, _i32],
     "dndc_allgather_rows": [_P, _P, _i64, _i64, _P, _P],
     "dndc_resplit": [_P, _P, _i32, _P, _i64, _i32, _i32, _P],
+    "dndc_file_read_to_device": [_P, C.c_char_p, _u64, C.c_size_t, _P],
+    "dndc_file_write_from_device": [_P, C.c_char_p, _u64, _P, C.c_size_t],
     "dndc_allreduce_f64": [_P, _P, _i64],
     "dndc_kmeans_step_f32": [_P, _P, _i64, _i64, _P, _i32, _P, _P],
     "dndc_fill_uniform_f32": [_P, _u64, _i64, _i64, _i64, _P],
@@ -120,4 +126,6 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == DNDC_ETRANSPORT:
         raise TransportError(msg)
+    if rc == DNDC_EDATA:
+        raise DataError(msg)
     raise DeviceError(f"libdndc error {rc}: {msg}")

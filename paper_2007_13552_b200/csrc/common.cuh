@@ -85,13 +85,18 @@ struct dndc_ctx {
     // the same addresses (CUDA-graph friendly).
     std::map<std::string, std::pair<void*, size_t>> slots;
     void* slot(const std::string& name, size_t bytes);
-    uint64_t slot_gen = 0;  // bumped on every (re)allocation: captured graphs key on it
+    uint64_t slot_gen = 0;  // bumped when a slot moves (reallocation): captured graphs key on it
 
     // stream-ordered pool behind dndc_alloc/dndc_free (hostio.cu): arrays the
     // host layer allocates per call (cdist outputs, results) reuse memory
     // instead of paying cudaMalloc/cudaFree each time; trimmed on OOM
     cudaMemPool_t pool = nullptr;
     void trim_pool();
+
+    // file <-> HBM streaming (dataio.cu): per I/O thread two pinned chunks,
+    // one in flight on the copy engine while the thread reads/writes the other
+    std::vector<void*> io_buf;
+    std::vector<cudaEvent_t> io_ev;
 
     // pinned host staging for small results
     void* pinned = nullptr;

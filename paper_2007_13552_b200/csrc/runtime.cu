@@ -135,6 +135,7 @@ void* dndc_ctx::slot(const std::string& name, size_t bytes) {
         DNDC_CUDA(cudaStreamSynchronize(stream));
         DNDC_CUDA(cudaFree(it->second.first));
         slots.erase(it);
+        ++slot_gen;  // a captured graph may hold the old address; a new name cannot be in one
     }
     void* p = nullptr;
     cudaError_t e = cudaMalloc(&p, bytes);
@@ -145,7 +146,6 @@ void* dndc_ctx::slot(const std::string& name, size_t bytes) {
     }
     DNDC_CUDA(e);
     slots[name] = {p, bytes};
-    ++slot_gen;
     return p;
 }
 
@@ -226,6 +226,8 @@ int dndc_destroy(dndc_ctx* ctx) {
         dndc::destroy_kmeans_state(ctx->km);
         for (auto& kv : ctx->slots) cudaFree(kv.second.first);
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        for (void* b : ctx->io_buf) cudaFreeHost(b);
+        for (cudaEvent_t e : ctx->io_ev) cudaEventDestroy(e);
         for (int r = 0; r < static_cast<int>(ctx->peer_bases.size()); ++r)
             if (r != ctx->rank && ctx->peer_bases[r]) cudaIpcCloseMemHandle(ctx->peer_bases[r]);
         if (ctx->peer_bases_dev) cudaFree(ctx->peer_bases_dev);

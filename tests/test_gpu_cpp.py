@@ -46,3 +46,19 @@ def test_cli_verify_distributed_vs_single(algo):
     """`dnd verify`: P ranks against one rank within the gate (tools/verify.cpp)."""
     rep = _dnd("verify", "--algo", algo, "--synthetic", "3000x18", "--ranks", str(_ranks()))
     assert rep["pass"] is True, rep
+
+
+def test_cli_bench_from_dnb_file(tmp_path):
+    """`dnd bench --data FILE.dnb`: the container is loaded straight into HBM
+    (dataio.hpp:102-142) and gives the same fit as the in-memory array."""
+    import numpy as np
+
+    x = np.random.default_rng(3).random((20000, 18), dtype=np.float32)
+    path = tmp_path / "x.dnb"
+    with open(path, "wb") as f:
+        f.write(b"DNB1" + bytes([1, 2]) + np.array(x.shape, "<u8").tobytes() + x.tobytes())
+    rep = _dnd("bench", "--algo", "kmeans", "--data", str(path), "--runs", "2", "--ranks", str(_ranks()))
+    assert rep["params"]["rows"] == 20000 and rep["params"]["cols"] == 18
+    r = subprocess.run([os.path.join(ROOT, "cpp", "build", "dnd"), "bench", "--data", str(tmp_path / "nope.dnb")],
+                       capture_output=True, text=True, timeout=60)
+    assert r.returncode == 1 and "cannot open" in r.stderr
