@@ -8,5 +8,6 @@
 #include "dnd/moments.hpp"
 #include "dnd/ndarray.hpp"
 #include "dnd/pairwise.hpp"
+#include "dnd/regression.hpp"
 #include "dnd/tile.hpp"
 #include "dnd/transport.hpp"

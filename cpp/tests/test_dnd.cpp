@@ -375,6 +375,129 @@ int main() {
         CHECK_THROWS_AS(dnd::csv_to_dnb(write_text("empty.csv", "\n"), (dir / "o").string()), dnd::DataError);
         fs::remove_all(dir);
     }
+
+    // LASSO (test_regression.cpp:83-230) against a sequential restatement of
+    // regression.cpp:25-102 (one rank, row order)
+    {
+        struct Problem {
+            index_t n, m;
+            std::vector<double> x, y;
+        };
+        auto make_problem = [](index_t n, index_t m, int seed) {
+            Problem p{n, m, std::vector<double>(n * m), std::vector<double>(n)};
+            std::vector<double> beta(m);
+            for (index_t j = 0; j < m; ++j) beta[j] = std::sin(1.3 * (j + seed)) * 3.0;
+            for (index_t i = 0; i < n; ++i) {
+                double yi = 0.0;
+                for (index_t j = 0; j < m; ++j) {
+                    // hash-style pseudo-random features (independent columns)
+                    const double h = std::sin(12.9898 * static_cast<double>(i) + 78.233 * static_cast<double>(j) +
+                                              static_cast<double>(seed)) * 43758.5453;
+                    const double v = j == 0 ? 1.0 : h - std::floor(h) - 0.5;
+                    p.x[i * m + j] = v;
+                    yi += v * beta[j];
+                }
+                p.y[i] = yi + 0.05 * std::cos(3.1 * i + seed);
+            }
+            return p;
+        };
+        auto naive = [](const Problem& p, double lam, int sweeps, double tol, std::vector<double>& trace) {
+            std::vector<double> sq(p.m, 0.0), w(p.m, 0.0), r = p.y;
+            for (index_t i = 0; i < p.n; ++i)
+                for (index_t j = 0; j < p.m; ++j) sq[j] += p.x[i * p.m + j] * p.x[i * p.m + j];
+            trace.clear();
+            for (int s = 0; s < sweeps; ++s) {
+                double mc = 0.0;
+                for (index_t j = 0; j < p.m; ++j) {
+                    if (sq[j] == 0.0) continue;
+                    double rho = 0.0;
+                    for (index_t i = 0; i < p.n; ++i) {
+                        const double x = p.x[i * p.m + j];
+                        rho += x * (r[i] + w[j] * x);
+                    }
+                    const double wn = j == 0 ? rho / sq[0] : dnd::soft_threshold(rho, lam / 2.0) / sq[j];
+                    if (wn != w[j])
+                        for (index_t i = 0; i < p.n; ++i) r[i] += (w[j] - wn) * p.x[i * p.m + j];
+                    mc = std::max(mc, std::abs(wn - w[j]));
+                    w[j] = wn;
+                }
+                double ssr = 0.0, pen = 0.0;
+                for (double v : r) ssr += v * v;
+                for (index_t j = 1; j < p.m; ++j) pen += std::abs(w[j]);
+                trace.push_back(ssr + lam * pen);
+                if (mc < tol) break;
+            }
+            return w;
+        };
+        CHECK(dnd::soft_threshold(0.5, 1.0) == 0.0 && dnd::soft_threshold(2.0, 0.5) == 1.5);
+        CHECK(dnd::soft_threshold(-2.0, 0.5) == -1.5 && dnd::soft_threshold(3.0, 0.0) == 3.0);
+        const auto p1 = make_problem(300, 20, 151), p2 = make_problem(2000, 7, 3);
+        auto zc = make_problem(40, 6, 167);
+        for (index_t i = 0; i < zc.n; ++i) zc.x[i * zc.m + 3] = 0.0;
+        each_world([&](const Communicator& comm) {
+            for (const Problem* pp : {&p1, &p2, static_cast<const Problem*>(&zc)}) {
+                const Problem& p = *pp;
+                for (double lam : {0.0, 1.0, 30.0}) {
+                    std::vector<double> tr;
+                    const auto want = naive(p, lam, 25, 0.0, tr);
+                    auto x = dnd::from_global(p.x, {p.n, p.m}, 0, comm);
+                    auto y = dnd::from_global(p.y, {p.n}, 0, comm);
+                    const auto model = dnd::lasso_fit(x, y, lam, 25);
+                    CHECK(model.sweeps_run == 25 && model.objective_trace.size() == 25);
+                    bool ok = true;
+                    for (index_t j = 0; j < p.m; ++j) ok &= close_rel(model.weights[j], want[j], 1e-9);
+                    for (int t = 0; t < 25; ++t) ok &= close_rel(model.objective_trace[t], tr[t], 1e-10);
+                    for (int t = 1; t < 25; ++t) ok &= model.objective_trace[t] <= model.objective_trace[t - 1] + 1e-9;
+                    CHECK(ok);
+                }
+            }
+            CHECK(dnd::lasso_fit(dnd::from_global(zc.x, {zc.n, zc.m}, 0, comm),
+                                 dnd::from_global(zc.y, {zc.n}, 0, comm), 0.5, 50)
+                      .weights[3] == 0.0);
+            // tol stops early, the same sweep as the restatement
+            std::vector<double> tr;
+            naive(p2, 1.0, 500, 1e-10, tr);
+            const auto mt = dnd::lasso_fit(dnd::from_global(p2.x, {p2.n, p2.m}, 0, comm),
+                                           dnd::from_global(p2.y, {p2.n}, 0, comm), 1.0, 500, 1e-10);
+            CHECK(mt.sweeps_run < 500 && std::abs(mt.sweeps_run - static_cast<int>(tr.size())) <= 1);
+            // replicated / split=1 inputs give the split=0 fit
+            const auto ms = dnd::lasso_fit(dnd::from_global(p2.x, {p2.n, p2.m}, 1, comm),
+                                           dnd::from_global(p2.y, {p2.n}, std::nullopt, comm), 1.0, 20);
+            const auto m0 = dnd::lasso_fit(dnd::from_global(p2.x, {p2.n, p2.m}, 0, comm),
+                                           dnd::from_global(p2.y, {p2.n}, 0, comm), 1.0, 20);
+            CHECK(ms.weights == m0.weights);
+            // y = 1 + 2x on 3 samples (more ranks than samples on 2+ GPUs)
+            const auto tiny = dnd::lasso_fit(dnd::from_global<double>({1, 0.0, 1, 1.0, 1, 2.0}, {3, 2}, 0, comm),
+                                             dnd::from_global<double>({1.0, 3.0, 5.0}, {3}, 0, comm), 0.0, 200,
+                                             1e-15);
+            CHECK(std::abs(tiny.weights[0] - 1.0) <= 1e-10 && std::abs(tiny.weights[1] - 2.0) <= 1e-10);
+            // predict: bit-identical to the row loop
+            auto xp = dnd::from_global(p1.x, {p1.n, p1.m}, 0, comm);
+            dnd::LassoModel dense;
+            for (index_t j = 0; j < p1.m; ++j) dense.weights.push_back(0.25 * j - 1.0);
+            const auto got = dnd::gather(dnd::lasso_predict(dense, xp));
+            bool exact = true;
+            for (index_t i = 0; i < p1.n; ++i) {
+                volatile double acc = 0.0;
+                for (index_t j = 0; j < p1.m; ++j) {
+                    volatile double prod = p1.x[i * p1.m + j] * dense.weights[j];
+                    acc = acc + prod;
+                }
+                exact &= got[i] == acc;
+            }
+            CHECK(exact);
+            // validation (test_regression.cpp:214-230): every rank raises
+            auto x4 = dnd::from_global<double>({1, 1, 1, 1, 1, 1, 1, 1}, {4, 2}, 0, comm);
+            auto y4 = dnd::from_global<double>({1, 1, 1, 1}, {4}, 0, comm);
+            auto y3 = dnd::from_global<double>({1, 1, 1}, {3}, 0, comm);
+            CHECK_THROWS_AS(dnd::lasso_fit(x4, y3, 0.1, 5), dnd::ValueError);
+            CHECK_THROWS_AS(dnd::lasso_fit(x4, y4, -1.0, 5), dnd::ValueError);
+            CHECK_THROWS_AS(dnd::lasso_fit(x4, y4, 0.1, 0), dnd::ValueError);
+            CHECK_THROWS_AS(dnd::lasso_fit(y4, y4, 0.1, 5), dnd::ValueError);
+            auto xbad = dnd::from_global<double>({1, 1, 1, 1, 1, 1, 2, 1}, {4, 2}, 0, comm);
+            CHECK_THROWS_AS(dnd::lasso_fit(xbad, y4, 0.1, 5), dnd::ValueError);
+        });
+    }
     std::printf("test_dnd: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
 }

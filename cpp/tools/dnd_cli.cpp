@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <filesystem>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -45,7 +46,7 @@ struct Options {
 
 [[noreturn]] void usage(const char* why) {
     std::fprintf(stderr,
-                 "dnd: %s\nusage: dnd bench|verify --algo kmeans|cdist|moments|load --synthetic ROWSxCOLS | --data FILE.dnb [--k K] "
+                 "dnd: %s\nusage: dnd bench|verify --algo kmeans|cdist|moments|load|lasso --synthetic ROWSxCOLS | --data FILE.dnb [--k K] "
                  "[--iters N] [--ranks P] [--warmup W] [--runs R] [--seed S] [--peak-gbs G]\n",
                  why);
     std::exit(2);
@@ -76,7 +77,8 @@ Options parse(int argc, char** argv) {
         else if (a == "--peak-gbs") o.peak_gbs = std::atof(v.c_str());
         else usage(("unknown option " + a).c_str());
     }
-    if (o.algo != "kmeans" && o.algo != "cdist" && o.algo != "moments" && o.algo != "load") usage("unknown --algo");
+    if (o.algo != "kmeans" && o.algo != "cdist" && o.algo != "moments" && o.algo != "load" && o.algo != "lasso")
+        usage("unknown --algo");
     if (o.algo == "load" && o.data.empty()) usage("--algo load times dnb_load of --data");
     if (!o.data.empty()) {  // shape from the container header (options.hpp:71-90)
         const auto h = dnd::dnb_read_header(o.data);
@@ -88,10 +90,26 @@ Options parse(int argc, char** argv) {
     return o;
 }
 
+using LassoData = std::pair<dnd::DndArray<double>, dnd::DndArray<double>>;
+
+// LASSO input built once per rank from x: column 0 ones, the rest x widened
+// to f64, y = a fixed sparse linear model of the row plus a little of x[:,0]
+LassoData make_lasso(const Options& o, const dnd::DndArray<float>& xin) {
+    const auto xf = dnd::gather(xin);
+    std::vector<double> x(xf.begin(), xf.end()), y(static_cast<std::size_t>(o.rows));
+    for (dnd::index_t i = 0; i < o.rows; ++i) {
+        double acc = 0.0;
+        for (dnd::index_t j = 1; j < o.cols; ++j) acc += (j % 3 == 0 ? 0.0 : 1.0 / j) * x[i * o.cols + j];
+        y[i] = 0.5 + acc + 0.01 * (x[i * o.cols] - 0.5);
+        x[i * o.cols] = 1.0;
+    }
+    return {dnd::from_global(x, {o.rows, o.cols}, 0, xin.comm()), dnd::from_global(y, {o.rows}, 0, xin.comm())};
+}
+
 // one run of the algorithm; returns a scalar that depends on the result
 // (kept, like the reference's sink, so nothing is optimised away) and fills
 // `out` with the replicated result for verify
-double run_algo(const Options& o, const dnd::DndArray<float>& x, std::vector<double>* out) {
+double run_algo(const Options& o, const dnd::DndArray<float>& x, const LassoData* ld, std::vector<double>* out) {
     const dnd::Communicator& comm = x.comm();
     if (o.algo == "load") {  // the DNB container into the HBM shards (dataio.hpp:102-142)
         const auto y = dnd::dnb_load<float>(o.data, 0, comm);
@@ -100,6 +118,11 @@ double run_algo(const Options& o, const dnd::DndArray<float>& x, std::vector<dou
             out->assign(g.begin(), g.end());
         }
         return y.numel_local() > 0 ? 1.0 : 0.0;
+    }
+    if (o.algo == "lasso") {  // --iters sweeps, lambda 1 (regression.cpp:25-102)
+        const auto model = dnd::lasso_fit(ld->first, ld->second, 1.0, o.iters, 0.0);
+        if (out) *out = model.weights;
+        return model.objective_trace.back();
     }
     if (o.algo == "kmeans") {
         const auto model = dnd::kmeans_fit(x, o.k, o.iters, 0.0, o.seed);
@@ -201,6 +224,7 @@ double bytes_per_run(const Options& o) {
     if (o.algo == "kmeans") return xb * o.iters;
     if (o.algo == "cdist") return 4.0 * o.rows * o.rows + xb;
     if (o.algo == "load") return static_cast<double>(std::filesystem::file_size(o.data));
+    if (o.algo == "lasso") return 8.0 * o.rows * o.cols * o.iters;  // X (f64) once per sweep
     return xb;
 }
 
@@ -210,8 +234,10 @@ int bench(const Options& o) {
     ClockSampler clocks;
     dnd::run_world(o.ranks, [&](const dnd::Communicator& comm) {
         const auto x = make_input(o, comm);
+        std::unique_ptr<LassoData> ld;
+        if (o.algo == "lasso") ld = std::make_unique<LassoData>(make_lasso(o, x));
         double sink = 0.0;
-        for (int w = 0; w < o.warmup; ++w) sink += run_algo(o, x, nullptr);
+        for (int w = 0; w < o.warmup; ++w) sink += run_algo(o, x, ld.get(), nullptr);
         if (comm.rank() == 0) clocks.start();
         // slowest rank per run (bench.cpp:102-112): the ranks are threads of
         // this process, so the max is taken under a mutex after the runs
@@ -219,7 +245,7 @@ int bench(const Options& o) {
         for (int r = 0; r < o.runs; ++r) {
             comm.barrier();
             const auto t0 = std::chrono::steady_clock::now();
-            sink += run_algo(o, x, nullptr);
+            sink += run_algo(o, x, ld.get(), nullptr);
             comm.barrier();
             mine.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
         }
@@ -249,8 +275,10 @@ int verify(const Options& o) {
     auto collect = [&](int ranks, std::vector<double>& dst) {
         dnd::run_world(ranks, [&](const dnd::Communicator& comm) {
             const auto x = make_input(o, comm);
+            std::unique_ptr<LassoData> ld;
+            if (o.algo == "lasso") ld = std::make_unique<LassoData>(make_lasso(o, x));
             std::vector<double> r;
-            run_algo(o, x, &r);
+            run_algo(o, x, ld.get(), &r);
             std::lock_guard<std::mutex> lock(mu);
             if (comm.rank() == 0) dst = r;
         });

@@ -115,6 +115,21 @@ int dndc_file_read_to_device(dndc_ctx* ctx, const char* path, uint64_t byte_offs
 int dndc_file_write_from_device(dndc_ctx* ctx, const char* path, uint64_t byte_offset, const void* dev_src,
                                 size_t bytes);
 
+/* lasso_fit (regression.cpp:25-102, F4), collective: cyclic coordinate descent
+ * on this rank's rows x_local (rows x m, f64, column 0 all ones) and targets
+ * y_local (rows); weights_out[m] and trace_out[sweeps] (objective per sweep)
+ * in host memory, identical on every rank; *sweeps_run <= sweeps (stops when
+ * the largest coordinate change < tol).  DNDC_EVALUE for bad arguments or a
+ * bias column that is not all ones on any rank (raised on every rank). */
+int dndc_lasso_fit_f64(dndc_ctx* ctx, const double* x_local, int64_t rows, int64_t n_global, int64_t m,
+                       const double* y_local, double lambda, int sweeps, double tol, double* weights_out,
+                       double* trace_out, int* sweeps_run);
+/* lasso_predict (regression.cpp:105-127): out_local[i] = sum_j x[i,j] w[j] in
+ * column order without FMA contraction (bit-identical to the reference);
+ * weights in host memory, out_local on the device; local, no communication. */
+int dndc_lasso_predict_f64(dndc_ctx* ctx, const double* x_local, int64_t rows, int64_t m, const double* weights,
+                           double* out_local);
+
 /* Communicator::allreduce(plus) (transport.hpp:136-148, A15), collective, in
  * place on a device buffer: sum over ranks folded in rank order 0..p-1 from
  * the zero identity, bit-identical on every rank. */

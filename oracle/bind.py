@@ -61,6 +61,9 @@ class Oracle:
         L.dno_moments_axis0.argtypes = [_P, _i64, _i64, _i32, _i64, _P, _P]
         L.dno_local_moments_axis0.argtypes = [_P, _i64, _i64, _P, _P, _P]
         L.dno_kmeanspp_indices_f32.argtypes = [_P, _i64, _i64, _i32, _i32, _u64, _P]
+        L.dno_lasso_fit.argtypes = [_P, _P, _i64, _i64, _i32, _f64, _i32, _f64, _P, _P, _P]
+        L.dno_soft_threshold.argtypes = [_f64, _f64]
+        L.dno_soft_threshold.restype = _f64
 
     def uniform_f32(self, rows, m, seed, row0=0):
         out = np.empty((rows, m), np.float32)
@@ -168,6 +171,26 @@ class Oracle:
         return out
 
 
+def _oracle_lasso(self, x, y, lam, sweeps, tol=0.0, p=1):
+    rc, w, trace, run = _lasso_call(self.lib.dno_lasso_fit, x, y, lam, sweeps, tol, p)
+    if rc == -1:
+        raise ValueError("lasso_fit: invalid arguments")
+    if rc == -2:
+        raise ValueError("lasso_fit: column 0 must be the all-ones bias column")
+    return w, trace, run
+
+
+def _lasso_call(fn, x, y, lam, sweeps, tol, p):
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64).reshape(-1)
+    n, m = x.shape
+    w = np.zeros(m, np.float64)
+    trace = np.zeros(sweeps, np.float64)
+    run = np.zeros(1, np.int32)
+    rc = fn(_ptr(x), _ptr(y), n, m, p, lam, sweeps, tol, _ptr(w), _ptr(trace), _ptr(run))
+    return rc, w, trace[: run[0]].copy(), int(run[0])
+
+
 class ReferenceError_(RuntimeError):
     pass
 
@@ -195,6 +218,7 @@ class Reference:
         L.ref_kmeans_predict.argtypes = [_P, _i64, _i64, _i32, _P, _i32, _P]
         L.ref_moments_axis0.argtypes = [_P, _i64, _i64, _i32, _i64, _P, _P]
         L.ref_bench.argtypes = [_i32, _i64, _i64, _i32, _i32, _u64, _i32, _i32, _i32, _P, _P]
+        L.ref_lasso_fit.argtypes = [_P, _P, _i64, _i64, _i32, _f64, _i32, _f64, _P, _P, _P]
 
     def _check(self, rc):
         if rc == -1:
@@ -281,3 +305,15 @@ class Reference:
         self._check(self.lib.ref_bench(algo, n, m, k, iters, seed, p, warmup, runs, _ptr(secs),
                                        _ptr(chk)))
         return secs[:runs], float(chk[0])
+
+
+Oracle.lasso_fit = _oracle_lasso
+
+
+def _reference_lasso(self, x, y, lam, sweeps, tol=0.0, p=1):
+    rc, w, trace, run = _lasso_call(self.lib.ref_lasso_fit, x, y, lam, sweeps, tol, p)
+    self._check(rc)
+    return w, trace, run
+
+
+Reference.lasso_fit = _reference_lasso

@@ -544,3 +544,85 @@ int dno_kmeanspp_indices_f32(const float* x, int64_t n, int64_t m, int p, int k,
     free(d2); free(S); free(T);
     return 0;
 }
+
+/* ------------------------------------------------------------ LASSO (F4)
+ *
+ * Cyclic coordinate descent, regression.cpp:25-102: every rank owns the
+ * chunk-map rows of x (bias column 0 all ones) and their residual; column
+ * squared norms and, per coordinate, the correlation rho are summed over
+ * ranks in rank order from 0.0 (allreduce(plus), transport.hpp:140-146);
+ * w_0 = rho / sq_0, w_j = soft_threshold(rho, lambda / 2) / sq_j; columns with
+ * zero norm are skipped; one objective |r|^2 + lambda sum_{j>0} |w_j| per
+ * sweep; stop when the largest change < tol.  Returns -1 on invalid
+ * arguments, -2 when column 0 is not all ones. */
+
+/* regression.cpp:19-23 */
+double dno_soft_threshold(double rho, double t) {
+    if (rho > t) return rho - t;
+    if (rho < -t) return rho + t;
+    return 0.0;
+}
+
+int dno_lasso_fit(const double* x, const double* y, int64_t n, int64_t m, int p, double lambda, int sweeps,
+                  double tol, double* weights, double* trace, int* sweeps_run) {
+    if (n < 1 || m < 1 || lambda < 0.0 || sweeps < 1 || p < 1) return -1;
+    for (int64_t i = 0; i < n; ++i)
+        if (x[i * m] != 1.0) return -2;
+    int64_t* off = (int64_t*)malloc(sizeof(int64_t) * (size_t)p);
+    int64_t* ext = (int64_t*)malloc(sizeof(int64_t) * (size_t)p);
+    dno_chunk_map(n, p, off, ext);
+    double* sq = (double*)calloc((size_t)m, sizeof(double));
+    double* sql = (double*)malloc(sizeof(double) * (size_t)m);
+    double* res = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int r = 0; r < p; ++r) { /* regression.cpp:52-60 per rank, then the fold */
+        for (int64_t j = 0; j < m; ++j) sql[j] = 0.0;
+        for (int64_t i = off[r]; i < off[r] + ext[r]; ++i)
+            for (int64_t j = 0; j < m; ++j) sql[j] += x[i * m + j] * x[i * m + j];
+        for (int64_t j = 0; j < m; ++j) sq[j] += sql[j];
+    }
+    for (int64_t i = 0; i < n; ++i) res[i] = y[i];
+    for (int64_t j = 0; j < m; ++j) weights[j] = 0.0;
+    int run = 0;
+    for (int s = 0; s < sweeps; ++s) {
+        double max_change = 0.0;
+        for (int64_t j = 0; j < m; ++j) {
+            if (sq[j] == 0.0) continue;
+            const double w_old = weights[j];
+            double rho = 0.0;
+            for (int r = 0; r < p; ++r) { /* regression.cpp:73-78 */
+                double loc = 0.0;
+                for (int64_t i = off[r]; i < off[r] + ext[r]; ++i) {
+                    const double xij = x[i * m + j];
+                    loc += xij * (res[i] + w_old * xij);
+                }
+                rho += loc;
+            }
+            const double w_new = j == 0 ? rho / sq[0] : dno_soft_threshold(rho, lambda / 2.0) / sq[j];
+            if (w_new != w_old) { /* regression.cpp:83-88 */
+                const double shift = w_old - w_new;
+                for (int64_t i = 0; i < n; ++i) res[i] += shift * x[i * m + j];
+                weights[j] = w_new;
+            }
+            const double ch = fabs(w_new - w_old);
+            if (ch > max_change) max_change = ch;
+        }
+        double ssr = 0.0; /* regression.cpp:92-99 */
+        for (int r = 0; r < p; ++r) {
+            double loc = 0.0;
+            for (int64_t i = off[r]; i < off[r] + ext[r]; ++i) loc += res[i] * res[i];
+            ssr += loc;
+        }
+        double pen = 0.0;
+        for (int64_t j = 1; j < m; ++j) pen += fabs(weights[j]);
+        trace[s] = ssr + lambda * pen;
+        run = s + 1;
+        if (max_change < tol) break;
+    }
+    *sweeps_run = run;
+    free(off);
+    free(ext);
+    free(sq);
+    free(sql);
+    free(res);
+    return 0;
+}

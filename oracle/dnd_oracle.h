@@ -86,6 +86,11 @@ int dno_moments_axis0(const double* x, int64_t n, int64_t m, int p, int64_t ddof
 int dno_kmeanspp_indices_f32(const float* x, int64_t n, int64_t m, int p, int k, uint64_t seed,
                              int64_t* indices);
 
+/* LASSO coordinate descent (regression.cpp:19-102) */
+double dno_soft_threshold(double rho, double t);
+int dno_lasso_fit(const double* x, const double* y, int64_t n, int64_t m, int p, double lambda, int sweeps,
+                  double tol, double* weights, double* trace, int* sweeps_run);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,7 @@
 #include "dnd/moments.hpp"
 #include "dnd/ndarray.hpp"
 #include "dnd/pairwise.hpp"
+#include "dnd/regression.hpp"
 #include "dnd/transport.hpp"
 
 namespace {
@@ -233,6 +234,25 @@ int ref_bench(int algo, std::int64_t n, std::int64_t m, int k, int iters, std::u
             if (comm.rank() == 0) {
                 std::lock_guard<std::mutex> lock(mu);
                 *checksum = sink;
+            }
+        });
+    });
+}
+
+// lasso_fit (regression.cpp:25-102) on p ranks: x n x m row-major with the
+// bias column, y n targets, both split=0
+int ref_lasso_fit(const double* x, const double* y, std::int64_t n, std::int64_t m, int p, double lambda,
+                  int sweeps, double tol, double* weights, double* trace, int* sweeps_run) {
+    return guarded([&] {
+        dnd::run_world(p, [&](const dnd::Communicator& comm) {
+            auto a = shard_rows(x, n, m, comm);
+            auto b = shard_rows(y, n, 1, comm);
+            auto t = dnd::DndArray<double>({n}, 0, comm, dnd::Tile<double>{{b.tile().extents[0]}, b.tile().data});
+            auto model = dnd::lasso_fit(a, t, lambda, sweeps, tol);
+            if (comm.rank() == 0) {
+                std::memcpy(weights, model.weights.data(), sizeof(double) * model.weights.size());
+                std::memcpy(trace, model.objective_trace.data(), sizeof(double) * model.objective_trace.size());
+                *sweeps_run = model.sweeps_run;
             }
         });
     });

@@ -61,6 +61,8 @@ _SIGS = {
     "dndc_allgather_rows": [_P, _P, _i64, _i64, _P, _P],
     "dndc_resplit": [_P, _P, _i32, _P, _i64, _i32, _i32, _P],
     "dndc_file_read_to_device": [_P, C.c_char_p, _u64, C.c_size_t, _P],
+    "dndc_lasso_fit_f64": [_P, _P, _i64, _i64, _i64, _P, _f64, _i32, _f64, _P, _P, _P],
+    "dndc_lasso_predict_f64": [_P, _P, _i64, _i64, _P, _P],
     "dndc_file_write_from_device": [_P, C.c_char_p, _u64, _P, C.c_size_t],
     "dndc_allreduce_f64": [_P, _P, _i64],
     "dndc_kmeans_step_f32": [_P, _P, _i64, _i64, _P, _i32, _P, _P],

@@ -16,6 +16,8 @@ live in HBM as torch CUDA tensors, which are used only as device memory.
   cdist / cdist_xy (pairwise.hpp:15-19)       cdist / cdist_xy
   kmeans_* (cluster.hpp:25-42)                kmeans_init_indices / _centroids / fit / predict
   mean_axis / var_axis / stddev_axis          same names (axis 0 = the split axis)
+  resplit (ndarray.hpp:340-386)               resplit (dndc_resplit, NCCL send/recv)
+  lasso_fit / lasso_predict (regression.hpp)  same names (dndc_lasso_*_f64)
   (not in the reference)                      kmeanspp_indices (BASELINE config 5)
 """
 from __future__ import annotations
@@ -34,7 +36,8 @@ __all__ = [
     "Communicator", "DndArray", "KMeansModel", "MomentState", "TransportError", "chunk_map",
     "random_uniform", "from_global", "gather", "resplit", "row_norms", "distance_block", "cdist", "cdist_xy",
     "kmeans_init_indices", "kmeans_init_centroids", "kmeans_fit", "kmeans_predict", "mean_axis",
-    "var_axis", "stddev_axis", "moments_axis0", "kmeanspp_indices",
+    "var_axis", "stddev_axis", "moments_axis0", "kmeanspp_indices", "LassoModel", "soft_threshold",
+    "lasso_fit", "lasso_predict",
 ]
 
 _SUFFIX = {torch.float32: "f32", torch.float64: "f64"}
@@ -472,3 +475,63 @@ def kmeanspp_indices(x: DndArray, k: int, seed: int) -> np.ndarray:
 
 
 del math
+
+
+@dataclass
+class LassoModel:
+    """regression.hpp:10-19 (weights[0] is the unpenalised bias)."""
+
+    weights: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    lambda_: float = 0.0
+    objective_trace: list = field(default_factory=list)
+    sweeps_run: int = 0
+
+
+def soft_threshold(rho: float, threshold: float) -> float:
+    """regression.cpp:19-23."""
+    if rho > threshold:
+        return rho - threshold
+    if rho < -threshold:
+        return rho + threshold
+    return 0.0
+
+
+def lasso_fit(x: DndArray, y: DndArray, lam: float, sweeps: int, tol: float = 0.0) -> LassoModel:
+    """Cyclic coordinate descent (regression.cpp:25-102): one GPU kernel per
+    coordinate, the cross-GPU sum over NVLink inside it (dndc_lasso_fit_f64)."""
+    if x.ndim() != 2:
+        raise ValueError("lasso_fit: design matrix must be 2-D")
+    if y.ndim() != 1:
+        raise ValueError("lasso_fit: targets must be 1-D")
+    if x.shape[0] != y.shape[0]:
+        raise ValueError(f"lasso_fit: {x.shape[0]} rows vs {y.shape[0]} targets")
+    if x.tile.dtype != torch.float64 or y.tile.dtype != torch.float64:
+        raise ValueError("lasso_fit: float64 arrays (the reference's DndArray<double>)")
+    if x.split != 0:
+        x = resplit(x, 0)
+    if y.split != 0:
+        y = resplit(y, 0)
+    m = x.shape[1]
+    w = np.zeros(max(m, 1), np.float64)
+    trace = np.zeros(max(int(sweeps), 1), np.float64)
+    run = C.c_int(0)
+    check(lib().dndc_lasso_fit_f64(x.comm.handle, _ptr(x.tile), x.tile.shape[0], x.shape[0], m, _ptr(y.tile),
+                                   float(lam), int(sweeps), float(tol), w.ctypes.data, trace.ctypes.data,
+                                   C.byref(run)))
+    return LassoModel(w[:m].copy(), float(lam), list(trace[: run.value]), run.value)
+
+
+def lasso_predict(model: LassoModel, x: DndArray) -> DndArray:
+    """Xw per local row (regression.cpp:105-127), bit-identical to the reference."""
+    if x.ndim() != 2:
+        raise ValueError("lasso_predict: input must be 2-D")
+    if x.shape[1] != len(model.weights):
+        raise ValueError(f"lasso_predict: input has {x.shape[1]} columns, model expects {len(model.weights)}")
+    if x.split not in (None, 0):
+        raise ValueError("lasso_predict: input must be split=0 or replicated")
+    w = np.ascontiguousarray(model.weights, np.float64)
+    out = torch.empty(x.tile.shape[0], dtype=torch.float64, device=x.tile.device)
+    check(lib().dndc_lasso_predict_f64(x.comm.handle, _ptr(x.tile), x.tile.shape[0], x.shape[1], w.ctypes.data,
+                                       _ptr(out)))
+    return DndArray((x.shape[0],), x.split, x.comm, out)
+

@@ -164,3 +164,36 @@ def test_kmeanspp_oracle_properties(oracle):
     assert a[0] == oracle.kmeans_init_indices(5000, 1, 11)[0]
     # rank layout changes the summation blocks only
     assert len(set(oracle.kmeanspp_indices(x, 8, 11, p=3).tolist())) == 8
+
+
+def _lasso_problem(n, m, seed):
+    rng = np.random.default_rng(seed)
+    x = np.hstack([np.ones((n, 1)), rng.normal(size=(n, m - 1))])
+    y = x @ rng.normal(size=m) + 0.1 * rng.normal(size=n)
+    return x, y
+
+
+@pytest.mark.parametrize("n,m,lam,sweeps,tol,p", [(301, 7, 2.0, 30, 0.0, 1), (301, 7, 2.0, 30, 0.0, 3),
+                                                   (120, 8, 1e4, 5, 0.0, 2), (200, 12, 30.0, 500, 1e-12, 3),
+                                                   (3, 2, 0.0, 50, 1e-15, 5)])
+def test_lasso_oracle_matches_reference(oracle, reference, n, m, lam, sweeps, tol, p):
+    """F4: the C restatement of lasso_fit (regression.cpp:25-102) is bit-exact
+    with the compiled reference, every rank count, tol stop included."""
+    x, y = _lasso_problem(n, m, n + m)
+    a, b = oracle.lasso_fit(x, y, lam, sweeps, tol, p), reference.lasso_fit(x, y, lam, sweeps, tol, p)
+    assert a[2] == b[2]
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_lasso_oracle_edge_cases(oracle):
+    """soft_threshold hand values, zero column skipped, bias column enforced
+    (test_regression.cpp:83-89, :172-179, :214-230)."""
+    st = oracle.lib.dno_soft_threshold
+    assert (st(0.5, 1.0), st(2.0, 0.5), st(-2.0, 0.5), st(0.0, 0.0), st(3.0, 0.0)) == (0.0, 1.5, -1.5, 0.0, 3.0)
+    x, y = _lasso_problem(40, 6, 167)
+    x[:, 3] = 0.0
+    w, trace, _ = oracle.lasso_fit(x, y, 0.5, 50, 0.0, 2)
+    assert w[3] == 0.0 and np.all(np.diff(trace) <= 1e-9)
+    x[5, 0] = 2.0
+    with pytest.raises(ValueError):
+        oracle.lasso_fit(x, y, 0.5, 5)

@@ -111,6 +111,14 @@ def main():
     xs1 = dnd.resplit(xk, 1)
     m1 = dnd.kmeans_fit(xs1, 8, 10, 0.0, 42)
     report("kmeans_fit on split=1 input", np.array_equal(m1.centroids, model.centroids))
+    # LASSO (regression.cpp:25-102): rho summed across ranks inside the kernel
+    rng = np.random.default_rng(11)
+    xl = np.hstack([np.ones((4001, 1)), rng.normal(size=(4001, 9))])
+    yl = xl @ rng.normal(size=10) + 0.1 * rng.normal(size=4001)
+    ml = dnd.lasso_fit(dnd.from_global(xl, xl.shape, 0, comm), dnd.from_global(yl, yl.shape, 0, comm), 3.0, 40)
+    wl, tl, _ = O.lasso_fit(xl, yl, 3.0, 40, 0.0, p)
+    report("lasso_fit", rel_dev(ml.weights, wl) <= 1e-9 and rel_dev(ml.objective_trace, tl) <= 1e-10,
+           f"dev={rel_dev(ml.weights, wl):.2e}")
 
     dist.barrier()
     comm.close()
