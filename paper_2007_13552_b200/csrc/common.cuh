@@ -98,6 +98,10 @@ struct dndc_ctx {
     std::vector<void*> io_buf;
     std::vector<cudaEvent_t> io_ev;
 
+    // LASSO: the instantiated one-sweep graph of the last fit and its key (lasso.cu)
+    cudaGraphExec_t ls_exec = nullptr;
+    std::string ls_key;
+
     // pinned host staging for small results
     void* pinned = nullptr;
     size_t pinned_bytes = 0;

@@ -24,7 +24,9 @@
 // predict is the reference's row loop, multiply then add without FMA
 // contraction, so its output is bit-identical.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -240,15 +242,27 @@ __global__ void lasso_transpose_kernel(const double* __restrict__ x, int64_t row
     }
 }
 
-// column j: sum of squares (blockIdx.x = j), fixed order
+// column sums of squares: CTA (j, b) sums slice b of column j into
+// part[j][b]; lasso_sq_final_kernel adds the LS_SQ_SLICES slices in order
+constexpr int LS_SQ_SLICES = 64;
 __global__ void __launch_bounds__(LS_THREADS) lasso_sq_kernel(const double* __restrict__ xt, int64_t rows,
-                                                              double* __restrict__ sq) {
+                                                              double* __restrict__ part) {
     __shared__ double sh[LS_THREADS / 32];
     const double* col = xt + static_cast<int64_t>(blockIdx.x) * rows;
+    const int64_t per = (rows + LS_SQ_SLICES - 1) / LS_SQ_SLICES;
+    const int64_t lo = blockIdx.y * per, hi = min(rows, lo + per);
     double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < rows; i += LS_THREADS) acc += col[i] * col[i];
+    for (int64_t i = lo + threadIdx.x; i < hi; i += LS_THREADS) acc += col[i] * col[i];
     const double t = ls_block_sum(acc, sh);
-    if (threadIdx.x == 0) sq[blockIdx.x] = t;
+    if (threadIdx.x == 0) part[blockIdx.x * LS_SQ_SLICES + blockIdx.y] = t;
+}
+
+__global__ void lasso_sq_final_kernel(const double* __restrict__ part, int m, double* __restrict__ sq) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    double t = 0.0;
+    for (int b = 0; b < LS_SQ_SLICES; ++b) t += part[j * LS_SQ_SLICES + b];
+    sq[j] = t;
 }
 
 // Xw per row in column order, products rounded before the add
@@ -271,6 +285,14 @@ static void lasso_fit(dndc_ctx* ctx, const double* x, int64_t rows, int64_t n_gl
     if (rows < 0) value_error("lasso_fit: negative row count");
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
+    static const bool trace_on = std::getenv("DNDC_LASSO_TRACE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace_on) return;
+        DNDC_CUDA(cudaDeviceSynchronize());
+        std::fprintf(stderr, "lasso rank %d %-12s %.3f ms\n", ctx->rank, what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+    };
     const int64_t R = std::max<int64_t>(rows, 1);
     double* xt = static_cast<double*>(ctx->slot("ls_xt", sizeof(double) * R * m));
     double* r = static_cast<double*>(ctx->slot("ls_r", sizeof(double) * R));
@@ -289,7 +311,10 @@ static void lasso_fit(dndc_ctx* ctx, const double* x, int64_t rows, int64_t n_gl
         lasso_transpose_kernel<<<dim3(static_cast<unsigned>(ceil_div(rows, 32)), (m + 31) / 32), dim3(32, 8), 0, s>>>(
             x, rows, m, xt, bad);
         DNDC_LAUNCHED(ctx);
-        lasso_sq_kernel<<<m, LS_THREADS, 0, s>>>(xt, rows, sq);
+        double* sq_part = static_cast<double*>(ctx->slot("ls_sq_part", sizeof(double) * m * LS_SQ_SLICES));
+        lasso_sq_kernel<<<dim3(m, LS_SQ_SLICES), LS_THREADS, 0, s>>>(xt, rows, sq_part);
+        DNDC_LAUNCHED(ctx);
+        lasso_sq_final_kernel<<<(m + 127) / 128, 128, 0, s>>>(sq_part, m, sq);
         DNDC_LAUNCHED(ctx);
         DNDC_CUDA(cudaMemcpyAsync(r, y, sizeof(double) * rows, cudaMemcpyDeviceToDevice, s));  // r = y - X0
     }
@@ -302,6 +327,7 @@ static void lasso_fit(dndc_ctx* ctx, const double* x, int64_t rows, int64_t n_gl
         DNDC_CUDA(cudaMemcpyAsync(sq + m, &nb, sizeof(double), cudaMemcpyHostToDevice, s));
         DNDC_CUDA(cudaStreamSynchronize(s));
     }
+    mark("norms");
     if (ctx->world > 1) {
         const int rc = dndc_allreduce_f64(ctx, sq, m + 1);  // rank-order fold (regression.cpp:61-62)
         if (rc != DNDC_OK) throw Error(rc, dndc_last_error());
@@ -310,6 +336,7 @@ static void lasso_fit(dndc_ctx* ctx, const double* x, int64_t rows, int64_t n_gl
     DNDC_CUDA(cudaMemcpyAsync(&bad_total, sq + m, sizeof(double), cudaMemcpyDeviceToHost, s));
     DNDC_CUDA(cudaStreamSynchronize(s));
     if (bad_total != 0.0) value_error("lasso_fit: column 0 must be the all-ones bias column");
+    mark("allreduce");
 
     LassoCtl c0{0.0, 0.0, 0.0, 0.0, -1, 0, 0, 0};
     DNDC_CUDA(cudaMemcpyAsync(ctl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
@@ -329,29 +356,36 @@ static void lasso_fit(dndc_ctx* ctx, const double* x, int64_t rows, int64_t n_gl
             }
         }
     };
-    // one sweep as a graph, replayed (launch cost of m+1 kernels -> one)
+    // one sweep as a graph, replayed (launch cost of m+1 kernels -> one);
+    // instantiated once per (buffers, shape, lambda, tol, transport) and kept
     cudaStream_t gs = ctx->own_stream;
     cudaEvent_t ev = ctx->ev_a;
     DNDC_CUDA(cudaEventRecord(ev, s));
     DNDC_CUDA(cudaStreamWaitEvent(gs, ev, 0));
-    cudaGraph_t graph;
-    DNDC_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
-    try {
-        sweep(gs);
-    } catch (...) {
-        cudaStreamEndCapture(gs, &graph);
-        throw;
-    }
-    DNDC_CUDA(cudaStreamEndCapture(gs, &graph));
-    cudaGraphExec_t exec;
-    DNDC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-    DNDC_CUDA(cudaGraphDestroy(graph));
-    for (int sw = 0; sw < sweeps; ++sw) {
-        cudaError_t e = cudaGraphLaunch(exec, gs);
-        if (e != cudaSuccess) {
-            cudaGraphExecDestroy(exec);
-            DNDC_CUDA(e);
+    char keybuf[256];
+    std::snprintf(keybuf, sizeof(keybuf), "%p/%p/%lld/%d/%.17g/%.17g/%d/%d/%d/%llu", (const void*)xt, (void*)r,
+                  (long long)rows, m, lambda, tol, G, ctx->world, nccl ? 1 : 0,
+                  static_cast<unsigned long long>(ctx->slot_gen));
+    if (!ctx->ls_exec || ctx->ls_key != keybuf) {
+        if (ctx->ls_exec) cudaGraphExecDestroy(ctx->ls_exec);
+        ctx->ls_exec = nullptr;
+        cudaGraph_t graph;
+        DNDC_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+        try {
+            sweep(gs);
+        } catch (...) {
+            cudaStreamEndCapture(gs, &graph);
+            throw;
         }
+        DNDC_CUDA(cudaStreamEndCapture(gs, &graph));
+        DNDC_CUDA(cudaGraphInstantiate(&ctx->ls_exec, graph, 0));
+        DNDC_CUDA(cudaGraphDestroy(graph));
+        ctx->ls_key = keybuf;
+    }
+    cudaGraphExec_t exec = ctx->ls_exec;
+    mark("instantiate");
+    for (int sw = 0; sw < sweeps; ++sw) {
+        DNDC_CUDA(cudaGraphLaunch(exec, gs));
         ctx->launches += static_cast<uint64_t>(m + 1);
     }
     DNDC_CUDA(cudaEventRecord(ev, gs));
@@ -361,7 +395,7 @@ static void lasso_fit(dndc_ctx* ctx, const double* x, int64_t rows, int64_t n_gl
     DNDC_CUDA(cudaMemcpyAsync(w_host, w, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
     DNDC_CUDA(cudaMemcpyAsync(trace_host, trace, sizeof(double) * sweeps, cudaMemcpyDeviceToHost, s));
     DNDC_CUDA(cudaStreamSynchronize(s));
-    cudaGraphExecDestroy(exec);
+    mark("sweeps");
     *sweeps_run = ch.sweep;
 }
 

@@ -226,6 +226,7 @@ int dndc_destroy(dndc_ctx* ctx) {
         dndc::destroy_kmeans_state(ctx->km);
         for (auto& kv : ctx->slots) cudaFree(kv.second.first);
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        if (ctx->ls_exec) cudaGraphExecDestroy(ctx->ls_exec);
         for (void* b : ctx->io_buf) cudaFreeHost(b);
         for (cudaEvent_t e : ctx->io_ev) cudaEventDestroy(e);
         for (int r = 0; r < static_cast<int>(ctx->peer_bases.size()); ++r)
