@@ -18,6 +18,7 @@ live in HBM as torch CUDA tensors, which are used only as device memory.
   mean_axis / var_axis / stddev_axis          same names (axis 0 = the split axis)
   resplit (ndarray.hpp:340-386)               resplit (dndc_resplit, NCCL send/recv)
   lasso_fit / lasso_predict (regression.hpp)  same names (dndc_lasso_*_f64)
+  dnb_read_header / dnb_save / dnb_load       same names (payload file <-> HBM, dndc_file_*)
   (not in the reference)                      kmeanspp_indices (BASELINE config 5)
 """
 from __future__ import annotations
@@ -30,14 +31,14 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import TransportError, check, lib
+from ._lib import DataError, TransportError, check, lib
 
 __all__ = [
     "Communicator", "DndArray", "KMeansModel", "MomentState", "TransportError", "chunk_map",
     "random_uniform", "from_global", "gather", "resplit", "row_norms", "distance_block", "cdist", "cdist_xy",
     "kmeans_init_indices", "kmeans_init_centroids", "kmeans_fit", "kmeans_predict", "mean_axis",
     "var_axis", "stddev_axis", "moments_axis0", "kmeanspp_indices", "LassoModel", "soft_threshold",
-    "lasso_fit", "lasso_predict",
+    "lasso_fit", "lasso_predict", "DataError", "dnb_read_header", "dnb_save", "dnb_load",
 ]
 
 _SUFFIX = {torch.float32: "f32", torch.float64: "f64"}
@@ -111,6 +112,10 @@ class Communicator:
 
     def synchronize(self) -> None:
         check(lib().dndc_synchronize(self.handle))
+
+    def barrier(self) -> None:
+        """Communicator::barrier (transport.hpp:86-88)."""
+        check(lib().dndc_barrier(self.handle))
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -534,4 +539,77 @@ def lasso_predict(model: LassoModel, x: DndArray) -> DndArray:
     check(lib().dndc_lasso_predict_f64(x.comm.handle, _ptr(x.tile), x.tile.shape[0], x.shape[1], w.ctypes.data,
                                        _ptr(out)))
     return DndArray((x.shape[0],), x.split, x.comm, out)
+
+
+_DNB_DTYPES = {1: (torch.float32, 4), 2: (torch.float64, 8)}
+
+
+def dnb_read_header(path: str):
+    """dataio.cpp:57-88: (dtype, extents, header_bytes); DataError on a missing
+    file, bad magic, unknown dtype_code, ndim 0 or truncated extents."""
+    import os
+
+    if not os.path.exists(path):
+        raise DataError(f"dnb_read_header: cannot open {path}")
+    with open(path, "rb") as f:
+        fixed = f.read(6)
+        if len(fixed) != 6:
+            raise DataError(f"dnb_read_header: {path} is shorter than the fixed header")
+        if fixed[:4] != b"DNB1":
+            raise DataError(f'dnb_read_header: bad magic in {path}, expected "DNB1"')
+        if fixed[4] not in _DNB_DTYPES:
+            raise DataError(f"dnb_read_header: unknown dtype_code {fixed[4]} in {path}")
+        if fixed[5] == 0:
+            raise DataError(f"dnb_read_header: ndim must be at least 1 in {path}")
+        raw = f.read(8 * fixed[5])
+        if len(raw) != 8 * fixed[5]:
+            raise DataError(f"dnb_read_header: truncated extents in {path}")
+    ext = tuple(int(e) for e in np.frombuffer(raw, "<u8"))
+    return _DNB_DTYPES[fixed[4]][0], ext, 6 + 8 * len(ext)
+
+
+def dnb_save(a: DndArray, path: str) -> None:
+    """Collective save (dataio.hpp:61-100): rank 0 writes the header (and a
+    replicated payload); split=0 ranks write their rows from HBM at their offset."""
+    if a.split not in (None, 0):
+        a = resplit(a, 0)
+    code = {torch.float32: 1, torch.float64: 2}.get(a.tile.dtype)
+    if code is None:
+        raise ValueError("dnb_save: float32 or float64 arrays")
+    head = b"DNB1" + bytes([code, len(a.shape)]) + np.asarray(a.shape, "<u8").tobytes()
+    esz = a.tile.element_size()
+    if a.comm.rank() == 0:
+        with open(path, "wb") as f:
+            f.write(head)
+        if a.split is None and a.tile.numel():
+            check(lib().dndc_file_write_from_device(a.comm.handle, path.encode(), len(head), _ptr(a.tile),
+                                                    a.tile.numel() * esz))
+    a.comm.barrier()
+    if a.split == 0 and a.tile.numel():
+        row = a.tile.numel() // a.tile.shape[0]
+        check(lib().dndc_file_write_from_device(a.comm.handle, path.encode(), len(head) + a.row_offset() * row * esz,
+                                                _ptr(a.tile), a.tile.numel() * esz))
+    a.comm.barrier()
+
+
+def dnb_load(path: str, split, comm: Communicator) -> DndArray:
+    """Collective load (dataio.hpp:102-142): split=0 ranks read only their byte
+    range, straight into HBM; other splits load as split=0 and resplit."""
+    import os
+
+    dtype, shape, hb = dnb_read_header(path)
+    esz = _DNB_DTYPES[{torch.float32: 1, torch.float64: 2}[dtype]][1]
+    want = hb + int(np.prod(shape)) * esz
+    have = os.path.getsize(path)
+    if have != want:
+        raise DataError(f"dnb_load: truncated payload in {path}: expected {want} bytes, file has {have}")
+    _check_split(shape, split)
+    if split not in (None, 0):
+        return resplit(dnb_load(path, 0, comm), split)
+    tile = torch.empty(_local_shape(shape, split, comm), dtype=dtype, device=f"cuda:{comm.device}")
+    if tile.numel():
+        row = tile.numel() // tile.shape[0]
+        off = hb + (int(chunk_map(shape[0], comm.size())[0][comm.rank()]) * row * esz if split == 0 else 0)
+        check(lib().dndc_file_read_to_device(comm.handle, path.encode(), off, tile.numel() * esz, _ptr(tile)))
+    return DndArray(shape, split, comm, tile)
 

@@ -100,14 +100,25 @@ def main():
     lo, hi = sorted(mt.centroids[:, 0])
     report("kmeans more ranks than rows", abs(hi - 10.0) <= 1e-12 and abs(lo - (np.float32(0.1) / 2)) <= 1e-7)
     # resplit (ndarray.hpp:340-386): all transitions bitwise, then the ops on split=1 input
-    shape3 = (7, 6, 5)
-    d3 = np.arange(np.prod(shape3), dtype=np.float64) * 0.5 - 7.0
     good = True
-    for src in (None, 0, 1, 2):
-        for dst in (None, 0, 1, 2):
-            r = dnd.resplit(dnd.from_global(d3, shape3, src, comm), dst)
-            good &= r.split == dst and np.array_equal(dnd.gather(r).ravel(), d3)
-    report("resplit all transitions (7,6,5)", good)
+    for shape3 in ((7, 6, 5), (2, 6, 1), (1, 1, 1), (5, 4, 3)):
+        d3 = np.arange(np.prod(shape3), dtype=np.float64) * 0.5 - 7.0
+        for src in (None, 0, 1, 2):
+            for dst in (None, 0, 1, 2):
+                r = dnd.resplit(dnd.from_global(d3, shape3, src, comm), dst)
+                good &= r.split == dst and np.array_equal(dnd.gather(r).ravel(), d3)
+    report("resplit all transitions, acceptance shapes", good)
+    # DNB round trip through a shared file (dataio.hpp:61-142)
+    import tempfile
+    path = os.path.join(tempfile.gettempdir(), f"dist_check_{os.environ.get('MASTER_PORT', '0')}.dnb")
+    d60 = np.sin(np.arange(60) * 1.7)
+    good = True
+    for ss in (None, 0, 1, 2):
+        for ls in (None, 0, 1, 2):
+            dnd.dnb_save(dnd.from_global(d60, (5, 4, 3), ss, comm), path)
+            good &= np.array_equal(dnd.gather(dnd.dnb_load(path, ls, comm)).ravel(), d60)
+            dist.barrier()
+    report("dnb save/load every split pair", good)
     xs1 = dnd.resplit(xk, 1)
     m1 = dnd.kmeans_fit(xs1, 8, 10, 0.0, 42)
     report("kmeans_fit on split=1 input", np.array_equal(m1.centroids, model.centroids))
