@@ -51,6 +51,16 @@ def main():
         print(json.dumps({"config": "cfg2 cdist_xy 200k x 18 vs 200k x 18 (1 GPU)", "seconds": t,
                           "GB/s": byt / t / 1e9, "frac_hbm": byt / t / 1e9 / PEAK,
                           "pairs_per_s": n * n / t, "TFLOP/s": 2.0 * n * n * m / t / 1e12}), flush=True)
+
+        # self mode cdist(X) (pairwise.cpp:37-85), reported separately
+        def run_self():
+            _lib.check(L.dndc_cdist_f32(comm.handle, x.tile.data_ptr(), n, n, m, out.data_ptr()))
+
+        t = timed(run_self)
+        byt = 4.0 * n * n + 4.0 * n * m
+        print(json.dumps({"config": "cfg2 self cdist(X) 200k x 18 (1 GPU, diagonal zeroed)", "seconds": t,
+                          "GB/s": byt / t / 1e9, "frac_hbm": byt / t / 1e9 / PEAK,
+                          "pairs_per_s": n * n / t}), flush=True)
         del out
         torch.cuda.empty_cache()
     if "cfg4" in want:
