@@ -82,6 +82,30 @@ def test_cpp_dropin_compiles_against_the_c_abi():
     r = subprocess.run(["make", "-C", os.path.join(root, "cpp")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:]
     assert os.path.exists(os.path.join(root, "cpp", "build", "test_dnd"))
-    for h in ("ndarray.hpp", "pairwise.hpp", "cluster.hpp", "moments.hpp", "transport.hpp", "chunking.hpp"):
+    assert os.path.exists(os.path.join(root, "cpp", "build", "dnd"))
+    for h in ("ndarray.hpp", "pairwise.hpp", "cluster.hpp", "moments.hpp", "transport.hpp", "chunking.hpp",
+              "dataio.hpp", "regression.hpp"):
         src = open(os.path.join(root, "cpp", "include", "dnd", h)).read()
         assert "cuda_runtime" not in src and "#include <cuda" not in src
+
+
+def test_cli_usage_errors_and_no_cpu_fallback():
+    """`dnd` (F3, tools/main.cpp:12-63): bad flags exit 2 with the usage line;
+    a valid command on a host without a GPU fails loudly (exit 1, CUDA error),
+    it never computes on the CPU."""
+    import subprocess
+
+    import torch
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-C", os.path.join(root, "cpp")], capture_output=True, check=True)
+    exe = os.path.join(root, "cpp", "build", "dnd")
+    for args in (["frobnicate"], ["bench", "--algo", "svm"], ["bench", "--synthetic", "12"], ["bench", "--k"],
+                 ["bench", "--algo", "load"]):
+        r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 2 and "usage: dnd" in r.stderr, (args, r.stderr)
+    if not torch.cuda.is_available():
+        r = subprocess.run([exe, "bench", "--algo", "kmeans", "--synthetic", "100x4"], capture_output=True,
+                           text=True, timeout=60)
+        assert r.returncode == 1 and r.stderr.startswith("dnd: ")
+
