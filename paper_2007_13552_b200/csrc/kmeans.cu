@@ -1754,7 +1754,7 @@ static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n, const T* x) {
         if (P > 0) {
             A.tc = true;
             A.tmap = make_tmap_2d_f32(x, static_cast<uint64_t>(n / P), static_cast<uint64_t>(P * d),
-                                      static_cast<uint64_t>(P * d * 4), 4, 128);
+                                      static_cast<uint64_t>(P * d * 4), 32, 128, true);
             DNDC_CUDA(cudaFuncSetAttribute(A.tfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(A.tsmem)));
             int per_sm = 1;

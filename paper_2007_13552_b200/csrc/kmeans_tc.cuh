@@ -4,8 +4,12 @@
 // The K*D score FMAs per row run on the 5th-gen tensor cores:
 //   * X is streamed by TMA 2-D tile loads as P rows per MMA row ("packed
 //     rows": X viewed as [n/P x P*D]; D = 18 rows pair up into 36 columns with
-//     a 144-byte pitch), box {4 columns, 128 packed rows} = the SWIZZLE_NONE
-//     K-major canonical layout of tc.cuh.  3-stage ring, one producer thread.
+//     a 144-byte pitch), box {32 columns, 128 packed rows} with SWIZZLE_128B:
+//     each K-block of 32 columns is one [128 rows x 128 B] swizzle-atom stack
+//     (the K-major SW128 layout of cdist_tc.cu), so a tile is ceil(KC/32)
+//     boxes of 128-byte row segments (the earlier 4-column SWIZZLE_NONE boxes
+//     cost 16 TMA requests of 16 B per row and bounded the kernel at ~0.6 TB/s).
+//     2-3 stage ring, one producer thread.
 //   * scores[packed row][h*K + j] = x_h . (-2 c_j) with a block-diagonal
 //     centroid operand (N = P*K), 3xTF32: the tensor core truncates fp32
 //     inputs to tf32 (pinned by tests/test_gpu_tc.py), so hi = the raw TMA
@@ -40,6 +44,7 @@ template <int D, int K, int P, int WG_ = 2>
 struct TcCfg {
     static constexpr int KC = ((P * D + 7) / 8) * 8;  // MMA K (tf32 steps of 8)
     static constexpr int NCH = KC / 4;                // 16-byte column chunks
+    static constexpr int NKB = (KC + 31) / 32;        // 128-byte K-blocks (TMA boxes) per tile
     static constexpr int NS = P * K;                  // MMA N: score slots
     static constexpr int PR = 128;                    // packed rows per tile (MMA M)
     static constexpr int TROWS = PR * P;              // data rows per tile
@@ -47,7 +52,7 @@ struct TcCfg {
     static constexpr int WGS = WG_;                   // epilogue warpgroups
     static constexpr int EPI = 128 * WGS;
     static constexpr int THREADS = EPI + 32;          // + the producer / MMA warp
-    static constexpr int TILE_BYTES = NCH * PR * 16;
+    static constexpr int TILE_BYTES = NKB * PR * 128;
     static constexpr int SORT_BYTES = TROWS * D * 4;
     static constexpr int WORK_BYTES = TILE_BYTES > SORT_BYTES ? TILE_BYTES : SORT_BYTES;  // lo, then sorted rows
     static constexpr int B_BYTES = NCH * NS * 16;
@@ -69,6 +74,7 @@ struct TcCfg {
     static_assert(D % 2 == 0 && D <= 64 && K <= 64, "tc kernel shape");
     static_assert(WGS * K * D * 8 <= WGS * WORK_BYTES, "final combine scratch");
     static_assert(OFF_TMEM + 16 <= 232448, "shared memory");
+    static_assert(TILE_BYTES % 1024 == 0 && WORK_BYTES % 1024 == 0, "SW128 tiles need 1024-byte alignment");
 };
 
 template <int D, int K, int P, int WG_>
@@ -83,6 +89,7 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
     if (p.done && *p.done) return;
 
     extern __shared__ __align__(1024) unsigned char smem[];
+    if (tc::smem_u32(smem) & 1023u) __trap();  // SW128 atoms: the dynamic window must start 1024-aligned
     float* tiles = reinterpret_cast<float*>(smem + C::OFF_TILE);
     float* bhi = reinterpret_cast<float*>(smem + C::OFF_BHI);
     float* blo = reinterpret_cast<float*>(smem + C::OFF_BLO);
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                     tc::mbar_expect_tx(&full[st], C::TILE_BYTES);
                     float* dst = tiles + st * (C::TILE_BYTES / 4);
 #pragma unroll
-                    for (int c = 0; c < NCH; ++c) tc::tma_load_2d(dst + c * PR * 4, &map, &full[st], c * 4, prow);
+                    for (int kb = 0; kb < C::NKB; ++kb) tc::tma_load_2d(dst + kb * PR * 32, &map, &full[st], kb * 32, prow);
                     ++issued;
                 }
                 const int st = static_cast<int>(it % S), w = static_cast<int>(it % WGS);
@@ -165,8 +172,9 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                 const uint32_t dt = tmem + w * NS;
 #pragma unroll
                 for (int ks = 0; ks < C::KC / 8; ++ks) {
-                    const uint64_t ahi = tc::smem_desc(a0 + ks * 2 * PR * 16, PR * 16, 128);
-                    const uint64_t alo = tc::smem_desc(l0 + ks * 2 * PR * 16, PR * 16, 128);
+                    const uint32_t ko = (ks / 4) * PR * 128 + (ks % 4) * 32;  // K-block, then bytes inside the atom
+                    const uint64_t ahi = tc::smem_desc(a0 + ko, 16, 1024, 2);
+                    const uint64_t alo = tc::smem_desc(l0 + ko, 16, 1024, 2);
                     const uint64_t bh = tc::smem_desc(bh0 + ks * 2 * NS * 16, NS * 16, 128);
                     const uint64_t bl = tc::smem_desc(bl0 + ks * 2 * NS * 16, NS * 16, 128);
                     tc::mma_tf32(dt, ahi, bh, idesc, ks > 0);
@@ -204,14 +212,16 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             float4 xr[NCH];
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
-                const float4 v = *reinterpret_cast<const float4*>(xt + c * PR * 4 + t * 4);
+                // 16-byte chunk c of row t: K-block c/8, chunk (c%8) ^ (t%8) of the row's 128-byte line
+                const int off = (c / 8) * PR * 32 + t * 32 + (((c % 8) ^ (t & 7)) * 4);
+                const float4 v = *reinterpret_cast<const float4*>(xt + off);
                 xr[c] = v;
                 float4 l;
                 l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
                 l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
                 l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
                 l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                *reinterpret_cast<float4*>(work + c * PR * 4 + t * 4) = l;
+                *reinterpret_cast<float4*>(work + off) = l;
             }
             tc::fence_async_smem();
             tc::named_sync(bar_id, 128);
@@ -243,7 +253,11 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                 i1[h] = 0;
             }
 #pragma unroll
+#ifdef KT_EXP_NOSCORE
+            for (int q16 = 0; q16 < 1; ++q16) {
+#else
             for (int q16 = 0; q16 < NS / 16; ++q16) {
+#endif
                 float v[16];
                 tc::tmem_ld16(trow + q16 * 16, v);
 #pragma unroll
@@ -271,6 +285,9 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             // near-ties: candidate clusters (score within tau of the best) from a
             // second, warp-uniform TMEM pass (tcgen05.ld is .sync.aligned), then
             // the exact f64 decision over the candidates only
+#ifdef KT_EXP_NOREFINE
+            any_flag = false;
+#endif
             if (__any_sync(FULL, any_flag)) {
                 uint64_t cand[P];
 #pragma unroll
@@ -285,14 +302,54 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                         if (cn[j] + v[i] <= b1[h] + tau[h]) cand[h] |= 1ull << j;
                     }
                 }
+                // warp-cooperative exact decision: the flagged rows one at a
+                // time, the lanes spread over that row's candidates (one f64
+                // dot-product chain each, the row broadcast by shuffles), then
+                // a warp argmin with the reference's lowest-index tie rule.
+                // (A per-lane ref_argmin_cand ran ncand + 1 serial chains in a
+                // divergent branch and cost half the kernel at K = 64.)
 #pragma unroll
                 for (int h = 0; h < P; ++h) {
-                    if (flag[h]) {
-                        float xv[D];
+                    unsigned fm = __ballot_sync(FULL, flag[h]);
+                    while (fm) {
+                        const int src = __ffs(fm) - 1;
+                        fm &= fm - 1;
+                        uint64_t rest = __shfl_sync(FULL, cand[h], src);
+                        int best = K;
+                        double bd = 0.0;
+                        while (rest) {  // rounds of up to 32 candidates, ascending j
+                            uint64_t mm = rest;
+                            for (int i = 0; i < lane && mm; ++i) mm &= mm - 1;
+                            const int j = mm ? __ffsll(static_cast<long long>(mm)) - 1 : -1;
+                            for (int i = 0; i < 32 && rest; ++i) rest &= rest - 1;
+                            const double* c = p.c64 + static_cast<int64_t>(j < 0 ? 0 : j) * D;
+                            double xn = 0.0, g = 0.0;
 #pragma unroll
-                        for (int f = 0; f < D; ++f) xv[f] = xval(h * D + f);
-                        label[h] = ref_argmin_cand<D>(xv, cand[h], p.c64, p.cn64);
-                        ++refined;
+                            for (int f = 0; f < D; ++f) {
+                                const double xf = static_cast<double>(__shfl_sync(FULL, xval(h * D + f), src));
+                                xn = add_rn(xn, mul_rn(xf, xf));
+                                g = add_rn(g, mul_rn(xf, c[f]));
+                            }
+                            double dj = j < 0 ? 0.0 : ref_distance(xn, p.cn64[j], g);
+                            int jj = j < 0 ? K : j;
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) {
+                                const double od = __shfl_xor_sync(FULL, dj, o);
+                                const int oj = __shfl_xor_sync(FULL, jj, o);
+                                if (oj < K && (jj == K || od < dj || (od == dj && oj < jj))) {
+                                    dj = od;
+                                    jj = oj;
+                                }
+                            }
+                            if (jj < K && (best == K || dj < bd)) {  // later rounds hold larger j: strict <
+                                bd = dj;
+                                best = jj;
+                            }
+                        }
+                        if (lane == src) {
+                            label[h] = best;
+                            ++refined;
+                        }
                     }
                 }
             }
