@@ -178,8 +178,10 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                     const uint64_t bh = tc::smem_desc(bh0 + ks * 2 * NS * 16, NS * 16, 128);
                     const uint64_t bl = tc::smem_desc(bl0 + ks * 2 * NS * 16, NS * 16, 128);
                     tc::mma_tf32(dt, ahi, bh, idesc, ks > 0);
+#ifndef KT_EXP_ONEMMA
                     tc::mma_tf32(dt, ahi, bl, idesc, 1);
                     tc::mma_tf32(dt, alo, bh, idesc, 1);
+#endif
                 }
                 tc::mma_commit(&dfull[w]);
             }
@@ -238,6 +240,9 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                 xx[h] = 0.f;
 #pragma unroll
                 for (int f = 0; f < D; ++f) xx[h] = fmaf(xval(h * D + f), xval(h * D + f), xx[h]);
+#ifdef KT_EXP_NOXX
+                xx[h] = 16.f;
+#endif
             }
 
             // scores: running top-2 over 16-column TMEM chunks
@@ -314,21 +319,102 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                     while (fm) {
                         const int src = __ffs(fm) - 1;
                         fm &= fm - 1;
-                        uint64_t rest = __shfl_sync(FULL, cand[h], src);
+                        const uint64_t cm = __shfl_sync(FULL, cand[h], src);
+                        // (1) fast filter: f64 distances with the lanes over the
+                        // features (any summation order).  Its error and the
+                        // reference's are both <= (D+2)*2^-53*S, S = |x|^2 +
+                        // max|c|^2 + 2|x|max|c|, so a winner whose margin over
+                        // the runner-up (and over the clamp at 0) exceeds
+                        // 2^-40*S is the reference's choice, sqrt rounding
+                        // included.  The row goes through this warp's own rows
+                        // of the lo buffer (free: the tile's MMAs completed).
+                        float* scr = work + wq * 32 * 32;
+                        if (lane == src) {
+#pragma unroll
+                            for (int f = 0; f < D; ++f) scr[f] = xval(h * D + f);
+                        }
+                        __syncwarp();
+                        constexpr int FL = (D + 31) / 32;
+                        double xf[FL];
+                        double xn = 0.0;
+#pragma unroll
+                        for (int u = 0; u < FL; ++u) {
+                            const int f = lane + 32 * u;
+                            xf[u] = f < D ? static_cast<double>(scr[f]) : 0.0;
+                            xn = fma(xf[u], xf[u], xn);
+                        }
+                        __syncwarp();
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) xn += __shfl_xor_sync(FULL, xn, o);
+                        double d1 = DBL_MAX, d2 = DBL_MAX;
                         int best = K;
+                        for (uint64_t rest = cm; rest;) {
+                            int js[4];
+                            double gp[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                js[q] = rest ? __ffsll(static_cast<long long>(rest)) - 1 : -1;
+                                rest &= rest - 1;
+                                gp[q] = 0.0;
+                                const double* cq = p.c64 + static_cast<int64_t>(js[q] < 0 ? 0 : js[q]) * D;
+#pragma unroll
+                                for (int u = 0; u < FL; ++u) {
+                                    const int f = lane + 32 * u;
+                                    if (f < D) gp[q] = fma(xf[u], __ldg(cq + f), gp[q]);
+                                }
+                            }
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) gp[q] += __shfl_xor_sync(FULL, gp[q], o);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                if (js[q] < 0) continue;
+                                const double dq = xn + p.cn64[js[q]] - 2.0 * gp[q];
+                                if (dq < d1) {
+                                    d2 = d1;
+                                    d1 = dq;
+                                    best = js[q];
+                                } else if (dq < d2) {
+                                    d2 = dq;
+                                }
+                            }
+                        }
+                        const double margin =
+                            0x1.0p-40 * (xn + static_cast<double>(cnmax) + 2.0 * sqrt(xn) * static_cast<double>(cmax));
+                        const bool decided = d1 > margin && d2 - d1 > margin;
+#ifdef KT_EXP_COUNT_FALLBACK
+                        if (!decided && lane == src) atomicAdd(p.refined + 1, 1ull);
+#endif
+                        // (2) otherwise the reference's own operation order
                         double bd = 0.0;
-                        while (rest) {  // rounds of up to 32 candidates, ascending j
+                        if (!decided) best = K;
+                        for (uint64_t rest = decided ? 0 : cm; rest;) {  // rounds of up to 32 candidates, ascending j
                             uint64_t mm = rest;
                             for (int i = 0; i < lane && mm; ++i) mm &= mm - 1;
                             const int j = mm ? __ffsll(static_cast<long long>(mm)) - 1 : -1;
                             for (int i = 0; i < 32 && rest; ++i) rest &= rest - 1;
                             const double* c = p.c64 + static_cast<int64_t>(j < 0 ? 0 : j) * D;
                             double xn = 0.0, g = 0.0;
+                            // batches of 16 features: the centroid loads and the
+                            // row broadcast are issued ahead of the two serial
+                            // f64 chains (one L1 round trip per batch, not per step)
+                            constexpr int FB = D % 16 == 0 ? 16 : D % 8 == 0 ? 8 : 2;
 #pragma unroll
-                            for (int f = 0; f < D; ++f) {
-                                const double xf = static_cast<double>(__shfl_sync(FULL, xval(h * D + f), src));
-                                xn = add_rn(xn, mul_rn(xf, xf));
-                                g = add_rn(g, mul_rn(xf, c[f]));
+                            for (int f0 = 0; f0 < D; f0 += FB) {
+                                double2 cb[FB / 2];
+                                float xb[FB];
+#pragma unroll
+                                for (int u = 0; u < FB / 2; ++u)
+                                    cb[u] = __ldg(reinterpret_cast<const double2*>(c + f0) + u);
+#pragma unroll
+                                for (int u = 0; u < FB; ++u) xb[u] = __shfl_sync(FULL, xval(h * D + f0 + u), src);
+#pragma unroll
+                                for (int u = 0; u < FB; ++u) {
+                                    const double xf = static_cast<double>(xb[u]);
+                                    xn = add_rn(xn, mul_rn(xf, xf));
+                                    g = add_rn(g, mul_rn(xf, u % 2 ? cb[u / 2].y : cb[u / 2].x));
+                                }
                             }
                             double dj = j < 0 ? 0.0 : ref_distance(xn, p.cn64[j], g);
                             int jj = j < 0 ? K : j;
