@@ -184,6 +184,10 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
 #endif
                 }
                 tc::mma_commit(&dfull[w]);
+                // the stage is free once its MMAs retire (the split already read
+                // it): released here rather than after the epilogue's readback
+                // and near-tie work, so TMA runs ahead of a slow tile
+                tc::mma_commit(&empty[st]);
             }
         }
     } else {
@@ -448,7 +452,6 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             }
             tc::tc_fence_before();
             tc::mbar_arrive(&dempty[wg]);
-            if (t == 0) tc::mbar_arrive(&empty[st]);  // the tile is in registers; its MMAs completed
             if (!accumulate) continue;
 
             // ---------------- counting sort of the tile by label (groups vw = h*4 + wq)

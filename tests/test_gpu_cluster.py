@@ -229,3 +229,25 @@ def test_fused_fit_rejects_non_finite_then_recovers(comm, oracle):
     c_ref, t_ref, _ = oracle.kmeans_fit(xh.astype(np.float64), k, 5, 0.0, 3)
     assert rel_dev(model.centroids, c_ref) <= 1e-6
     assert model.iterations_run == 5
+
+
+@pytest.mark.parametrize("n", [4096, 20_001])
+def test_tc_predict_exact_ties_and_zero_distances(comm, oracle, n):
+    # The tcgen05 kernel (k*d >= 1024) re-decides near-ties in f64: a fast
+    # lanes-over-features pass accepts a winner only with a 2^-40 relative
+    # margin, otherwise the reference's own operation order runs.  Duplicate
+    # centroids (exact ties: lowest index wins, cluster.cpp:44-56), rows equal
+    # to a centroid (clamp at 0) and rows midway between two centroids all
+    # take the fallback; the labels must still equal the reference's.
+    m, k = 64, 64
+    cents = oracle.uniform_f64(k, m, 11).astype(np.float32).astype(np.float64)
+    cents[5] = cents[9]
+    cents[40] = cents[3]
+    xh = oracle.uniform_f32(n, m, 12)
+    xh[0:64] = cents.astype(np.float32)
+    xh[64:128] = ((cents[:64] + cents[np.arange(64) ^ 1]) * 0.5).astype(np.float32)
+    x = dnd.from_global(xh, (n, m), 0, comm)
+    got = dnd.gather(dnd.kmeans_predict(dnd.KMeansModel(k, m, cents), x))
+    want = oracle.kmeans_predict(xh.astype(np.float64), cents)
+    assert np.array_equal(got, want)
+    assert got[9] == 5 and got[3] == 3  # duplicated pairs resolve to the lower index
