@@ -83,6 +83,19 @@ def main():
     c2, t2, it2 = O.kmeans_fit(O.uniform_f32(5000, 5, 9).astype(np.float64), 6, 50, 1e-4, 3, p)
     report("kmeans_fit tol (generic kernel)", m2.iterations_run == it2 and rel_dev(m2.centroids, c2) <= 1e-5,
            f"iters {m2.iterations_run} vs {it2}")
+    # tcgen05 kernel shape (cfg3: d = 64, k = 64) through the multi-GPU stats exchange
+    n3 = 40_001
+    x3 = dnd.random_uniform((n3, 64), 0, 44, comm)
+    m3 = dnd.kmeans_fit(x3, 64, 5, 0.0, 44)
+    x3h = O.uniform_f32(n3, 64, 44).astype(np.float64)
+    c3, t3, _ = O.kmeans_fit(x3h, 64, 5, 0.0, 44, p)
+    all3 = [None] * p
+    dist.all_gather_object(all3, m3.centroids)
+    report("kmeans_fit 40k x 64 k=64 (tcgen05)", rel_dev(m3.centroids, c3) <= 1e-5 and rel_dev(m3.inertia_trace, t3) <= 1e-5
+           and all(np.array_equal(all3[0], c) for c in all3),
+           f"centroids dev={rel_dev(m3.centroids, c3):.2e} trace dev={rel_dev(m3.inertia_trace, t3):.2e}")
+    lab3 = dnd.gather(dnd.kmeans_predict(m3, x3))
+    report("kmeans_predict k=64 (tcgen05)", np.array_equal(lab3, O.kmeans_predict(x3h, m3.centroids)))
     # predict
     lab = dnd.gather(dnd.kmeans_predict(model, xk))
     report("kmeans_predict", np.array_equal(lab, O.kmeans_predict(O.uniform_f32(n2, 18, 42).astype(np.float64),
