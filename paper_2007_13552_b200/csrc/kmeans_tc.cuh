@@ -253,31 +253,50 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             tc::mbar_wait(&dfull[wg], static_cast<uint32_t>(use & 1));
             tc::tc_fence_after();
             const uint32_t trow = tmem + (static_cast<uint32_t>(wq * 32) << 16) + wg * NS;
-            float b1[P], b2[P];
-            int i1[P];
+            // two interleaved top-2 chains per row (even / odd score columns),
+            // merged below: halves the serial min chain.  Which of two equal fp32
+            // scores wins does not matter: a zero gap is always a flagged near-tie.
+            float b1x[2][P], b2x[2][P];
+            int i1x[2][P];
 #pragma unroll
             for (int h = 0; h < P; ++h) {
-                b1[h] = FLT_MAX;
-                b2[h] = FLT_MAX;
-                i1[h] = 0;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    b1x[e][h] = FLT_MAX;
+                    b2x[e][h] = FLT_MAX;
+                    i1x[e][h] = 0;
+                }
             }
+            // (32-column loads where NS allows: one TMEM round trip per 32 scores)
+            constexpr int QC = NS % 32 == 0 ? 32 : 16;
 #pragma unroll
 #ifdef KT_EXP_NOSCORE
             for (int q16 = 0; q16 < 1; ++q16) {
 #else
-            for (int q16 = 0; q16 < NS / 16; ++q16) {
+            for (int q16 = 0; q16 < NS / QC; ++q16) {
 #endif
-                float v[16];
-                tc::tmem_ld16(trow + q16 * 16, v);
+                float v[QC];
+                if constexpr (QC == 32) tc::tmem_ld32(trow + q16 * QC, v);
+                else tc::tmem_ld16(trow + q16 * QC, v);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int slot = q16 * 16 + i, h = slot / K, j = slot % K;
+                for (int i = 0; i < QC; ++i) {
+                    const int slot = q16 * QC + i, h = slot / K, j = slot % K;
                     const float s = cn[j] + v[i];
-                    const bool lt = s < b1[h];
-                    b2[h] = fminf(b2[h], fmaxf(b1[h], s));
-                    b1[h] = fminf(b1[h], s);
-                    i1[h] = lt ? j : i1[h];
+                    float& c1 = b1x[i & 1][h];
+                    const bool lt = s < c1;
+                    b2x[i & 1][h] = fminf(b2x[i & 1][h], fmaxf(c1, s));
+                    c1 = fminf(c1, s);
+                    i1x[i & 1][h] = lt ? j : i1x[i & 1][h];
                 }
+            }
+            float b1[P], b2[P];
+            int i1[P];
+#pragma unroll
+            for (int h = 0; h < P; ++h) {
+                const bool second = b1x[1][h] < b1x[0][h];
+                b1[h] = fminf(b1x[0][h], b1x[1][h]);
+                b2[h] = fminf(fmaxf(b1x[0][h], b1x[1][h]), fminf(b2x[0][h], b2x[1][h]));
+                i1[h] = second ? i1x[1][h] : i1x[0][h];
             }
             int label[P];
             bool flag[P];
@@ -302,12 +321,13 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
 #pragma unroll
                 for (int h = 0; h < P; ++h) cand[h] = 0;
 #pragma unroll
-                for (int q16 = 0; q16 < NS / 16; ++q16) {
-                    float v[16];
-                    tc::tmem_ld16(trow + q16 * 16, v);
+                for (int q16 = 0; q16 < NS / QC; ++q16) {
+                    float v[QC];
+                    if constexpr (QC == 32) tc::tmem_ld32(trow + q16 * QC, v);
+                    else tc::tmem_ld16(trow + q16 * QC, v);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int slot = q16 * 16 + i, h = slot / K, j = slot % K;
+                    for (int i = 0; i < QC; ++i) {
+                        const int slot = q16 * QC + i, h = slot / K, j = slot % K;
                         if (cn[j] + v[i] <= b1[h] + tau[h]) cand[h] |= 1ull << j;
                     }
                 }
