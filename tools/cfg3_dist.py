@@ -1,0 +1,63 @@
+"""BASELINE config 3 at full size across GPUs: k-means k=64, 20 Lloyd iterations
+on synthetic 50M x 64 fp32 (random_uniform<float> seed 42), split=0.
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 tools/cfg3_dist.py [rows]
+
+One process per GPU; each holds its chunk_map row shard (50M / N rows) in HBM.
+The whole fit (kmeans_fit as a user calls it: validation, init and 20 iterations)
+is timed with CUDA events on every rank, barrier on both sides, max over ranks.
+Prints one JSON line on rank 0.
+"""
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2007_13552_b200.api as dnd  # noqa: E402
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    p = dist.get_world_size()
+    comm = dnd.Communicator.from_torch_distributed(local)
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 50_000_000
+    m, k, iters = 64, 64, 20
+    x = dnd.random_uniform((n, m), 0, 42, comm)
+    dnd.kmeans_fit(x, k, 2, 0.0, 42)  # warm: plans, graphs, exchange buffers
+    times = []
+    for _ in range(3):
+        dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        model = dnd.kmeans_fit(x, k, iters, 0.0, 42)
+        e.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([s.elapsed_time(e) / 1e3], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times.append(float(t))
+    best = min(times)
+    shard = x.lshape[0]
+    # every rank's centroids must be identical (rank-order fold everywhere)
+    allc = [None] * p
+    dist.all_gather_object(allc, model.centroids)
+    same = all((c == allc[0]).all() for c in allc)
+    if dist.get_rank() == 0:
+        print(json.dumps({
+            "config": f"cfg3 k-means k={k}, {iters} iters on {n} x {m} fp32 over {p} GPU(s)",
+            "rows_per_gpu": shard, "seconds_per_fit": best, "fits": times,
+            "ms_per_iter": best / iters * 1e3, "iters_per_s": iters / best,
+            "GB/s_aggregate": 4.0 * n * m * iters / best / 1e9,
+            "GB/s_per_gpu": 4.0 * n * m * iters / best / 1e9 / p,
+            "iterations_run": model.iterations_run, "final_inertia": float(model.inertia_trace[-1]),
+            "replicated_bit_identical": bool(same)}), flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
