@@ -42,7 +42,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         times.append(float(t))
     best = min(times)
-    shard = x.lshape[0]
+    shard = x.lshape()[0]
     # every rank's centroids must be identical (rank-order fold everywhere)
     allc = [None] * p
     dist.all_gather_object(allc, model.centroids)
