@@ -538,38 +538,55 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             }
             tc::named_sync(bar_id, 128);
 
-            // warp wq sums the sorted runs of clusters wq, wq+4, ... (f64 from the fp32 rows)
+            // warp wq sums the sorted runs of clusters wq, wq+4, ... (f64 from the
+            // fp32 rows), two clusters at a time so their load/add chains overlap;
+            // each run is still summed in row order (bit-identical), and empty runs
+            // skip the shared-memory update (adding +0.0 would be a no-op)
 #pragma unroll
-            for (int jj = 0; jj < JW; ++jj) {
-                const int j = wq + jj * 4;
-                if (j >= K) break;
-                const int r0 = __shfl_sync(FULL, start[j / 32], j % 32);
-                const int r1 = r0 + __shfl_sync(FULL, total[j / 32], j % 32);
-                double2 part = make_double2(0.0, 0.0);
+            for (int jj = 0; jj < JW; jj += 2) {
+                int js[2], rs[2], re[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    js[u] = wq + (jj + u) * 4;
+                    const int jc = js[u] < K ? js[u] : 0;
+                    rs[u] = __shfl_sync(FULL, start[jc / 32], jc % 32);
+                    re[u] = js[u] < K && jj + u < JW ? rs[u] + __shfl_sync(FULL, total[jc / 32], jc % 32) : rs[u];
+                }
+                double2 part[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
                 if (g < G) {
-                    const float* src = work + 2 * q;
-#pragma unroll 4
-                    for (int r = r0 + g; r < r1; r += G) {
-                        const float2 v = *reinterpret_cast<const float2*>(src + r * D);
-                        part.x += static_cast<double>(v.x);
-                        part.y += static_cast<double>(v.y);
+                    const int n0 = re[0] - rs[0], n1 = re[1] - rs[1];
+                    const int nmax = n0 > n1 ? n0 : n1;
+#pragma unroll 2
+                    for (int i = g; i < nmax; i += G) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            if (i < re[u] - rs[u]) {
+                                const float2 v = *reinterpret_cast<const float2*>(work + (rs[u] + i) * D + 2 * q);
+                                part[u].x += static_cast<double>(v.x);
+                                part[u].y += static_cast<double>(v.y);
+                            }
+                        }
                     }
                 }
 #pragma unroll
-                for (int o = 1; o < G; o <<= 1) {
-                    const double vx = __shfl_down_sync(FULL, part.x, o * L);
-                    const double vy = __shfl_down_sync(FULL, part.y, o * L);
-                    if (g + o < G) {
-                        part.x += vx;
-                        part.y += vy;
+                for (int u = 0; u < 2; ++u) {
+                    if (re[u] == rs[u]) continue;  // warp-uniform
+#pragma unroll
+                    for (int o = 1; o < G; o <<= 1) {
+                        const double vx = __shfl_down_sync(FULL, part[u].x, o * L);
+                        const double vy = __shfl_down_sync(FULL, part[u].y, o * L);
+                        if (g + o < G) {
+                            part[u].x += vx;
+                            part[u].y += vy;
+                        }
                     }
-                }
-                if (g == 0 && q < L) {
-                    double2* a = reinterpret_cast<double2*>(acc + j * D + 2 * q);
-                    double2 v = *a;
-                    v.x += part.x;
-                    v.y += part.y;
-                    *a = v;
+                    if (g == 0 && q < L) {
+                        double2* a = reinterpret_cast<double2*>(acc + js[u] * D + 2 * q);
+                        double2 v = *a;
+                        v.x += part[u].x;
+                        v.y += part[u].y;
+                        *a = v;
+                    }
                 }
             }
             // the next tile's split rewrites `work` (lo): all warps must be done reading it
