@@ -86,6 +86,10 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
     constexpr int G = 32 / L;               // rows summed in parallel per warp
     constexpr int JW = (K + 3) / 4;         // clusters owned per epilogue warp
     constexpr int KL = (K + 31) / 32;       // clusters per lane in the scans
+#ifndef KT_NU
+#define KT_NU 4
+#endif
+    constexpr int NU = KT_NU;               // cluster runs summed together per warp
     if (p.done && *p.done) return;
 
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -539,27 +543,30 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             tc::named_sync(bar_id, 128);
 
             // warp wq sums the sorted runs of clusters wq, wq+4, ... (f64 from the
-            // fp32 rows), two clusters at a time so their load/add chains overlap;
+            // fp32 rows), NU clusters at a time so their load/add chains overlap;
             // each run is still summed in row order (bit-identical), and empty runs
             // skip the shared-memory update (adding +0.0 would be a no-op)
 #pragma unroll
-            for (int jj = 0; jj < JW; jj += 2) {
-                int js[2], rs[2], re[2];
+            for (int jj = 0; jj < JW; jj += NU) {
+                int js[NU], rs[NU], re[NU];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < NU; ++u) {
                     js[u] = wq + (jj + u) * 4;
                     const int jc = js[u] < K ? js[u] : 0;
                     rs[u] = __shfl_sync(FULL, start[jc / 32], jc % 32);
                     re[u] = js[u] < K && jj + u < JW ? rs[u] + __shfl_sync(FULL, total[jc / 32], jc % 32) : rs[u];
                 }
-                double2 part[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+                double2 part[NU];
+#pragma unroll
+                for (int u = 0; u < NU; ++u) part[u] = make_double2(0.0, 0.0);
                 if (g < G) {
-                    const int n0 = re[0] - rs[0], n1 = re[1] - rs[1];
-                    const int nmax = n0 > n1 ? n0 : n1;
+                    int nmax = 0;
+#pragma unroll
+                    for (int u = 0; u < NU; ++u) nmax = max(nmax, re[u] - rs[u]);
 #pragma unroll 2
                     for (int i = g; i < nmax; i += G) {
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
+                        for (int u = 0; u < NU; ++u) {
                             if (i < re[u] - rs[u]) {
                                 const float2 v = *reinterpret_cast<const float2*>(work + (rs[u] + i) * D + 2 * q);
                                 part[u].x += static_cast<double>(v.x);
@@ -569,7 +576,7 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < NU; ++u) {
                     if (re[u] == rs[u]) continue;  // warp-uniform
 #pragma unroll
                     for (int o = 1; o < G; o <<= 1) {
