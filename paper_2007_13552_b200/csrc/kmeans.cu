@@ -1645,6 +1645,7 @@ template <typename T>
 struct Assigner {
     bool small = false;
     bool tc = false;
+    bool tc_delta = false;  // the tc instantiation supports delta iterations (TcCfg::DELTA_OK)
     void (*tfn)(CUtensorMap, TcParams) = nullptr;
     CUtensorMap tmap{};
     size_t tsmem = 0;
@@ -1674,6 +1675,8 @@ struct Assigner {
             tp.labels = labels;
             tp.refined = b.refined;
             tp.done = use_done ? b.flags : nullptr;
+            tp.prev = tc_delta ? prev : nullptr;
+            tp.lab8 = tc_delta ? lab8 : nullptr;
             tfn<<<sgrid, tthreads, tsmem, st>>>(tmap, tp);
         } else if (small) {
             DNDC_CUDA(cudaMemcpyToSymbolAsync(c_km_table, b.ctab, sizeof(float) * (k * d + k),
@@ -1723,11 +1726,14 @@ static void pick_tc(Assigner<float>& A) {
         A.tfn = kmeans_tc_kernel<D, K, P, 1>;
         A.tsmem = TcCfg<D, K, P, 1>::SMEM;
         A.tthreads = TcCfg<D, K, P, 1>::THREADS;
+        A.tc_delta = TcCfg<D, K, P, 1>::DELTA_OK;
     } else {
         A.tfn = kmeans_tc_kernel<D, K, P, 2>;
         A.tsmem = TcCfg<D, K, P, 2>::SMEM;
         A.tthreads = TcCfg<D, K, P, 2>::THREADS;
+        A.tc_delta = TcCfg<D, K, P, 2>::DELTA_OK;
     }
+    if (std::getenv("DNDC_TC_NO_DELTA")) A.tc_delta = false;
 }
 
 // DNDC_KMEANS_KERNEL=tc|small|generic overrides the automatic choice (tests, A/B timing).
@@ -1932,7 +1938,8 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     // ---- the Lloyd loop, one graph per (shape, buffers, max_iter, tol)
     // small kernel: every iteration records int8 labels; the first ones
     // accumulate full sums, later ones only the rows whose label changed
-    int8_t* lab8 = A.small ? static_cast<int8_t*>(ctx->slot("km_lab8", std::max<int64_t>(n_local, 1))) : nullptr;
+    const bool use_delta = A.small || (A.tc && A.tc_delta);
+    int8_t* lab8 = use_delta ? static_cast<int8_t*>(ctx->slot("km_lab8", std::max<int64_t>(n_local, 1))) : nullptr;
     if (!ctx->km) ctx->km = new KMeansState();
     KMeansState* km = ctx->km;
     if (km->timing && km->ev.size() < 2 * static_cast<size_t>(max_iter)) {
@@ -1951,7 +1958,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
         for (int it = 0; it < max_iter; ++it) {
             // iterations 0 and 1 accumulate every row (after the first update most
             // labels still move); from iteration 2 on only the rows that changed
-            const bool delta = A.small && it > KS_FULL_ITERS - 1;
+            const bool delta = use_delta && it > KS_FULL_ITERS - 1;
             FuseArgs fa{};
             if (fuse) {
                 fa.on = 1;
@@ -1974,7 +1981,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
             reduce_partials_kernel<<<(S + 7) / 8, 256, 0, st>>>(b.partials, A.grid_for(delta), S, b.stats, b.flags);
             if (ctx->world > 1) allgather_f64(ctx, b.stats, b.gathered, S, st);
             const UpdArgs ua = upd_args(b, k, m, ctx->world, ctx->world > 1 ? b.gathered : b.stats,
-                                        A.small ? b.running : nullptr, delta, it, tol);
+                                        use_delta ? b.running : nullptr, delta, it, tol);
             kmeans_update_kernel<<<1, 256, update_smem(k, m), st>>>(ua);
         }
     };

@@ -34,6 +34,8 @@ struct TcParams {
     int32_t* labels;
     unsigned long long* refined;
     const int* done;
+    const int8_t* prev;   // delta iterations: last iteration's labels (null: full accumulation)
+    int8_t* lab8;         // this iteration's labels (fit only; null in predict)
 };
 
 __host__ __device__ constexpr int tc_pow2_cols(int c) {
@@ -75,6 +77,11 @@ struct TcCfg {
     static_assert(WGS * K * D * 8 <= WGS * WORK_BYTES, "final combine scratch");
     static_assert(OFF_TMEM + 16 <= 232448, "shared memory");
     static_assert(TILE_BYTES % 1024 == 0 && WORK_BYTES % 1024 == 0, "SW128 tiles need 1024-byte alignment");
+    // delta iterations reuse the count area: 4 counts, 4 warps' slot lists (u8)
+    // and the new/old label per slot (i8); shapes where it does not fit run
+    // full accumulation every iteration
+    static constexpr bool DELTA_OK = P == 1 && K <= 127 && TROWS <= 256 &&
+                                     16 + 4 * 32 * P + 2 * TROWS <= ((VW * K * 4 + 15) / 16) * 16;
 };
 
 template <int D, int K, int P, int WG_>
@@ -474,9 +481,88 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                     if (row < p.n) p.labels[row] = label[h];
                 }
             }
+            int oldl[P];
+#pragma unroll
+            for (int h = 0; h < P; ++h) {
+                const int64_t row = (prow0 + t) * P + h;
+                oldl[h] = -1;
+                if (row < p.n) {
+                    if (p.prev) oldl[h] = p.prev[row];
+                    if (p.lab8) p.lab8[row] = static_cast<int8_t>(label[h]);
+                }
+            }
             tc::tc_fence_before();
             tc::mbar_arrive(&dempty[wg]);
             if (!accumulate) continue;
+
+            if (C::DELTA_OK && p.prev) {
+                // ---------------- delta iteration: only rows whose label changed,
+                // +x into the new cluster and -x out of the old one (the update
+                // adds these to the running sums).  A changed row is parked in
+                // its own thread's lo rows of `work` (free: the tile's MMAs
+                // completed; a warp only writes its own rows, so a slower warp
+                // still deciding near-ties in its own rows is not disturbed),
+                // feature f at K-block f/32, column f%32, unswizzled; a compact
+                // list per warp in row order; every warp walks the whole list and
+                // applies the entries of the clusters it owns (j % 4 == wq), so
+                // each cluster's updates land in row order from one warp.
+                int* qn = cnt;                                                   // [4] counts
+                uint8_t* lst = reinterpret_cast<uint8_t*>(cnt + 4);              // [4][32 * P] slots
+                int8_t* nl = reinterpret_cast<int8_t*>(lst + 4 * 32 * P);        // [TROWS] new label
+                int8_t* ol = nl + C::TROWS;                                      // [TROWS] old label
+                int nq = 0;
+#pragma unroll
+                for (int h = 0; h < P; ++h) {
+                    const bool ch = label[h] < K && label[h] != oldl[h];
+                    const unsigned fm = __ballot_sync(FULL, ch);
+                    if (ch) {
+                        const int slot = t * P + h;
+#pragma unroll
+                        for (int f = 0; f < D; ++f) work[(f / 32) * PR * 32 + slot * 32 + f % 32] = xval(h * D + f);
+                        nl[slot] = static_cast<int8_t>(label[h]);
+                        ol[slot] = static_cast<int8_t>(oldl[h]);
+                        lst[wq * 32 * P + nq + __popc(fm & ((1u << lane) - 1u))] = static_cast<uint8_t>(slot);
+                    }
+                    nq += __popc(fm);
+                }
+                if (lane == 0) qn[wq] = nq;
+                tc::named_sync(bar_id, 128);
+                for (int w = 0; w < 4; ++w) {
+                    const int cw = qn[w];
+                    for (int i = 0; i < cw; ++i) {
+                        const int slot = lst[w * 32 * P + i];
+                        const int jn = nl[slot], jo = ol[slot];
+                        // features 2*lane, 2*lane+1 (same K-block: 32 is even)
+                        const float2 xv2 = lane < L ? *reinterpret_cast<const float2*>(
+                                                          work + ((2 * lane) / 32) * PR * 32 + slot * 32 + (2 * lane) % 32)
+                                                    : make_float2(0.f, 0.f);
+                        if (jn % 4 == wq && lane < L) {
+                            double2* a = reinterpret_cast<double2*>(acc + jn * D + 2 * lane);
+                            double2 v = *a;
+                            v.x += static_cast<double>(xv2.x);
+                            v.y += static_cast<double>(xv2.y);
+                            *a = v;
+                        }
+                        if (jo >= 0 && jo % 4 == wq && lane < L) {
+                            double2* a = reinterpret_cast<double2*>(acc + jo * D + 2 * lane);
+                            double2 v = *a;
+                            v.x -= static_cast<double>(xv2.x);
+                            v.y -= static_cast<double>(xv2.y);
+                            *a = v;
+                        }
+                        if (wq == 0) {
+#pragma unroll
+                            for (int u = 0; u < KL; ++u) {
+                                if (jn / 32 == u && lane == jn % 32) count_acc[u] += 1;
+                                if (jo >= 0 && jo / 32 == u && lane == jo % 32) count_acc[u] -= 1;
+                            }
+                        }
+                    }
+                }
+                // the next tile's split rewrites `work`: all warps must be done reading it
+                tc::named_sync(bar_id, 128);
+                continue;
+            }
 
             // ---------------- counting sort of the tile by label (groups vw = h*4 + wq)
             unsigned mine[P];
