@@ -3,7 +3,7 @@
  *
  * This is the drop-in boundary below the reference's C++ API (proj/include/dnd):
  * plain pointers, sizes and status codes, no torch or C++ types.  The C++
- * surface in include/dnd_b200/ and the Python mirror in paper_2007_13552_b200/
+ * surface in cpp/include/dnd/ and the Python mirror in paper_2007_13552_b200/
  * both sit on top of it; INTEGRATION.md shows the binding a maintainer adds.
  *
  * Conventions

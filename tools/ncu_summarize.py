@@ -75,11 +75,14 @@ def full(rep, prefix, algo_bytes=None):
         tot = sum(v for v, _ in stalls) or 1.0
         rd = float(m["dram__bytes_read.sum"][0].replace(",", ""))
         wr = float(m["dram__bytes_write.sum"][0].replace(",", ""))
-        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
         rd *= mult.get(m["dram__bytes_read.sum"][1], 1)
         wr *= mult.get(m["dram__bytes_write.sum"][1], 1)
         dur = float(m["gpu__time_duration.sum"][0].replace(",", ""))
-        dur_s = dur * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(m["gpu__time_duration.sum"][1], 1e-6)
+        # ncu prints the unit either spelled out ("msecond") or abbreviated ("ms")
+        tunit = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0,
+                 "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
+        dur_s = dur * tunit[m["gpu__time_duration.sum"][1]]
         out.setdefault("kernels", []).append({
             "kernel": name, "gpu_time_s": dur_s, "dram_bytes_read": rd, "dram_bytes_write": wr,
             "dram_bytes_per_launch": rd + wr, "dram_gbs": (rd + wr) / dur_s / 1e9,
