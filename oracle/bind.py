@@ -60,6 +60,7 @@ class Oracle:
         L.dno_kmeans_predict.argtypes = [_P, _i64, _i64, _P, _i32, _P]
         L.dno_moments_axis0.argtypes = [_P, _i64, _i64, _i32, _i64, _P, _P]
         L.dno_local_moments_axis0.argtypes = [_P, _i64, _i64, _P, _P, _P]
+        L.dno_welford_axis0_f32_continue.argtypes = [_P, _i64, _i64, _P, _P, _P]
         L.dno_kmeanspp_indices_f32.argtypes = [_P, _i64, _i64, _i32, _i32, _u64, _P]
         L.dno_lasso_fit.argtypes = [_P, _P, _i64, _i64, _i32, _f64, _i32, _f64, _P, _P, _P]
         L.dno_soft_threshold.argtypes = [_f64, _f64]
@@ -161,6 +162,17 @@ class Oracle:
         m2 = np.empty(m, np.float64)
         self.lib.dno_local_moments_axis0(_ptr(x), n, m, _ptr(c), _ptr(mean), _ptr(m2))
         return int(c[0]), mean, m2
+
+    def welford_stream(self, blocks, m):
+        """The reference's single-rank Welford (moments.cpp:100-114) over an
+        iterable of fp32 [rows x m] blocks, in order; returns (count, mean, m2)."""
+        cnt = np.zeros(1, np.int64)
+        mean = np.zeros(m, np.float64)
+        m2 = np.zeros(m, np.float64)
+        for b in blocks:
+            b = np.ascontiguousarray(b, np.float32)
+            self.lib.dno_welford_axis0_f32_continue(_ptr(b), b.shape[0], m, _ptr(cnt), _ptr(mean), _ptr(m2))
+        return int(cnt[0]), mean, m2
 
     def kmeanspp_indices(self, x, k, seed, p=1):
         x = np.ascontiguousarray(x, np.float32)

@@ -329,6 +329,21 @@ void dno_local_moments_axis0(const double* x, int64_t rows, int64_t m, int64_t* 
         for (int64_t i = 0; i < m; ++i) welford_update(x[k * m + i], &mean[i], &m2[i], k + 1);
 }
 
+/* moments.cpp:100-114 fed in row blocks: the same sequential welford_update
+ * chain as dno_local_moments_axis0 over rows [0, count_in + rows), continued
+ * from the state (count, mean, m2) of the rows already seen.  Lets a test run
+ * the reference's single-rank Welford over an array too large for host f64
+ * (cfg5, 100M x 32) one fp32 block at a time; the values are widened exactly. */
+void dno_welford_axis0_f32_continue(const float* x, int64_t rows, int64_t m, int64_t* count,
+                                    double* mean, double* m2) {
+    int64_t c = *count;
+    for (int64_t k = 0; k < rows; ++k) {
+        ++c;
+        for (int64_t i = 0; i < m; ++i) welford_update((double)x[k * m + i], &mean[i], &m2[i], c);
+    }
+    *count = c;
+}
+
 /* moments.cpp:91-98 */
 void dno_local_moments_flat(const double* x, int64_t numel, int64_t* count, double* mean,
                             double* m2) {

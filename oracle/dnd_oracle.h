@@ -69,6 +69,9 @@ void dno_kmeans_predict(const double* x, int64_t n, int64_t m, const double* cen
 /* moments.cpp:100-114 (axis 0 of a rows x m tile) */
 void dno_local_moments_axis0(const double* x, int64_t rows, int64_t m, int64_t* count,
                              double* mean, double* m2);
+/* moments.cpp:100-114 continued over fp32 row blocks (state in/out) */
+void dno_welford_axis0_f32_continue(const float* x, int64_t rows, int64_t m, int64_t* count,
+                                    double* mean, double* m2);
 /* moments.cpp:91-98 (flattened tile) */
 void dno_local_moments_flat(const double* x, int64_t numel, int64_t* count, double* mean,
                             double* m2);

@@ -71,7 +71,9 @@ def test_cdist_f32_shapes(comm, oracle, n, m):
     x = dnd.from_global(xh, (n, m), 0, comm)
     d = dnd.gather(dnd.cdist(x))
     ref = oracle.cdist(xh.astype(np.float64))
-    assert rel_dev(d, ref) <= 1e-5 * max(1.0, m / 18.0)
+    dev = rel_dev(d, ref)
+    print(f"cdist f32 n={n} m={m}: rel dev {dev:.3e}")
+    assert dev <= 1e-5
     assert np.all(np.diag(d) == 0.0)
 
 
@@ -85,12 +87,16 @@ def test_cdist_tensor_core_path(comm, oracle, n, ny, m):
     yh[3] = xh[9]
     x = dnd.from_global(xh, (n, m), 0, comm)
     y = dnd.from_global(yh, (ny, m), None, comm)
-    tol = 1e-5 * m / 18.0
+    tol = 1e-5  # BASELINE's distance gate, independent of m
     d = dnd.gather(dnd.cdist(x))
-    assert rel_dev(d, oracle.cdist(xh.astype(np.float64))) <= tol
+    dev = rel_dev(d, oracle.cdist(xh.astype(np.float64)))
+    print(f"cdist tc n={n} ny={ny} m={m}: self rel dev {dev:.3e}")
+    assert dev <= tol
     assert np.all(np.diag(d) == 0.0) and d[5, 77] == 0.0 and d[77, 5] == 0.0
     dxy = dnd.gather(dnd.cdist_xy(x, y))
-    assert rel_dev(dxy, oracle.cdist_xy(xh.astype(np.float64), yh.astype(np.float64))) <= tol
+    dev = rel_dev(dxy, oracle.cdist_xy(xh.astype(np.float64), yh.astype(np.float64)))
+    print(f"cdist tc n={n} ny={ny} m={m}: xy rel dev {dev:.3e}")
+    assert dev <= tol
     assert dxy[9, 3] == 0.0
 
 
