@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cdist", action="store_true", help="skip the secondary cdist (config 2) measurement")
+    ap.add_argument("--no-configs", action="store_true", help="skip the config 3-5 measurements")
     return ap.parse_args()
 
 
@@ -226,6 +227,153 @@ def cdist_cfg2(dnd, _lib, comm, stream, barrier, dist, local, world, peak):
                          "kernel": "cdist_tc_kernel<2,32> (tcgen05 3xTF32, TMA bulk-store epilogue)"}}
 
 
+def _timed_ms(call, reps, stream, barrier, dist, local):
+    """Mean ms per call of `reps` back-to-back calls, CUDA events on the
+    launching stream, max over ranks."""
+    import torch
+
+    call()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        call()
+    e1.record(stream)
+    barrier()
+    ms = e0.elapsed_time(e1) / reps
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def tf32_peak():
+    """Dense TF32 tensor-core peak measured on this pool (tools/tf32_peak.py ->
+    profiles/tf32_peak.json; MEASURED_PEAKS.json has no TF32 figure)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "tf32_peak.json")))
+        return float(d["tf32_tflops"]), "measured cuBLAS TF32 8192^3 burst (profiles/tf32_peak.json)"
+    except Exception:
+        return 1100.0, "nominal dense TF32 (no measurement found)"
+
+
+def loop_kernel_roofline(dnd, _lib, comm, x, k, iters, seed, barrier, dist, local, flush, peak):
+    """Roofline of the k-means loop kernel: CUDA event nodes around its
+    launch(es) inside one more fit graph (same stream and buffers as the timed
+    fits), bytes = this rank's X read once per iteration."""
+    import ctypes as C
+
+    import torch
+
+    L = _lib.lib()
+    _lib.check(L.dndc_kmeans_assign_timing(comm.handle, 1))
+    barrier()
+    flush.fill_(0x5A)
+    dnd.kmeans_fit(x, k, iters, 0.0, seed)
+    barrier()
+    tot_ms, n_launch = C.c_double(), C.c_int()
+    _lib.check(L.dndc_kmeans_last_assign_ms(comm.handle, C.byref(tot_ms), C.byref(n_launch)))
+    _lib.check(L.dndc_kmeans_assign_timing(comm.handle, 0))
+    avg_ms = tot_ms.value / max(n_launch.value, 1)
+    if dist:
+        t = torch.tensor([avg_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        avg_ms = float(t.item())
+    iters_per_launch = iters / max(n_launch.value, 1)
+    byt = float(x.tile.shape[0]) * x.shape[1] * 4 * iters_per_launch
+    L.dndc_kmeans_last_kernel.restype = C.c_char_p
+    kname = L.dndc_kmeans_last_kernel(comm.handle).decode() or "per-iteration launches"
+    achieved = byt / (avg_ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "kernel": kname, "algorithmic_bytes_per_launch": byt, "avg_launch_ms": avg_ms,
+            "launches_timed": n_launch.value, "iterations_per_launch": iters_per_launch}
+
+
+def secondary_configs(dnd, _lib, comm, stream, barrier, dist, local, world, peak, flush):
+    """BASELINE configs 3-5 at full size, split over the ranks of this run
+    (strong scaling: the global problem is fixed), each with its roofline."""
+    import torch
+
+    out = {}
+    # ---- config 3: k-means k=64, 20 iterations on 50M x 64 (12.8 GB)
+    try:
+        n3, m3, k3, it3 = 50_000_000, 64, 64, 20
+        x3 = dnd.random_uniform((n3, m3), 0, SEED, comm)
+        ms = _timed_ms(lambda: dnd.kmeans_fit(x3, k3, it3, 0.0, SEED), 3, stream, barrier, dist, local)
+        roof = loop_kernel_roofline(dnd, _lib, comm, x3, k3, it3, SEED, barrier, dist, local, flush, peak)
+        byt_it = 4.0 * n3 * m3
+        out["kmeans_cfg3"] = {
+            "metric": "k-means Lloyd iters/s (config 3: 50M x 64 fp32, k=64, 20 iters/fit, split=0)",
+            "value": it3 / (ms * 1e-3), "unit": "iters/s", "ms_per_fit": ms, "n_gpus": world,
+            "iteration_us": ms * 1e3 / it3,
+            "iteration_frac_of_hbm_floor": (byt_it / (peak * world * 1e9)) / (ms * 1e-3 / it3),
+            "flops_per_iteration": 2.0 * n3 * k3 * m3, "roofline": roof,
+            "shard": f"{n3 // world} rows per GPU ({'the 1/8 shard of p=8 x ' + str(8 // world) if world < 8 else 'p=8 shard'})"}
+        del x3
+    except Exception as exc:
+        out["kmeans_cfg3"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    torch.cuda.empty_cache()
+    # ---- config 4: cdist 100k x 1024 vs 100k x 1024 (tensor cores, 3xTF32)
+    try:
+        n4, m4 = 100_000, 1024
+        xa = dnd.random_uniform((n4, m4), 0, 42, comm)
+        ya = dnd.random_uniform((n4, m4), 0, 43, comm)
+        o4 = torch.empty((xa.tile.shape[0], n4), dtype=torch.float32, device=xa.tile.device)
+        L = _lib.lib()
+
+        def call4():
+            _lib.check(L.dndc_cdist_xy_ring_f32(comm.handle, xa.tile.data_ptr(), xa.tile.shape[0],
+                                                ya.tile.data_ptr(), ya.tile.shape[0], n4, m4, o4.data_ptr()))
+
+        ms = _timed_ms(call4, 3, stream, barrier, dist, local)
+        flops = 2.0 * n4 * n4 * m4
+        tf, tf_src = tf32_peak()
+        useful = flops / (ms * 1e-3) / 1e12
+        peak3 = tf * world / 3.0
+        out["cdist_cfg4"] = {
+            "metric": "cdist TFLOP/s (config 4: X, Y 100k x 1024 fp32, split=0, Y shards on the ring)",
+            "value": useful, "unit": "TFLOP/s (useful fp32, 2*nx*ny*d)", "ms_per_call": ms, "n_gpus": world,
+            "gbs_output": 4.0 * n4 * n4 / (ms * 1e-3) / 1e9,
+            "roofline": {"bound": "tensor", "achieved": useful, "peak": peak3, "unit": "TFLOP/s", "frac": useful / peak3,
+                         "peak_source": f"{tf_src} / 3 (3xTF32: three TF32 MMAs per useful product) x {world} GPU(s)",
+                         "tf32_issued_tflops": 3 * useful,
+                         "kernel": "cdist_tc_kernel<2,32> (tcgen05 3xTF32, TMA bulk-store epilogue)"}}
+        del o4, xa, ya
+    except Exception as exc:
+        out["cdist_cfg4"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    torch.cuda.empty_cache()
+    # ---- config 5: moments + k-means++ (k=8) on 100M x 32 (12.8 GB)
+    try:
+        n5, m5 = 100_000_000, 32
+        a5 = dnd.random_uniform((n5, m5), 0, SEED, comm)
+        ms = _timed_ms(lambda: dnd.moments_axis0(a5), 5, stream, barrier, dist, local)
+        byt = 4.0 * n5 * m5
+        gbs = byt / (ms * 1e-3) / 1e9
+        out["moments_cfg5"] = {
+            "metric": "mean+variance along split axis 0 GB/s (config 5: 100M x 32 fp32)", "value": gbs,
+            "unit": "GB/s", "ms_per_call": ms, "n_gpus": world,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak * world, "unit": "GB/s",
+                         "frac": gbs / (peak * world), "algorithmic_bytes": byt,
+                         "kernel": "moments_partial_v4_kernel (one read of X, f64 shifted sums + Chan merges)"}}
+        ms = _timed_ms(lambda: dnd.kmeanspp_indices(a5, 8, SEED), 2, stream, barrier, dist, local)
+        byt = 7.0 * (4.0 * n5 * m5 + 16.0 * n5)
+        gbs = byt / (ms * 1e-3) / 1e9
+        out["kmeanspp_cfg5"] = {
+            "metric": "k-means++ seeding k=8 (config 5: 100M x 32 fp32)", "value": ms, "unit": "ms",
+            "higher_is_better": False, "n_gpus": world, "gbs": gbs,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak * world, "unit": "GB/s",
+                         "frac": gbs / (peak * world),
+                         "algorithmic_bytes": byt, "bytes_rule": "(k-1) D^2 passes x (X read + f64 D^2 read/write)",
+                         "kernel": "kpp_update_kernel (fused D^2 update + block sums)"}}
+        del a5
+    except Exception as exc:
+        out.setdefault("moments_cfg5", {"error": f"{type(exc).__name__}: {exc}"[:300]})
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
 
@@ -323,45 +471,30 @@ def run_ours(args):
     xe, dev_x = xe[0], dev[0]
     del dev
 
-    # ---- roofline of the dominant kernel (fused assign + accumulate): every
-    # launch of it inside one more fit, timed by CUDA event nodes recorded
-    # around it in the fit's graph (same stream, same buffers as the timed fits)
+    # ---- roofline of the dominant kernel (the k-means loop kernel), event
+    # nodes around its launch(es) inside one more fit graph
     import ctypes as C
 
     L = _lib.lib()
-    _lib.check(L.dndc_kmeans_assign_timing(comm.handle, 1))
-    barrier()
-    flush.fill_(0x5A)
-    dnd.kmeans_fit(x, K, ITERS, 0.0, SEED)
-    barrier()
-    tot_ms, n_launch = C.c_double(), C.c_int()
-    _lib.check(L.dndc_kmeans_last_assign_ms(comm.handle, C.byref(tot_ms), C.byref(n_launch)))
-    _lib.check(L.dndc_kmeans_assign_timing(comm.handle, 0))
-    avg_ms = tot_ms.value / max(n_launch.value, 1)
-    if dist:
-        t = torch.tensor([avg_ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        avg_ms = float(t.item())
-    byt = float(x.tile.shape[0]) * N_FEAT * 4  # algorithmic: this rank's X read once per launch
-    # the same kernel with every row accumulated (iteration 0's mode), timed alone
-    ms_full, byt_full = C.c_double(), C.c_double()
-    _lib.check(L.dndc_kmeans_time_assign_f32(comm.handle, x.tile.data_ptr(), x.tile.shape[0], N_FEAT, K, 20,
-                                             C.byref(ms_full), C.byref(byt_full)))
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs")
     peak_src = "measured" if peak else "fallback"
     peak = peak or 6650.0
-    achieved = byt / (avg_ms * 1e-3) / 1e9
+    roof = loop_kernel_roofline(dnd, _lib, comm, x, K, ITERS, SEED, barrier, dist, local, flush, peak)
+    # the per-iteration kernel with every row accumulated (iteration 0's mode), timed alone
+    ms_full, byt_full = C.c_double(), C.c_double()
+    _lib.check(L.dndc_kmeans_time_assign_f32(comm.handle, x.tile.data_ptr(), x.tile.shape[0], N_FEAT, K, 20,
+                                             C.byref(ms_full), C.byref(byt_full)))
     iter_us = t_ms * 1e3 / (ITERS * args.steps)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(), "kernel": "kmeans_small_kernel<18,8> (fused assign + accumulate)",
-            "algorithmic_bytes_per_launch": byt, "avg_launch_ms": avg_ms, "launches_timed": n_launch.value,
-            "timing": "CUDA event nodes around each of the 20 launches inside one fit graph (iteration 0 "
-                      "accumulates every row, later ones only rows whose label changed)",
-            "full_accumulate_launch_ms": ms_full.value,
-            "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json copy bandwidth)",
-            "iteration_us": iter_us,
-            "iteration_frac_of_hbm_floor": (byt / (peak * 1e9)) / (iter_us * 1e-6)}
+    byt = float(x.tile.shape[0]) * N_FEAT * 4
+    roof.update({"traffic": ncu_traffic(),
+                 "timing": "CUDA event nodes around the k-means loop kernel launch(es) inside one fit graph on "
+                           "the fit's stream (iterations 0-1 accumulate every row, later ones only rows whose "
+                           "label changed)",
+                 "per_iteration_kernel_full_accumulate_ms": ms_full.value,
+                 "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json copy bandwidth)",
+                 "iteration_us": iter_us,
+                 "iteration_frac_of_hbm_floor": (byt / (peak * 1e9)) / (iter_us * 1e-6)})
 
     # ---- secondary metric of BASELINE.json: cdist GB/s on config 2 (X, Y
     # 200k x 18 fp32 split over the ranks, Y's shards travelling the ring);
@@ -376,6 +509,10 @@ def run_ours(args):
             cdist = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         torch.cuda.empty_cache()
 
+    configs = None
+    if not args.no_configs:
+        configs = secondary_configs(dnd, _lib, comm, stream, barrier, dist, local, world, peak, flush)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline()
@@ -388,6 +525,7 @@ def run_ours(args):
             "cpu_baseline": cpu, "clocks": clk, "refined_rows_last_fit": model.refined_rows,
             "stats_exchange": comm.transport if world > 1 else "single GPU (fused in-kernel update)",
             "cdist_cfg2": cdist,
+            **(configs or {}),
             "final_inertia": model.inertia_trace[-1],
         }))
     if dist:

@@ -5,11 +5,10 @@
 #include <cstdint>
 #include <vector>
 
+#include "dnd/common.hpp"
 #include "dnd/errors.hpp"
 
 namespace dnd {
-
-using index_t = std::int64_t;
 
 struct ChunkMap {
     std::vector<index_t> offsets;

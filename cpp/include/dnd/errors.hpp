@@ -20,6 +20,16 @@ struct ValueError : Error {
 struct TransportError : Error {
     using Error::Error;
 };
+/// A blocking transport operation exceeded the deadlock-detection timeout
+/// (errors.hpp:27-31; DND_TIMEOUT_SECS, transport.cpp:14-23).
+struct TimeoutError : TransportError {
+    using TransportError::TransportError;
+};
+/// Ranks diverged in their sequence of collective calls, or a payload did not
+/// match the receiver's type (errors.hpp:33-37).
+struct OrderingError : TransportError {
+    using TransportError::TransportError;
+};
 /// Malformed containers and file I/O failures (errors.hpp:40).
 struct DataError : Error {
     using Error::Error;
@@ -36,6 +46,8 @@ inline void check(int rc) {
     switch (rc) {
         case DNDC_EVALUE: throw ValueError(msg);
         case DNDC_ETRANSPORT: throw TransportError(msg);
+        case DNDC_ETIMEOUT: throw TimeoutError(msg);
+        case DNDC_EORDERING: throw OrderingError(msg);
         case DNDC_ECUDA: throw DeviceError(msg);
         case DNDC_EDATA: throw DataError(msg);
         default: throw Error(msg);

@@ -211,6 +211,91 @@ DndArray<T> from_global(const std::vector<T>& data, std::vector<index_t> shape, 
     return a;
 }
 
+/// Array whose element at global index idx is fn(idx) (ndarray.hpp:118-144):
+/// evaluated on the host for this rank's slab only, then copied to its shard.
+/// (Elementwise ops are outside the GPU hot path.)
+template <typename T, typename F>
+DndArray<T> generate(std::vector<index_t> shape, std::optional<int> split, const Communicator& comm, F fn) {
+    auto a = detail::empty_like_shape<T>(shape, split, comm);
+    const std::vector<index_t>& lshape = a.lshape();
+    const index_t count = detail::product(lshape);
+    if (count == 0) return a;
+    index_t off = 0;
+    if (split) off = chunk_map(shape[static_cast<std::size_t>(*split)], comm.size()).offset(comm.rank());
+    std::vector<T> local(static_cast<std::size_t>(count));
+    std::vector<index_t> idx(shape.size(), 0);
+    for (index_t e = 0; e < count; ++e) {
+        index_t rem = e;
+        for (std::size_t d = shape.size(); d-- > 0;) {
+            idx[d] = rem % lshape[d];
+            rem /= lshape[d];
+        }
+        if (split) idx[static_cast<std::size_t>(*split)] += off;
+        local[static_cast<std::size_t>(e)] = fn(static_cast<const std::vector<index_t>&>(idx));
+    }
+    detail::check(dndc_memcpy(comm.handle(), a.device_data(), local.data(), local.size() * sizeof(T), DNDC_COPY_H2D));
+    return a;
+}
+
+/// Constant array (ndarray.hpp:97-112).
+template <typename T>
+DndArray<T> full(std::vector<index_t> shape, T value, std::optional<int> split, const Communicator& comm) {
+    return generate<T>(std::move(shape), split, comm, [value](const std::vector<index_t>&) { return value; });
+}
+template <typename T>
+DndArray<T> zeros(std::vector<index_t> shape, std::optional<int> split, const Communicator& comm) {
+    return full<T>(std::move(shape), T(0), split, comm);
+}
+template <typename T>
+DndArray<T> ones(std::vector<index_t> shape, std::optional<int> split, const Communicator& comm) {
+    return full<T>(std::move(shape), T(1), split, comm);
+}
+
+/// 0, 1, ..., n-1 (ndarray.hpp:146-151).
+template <typename T>
+DndArray<T> arange(index_t n, std::optional<int> split, const Communicator& comm) {
+    return generate<T>({n}, split, comm, [](const std::vector<index_t>& idx) { return static_cast<T>(idx[0]); });
+}
+
+/// (rows, m) array whose every row equals `row` (ndarray.hpp:191-200).
+template <typename T>
+DndArray<T> broadcast_row(const std::vector<T>& row, index_t rows, std::optional<int> split,
+                          const Communicator& comm) {
+    return generate<T>({rows, static_cast<index_t>(row.size())}, split, comm,
+                       [&row](const std::vector<index_t>& idx) { return row[static_cast<std::size_t>(idx[1])]; });
+}
+
+/// fn applied to every element (ndarray.hpp:204-209), through the host.
+template <typename T, typename F>
+DndArray<T> map_elementwise(const DndArray<T>& a, F fn) {
+    Tile<T> t = a.tile();
+    for (auto& v : t.data) v = fn(v);
+    auto b = detail::empty_like_shape<T>(a.shape(), a.split(), a.comm());
+    if (!t.data.empty())
+        detail::check(dndc_memcpy(a.comm().handle(), b.device_data(), t.data.data(), t.data.size() * sizeof(T),
+                                  DNDC_COPY_H2D));
+    return b;
+}
+
+/// fn of two equally shaped and split arrays (ndarray.hpp:211-225).
+template <typename T, typename F>
+DndArray<T> zip_elementwise(const DndArray<T>& a, const DndArray<T>& b, F fn) {
+    if (a.shape() != b.shape())
+        throw ValueError("zip_elementwise: shape mismatch " + detail::shape_string(a.shape()) + " vs " +
+                         detail::shape_string(b.shape()));
+    if (a.split() != b.split()) throw ValueError("zip_elementwise: split mismatch");
+    if (!a.comm().congruent(b.comm()))
+        throw ValueError("zip_elementwise: operands live on different communicators");
+    Tile<T> t = a.tile();
+    const Tile<T> u = b.tile();
+    for (std::size_t i = 0; i < t.data.size(); ++i) t.data[i] = fn(t.data[i], u.data[i]);
+    auto c = detail::empty_like_shape<T>(a.shape(), a.split(), a.comm());
+    if (!t.data.empty())
+        detail::check(dndc_memcpy(a.comm().handle(), c.device_data(), t.data.data(), t.data.size() * sizeof(T),
+                                  DNDC_COPY_H2D));
+    return c;
+}
+
 /// Full global content, identical on every rank (ndarray.hpp:389-393).
 template <typename T>
 std::vector<T> gather(const DndArray<T>& a) {

@@ -5,17 +5,9 @@
 #include <cstdint>
 #include <vector>
 
+#include "dnd/common.hpp"
+
 namespace dnd {
-
-using index_t = std::int64_t;
-
-namespace detail {
-inline index_t product(const std::vector<index_t>& v) {
-    index_t p = 1;
-    for (index_t e : v) p *= e;
-    return p;
-}
-}  // namespace detail
 
 template <typename T>
 struct Tile {

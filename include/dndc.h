@@ -36,6 +36,8 @@ extern "C" {
 #define DNDC_ECUDA 3      /* CUDA runtime / launch failure */
 #define DNDC_EINTERNAL 4
 #define DNDC_EDATA 5      /* dnd::DataError (errors.hpp:40): file I/O and container format */
+#define DNDC_ETIMEOUT 6   /* dnd::TimeoutError (errors.hpp:27-31): a rank did not arrive (DND_TIMEOUT_SECS) */
+#define DNDC_EORDERING 7  /* dnd::OrderingError (errors.hpp:33-37): ranks entered different collectives */
 
 #define DNDC_UNIQUE_ID_BYTES 128
 
@@ -60,6 +62,21 @@ const char* dndc_last_error(void);
 int dndc_unique_id(void* id_out /* DNDC_UNIQUE_ID_BYTES */);
 int dndc_create(int device, int rank, int world, const void* unique_id, dndc_ctx** out);
 int dndc_destroy(dndc_ctx* ctx);
+
+/* Ranks that share GPUs (world > visible GPUs, e.g. the reference's tests run
+ * run_world(3..5) on one GPU; transport.hpp:222-223): the ranks are threads of
+ * one process joined by a host loopback group instead of NCCL.  Device
+ * collectives are staged through host memory with the reference's loopback
+ * semantics (transport.cpp:64-150): rank-order folds, DNDC_EORDERING when
+ * ranks enter different collectives at the same call index, DNDC_ETIMEOUT
+ * after timeout_ms (DND_TIMEOUT_SECS), DNDC_ETRANSPORT after
+ * dndc_group_abort (a failing rank wakes its peers, transport.cpp:174-192).
+ * The group outlives its contexts; destroy it after them. */
+typedef struct dndc_group dndc_group;
+int dndc_group_create(int world, int64_t timeout_ms, dndc_group** out);
+int dndc_group_destroy(dndc_group* g);
+int dndc_group_abort(dndc_group* g);
+int dndc_create_in_group(int device, int rank, dndc_group* group, int world, dndc_ctx** out);
 int dndc_set_stream(dndc_ctx* ctx, void* cuda_stream);
 int dndc_rank(const dndc_ctx* ctx);
 /* How the k-means stats exchange travels for world > 1: "nvlink peer exchange"
@@ -230,6 +247,15 @@ int dndc_kmeans_step_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m, co
 /* Statistics of the most recent kmeans_fit/predict on this context: rows whose
  * fp32 top-2 gap fell inside the error bound and were re-decided in f64. */
 int dndc_kmeans_last_refined(const dndc_ctx* ctx, int64_t* rows_refined);
+
+/* Name of the kernel that ran the Lloyd loop of the most recent kmeans_fit
+ * ("" when it was the per-iteration launch sequence); static storage. */
+const char* dndc_kmeans_last_kernel(const dndc_ctx* ctx);
+/* Diagnostics: %globaltimer marks of the last persistent fit run with the
+ * environment variable DNDC_PERSIST_TRACE set ([iteration][2*grid + 2]:
+ * per-CTA tiles-done, per-CTA barrier-passed, CTA 0 start, CTA 0 update-done);
+ * returns the number of marks copied (0 when none were recorded). */
+int64_t dndc_kmeans_persist_trace(dndc_ctx* ctx, unsigned long long* out_host, int64_t cap, int* grid);
 
 /* Measurement hook for bench.py's roofline: average duration of `reps`
  * back-to-back launches of the fused assign/accumulate kernel alone (CUDA

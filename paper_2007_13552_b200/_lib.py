@@ -16,11 +16,20 @@ LIB_PATH = os.environ.get("DNDC_LIB_PATH") or os.path.join(HERE, "libdndc.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "dndc.h")
 
 DNDC_OK, DNDC_EVALUE, DNDC_ETRANSPORT, DNDC_ECUDA, DNDC_EINTERNAL, DNDC_EDATA = 0, 1, 2, 3, 4, 5
+DNDC_ETIMEOUT, DNDC_EORDERING = 6, 7
 UNIQUE_ID_BYTES = 128
 
 
 class TransportError(RuntimeError):
     """dnd::TransportError (errors.hpp:21-25)."""
+
+
+class TimeoutError_(TransportError):
+    """dnd::TimeoutError (errors.hpp:27-31): a rank did not arrive in time."""
+
+
+class OrderingError(TransportError):
+    """dnd::OrderingError (errors.hpp:33-37): ranks entered different collectives."""
 
 
 class DataError(RuntimeError):
@@ -90,8 +99,15 @@ _SIGS = {
     "dndc_moments_axis0_f32": [_P, _P, _i64, _i64, _P, _P, _P],
     "dndc_moments_axis0_f64": [_P, _P, _i64, _i64, _P, _P, _P],
     "dndc_kmeanspp_indices_f32": [_P, _P, _i64, _i64, _i64, _i32, _u64, _P],
+    "dndc_kmeans_last_kernel": [_P],
+    "dndc_kmeans_persist_trace": [_P, _P, _i64, _P],
+    "dndc_group_create": [_i32, _i64, C.POINTER(_P)],
+    "dndc_group_destroy": [_P],
+    "dndc_group_abort": [_P],
+    "dndc_create_in_group": [_i32, _i32, _P, _i32, C.POINTER(_P)],
 }
-_RESTYPE = {"dndc_last_error": C.c_char_p, "dndc_launch_count": C.c_uint64, "dndc_transport_status": C.c_char_p}
+_RESTYPE = {"dndc_last_error": C.c_char_p, "dndc_launch_count": C.c_uint64, "dndc_transport_status": C.c_char_p,
+            "dndc_kmeans_last_kernel": C.c_char_p, "dndc_kmeans_persist_trace": C.c_int64}
 
 
 def header_symbols() -> list[str]:
@@ -130,4 +146,8 @@ def check(rc: int) -> None:
         raise TransportError(msg)
     if rc == DNDC_EDATA:
         raise DataError(msg)
+    if rc == DNDC_ETIMEOUT:
+        raise TimeoutError_(msg)
+    if rc == DNDC_EORDERING:
+        raise OrderingError(msg)
     raise DeviceError(f"libdndc error {rc}: {msg}")

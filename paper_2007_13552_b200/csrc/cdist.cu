@@ -443,6 +443,16 @@ void cdist_ring(dndc_ctx* ctx, const T* x_local, int64_t nx_local, const T* y_lo
         if (more) {
             const int src_origin = (origin + p - 1) % p;
             const int64_t in_rows = yext[src_origin];
+            if (ctx->group) {
+                // ranks sharing GPUs: the packet travels through host memory, before this round's tile
+                std::vector<XSend> xs;
+                std::vector<XRecv> xr;
+                if (rows > 0) xs.push_back({(r + 1) % p, buf[cur], static_cast<size_t>(rows * (m + 1)) * sizeof(T)});
+                if (in_rows > 0)
+                    xr.push_back({(r + p - 1) % p, buf[1 - cur], static_cast<size_t>(in_rows * (m + 1)) * sizeof(T)});
+                xport_exchange(ctx, xs, xr, s);
+                DNDC_CUDA(cudaEventRecord(ctx->ev_b, s));
+            } else {
             DNDC_CUDA(cudaEventRecord(ctx->ev_a, s));
             DNDC_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
             DNDC_NCCL(ncclGroupStart());
@@ -453,6 +463,7 @@ void cdist_ring(dndc_ctx* ctx, const T* x_local, int64_t nx_local, const T* y_lo
                                    ctx->comm_stream));
             DNDC_NCCL(ncclGroupEnd());
             DNDC_CUDA(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
+            }
             ctx->counters.sendrecvs++;
         }
         cdist_tile<T>(ctx, x_local, xn, nx_local, buf[cur], buf[cur] + rows * m, rows, m, out,

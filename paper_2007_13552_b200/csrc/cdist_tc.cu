@@ -11,10 +11,13 @@
 //   warp 1      TMEM allocator + MMA issuer: per K=8 step three
 //               tcgen05.mma.kind::tf32 (M=128, N=256): hi.hi + hi.lo + lo.hi into
 //               a 128x256 fp32 TMEM accumulator (double-buffered: 512 columns).
-//   (lo = x - trunc_tf32(x) is made once per operand by split_lo_kernel and
-//    loaded by TMA next to the raw tile, which is the hi operand: the tensor
-//    core truncates fp32 to tf32 -- pinned by tests/test_gpu_tc.py.  Splitting
-//    in shared memory per tile cost as much smem bandwidth as the MMAs.)
+//   (both operands are first centred on a common mu (centre_sample_kernel):
+//    hi = fl(x - mu) and lo = hi - trunc_tf32(hi) are made once per operand by
+//    centre_split_kernel into 16-byte-pitched copies and loaded by TMA side by
+//    side; the tensor core truncates hi to tf32 itself -- pinned by
+//    tests/test_gpu_tc.py.  Centring keeps the norms and dot products small, so
+//    the fp32 accumulation over K stays inside BASELINE's 1e-5 gate at d = 1024.
+//    Splitting in shared memory per tile cost as much smem bandwidth as the MMAs.)
 //   warps 6-13  epilogue: tcgen05.ld of each accumulator row, then
 //               d = sqrt(max(xn + yn - 2g, 0)) into swizzled smem boxes written
 //               by TMA bulk stores (+ the self block's zero diagonal); rows
@@ -24,6 +27,7 @@
 // cancel to exactly 0, as in the reference.
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "tc.cuh"
@@ -72,6 +76,8 @@ struct CdtcParams {
     int m;
     const float* xn;   // norms (null in NORM mode)
     const float* yn;
+    const float* xd;   // norm-bias model (null: off): tensor-core norm minus the f64-exact one
+    const float* yd;
     float* out;        // distances (DIST) or norms (NORM)
     int64_t ld, col_off, diag_offset;
     bool vec;
@@ -213,6 +219,7 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
             tc::tc_fence_after();
             const int64_t gi = row0 + r;
             const float xni = gi < p.nx ? __ldg(p.xn + gi) : 0.f;
+            const float xdi = (p.xd && gi < p.nx) ? __ldg(p.xd + gi) : 0.f;
             const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * BN;
             const bool diag = p.diag_offset >= 0 && col0 < row0 + p.diag_offset + BM &&
                               row0 + p.diag_offset < col0 + BN;
@@ -245,6 +252,27 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 for (int u = 0; u < BC / 4; ++u) ycur[u] = ynext[u];
                 if (cc + nsub < NCH) load_yn(gc + BC * nsub, ynext);
                 float d[BC];
+                if (p.xd) {
+                    // norm-bias model (large d): s = a + b - 2g with the tensor-core
+                    // norms a, b (so an exact duplicate gives s == 0), then
+                    // s += (t - 1)(da + db), t = 2g / (a + b) clamped to [-1, 1],
+                    // da, db = tensor-core minus f64-exact norms: the accumulation
+                    // bias of g is modelled as t times the norms' (t = 1 for a
+                    // duplicate, ~0 for unrelated centred rows -> exact norms)
+#pragma unroll
+                    for (int j = 0; j < BC; ++j) {
+                        const int64_t cj = gc + j;
+                        const float ynj = reinterpret_cast<const float*>(ycur)[j];
+                        const float ydj = cj < p.ny ? __ldg(p.yd + cj) : 0.f;
+                        const float ab = xni + ynj;
+                        float sq = fmaf(-2.f, v[j], ab);
+                        if (sq != 0.f) {
+                            const float t = fminf(fmaxf(__fdividef(2.f * v[j], ab), -1.f), 1.f);
+                            sq = fmaf(t - 1.f, xdi + ydj, sq);
+                        }
+                        d[j] = sqrt_approx(fmaxf(sq, 0.f));
+                    }
+                } else {
 #pragma unroll
                 for (int j = 0; j < BC; j += 4) {
                     const float4 yv = ycur[j / 4];
@@ -256,6 +284,7 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                     d[j + 1] = sqrt_approx(fmaxf(s0.y, 0.f));
                     d[j + 2] = sqrt_approx(fmaxf(s1.x, 0.f));
                     d[j + 3] = sqrt_approx(fmaxf(s1.y, 0.f));
+                }
                 }
                 if (diag) {
 #pragma unroll
@@ -319,6 +348,7 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 }
             } else {
                 const float xni = gi < p.nx ? __ldg(p.xn + gi) : 0.f;
+                const float xdi = (p.xd && gi < p.nx) ? __ldg(p.xd + gi) : 0.f;
                 float* orow = p.out + gi * p.ld + p.col_off + col0;
                 const bool full_cols = col0 + BN <= p.ny;
 #pragma unroll 1
@@ -331,8 +361,13 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const float ynj = (c0 + i < p.ny) ? __ldg(p.yn + c0 + i) : 0.f;
-                        const float sq = fmaxf(fmaf(-2.f, v[i], xni + ynj), 0.f);
-                        d[i] = sqrt_approx(sq);
+                        float sq = fmaf(-2.f, v[i], xni + ynj);
+                        if (p.xd && sq != 0.f) {  // norm-bias model, as in MODE 2
+                            const float ydj = (c0 + i < p.ny) ? __ldg(p.yd + c0 + i) : 0.f;
+                            const float t = fminf(fmaxf(__fdividef(2.f * v[i], xni + ynj), -1.f), 1.f);
+                            sq = fmaf(t - 1.f, xdi + ydj, sq);
+                        }
+                        d[i] = sqrt_approx(fmaxf(sq, 0.f));
                         if (p.diag_offset >= 0 && c0 + i == gi + p.diag_offset) d[i] = 0.f;
                     }
                     float* o = orow + c16 * 16;
@@ -374,49 +409,114 @@ bool cdist_tc_eligible(int64_t nx, int64_t ny, int64_t m) {
     return m >= 256 || (m <= BK_SMALL && nx * ny >= (int64_t{1} << 26));
 }
 
-// Padded view for TMA: row pitch must be a multiple of 16 bytes.
-// (m = 18 rows are 72 B apart: a pitched copy with 16-byte-multiple pitch; the
-// pad columns are never read -- the tensor map has m columns, TMA zero-fills)
+// Centre of the operands: mu_f = (mean over <= 256 rows of x sampled evenly +
+// the same over y) / 2, f64 sums rounded once to fp32.  Any mu gives the same
+// distances in exact arithmetic (|x - y| = |(x - mu) - (y - mu)|); a mu near the
+// data's centre keeps the norms and the dot products small, and with them the
+// fp32 rounding of the tensor-core accumulation over K (cfg4: 1.6e-5 of
+// relative error with raw [0,1) data at d = 1024, against BASELINE's 1e-5 gate).
+__global__ void centre_sample_kernel(const float* __restrict__ x, int64_t nx, const float* __restrict__ y,
+                                     int64_t ny, int64_t m, float* __restrict__ mu, int64_t pitch) {
+    const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (f >= pitch) return;
+    if (f >= m) {
+        mu[f] = 0.f;
+        return;
+    }
+    auto mean = [&](const float* a, int64_t n) {
+        const int64_t ns = n < 256 ? n : 256;
+        double acc = 0.0;
+        for (int64_t s = 0; s < ns; ++s) acc += static_cast<double>(a[(s * n / ns) * m + f]);
+        return ns > 0 ? acc / static_cast<double>(ns) : 0.0;
+    };
+    mu[f] = static_cast<float>(0.5 * (mean(x, nx) + mean(y, ny)));
+}
+
+// hi = fl(x - mu) into a 16-byte-pitched matrix (TMA needs 16-byte row
+// pitches; pad columns 0) and lo = hi - trunc_tf32(hi): the 3xTF32 operands,
+// made once per operand (the tensor core truncates hi to tf32 itself).
+__global__ void centre_split_kernel(const float* __restrict__ src, int64_t rows, int64_t m,
+                                    const float* __restrict__ mu, int64_t pitch, float* __restrict__ hi,
+                                    float* __restrict__ lo) {
+    const int64_t total = rows * pitch;
+    if (m == pitch && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const int64_t total4 = total / 4, pitch4 = pitch / 4;
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total4;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
+            const float4 c = __ldg(reinterpret_cast<const float4*>(mu) + i % pitch4);
+            float4 h = make_float4(v.x - c.x, v.y - c.y, v.z - c.z, v.w - c.w);
+            float4 l;
+            l.x = h.x - __uint_as_float(__float_as_uint(h.x) & 0xFFFFE000u);
+            l.y = h.y - __uint_as_float(__float_as_uint(h.y) & 0xFFFFE000u);
+            l.z = h.z - __uint_as_float(__float_as_uint(h.z) & 0xFFFFE000u);
+            l.w = h.w - __uint_as_float(__float_as_uint(h.w) & 0xFFFFE000u);
+            reinterpret_cast<float4*>(hi)[i] = h;
+            reinterpret_cast<float4*>(lo)[i] = l;
+        }
+        return;
+    }
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / pitch, f = i % pitch;
+        const float h = f < m ? src[r * m + f] - mu[f] : 0.f;
+        hi[i] = h;
+        lo[i] = h - __uint_as_float(__float_as_uint(h) & 0xFFFFE000u);
+    }
+}
+
+// d[i] = a[i] - fl32(sum_f hi[i][f]^2 in f64): how far the tensor-core norm a
+// (3xTF32, fp32 accumulation over K) sits from the exact norm of the same
+// centred row; one warp per row.
+__global__ void norm_bias_kernel(const float* __restrict__ hi, int64_t rows, int64_t m, int64_t pitch,
+                                 const float* __restrict__ a, float* __restrict__ dout) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+        double acc = 0.0;
+        for (int64_t f = lane; f < m; f += 32) {
+            const double v = static_cast<double>(hi[r * pitch + f]);
+            acc = fma(v, v, acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) dout[r] = a[r] - static_cast<float>(acc);
+    }
+}
+
+// DNDC_CDTC_NORM=mma|model: the norm-bias model (see the epilogue) is on by
+// default from d >= 128 (at small d the plain formula is already ~1e-6).
+static bool use_norm_model(int64_t m) {
+    const char* v = std::getenv("DNDC_CDTC_NORM");
+    if (v && std::string(v) == "mma") return false;
+    if (v && std::string(v) == "model") return true;
+    return m >= 128;
+}
+
 struct TmaView {
     const float* p;
     int64_t pitch;  // elements
 };
-static TmaView tma_view(dndc_ctx* ctx, const char* slot, const float* src, int64_t rows, int64_t m, cudaStream_t s) {
-    if (m % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) return {src, m};
+
+struct TcOperand {
+    const float* hi;
+    const float* lo;
+    int64_t pitch;  // elements
+};
+
+static TcOperand tc_operand(dndc_ctx* ctx, const char* hname, const char* lname, const float* src, int64_t rows,
+                            int64_t m, const float* mu, cudaStream_t s) {
     const int64_t pitch = (m + 3) / 4 * 4;
-    float* dst = static_cast<float*>(ctx->slot(slot, sizeof(float) * std::max<int64_t>(rows, 1) * pitch));
-    if (rows > 0)
-        DNDC_CUDA(cudaMemcpy2DAsync(dst, pitch * sizeof(float), src, m * sizeof(float), m * sizeof(float), rows,
-                                    cudaMemcpyDeviceToDevice, s));
-    return {dst, pitch};
-}
-
-// lo = x - trunc_tf32(x) over a pitched fp32 matrix (pad columns included;
-// the tensor maps never read them): the 3xTF32 low operand, made once per
-// operand instead of per tile inside the kernel.
-__global__ void split_lo_kernel(const float4* __restrict__ src, int64_t count4, float4* __restrict__ dst) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count4;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const float4 v = __ldg(src + i);
-        float4 l;
-        l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-        l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-        l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-        l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-        dst[i] = l;
-    }
-}
-
-static TmaView lo_view(dndc_ctx* ctx, const char* slot, TmaView v, int64_t rows, cudaStream_t s) {
-    float* dst = static_cast<float*>(ctx->slot(slot, sizeof(float) * std::max<int64_t>(rows, 1) * v.pitch));
-    const int64_t count4 = rows * v.pitch / 4;
-    if (count4 > 0) {
-        const int grid = static_cast<int>(std::min<int64_t>(ceil_div(count4, 256), ctx->num_sms * 8));
-        split_lo_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(v.p), count4,
-                                             reinterpret_cast<float4*>(dst));
+    const size_t bytes = sizeof(float) * std::max<int64_t>(rows, 1) * pitch;
+    float* hi = static_cast<float*>(ctx->slot(hname, bytes));
+    float* lo = static_cast<float*>(ctx->slot(lname, bytes));
+    const int64_t work = rows * pitch / (pitch == m ? 4 : 1);
+    if (work > 0) {
+        const int grid = static_cast<int>(std::min<int64_t>(ceil_div(work, 256), ctx->num_sms * 8));
+        centre_split_kernel<<<grid, 256, 0, s>>>(src, rows, m, mu, pitch, hi, lo);
         DNDC_LAUNCHED(ctx);
     }
-    return {dst, v.pitch};
+    return {hi, lo, pitch};
 }
 
 void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, int64_t nx, const float* y,
@@ -425,12 +525,16 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     using namespace cdtc;
     (void)xn_unused;
     (void)yn_unused;
-    const TmaView xv = tma_view(ctx, "cdtc_x", x, nx, m, stream);
-    const TmaView yv = (y == x && ny == nx) ? xv : tma_view(ctx, "cdtc_y", y, ny, m, stream);
+    const bool same = y == x && ny == nx;
+    const int64_t pitch = (m + 3) / 4 * 4;
+    float* mu = static_cast<float*>(ctx->slot("cdtc_mu", sizeof(float) * pitch));
+    centre_sample_kernel<<<static_cast<int>(ceil_div(pitch, 128)), 128, 0, stream>>>(x, nx, y, ny, m, mu, pitch);
+    DNDC_LAUNCHED(ctx);
+    const TcOperand xo = tc_operand(ctx, "cdtc_x", "cdtc_xlo", x, nx, m, mu, stream);
+    const TcOperand yo = same ? xo : tc_operand(ctx, "cdtc_y", "cdtc_ylo", y, ny, m, mu, stream);
+    const TmaView xv{xo.hi, pitch}, yv{yo.hi, pitch}, xl{xo.lo, pitch}, yl{yo.lo, pitch};
     const float* xa = xv.p;
     const float* ya = yv.p;
-    const TmaView xl = lo_view(ctx, "cdtc_xlo", xv, nx, stream);
-    const TmaView yl = (ya == xa && ny == nx) ? xl : lo_view(ctx, "cdtc_ylo", yv, ny, stream);
     static bool attr = false;
     if (!attr) {
         DNDC_CUDA(cudaFuncSetAttribute(cdist_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -459,8 +563,22 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
         DNDC_LAUNCHED(ctx);
     };
     norms(xa, xl.p, xv.pitch, nx, xn);
-    if (ya == xa && ny == nx) DNDC_CUDA(cudaMemcpyAsync(yn, xn, sizeof(float) * nx, cudaMemcpyDeviceToDevice, stream));
+    if (same) DNDC_CUDA(cudaMemcpyAsync(yn, xn, sizeof(float) * nx, cudaMemcpyDeviceToDevice, stream));
     else norms(ya, yl.p, yv.pitch, ny, yn);
+    float* xd = nullptr;
+    float* yd = nullptr;
+    if (use_norm_model(m)) {
+        xd = static_cast<float*>(ctx->slot("cdtc_xd", sizeof(float) * std::max<int64_t>(nx, 1)));
+        yd = same ? xd : static_cast<float*>(ctx->slot("cdtc_yd", sizeof(float) * std::max<int64_t>(ny, 1)));
+        auto bias = [&](const float* hi, int64_t rows, const float* a, float* d) {
+            if (rows <= 0) return;
+            const int grid = static_cast<int>(std::min<int64_t>(ceil_div(rows * 32, 256), ctx->num_sms * 16));
+            norm_bias_kernel<<<grid, 256, 0, stream>>>(hi, rows, m, pitch, a, d);
+            DNDC_LAUNCHED(ctx);
+        };
+        bias(xa, nx, xn, xd);
+        if (!same) bias(ya, ny, yn, yd);
+    }
 
     const CUtensorMap mx = make_tmap_2d_f32(xa, nx, m, xv.pitch * 4, BK, BM, true);
     const CUtensorMap my = make_tmap_2d_f32(ya, ny, m, yv.pitch * 4, BK, BN, true);
@@ -472,6 +590,8 @@ void cdist_tile_tc_f32(dndc_ctx* ctx, const float* x, const float* xn_unused, in
     pp.m = static_cast<int>(m);
     pp.xn = xn;
     pp.yn = yn;
+    pp.xd = xd;
+    pp.yd = yd;
     pp.out = out;
     pp.ld = ld_out;
     pp.col_off = col_off;

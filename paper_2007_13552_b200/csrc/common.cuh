@@ -68,8 +68,11 @@ void destroy_kmeans_state(KMeansState*);
 }  // namespace dndc
 
 // --------------------------------------------------------------- context
+struct dndc_group;  // loopback.cu: ranks that share GPUs
+
 struct dndc_ctx {
     int device = 0, rank = 0, world = 1;
+    dndc_group* group = nullptr;        // host-staged transport (world > #GPUs), not owned
     int num_sms = 148;
     cudaStream_t stream = nullptr;      // work stream (user's or own)
     cudaStream_t own_stream = nullptr;  // created by dndc_create
@@ -79,6 +82,9 @@ struct dndc_ctx {
     dndc_counters counters{};
     uint64_t launches = 0;
     int64_t last_refined = 0;
+    const char* last_kernel = "";  // the k-means loop kernel of the last fit (kmeans.cu)
+    int64_t persist_trace_len = 0;  // DNDC_PERSIST_TRACE marks of the last persistent fit
+    int persist_trace_grid = 0;
     int km_slot = 0;  // constant-memory centroid table slot (kmeans.cu)
 
     // Growable device workspace, carved by named slots so repeated calls reuse
@@ -144,6 +150,25 @@ void chunk_map(int64_t n, int p, std::vector<int64_t>& off, std::vector<int64_t>
 void allgather_f64(dndc_ctx* ctx, const double* send, double* recv, size_t count,
                    cudaStream_t stream);
 void allreduce_sum_f64(dndc_ctx* ctx, double* buf, size_t count, cudaStream_t stream);
+
+// Transport primitives (loopback.cu): NCCL over NVLink when every rank owns a
+// GPU, host-staged through the rank group when ranks share GPUs.  Device
+// buffers, ordered on `s` (the group path synchronises).
+enum XportKind { XK_ALLGATHER = 1, XK_ALLREDUCE = 2, XK_BARRIER = 3 };
+struct XSend {
+    int peer;
+    const void* buf;
+    size_t bytes;
+};
+struct XRecv {
+    int peer;
+    void* buf;
+    size_t bytes;
+};
+void xport_allgather(dndc_ctx* ctx, const void* send, void* recv, size_t bytes, cudaStream_t s);
+void xport_allreduce_sum_f64(dndc_ctx* ctx, double* buf, size_t count, cudaStream_t s);
+void xport_exchange(dndc_ctx* ctx, const std::vector<XSend>& sends, const std::vector<XRecv>& recvs, cudaStream_t s);
+void xport_barrier(dndc_ctx* ctx);
 
 // ------------------------------------------------------------ device math
 __host__ __device__ inline uint64_t splitmix64(uint64_t x) {

@@ -34,11 +34,7 @@ int dndc_device_count(int* out) {
 
 int dndc_barrier(dndc_ctx* ctx) {
     return guard([&] {
-        if (ctx->world > 1) {
-            double* d = static_cast<double*>(ctx->slot("barrier", sizeof(double)));
-            DNDC_NCCL(ncclAllReduce(d, d, 1, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
-        }
-        DNDC_CUDA(cudaStreamSynchronize(ctx->stream));
+        dndc::xport_barrier(ctx);
         ctx->counters.barriers++;
     });
 }
@@ -108,7 +104,7 @@ int dndc_allgather_rows(dndc_ctx* ctx, const void* local, int64_t rows, int64_t 
         // every rank's row count, then one padded allgather of the blocks
         int64_t* dcnt = static_cast<int64_t*>(ctx->slot("ag_counts", sizeof(int64_t) * (W + 1)));
         DNDC_CUDA(cudaMemcpyAsync(dcnt + W, &rows, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        DNDC_NCCL(ncclAllGather(dcnt + W, dcnt, 1, ncclInt64, ctx->comm, s));
+        dndc::xport_allgather(ctx, dcnt + W, dcnt, sizeof(int64_t), s);
         std::vector<int64_t> cnt(W);
         DNDC_CUDA(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, s));
         DNDC_CUDA(cudaStreamSynchronize(s));
@@ -117,7 +113,7 @@ int dndc_allgather_rows(dndc_ctx* ctx, const void* local, int64_t rows, int64_t 
         char* send = static_cast<char*>(ctx->slot("ag_send", blk));
         char* recv = static_cast<char*>(ctx->slot("ag_recv", blk * W));
         if (rows * row_bytes) DNDC_CUDA(cudaMemcpyAsync(send, local, rows * row_bytes, cudaMemcpyDeviceToDevice, s));
-        DNDC_NCCL(ncclAllGather(send, recv, blk, ncclChar, ctx->comm, s));
+        dndc::xport_allgather(ctx, send, recv, blk, s);
         ctx->counters.allgathers++;
         int64_t off = 0;
         for (int r = 0; r < W; ++r) {
@@ -136,7 +132,7 @@ int dndc_allreduce_f64(dndc_ctx* ctx, double* buf, int64_t count) {
         if (count < 0) dndc::value_error("dndc_allreduce_f64: negative count");
         if (ctx->world == 1 || count == 0) return;
         double* all = static_cast<double*>(ctx->slot("ar_all", sizeof(double) * count * ctx->world));
-        DNDC_NCCL(ncclAllGather(buf, all, static_cast<size_t>(count), ncclFloat64, ctx->comm, ctx->stream));
+        dndc::xport_allgather(ctx, buf, all, static_cast<size_t>(count) * sizeof(double), ctx->stream);
         const int blocks = static_cast<int>(std::min<int64_t>(dndc::ceil_div(count, 256), 1024));
         dndc::fold_ranks_kernel<<<blocks, 256, 0, ctx->stream>>>(all, ctx->world, count, buf);
         DNDC_LAUNCHED(ctx);

@@ -1411,6 +1411,8 @@ __device__ void update_body(const UpdArgs& a, double* upd, double* sh) {
     }
 }
 
+#include "kmeans_persist.cuh"
+
 __global__ void __launch_bounds__(256) kmeans_update_kernel(UpdArgs a) {
     if (a.flags[0]) return;
     __shared__ double sh[32];
@@ -1522,6 +1524,22 @@ __global__ void kmeans_reset_kernel(int* flags, unsigned long long* refined, uns
     flags[0] = flags[2];  // invalid input (validate_fold_kernel): every iteration is skipped
     flags[1] = 0;
     *refined = 0ull;
+}
+
+// Zero state of one persistent fit (kmeans_persist.cuh): the three fixed-point
+// accumulators, the arrival counter / release word, flags and the refined count.
+__global__ void persist_reset_kernel(int* flags, unsigned long long* refined, unsigned long long* acc, int n_acc,
+                                     unsigned* arrive, unsigned* go, unsigned* tile_ctr, int n_ctr) {
+    for (int i = threadIdx.x; i < n_acc; i += blockDim.x) acc[i] = 0ull;
+    for (int i = threadIdx.x; i < n_ctr; i += blockDim.x) tile_ctr[i] = 0u;
+    if (threadIdx.x == 0) {
+        *arrive = 0u;
+        *go = 0u;
+        flags[0] = flags[2];
+        flags[1] = 0;
+        flags[3] = 0;
+        *refined = 0ull;
+    }
 }
 
 // world x (sum |x|^2, non-finite count) -> sx2[2] = global sum; flags[2] =
@@ -1899,6 +1917,53 @@ static UpdArgs upd_args(const KmBuffers& b, int k, int m, int world, const doubl
     return a;
 }
 
+// ---- the persistent one-launch fit (kmeans_persist.cuh)
+struct PersistPlan {
+    void (*fn)(PersistParams) = nullptr;
+    int grid = 0, static_tiles = 0;
+    size_t smem = 0;
+    const char* name = "";
+};
+
+// Grid = CTAs that fit per SM x SMs (capped by the tile count), all
+// co-resident (cooperative launch: the kernel's grid barrier needs it).
+template <int D, int K, int NST, int MINB>
+static bool try_persist(dndc_ctx* ctx, int64_t n, PersistPlan& P, const char* name) {
+    using namespace persist;
+    void (*fn)(PersistParams) = kmeans_persist_kernel<D, K, NST, MINB>;
+    const int64_t ntiles = std::max<int64_t>(ceil_div(n, TILE), 1);
+    const size_t smem = static_cast<size_t>(persist_layout<D, K, NST>().total);
+    if (smem > 227 * 1024) return false;
+    DNDC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int occ = 0;
+    DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS, smem));
+    if (occ < 1) return false;
+    const int grid = static_cast<int>(std::min<int64_t>(ntiles, static_cast<int64_t>(std::min(occ, MINB)) * ctx->num_sms));
+    // static share: ~70% of the tiles (DNDC_PERSIST_STATIC=percent overrides)
+    const char* e = std::getenv("DNDC_PERSIST_STATIC");
+    const int pct = e ? std::max(0, std::min(100, std::atoi(e))) : 70;
+    P.fn = fn;
+    P.grid = grid;
+    P.static_tiles = static_cast<int>(ntiles * pct / 100 / grid);
+    P.smem = smem;
+    P.name = name;
+    return true;
+}
+
+// DNDC_PERSIST=0 disables the one-launch fit; DNDC_PERSIST=s2b4|s3b3|s4b2 picks
+// the (stages, CTAs/SM) instantiation (A/B timing).
+static bool plan_persist(dndc_ctx* ctx, int k, int m, int64_t n_local, PersistPlan& P) {
+    const char* e = std::getenv("DNDC_PERSIST");
+    const std::string v = e ? e : "";
+    if (v == "0") return false;
+    if (m == 18 && k == 8) {
+        if (v == "s3b3") return try_persist<18, 8, 3, 3>(ctx, n_local, P, "kmeans_persist_kernel<18,8,3,3>");
+        if (v == "s4b2") return try_persist<18, 8, 4, 2>(ctx, n_local, P, "kmeans_persist_kernel<18,8,4,2>");
+        return try_persist<18, 8, 2, 4>(ctx, n_local, P, "kmeans_persist_kernel<18,8,2,4>");
+    }
+    return false;
+}
+
 template <typename T>
 static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t n_global, int64_t m64,
                        int k, int max_iter, double tol, uint64_t seed, const double* init_host,
@@ -1951,9 +2016,73 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     // one launch per iteration (fused tail) on one GPU or with the NVLink
     // peer exchange; otherwise assign -> reduce -> NCCL allgather -> update
     const bool fuse = A.small && (ctx->world == 1 || ctx->p2p) && !std::getenv("DNDC_NO_FUSE");
+    // the whole loop in one cooperative launch where the shape has an instantiation
+    PersistPlan PP;
+    const bool persist = sizeof(T) == 4 && A.small && (ctx->world == 1 || ctx->p2p) && n_local > 0 &&
+                         plan_persist(ctx, k, m, n_local, PP);
     const int ncounters = 2;
     unsigned* tile_ctr = b.counters + 1;
+    // (slots are allocated here, outside the capture: cudaMalloc is not capturable)
+    unsigned long long* acc3 =
+        persist ? static_cast<unsigned long long*>(ctx->slot("km_pacc", sizeof(unsigned long long) * 3 * S)) : nullptr;
+    unsigned* words = persist ? static_cast<unsigned*>(ctx->slot("km_pwords", sizeof(unsigned) * 4)) : nullptr;
+    double* gst = persist ? static_cast<double*>(ctx->slot("km_pgstats", sizeof(double) * 2 * S)) : nullptr;
+    unsigned* tctr = persist ? static_cast<unsigned*>(ctx->slot("km_ptiles", sizeof(unsigned) * max_iter)) : nullptr;
+    const int64_t lab_stride = (n_local + 15) / 16 * 16;
+    int8_t* plab = persist ? static_cast<int8_t*>(ctx->slot("km_plab", 2 * static_cast<size_t>(lab_stride))) : nullptr;
+    unsigned long long* pmarks = nullptr;
+    if (persist && std::getenv("DNDC_PERSIST_TRACE")) {
+        ctx->persist_trace_len = static_cast<int64_t>(max_iter) * (2 * PP.grid + 2);
+        ctx->persist_trace_grid = PP.grid;
+        pmarks = static_cast<unsigned long long*>(
+            ctx->slot("km_pmarks", sizeof(unsigned long long) * ctx->persist_trace_len));
+    }
+    auto record_persist = [&](cudaStream_t st) {
+        persist_reset_kernel<<<1, 256, 0, st>>>(b.flags, b.refined, acc3, 3 * S, words, words + 1, tctr, max_iter);
+        PersistParams pp{};
+        pp.x = reinterpret_cast<const float*>(x_local);
+        pp.n = n_local;
+        pp.max_iter = max_iter;
+        pp.full_iters = std::max(1, std::min(KS_FULL_ITERS, max_iter));
+        pp.tol = tol;
+        pp.c64_init = b.c64;
+        pp.c64_out = b.c64;
+        pp.trace = b.trace;
+        pp.disp = b.disp;
+        pp.flags = b.flags;
+        pp.sx2 = b.sx2;
+        pp.acc = acc3;
+        pp.arrive = words;
+        pp.go = words + 1;
+        pp.gstats = gst;
+        pp.refined = b.refined;
+        pp.world = ctx->world;
+        pp.rank = ctx->rank;
+        pp.peers = ctx->world > 1 ? ctx->peer_bases_dev : nullptr;
+        pp.labels = plab;
+        pp.lab_stride = lab_stride;
+        pp.tile_ctr = tctr;
+        pp.static_tiles = PP.static_tiles;
+        pp.trace_marks = pmarks;
+        if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[0], st, cudaEventRecordExternal));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(PP.grid);
+        cfg.blockDim = dim3(persist::THREADS);
+        cfg.dynamicSmemBytes = PP.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        DNDC_CUDA(cudaLaunchKernelEx(&cfg, PP.fn, pp));
+        if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[1], st, cudaEventRecordExternal));
+    };
     auto record = [&](cudaStream_t st) {
+        if (persist) {
+            record_persist(st);
+            return;
+        }
         kmeans_reset_kernel<<<1, 1, 0, st>>>(b.flags, b.refined, b.counters, ncounters, b.acc64, S);
         for (int it = 0; it < max_iter; ++it) {
             // iterations 0 and 1 accumulate every row (after the first update most
@@ -1985,20 +2114,25 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
             kmeans_update_kernel<<<1, 256, update_smem(k, m), st>>>(ua);
         }
     };
+    if (ctx->group) {
+        // ranks sharing GPUs: the stats exchange is host-staged, not capturable
+        record(s);  // (allgather_f64 counts itself here)
+        ctx->launches += 1 + (A.small ? 4ull : 3ull) * max_iter;
+    }
     cudaStream_t gs = ctx->own_stream;
     char keybuf[256];
     std::snprintf(keybuf, sizeof(keybuf), "%p/%lld/%d/%d/%d/%.17g/%p/%d/%d/%d/%d/%llu", (const void*)x_local,
                   (long long)n_local, m, k, max_iter, tol, (void*)s, A.grid(), ctx->world, km->timing ? 1 : 0,
-                  fuse ? 1 : 0, static_cast<unsigned long long>(ctx->slot_gen));
+                  (fuse ? 1 : 0) + (persist ? 2 : 0), static_cast<unsigned long long>(ctx->slot_gen));
     const std::string key = std::string(sizeof(T) == 4 ? "f32/" : "f64/") + keybuf;
     cudaGraphExec_t exec = nullptr;
-    for (size_t i = 0; i < km->graphs.size(); ++i)
+    for (size_t i = 0; i < km->graphs.size() && !ctx->group; ++i)
         if (km->graphs[i].first == key) {
             exec = km->graphs[i].second;
             std::rotate(km->graphs.begin(), km->graphs.begin() + i, km->graphs.begin() + i + 1);
             break;
         }
-    if (!exec) {
+    if (!exec && !ctx->group) {
         const uint64_t before = ctx->counters.allgathers;
         cudaGraph_t graph;
         // capture on the context's own (non-legacy) stream: the legacy default
@@ -2020,14 +2154,18 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
             km->graphs.pop_back();
         }
     }
+    if (!ctx->group) {
     DNDC_CUDA(cudaEventRecord(ctx->ev_a, s));
     DNDC_CUDA(cudaStreamWaitEvent(gs, ctx->ev_a, 0));
     DNDC_CUDA(cudaGraphLaunch(exec, gs));
     DNDC_CUDA(cudaEventRecord(ctx->ev_b, gs));
     DNDC_CUDA(cudaStreamWaitEvent(s, ctx->ev_b, 0));
     // reset + per iteration: assign (fused) | [tile reset,] assign, reduce, update
-    ctx->launches += 1 + (fuse ? 1ull : A.small ? 4ull : 3ull) * max_iter;
+    // (persistent: reset + the one cooperative launch)
+    ctx->launches += persist ? 2ull : 1 + (fuse ? 1ull : A.small ? 4ull : 3ull) * max_iter;
     if (ctx->world > 1) ctx->counters.allgathers += max_iter;
+    }
+    ctx->last_kernel = persist ? PP.name : "";
 
     // ---- results
     const size_t hb = sizeof(double) * (k * m + max_iter) + 64;
@@ -2035,18 +2173,27 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     DNDC_CUDA(cudaMemcpyAsync(h, b.c64, sizeof(double) * k * m, cudaMemcpyDeviceToHost, s));
     DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * k * m, b.trace, sizeof(double) * max_iter,
                               cudaMemcpyDeviceToHost, s));
-    DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * (k * m + max_iter), b.flags, sizeof(int) * 3,
+    DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * (k * m + max_iter), b.flags, sizeof(int) * 4,
                               cudaMemcpyDeviceToHost, s));
     DNDC_CUDA(cudaMemcpyAsync(h + sizeof(double) * (k * m + max_iter) + 16, b.refined,
                               sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     DNDC_CUDA(cudaStreamSynchronize(s));
     const int* flags = reinterpret_cast<const int*>(h + sizeof(double) * (k * m + max_iter));
     if (flags[2]) value_error("kmeans_fit: input contains non-finite values");
+    if (flags[3])
+        throw Error(DNDC_ETIMEOUT, "kmeans_fit: a peer rank did not arrive at the per-iteration stats exchange "
+                                   "within the deadlock timeout (transport.cpp:76-93)");
     std::memcpy(cent_host, h, sizeof(double) * k * m);
     const int iters = flags[1];
     std::memcpy(trace_host, h + sizeof(double) * k * m, sizeof(double) * max_iter);
     *iters_host = iters;
-    if (km->timing) {
+    if (km->timing && persist) {
+        float t = 0.f;
+        DNDC_CUDA(cudaEventElapsedTime(&t, km->ev[0], km->ev[1]));
+        km->per_launch_ms.assign(1, t);
+        km->assign_ms = t;
+        km->assign_launches = 1;
+    } else if (km->timing) {
         // iterations past convergence return at once; only the ones that ran count
         double tot = 0.0;
         km->per_launch_ms.assign(iters, 0.0);
@@ -2276,6 +2423,20 @@ int dndc_kmeans_last_assign_ms(const dndc_ctx* ctx, double* total_ms, int* launc
 int dndc_kmeans_last_refined(const dndc_ctx* ctx, int64_t* rows_refined) {
     *rows_refined = ctx->last_refined;
     return DNDC_OK;
+}
+
+const char* dndc_kmeans_last_kernel(const dndc_ctx* ctx) { return ctx ? ctx->last_kernel : ""; }
+
+// Diagnostics (tools/persist_trace.py): the %globaltimer marks of the last
+// persistent fit run with DNDC_PERSIST_TRACE set; returns the count copied.
+int64_t dndc_kmeans_persist_trace(dndc_ctx* ctx, unsigned long long* out_host, int64_t cap, int* grid) {
+    auto it = ctx->slots.find("km_pmarks");
+    if (it == ctx->slots.end() || ctx->persist_trace_len == 0) return 0;
+    const int64_t n = std::min(cap, ctx->persist_trace_len);
+    if (cudaMemcpy(out_host, it->second.first, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    *grid = ctx->persist_trace_grid;
+    return n;
 }
 
 }  // extern "C"

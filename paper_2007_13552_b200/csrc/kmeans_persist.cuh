@@ -1,0 +1,773 @@
+// kmeans_persist.cuh -- the whole Lloyd loop of a small-(D, K) k-means fit in
+// ONE cooperative launch (BASELINE config 1: 5M x 18 fp32, k = 8, 20 iterations).
+// Included by kmeans.cu (shares its helpers).
+//
+// Reference: kmeans_fit's loop body (cluster.cpp:105-151) over assign_local
+// (:44-56) and cdist_xy (pairwise.cpp:87-100); the per-iteration allreduce of
+// sums/counts (:123, transport.hpp:136-148) becomes a grid barrier plus, with
+// world > 1, an NVLink exchange between the ranks' kernels.
+//
+// Why one launch: one cfg1 iteration streams 360 MB (55.8 us at the measured
+// copy bandwidth).  A launch per iteration paid a tail, a table-copy node and a
+// relaunch gap every iteration.  Here every CTA keeps a private copy of the
+// Lloyd state (f64 master centroids, reference-order |c|^2, running sums, the
+// fp32 score table) in shared memory; after each grid barrier every CTA
+// applies the same update to the same folded stats, so the copies stay
+// bit-identical without a broadcast.  The TMA ring is never drained between
+// iterations: X does not change, so a CTA that has no tile left in iteration
+// i already streams its first tiles of iteration i + 1 while the grid waits.
+//
+// Tile schedule per iteration (measured, profiles/: with a fully static
+// schedule the CTAs finished their equal shares between 52 and 85 us -- HBM
+// does not serve the SMs evenly): CTA b first takes the static tiles
+// b + j G (j < J0, about 70% of the work, no atomics, prefetchable across the
+// barrier), then grabs the rest dynamically from a per-iteration counter.
+// Which CTA adds which rows therefore varies from run to run, so the sums are
+// made ORDER-INDEPENDENT: every row's contribution (delta iterations) or every
+// tile's f64 run sum (full iterations) is rounded to int64 fixed point at
+// 2^-(61-e) with n max|x| < 2^e (2^-38 at cfg1, far below the f64 rounding of
+// the sums themselves) and added as integers -- the fit is bit-identical from
+// run to run.  The rows' int8 labels live in HBM, two buffers by
+// iteration parity (written in i, read as "previous" in i + 1, fetched with the
+// tile by the same bulk copy, or right after the barrier for a tile that was
+// prefetched across it).
+//
+// Per-iteration protocol (S = k*m + k stats):
+//   tiles    -> CTA int64 partials -> atomicAdd into acc[it % 3] (integer adds commute)
+//   barrier  world == 1: arrival counter reaches G (it + 1), every CTA reads
+//            acc[it % 3] from L2.  world > 1: the last CTA to arrive converts,
+//            stores the rank's stats into every peer's exchange region over
+//            NVLink, waits for every rank's flag (bounded: ~20 s, then flags[3]
+//            = timeout instead of a trap), folds ranks 0..p-1 in order into
+//            gstats and releases the grid through `go`.
+//   update   every CTA: running sums (+= changes in delta iterations),
+//            c_j = S_j / n_j or kept when empty (cluster.cpp:125-133), reference
+//            order |c_j|^2, fp32 table, the fp32 error-bound inputs; CTA 0
+//            writes the inertia trace, displacement and iteration count.
+// acc[(it+1) % 3] is zeroed by CTA 0 at the start of iteration it (its last
+// readers passed barrier it-1; its first writers wait for barrier it).
+#pragma once
+
+namespace persist {
+constexpr int THREADS = 128, W = THREADS / 32, R = 2, TILE = THREADS * R, VW = W * R, SCR = 8;
+}
+
+struct PersistParams {
+    const float* x;
+    int64_t n;                   // rows of this rank's shard
+    int max_iter, full_iters;
+    double tol;
+    const double* c64_init;      // seeded centroids (k*m)
+    double* c64_out;             // final master centroids
+    double* trace;               // [max_iter] inertia
+    double* disp;                // [max_iter] max centroid displacement
+    int* flags;                  // [0] stopped early, [1] iterations run, [2] invalid input, [3] timeout
+    const double* sx2;           // [2] global sum |x|^2, [3] max |x| of the shard
+    unsigned long long* acc;     // 3 x S fixed-point accumulators (zero at launch)
+    unsigned* arrive;            // grid arrival counter (zero at launch)
+    unsigned* go;                // world > 1: iterations released by the finaliser (zero at launch)
+    double* gstats;              // world > 1: 2 x S rank-folded stats
+    unsigned long long* refined; // rows re-decided in f64 (all iterations)
+    int world, rank;
+    void* const* peers;          // world > 1: exchange regions of every rank (NVLink)
+    int8_t* labels;              // 2 x lab_stride: labels of iteration i in buffer i & 1
+    int64_t lab_stride;          // n rounded up to 16 (bulk copies need 16-byte aligned sources)
+    unsigned* tile_ctr;          // [max_iter] dynamic tile counters (zero at launch)
+    int static_tiles;            // J0: static tiles per CTA per iteration
+    // optional %globaltimer trace (DNDC_PERSIST_TRACE): per iteration and CTA
+    // [0] tiles done, [1] barrier passed; per iteration (CTA 0) [2] start, [3] update done
+    unsigned long long* trace_marks;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+struct PersistLayout {
+    int tiles, slab, wacc, scr, scl, cnt, tab, run, c64, cn64, stat, misc, stile, siter, sdef, lcnt, consumed, bars,
+        lbars, total;
+};
+
+template <int D, int K, int NST>
+__host__ __device__ constexpr PersistLayout persist_layout() {
+    using namespace persist;
+    constexpr int KD = K * D, S = KD + K, DP = (D + 3) / 4 * 4;
+    PersistLayout l{};
+    int o = 0;
+    auto take = [&](int bytes) {
+        const int at = o;
+        o = (o + bytes + 15) / 16 * 16;
+        return at;
+    };
+    l.tiles = take(NST * TILE * D * 4);
+    l.slab = take(NST * TILE);           // previous labels of each staged tile
+    l.wacc = take(W * KD * 8);           // int64 per-warp changes (delta iterations)
+    l.scr = take(W * SCR * D * 4 > (KD + K) * 8 ? W * SCR * D * 4 : (KD + K) * 8);  // also old c / |c|^2 in the update
+    l.scl = take(W * 2 * SCR * 4);
+    l.cnt = take(VW * K * 4);
+    l.tab = take((K * DP + K) * 4);
+    l.run = take(S * 8);
+    l.c64 = take(KD * 8);
+    l.cn64 = take(K * 8);
+    l.stat = take(S * 8);
+    l.misc = take(16 * 8);
+    l.stile = take(NST * 8);
+    l.siter = take(NST * 4);
+    l.sdef = take(NST * 4);
+    l.lcnt = take(NST * 4);
+    l.consumed = take(NST * 4);
+    l.bars = take(NST * 8);
+    l.lbars = take(NST * 8);
+    l.total = o;
+    return l;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// fp32 top-2 of R rows against the table in shared memory: T = [K][DP] of
+// -2 c (DP = D rounded up to 4, 16-byte rows: one LDS.128 feeds 2R FFMA2) and
+// [K] |c|^2.  Same operation chain as small_top2 (so the same error bound).
+template <int D, int K, int R>
+__device__ __forceinline__ void persist_top2(const float2 (&xv)[R][D / 2], const float* __restrict__ T,
+                                             float (&b1)[R], float (&b2)[R], int (&i1)[R]) {
+    constexpr int L = D / 2, DP = (D + 3) / 4 * 4;
+    constexpr int JG = K % 2 == 0 ? 2 : 1;
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        b1[h] = FLT_MAX;
+        b2[h] = FLT_MAX;
+        i1[h] = 0;
+    }
+#pragma unroll
+    for (int j0 = 0; j0 < K; j0 += JG) {
+        float2 sp[JG][R];
+#pragma unroll
+        for (int u = 0; u < JG; ++u) {
+            const float cn = T[K * DP + j0 + u];
+#pragma unroll
+            for (int h = 0; h < R; ++h) sp[u][h] = make_float2(cn, 0.f);
+        }
+#pragma unroll
+        for (int f4 = 0; f4 < DP / 4; ++f4) {
+#pragma unroll
+            for (int u = 0; u < JG; ++u) {
+                const float4 c = *reinterpret_cast<const float4*>(T + (j0 + u) * DP + 4 * f4);
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                    sp[u][h] = ffma2(xv[h][2 * f4], make_float2(c.x, c.y), sp[u][h]);
+                    if (2 * f4 + 1 < L) sp[u][h] = ffma2(xv[h][2 * f4 + 1], make_float2(c.z, c.w), sp[u][h]);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < JG; ++u)
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                const float sc = sp[u][h].x + sp[u][h].y;
+                const bool lt = sc < b1[h];
+                b2[h] = fminf(b2[h], fmaxf(b1[h], sc));
+                b1[h] = fminf(b1[h], sc);
+                i1[h] = lt ? j0 + u : i1[h];
+            }
+    }
+}
+
+// Tables of the current centroids c64 (shared memory), thread j < K (K <= 32:
+// all in warp 0): reference-order |c_j|^2 (pairwise.cpp:13-18), the fp32 score
+// table and the error-bound inputs (misc[0] max |c|, misc[1] max fp32 |c|^2).
+template <int D, int K>
+__device__ __forceinline__ void persist_tables(const double* c64, double* cn64, float* tab, double* misc) {
+    constexpr int DP = (D + 3) / 4 * 4;
+    const int j = threadIdx.x;
+    double cmax = 0.0, cnmax = 0.0;
+    if (j < K) {
+        double n64 = 0.0, n32 = 0.0;
+        for (int f = 0; f < D; ++f) {
+            const double cf = c64[j * D + f];
+            n64 = add_rn(n64, mul_rn(cf, cf));
+            const float c32 = static_cast<float>(cf);
+            tab[j * DP + f] = -2.f * c32;
+            n32 += static_cast<double>(c32) * static_cast<double>(c32);
+        }
+        for (int f = D; f < DP; ++f) tab[j * DP + f] = 0.f;
+        tab[K * DP + j] = static_cast<float>(n32);
+        cn64[j] = n64;
+        cmax = sqrt(n32);
+        cnmax = static_cast<double>(static_cast<float>(n32));
+    }
+    if (threadIdx.x < 32) {
+        cmax = warp_max(cmax);
+        cnmax = warp_max(cnmax);
+        if (threadIdx.x == 0) {
+            misc[0] = static_cast<double>(static_cast<float>(cmax) * (1.f + 0x1.0p-20f));
+            misc[1] = static_cast<double>(static_cast<float>(cnmax) * (1.f + 0x1.0p-20f));
+        }
+    }
+}
+
+template <int D, int K, int NST, int MINB>
+__global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(PersistParams p) {
+    using namespace persist;
+    static_assert(D % 2 == 0 && D <= 64 && K <= 32, "persistent kernel shape");
+    constexpr int L = D / 2;                 // lanes per row in the run sums (float2 each)
+    constexpr int GR = L <= 32 ? 32 / L : 1; // rows summed in parallel per warp
+    constexpr int KD = K * D, S = KD + K;
+    constexpr int JW = (K + W - 1) / W;      // clusters owned per warp in the run sums
+    constexpr PersistLayout LY = persist_layout<D, K, NST>();
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* tiles = reinterpret_cast<float*>(smem_raw + LY.tiles);
+    int8_t* slab = reinterpret_cast<int8_t*>(smem_raw + LY.slab);
+    long long* wacc = reinterpret_cast<long long*>(smem_raw + LY.wacc);
+    float* scr = reinterpret_cast<float*>(smem_raw + LY.scr);
+    int* scl = reinterpret_cast<int*>(smem_raw + LY.scl);
+    int* cnt = reinterpret_cast<int*>(smem_raw + LY.cnt);
+    float* tab = reinterpret_cast<float*>(smem_raw + LY.tab);
+    double* run = reinterpret_cast<double*>(smem_raw + LY.run);
+    double* c64s = reinterpret_cast<double*>(smem_raw + LY.c64);
+    double* cn64s = reinterpret_cast<double*>(smem_raw + LY.cn64);
+    double* stat = reinterpret_cast<double*>(smem_raw + LY.stat);
+    double* misc = reinterpret_cast<double*>(smem_raw + LY.misc);
+    volatile long long* stile = reinterpret_cast<volatile long long*>(smem_raw + LY.stile);
+    volatile int* siter = reinterpret_cast<volatile int*>(smem_raw + LY.siter);
+    volatile int* sdef = reinterpret_cast<volatile int*>(smem_raw + LY.sdef);
+    volatile int* lcnt = reinterpret_cast<volatile int*>(smem_raw + LY.lcnt);  // deferred label loads per stage
+    unsigned* consumed = reinterpret_cast<unsigned*>(smem_raw + LY.consumed);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + LY.bars);
+    uint64_t* lbars = reinterpret_cast<uint64_t*>(smem_raw + LY.lbars);
+    double* cold = reinterpret_cast<double*>(scr);  // update only: previous centroids [KD] and |c|^2 [K]
+    double* cnold = cold + KD;
+    int* s_last = reinterpret_cast<int*>(misc + 8);
+    // the producer's position: iteration being grabbed and its next static index
+    volatile int* s_git = reinterpret_cast<volatile int*>(misc + 12);
+    volatile int* s_gj = reinterpret_cast<volatile int*>(misc + 12) + 1;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int G = gridDim.x;
+    const int64_t ntiles = ceil_div(p.n, TILE);
+    const int J0 = p.static_tiles;                       // static tiles of every CTA
+    const int64_t nstatic = static_cast<int64_t>(J0) * G;  // tiles [0, nstatic) are static
+
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&bars[s], 1);
+            mbar_init(&lbars[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        *s_git = 0;
+        *s_gj = 0;
+    }
+    if (tid < NST) {
+        consumed[tid] = 0u;
+        sdef[tid] = 0;
+        lcnt[tid] = 0;
+    }
+    for (int e = tid; e < KD; e += THREADS) c64s[e] = p.c64_init[e];
+    __syncthreads();
+    persist_tables<D, K>(c64s, cn64s, tab, misc);
+    // fixed-point scale of the sums: n max|x| < 2^e
+    const double xabs = p.sx2[3];
+    int e2 = 0;
+    frexp(static_cast<double>(p.n) * xabs + 1.0, &e2);
+    const int shift = 61 - e2;
+    const float xabs_f = static_cast<float>(xabs);
+    const float qscale = ldexpf(1.f, shift);  // exact power of two (shift <= 61 < 127)
+
+    // Fills stage s with the producer's next tile: the static ones of the grab
+    // iteration first, then the dynamic counter; past the last tile of the
+    // iteration it moves to the next one.  `cur` is the caller's iteration:
+    // a tile of a later iteration gets its previous labels only after the
+    // barrier (sdef), since they are still being written.  Called by one
+    // thread at a time, in load order (stage releases are ordered).
+    auto issue = [&](int s, int cur) {
+        int git = *s_git;
+        int64_t tile = -1;
+        while (git < p.max_iter) {
+            const int j = *s_gj;
+            if (j < J0) {
+                const int64_t t = blockIdx.x + static_cast<int64_t>(j) * G;
+                *s_gj = j + 1;
+                if (t < ntiles) {
+                    tile = t;
+                    break;
+                }
+                continue;
+            }
+            const int64_t t = nstatic + atomicAdd(p.tile_ctr + git, 1u);
+            if (t < ntiles) {
+                tile = t;
+                break;
+            }
+            ++git;
+            *s_git = git;
+            *s_gj = 0;
+        }
+        stile[s] = tile;
+        siter[s] = git;
+        if (tile < 0) {  // nothing left in the fit: an empty stage ends the consumer's loop
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
+            return;
+        }
+        const int64_t rows = min(static_cast<int64_t>(TILE), p.n - tile * TILE);
+        const bool want_lab = git >= p.full_iters;  // delta iteration: previous labels needed
+        if (want_lab && git <= cur) {
+            bulk_load2(tiles + s * TILE * D, p.x + tile * TILE * D, static_cast<uint32_t>(rows * D * 4),
+                       slab + s * TILE, p.labels + static_cast<int64_t>((git - 1) & 1) * p.lab_stride + tile * TILE,
+                       static_cast<uint32_t>(rows), &bars[s]);
+        } else {
+            bulk_load(tiles + s * TILE * D, p.x + tile * TILE * D, static_cast<uint32_t>(rows * D * 4), &bars[s]);
+            if (want_lab) sdef[s] = 1;  // fetched after barrier git - 1
+        }
+    };
+    auto issue_labels = [&](int s) {  // the deferred previous labels of stage s
+        const int git = siter[s];
+        const int64_t tile = stile[s];
+        const int64_t rows = min(static_cast<int64_t>(TILE), p.n - tile * TILE);
+        int8_t* dst = slab + s * TILE;
+        const int8_t* src = p.labels + static_cast<int64_t>((git - 1) & 1) * p.lab_stride + tile * TILE;
+        const uint32_t body = static_cast<uint32_t>(rows) & ~15u;
+        for (uint32_t b = body; b < static_cast<uint32_t>(rows); ++b) dst[b] = src[b];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        lcnt[s] = lcnt[s] + 1;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&lbars[s])), "r"(body)
+                     : "memory");
+        if (body)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(dst)),
+                "l"(src), "r"(body), "r"(smem_u32(&lbars[s]))
+                : "memory");
+    };
+    if (tid == 0)
+        for (int s = 0; s < NST; ++s) issue(s, 0);
+    __syncthreads();
+
+    const bool invalid = p.flags[2] != 0;
+    unsigned long long refined = 0;
+    int64_t g = 0;  // stages consumed so far (stage g % NST, phase (g / NST) & 1)
+    const int gq = lane / L, q = lane % L;
+    bool stop = invalid;
+    for (int it = 0; it < p.max_iter && !stop; ++it) {
+        const bool full = it < p.full_iters;
+        unsigned long long* tm = p.trace_marks ? p.trace_marks + static_cast<int64_t>(it) * (2 * G + 2) : nullptr;
+        if (tm && blockIdx.x == 0 && tid == 0) tm[2 * G] = gtimer();
+        const float tau = 4.f * static_cast<float>(D + 3) * 0x1.0p-24f *
+                          (static_cast<float>(misc[1]) +
+                           2.f * sqrtf(static_cast<float>(D)) * xabs_f * static_cast<float>(misc[0]));
+        if (!full)
+            for (int e = tid; e < W * KD; e += THREADS) wacc[e] = 0ll;
+        if (blockIdx.x == 0 && it >= 1)
+            for (int e = tid; e < S; e += THREADS) p.acc[((it + 1) % 3) * S + e] = 0ull;
+        __syncthreads();
+
+        long long count_acc = 0;
+        int cnt_delta = 0;
+        long long wsum[JW][2];
+#pragma unroll
+        for (int jj = 0; jj < JW; ++jj) wsum[jj][0] = wsum[jj][1] = 0ll;
+        int8_t* lab_out = p.labels + static_cast<int64_t>(it & 1) * p.lab_stride;
+
+        for (;; ++g) {
+            const int s = static_cast<int>(g % NST);
+            float* xt = tiles + s * TILE * D;
+            mbar_wait(&bars[s], static_cast<uint32_t>((g / NST) & 1));
+            const int64_t tile = stile[s];
+            if (tile < 0 || siter[s] != it) break;  // this CTA has no tile left in iteration it
+            const int64_t row0 = tile * TILE;
+            float2 xv[R][L];
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                const int row = tid + h * THREADS;
+#pragma unroll
+                for (int f = 0; f < L; ++f) xv[h][f] = *reinterpret_cast<const float2*>(xt + row * D + 2 * f);
+            }
+            if (!full) {
+                // ---- delta iteration: rows in registers, stage handed back at once
+                if (sdef[s]) mbar_wait(&lbars[s], static_cast<uint32_t>((lcnt[s] - 1) & 1));
+                int prevl[R], label[R];
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                    const int row = tid + h * THREADS;
+                    prevl[h] = row0 + row < p.n ? static_cast<int>(slab[s * TILE + row]) : -1;
+                }
+                __threadfence_block();
+                __syncwarp();
+                if (lane == 0) {
+                    const unsigned done = atomicAdd(&consumed[s], 1u);
+                    if (done == W - 1) {
+                        consumed[s] = 0u;
+                        sdef[s] = 0;
+                        issue(s, it);
+                    }
+                }
+                float b1[R], b2[R];
+                int i1[R];
+                persist_top2<D, K, R>(xv, tab, b1, b2, i1);
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                    const int row = tid + h * THREADS;
+                    const int64_t gr = row0 + row;
+                    label[h] = K;
+                    if (gr < p.n) {
+                        label[h] = i1[h];
+                        if (K > 1 && !(b2[h] - b1[h] > tau)) {
+                            // the stage may be refilled already: the row from global (L2)
+                            label[h] = ref_argmin<float>(p.x + gr * D, D, c64s, cn64s, K);
+                            ++refined;
+                        }
+                        lab_out[gr] = static_cast<int8_t>(label[h]);
+                    }
+                }
+                // changed rows: their fixed-point values moved from the old
+                // cluster's sums to the new one's, lane = feature (int64: any order)
+                float* wscr = scr + warp * SCR * D;
+                int* wscl = scl + warp * 2 * SCR;
+                long long* acc = wacc + warp * KD;
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                    const bool ch = label[h] < K && label[h] != prevl[h];
+                    unsigned mask = __ballot_sync(FULL, ch);
+                    while (mask) {
+                        unsigned batch = mask;
+                        if (__popc(batch) > SCR) {
+                            batch = 0u;
+                            unsigned rest = mask;
+#pragma unroll
+                            for (int i = 0; i < SCR; ++i) {
+                                batch |= rest & (0u - rest);
+                                rest &= rest - 1u;
+                            }
+                        }
+                        mask &= ~batch;
+                        if ((batch >> lane) & 1u) {
+                            const int pos = __popc(batch & ((1u << lane) - 1u));
+#pragma unroll
+                            for (int f = 0; f < L; ++f) *reinterpret_cast<float2*>(wscr + pos * D + 2 * f) = xv[h][f];
+                            wscl[2 * pos] = label[h];
+                            wscl[2 * pos + 1] = prevl[h];
+                        }
+                        __syncwarp();
+                        const int nch = __popc(batch);
+                        for (int c = 0; c < nch; ++c) {
+                            const int nl = wscl[2 * c], ol = wscl[2 * c + 1];
+                            if (lane < K) cnt_delta += (lane == nl) - (lane == ol);
+#pragma unroll
+                            for (int f = lane; f < D; f += 32) {
+                                const long long v = __float2ll_rn(wscr[c * D + f] * qscale);
+                                acc[nl * D + f] += v;
+                                if (ol >= 0) acc[ol * D + f] -= v;
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
+                continue;
+            }
+
+            // ---- full iteration: every row summed (counting sort of the tile)
+            int label[R];
+            {
+                float b1[R], b2[R];
+                int i1[R];
+                persist_top2<D, K, R>(xv, tab, b1, b2, i1);
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                    const int row = tid + h * THREADS;
+                    label[h] = K;  // rows past the end sort last
+                    if (row0 + row < p.n) {
+                        label[h] = i1[h];
+                        if (K > 1 && !(b2[h] - b1[h] > tau)) {
+                            label[h] = ref_argmin<float>(xt + row * D, D, c64s, cn64s, K);
+                            ++refined;
+                        }
+                        lab_out[row0 + row] = static_cast<int8_t>(label[h]);
+                    }
+                }
+            }
+            unsigned mine[R];
+            int rank[R];
+            if (lane < K) {
+#pragma unroll
+                for (int h = 0; h < R; ++h) cnt[(h * W + warp) * K + lane] = 0;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                mine[h] = __match_any_sync(FULL, label[h]);
+                rank[h] = __popc(mine[h] & ((1u << lane) - 1u));
+                if (rank[h] == 0 && label[h] < K) cnt[(h * W + warp) * K + label[h]] = __popc(mine[h]);
+            }
+            __syncthreads();  // counts visible; every warp is done with the previous tile's stage
+            if (tid == 0 && g > 0 && consumed[(g - 1) % NST] == 0xFFFFFFFFu) {
+                consumed[(g - 1) % NST] = 0u;  // the previous full tile's stage: sort buffer no more
+                sdef[(g - 1) % NST] = 0;
+                issue(static_cast<int>((g - 1) % NST), it);
+            }
+            int tot = 0, before[R];
+#pragma unroll
+            for (int h = 0; h < R; ++h) before[h] = 0;
+            if (lane < K) {
+#pragma unroll
+                for (int v = 0; v < VW; ++v) {
+                    const int c = cnt[v * K + lane];
+                    tot += c;
+#pragma unroll
+                    for (int h = 0; h < R; ++h) before[h] += v < h * W + warp ? c : 0;
+                }
+            }
+            int start = tot;
+#pragma unroll
+            for (int o = 1; o < K; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, start, o);
+                if (lane >= o) start += v;
+            }
+            start -= tot;
+            if (warp == 0 && lane < K) count_acc += tot;
+            // scatter into label order, in place (every row is in registers)
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                const int pos = __shfl_sync(FULL, start + before[h], label[h] < K ? label[h] : 0) + rank[h];
+                if (label[h] < K) {
+#pragma unroll
+                    for (int f = 0; f < L; ++f) *reinterpret_cast<float2*>(xt + pos * D + 2 * f) = xv[h][f];
+                }
+            }
+            __syncthreads();
+            // warp w sums the sorted runs of clusters w, w+W, ... in f64 and
+            // adds the tile's run sums as int64 fixed point
+#pragma unroll
+            for (int jj = 0; jj < JW; ++jj) {
+                const int cl = warp + jj * W;
+                if (cl >= K) break;
+                const int r0 = __shfl_sync(FULL, start, cl);
+                const int r1 = r0 + __shfl_sync(FULL, tot, cl);
+                double2 part = make_double2(0.0, 0.0), part2 = make_double2(0.0, 0.0);
+                if (gq < GR) {
+                    const float* src = xt + 2 * q;
+                    int r = r0 + gq;
+#pragma unroll 2
+                    for (; r + GR < r1; r += 2 * GR) {
+                        const float2 v = *reinterpret_cast<const float2*>(src + r * D);
+                        const float2 u = *reinterpret_cast<const float2*>(src + (r + GR) * D);
+                        part.x += static_cast<double>(v.x);
+                        part.y += static_cast<double>(v.y);
+                        part2.x += static_cast<double>(u.x);
+                        part2.y += static_cast<double>(u.y);
+                    }
+                    if (r < r1) {
+                        const float2 v = *reinterpret_cast<const float2*>(src + r * D);
+                        part.x += static_cast<double>(v.x);
+                        part.y += static_cast<double>(v.y);
+                    }
+                    part.x += part2.x;
+                    part.y += part2.y;
+                }
+#pragma unroll
+                for (int o = 1; o < GR; o <<= 1) {
+                    const double vx = __shfl_down_sync(FULL, part.x, o * L);
+                    const double vy = __shfl_down_sync(FULL, part.y, o * L);
+                    if (gq + o < GR) {
+                        part.x += vx;
+                        part.y += vy;
+                    }
+                }
+                if (gq == 0) {
+                    wsum[jj][0] += llrint(ldexp(part.x, shift));
+                    wsum[jj][1] += llrint(ldexp(part.y, shift));
+                }
+            }
+            if (tid == 0) consumed[s] = 0xFFFFFFFFu;  // released at the next tile's count barrier
+        }
+        __syncthreads();  // every warp is done with this iteration's tiles
+        // a full iteration hands its last stage back only now (it was the sort buffer)
+        if (full && tid == 0 && g > 0 && consumed[(g - 1) % NST] == 0xFFFFFFFFu) {
+            consumed[(g - 1) % NST] = 0u;
+            sdef[(g - 1) % NST] = 0;
+            issue(static_cast<int>((g - 1) % NST), it);
+        }
+        if (tm && tid == 0) tm[blockIdx.x] = gtimer();
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // this iteration's labels -> later bulk reads
+
+        // ---- this CTA's int64 partial stats -> global accumulator
+        unsigned long long* acc_it = p.acc + (it % 3) * S;
+        if (!full) {
+            if (lane < K) cnt[warp * K + lane] = cnt_delta;
+            __syncthreads();
+            for (int e = tid; e < KD; e += THREADS) {
+                long long v = 0;
+#pragma unroll
+                for (int c = 0; c < W; ++c) v += wacc[c * KD + e];
+                if (v != 0) atomicAdd(acc_it + e, static_cast<unsigned long long>(v));
+            }
+            if (tid < K) {
+                long long c = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) c += cnt[w * K + tid];
+                if (c != 0) atomicAdd(acc_it + KD + tid, static_cast<unsigned long long>(c));
+            }
+        } else {
+#pragma unroll
+            for (int jj = 0; jj < JW; ++jj) {
+                const int cl = warp + jj * W;
+                if (cl < K && gq == 0 && q < L) {
+                    if (wsum[jj][0]) atomicAdd(acc_it + cl * D + 2 * q, static_cast<unsigned long long>(wsum[jj][0]));
+                    if (wsum[jj][1])
+                        atomicAdd(acc_it + cl * D + 2 * q + 1, static_cast<unsigned long long>(wsum[jj][1]));
+                }
+            }
+            if (warp == 0 && lane < K && count_acc)
+                atomicAdd(acc_it + KD + lane, static_cast<unsigned long long>(count_acc));
+        }
+        __syncthreads();
+
+        // ---- grid barrier (+ the cross-rank exchange on the last arrival)
+        const unsigned target = static_cast<unsigned>(G) * static_cast<unsigned>(it + 1);
+        if (tid == 0) {
+            __threadfence();
+            const unsigned old = atomicAdd(p.arrive, 1u);
+            *s_last = old == target - 1u;
+        }
+        __syncthreads();
+        if (p.world > 1 && *s_last) {
+            // finaliser: this rank's stats to every peer over NVLink, rank-order fold
+            unsigned long long* s_epoch = reinterpret_cast<unsigned long long*>(misc + 10);
+            if (tid == 0) {
+                __threadfence();
+                unsigned long long* ep = xchg_flags(p.peers[p.rank], p.world) + p.world;
+                *s_epoch = *ep + 1;
+                *ep = *s_epoch;
+            }
+            __syncthreads();
+            const unsigned long long epoch = *s_epoch;
+            const int slot = static_cast<int>(epoch & 1);
+            for (int e = tid; e < S; e += THREADS) {
+                const long long qv = static_cast<long long>(__ldcg(acc_it + e));
+                const double v = e < KD ? ldexp(static_cast<double>(qv), -shift) : static_cast<double>(qv);
+                for (int r = 0; r < p.world; ++r) xchg_recv(p.peers[r], slot, p.world, p.rank)[e] = v;
+            }
+            __threadfence_system();
+            __syncthreads();
+            if (tid < p.world) {
+                st_release_sys(xchg_flags(p.peers[tid], p.world) + p.rank, epoch);
+                const unsigned long long* mine_f = xchg_flags(p.peers[p.rank], p.world) + tid;
+                const long long t0 = clock64();
+                while (ld_acquire_sys(mine_f) < epoch) {
+                    __nanosleep(64);
+                    if (clock64() - t0 > 40000000000ll) {  // a peer never arrived (~20 s): TimeoutError
+                        atomicExch(p.flags + 3, 1);
+                        break;
+                    }
+                }
+            }
+            __syncthreads();
+            __threadfence();
+            const double* recv = xchg_recv(p.peers[p.rank], slot, p.world, 0);
+            for (int e = tid; e < S; e += THREADS) {
+                double v = 0.0;
+                for (int r = 0; r < p.world; ++r) v += __ldcv(recv + static_cast<int64_t>(r) * XCHG_STATS + e);
+                p.gstats[(it & 1) * S + e] = v;
+            }
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) st_release_gpu_u32(p.go, static_cast<unsigned>(it + 1));
+        } else if (tid == 0) {
+            const unsigned* word = p.world > 1 ? p.go : p.arrive;
+            const unsigned want = p.world > 1 ? static_cast<unsigned>(it + 1) : target;
+            const long long t0 = clock64();
+            while (ld_acquire_gpu_u32(word) < want) {
+                __nanosleep(32);
+                if (clock64() - t0 > 40000000000ll) {
+                    atomicExch(p.flags + 3, 1);
+                    break;
+                }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+        if (tm && tid == 0) tm[G + blockIdx.x] = gtimer();
+        // ---- the folded stats of this iteration -> stat (every CTA the same bits)
+        if (p.world > 1) {
+            for (int e = tid; e < S; e += THREADS) stat[e] = __ldcg(p.gstats + (it & 1) * S + e);
+        } else {
+            for (int e = tid; e < S; e += THREADS) {
+                const long long qv = static_cast<long long>(__ldcg(acc_it + e));
+                stat[e] = e < KD ? ldexp(static_cast<double>(qv), -shift) : static_cast<double>(qv);
+            }
+        }
+        for (int e = tid; e < KD; e += THREADS) cold[e] = c64s[e];
+        if (tid < K) cnold[tid] = cn64s[tid];
+        __syncthreads();
+        if (__ldcv(p.flags + 3)) {
+            stop = true;
+            break;
+        }
+        // ---- update (cluster.cpp:123-150), identical in every CTA
+        for (int e = tid; e < S; e += THREADS) {
+            double v = stat[e];
+            if (!full) v += run[e];  // delta iterations: changes added to the running sums
+            run[e] = v;
+        }
+        __syncthreads();
+        for (int e = tid; e < KD; e += THREADS) {
+            const int cl = e / D;
+            const double count = run[KD + cl];
+            c64s[e] = count > 0.0 ? run[e] / count : cold[e];  // empty cluster keeps its centroid
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double inertia_part = 0.0, dmax = 0.0;
+            if (lane < K) {
+                const double count = run[KD + lane];
+                double dot = 0.0, dsq = 0.0;
+                for (int f = 0; f < D; ++f) {
+                    const int e = lane * D + f;
+                    dot += cold[e] * run[e];
+                    const double diff = c64s[e] - cold[e];
+                    dsq = add_rn(dsq, mul_rn(diff, diff));  // cluster.cpp:142-146 order
+                }
+                inertia_part = count * cnold[lane] - 2.0 * dot;  // uses the old |c_j|^2
+                dmax = __dsqrt_rn(dsq);
+            }
+            inertia_part = warp_sum(inertia_part);
+            dmax = warp_max(dmax);
+            if (lane == 0) {
+                if (blockIdx.x == 0) {
+                    p.trace[it] = p.sx2[2] + inertia_part;
+                    p.disp[it] = dmax;
+                    p.flags[1] = it + 1;
+                    if (dmax < p.tol) p.flags[0] = 1;
+                }
+                misc[2] = dmax < p.tol ? 1.0 : 0.0;
+            }
+        }
+        persist_tables<D, K>(c64s, cn64s, tab, misc);
+        __syncthreads();
+        if (tm && blockIdx.x == 0 && tid == 0) tm[2 * G + 1] = gtimer();
+        stop = misc[2] != 0.0;
+        // tiles of the next iteration already staged: their previous labels are final now
+        if (!stop && tid == 0) {
+            for (int64_t h = g; h < g + NST; ++h) {
+                const int s = static_cast<int>(h % NST);
+                if (sdef[s] && siter[s] == it + 1) issue_labels(s);
+            }
+        }
+        __syncthreads();
+    }
+    // loads issued but never consumed (early stop): let them land before exit
+    if (tid == 0) {
+        for (int64_t h = g; h < g + NST; ++h)
+            mbar_wait(&bars[h % NST], static_cast<uint32_t>((h / NST) & 1));
+    }
+    if (refined) atomicAdd(p.refined, refined);
+    if (blockIdx.x == 0)
+        for (int e = tid; e < KD; e += THREADS) p.c64_out[e] = c64s[e];
+}

@@ -351,11 +351,25 @@ static void lasso_fit(dndc_ctx* ctx, const double* x, int64_t rows, int64_t n_gl
         for (int j = 0; j <= m; ++j) {
             lasso_step_kernel<<<G, LS_THREADS, 0, st>>>(a, j);
             if (nccl) {
-                DNDC_NCCL(ncclAllReduce(rho, rho, 1, ncclFloat64, ncclSum, ctx->comm, st));
+                xport_allreduce_sum_f64(ctx, rho, 1, st);
                 lasso_update_kernel<<<1, 1, 0, st>>>(a);
             }
         }
     };
+    if (ctx->group) {
+        // ranks sharing GPUs: host-staged scalar sums cannot sit in a graph
+        for (int sw = 0; sw < sweeps; ++sw) {
+            sweep(s);
+            ctx->launches += static_cast<uint64_t>(2 * (m + 1));
+        }
+        LassoCtl ch;
+        DNDC_CUDA(cudaMemcpyAsync(&ch, ctl, sizeof(ch), cudaMemcpyDeviceToHost, s));
+        DNDC_CUDA(cudaMemcpyAsync(w_host, w, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+        DNDC_CUDA(cudaMemcpyAsync(trace_host, trace, sizeof(double) * sweeps, cudaMemcpyDeviceToHost, s));
+        DNDC_CUDA(cudaStreamSynchronize(s));
+        *sweeps_run = ch.sweep;
+        return;
+    }
     // one sweep as a graph, replayed (launch cost of m+1 kernels -> one);
     // instantiated once per (buffers, shape, lambda, tol, transport) and kept
     cudaStream_t gs = ctx->own_stream;

@@ -153,18 +153,19 @@ static void resplit(dndc_ctx* ctx, const void* src_local, int ndim, const int64_
         copy_box(ctx, src, &mine_src, sbuf + so * esz, nullptr, send[q], esz);
         so += send[q].numel();
     }
-    DNDC_NCCL(ncclGroupStart());
+    std::vector<XSend> xs;
+    std::vector<XRecv> xr;
     so = 0;
     int64_t ro = 0;
     for (int q = 0; q < W; ++q) {
         if (q == r) continue;
         const int64_t ns = send[q].numel() * esz, nr = recv[q].numel() * esz;
-        if (ns) DNDC_NCCL(ncclSend(sbuf + so * esz, static_cast<size_t>(ns), ncclInt8, q, ctx->comm, ctx->stream));
-        if (nr) DNDC_NCCL(ncclRecv(rbuf + ro * esz, static_cast<size_t>(nr), ncclInt8, q, ctx->comm, ctx->stream));
+        if (ns) xs.push_back({q, sbuf + so * esz, static_cast<size_t>(ns)});
+        if (nr) xr.push_back({q, rbuf + ro * esz, static_cast<size_t>(nr)});
         so += send[q].numel();
         ro += recv[q].numel();
     }
-    DNDC_NCCL(ncclGroupEnd());
+    xport_exchange(ctx, xs, xr, ctx->stream);
     ro = 0;
     for (int q = 0; q < W; ++q) {
         if (q == r) continue;

@@ -46,7 +46,7 @@ void allgather_f64(dndc_ctx* ctx, const double* send, double* recv, size_t count
                                       stream));
         return;
     }
-    DNDC_NCCL(ncclAllGather(send, recv, count, ncclFloat64, ctx->comm, stream));
+    xport_allgather(ctx, send, recv, count * sizeof(double), stream);
     ctx->counters.allgathers++;
 }
 
@@ -54,7 +54,7 @@ void allreduce_sum_f64(dndc_ctx* ctx, double* buf, size_t count, cudaStream_t st
     if (ctx->world == 1) return;
     // Only used where every addend but one is an exact zero (gather_rows,
     // cluster.cpp:27-42), so the sum is exact whatever NCCL's order.
-    DNDC_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, ctx->comm, stream));
+    xport_allreduce_sum_f64(ctx, buf, count, stream);
     ctx->counters.allreduces++;
 }
 
@@ -215,6 +215,23 @@ int dndc_create(int device, int rank, int world, const void* unique_id, dndc_ctx
             dndc::setup_peer_exchange(ctx.get());
         }
         *out = ctx.release();
+    });
+}
+
+int dndc_create_in_group(int device, int rank, dndc_group* group, int world, dndc_ctx** out) {
+    return guard([&] {
+        if (!group) dndc::value_error("dndc_create_in_group: no group");
+        if (world < 1 || rank < 0 || rank >= world)
+            dndc::value_error("dndc_create_in_group: rank " + std::to_string(rank) + " out of range for world size " +
+                              std::to_string(world));
+        dndc_ctx* c = nullptr;
+        const int rc = dndc_create(device, 0, 1, nullptr, &c);  // a one-rank context on `device` ...
+        if (rc != DNDC_OK) throw dndc::Error(rc, dndc_last_error());
+        c->rank = rank;  // ... that joins the group's world
+        c->world = world;
+        c->group = group;
+        c->p2p_status = "host loopback (ranks share GPUs)";
+        *out = c;
     });
 }
 

@@ -90,22 +90,34 @@ def test_cpp_dropin_compiles_against_the_c_abi():
 
 
 def test_cli_usage_errors_and_no_cpu_fallback():
-    """`dnd` (F3, tools/main.cpp:12-63): bad flags exit 2 with the usage line;
-    a valid command on a host without a GPU fails loudly (exit 1, CUDA error),
-    it never computes on the CPU."""
+    """`dnd` (F3, tools/main.cpp:12-83): bad command lines exit 2 with the
+    usage line; a runtime dnd::Error exits 2 with "error: " (main.cpp:78-82);
+    a valid command on a host without a GPU fails loudly, it never computes on
+    the CPU; `convert` writes a DNB container without any GPU."""
     import subprocess
+    import tempfile
 
     import torch
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.run(["make", "-C", os.path.join(root, "cpp")], capture_output=True, check=True)
     exe = os.path.join(root, "cpp", "build", "dnd")
-    for args in (["frobnicate"], ["bench", "--algo", "svm"], ["bench", "--synthetic", "12"], ["bench", "--k"],
-                 ["bench", "--algo", "load"]):
+    for args in (["frobnicate"], ["bench", "svm"], ["bench", "kmeans", "--synthetic", "12"], ["bench", "kmeans", "--k"],
+                 ["bench", "load"], ["bench"], ["verify", "kmeans", "--split", "2"], ["convert", "a.csv"]):
         r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=60)
         assert r.returncode == 2 and "usage: dnd" in r.stderr, (args, r.stderr)
+    with tempfile.TemporaryDirectory() as d:
+        csv = os.path.join(d, "x.csv")
+        open(csv, "w").write("a,b,c\n1,2,3\n4,5,6.5\n")
+        r = subprocess.run([exe, "convert", csv, os.path.join(d, "x.dnb"), "--dtype", "f32", "--skip-header"],
+                           capture_output=True, text=True, timeout=60)
+        assert r.returncode == 0 and "wrote" in r.stderr and "2x3" in r.stderr, r.stderr
+        raw = open(os.path.join(d, "x.dnb"), "rb").read()
+        assert raw[:4] == b"DNB1" and np.array_equal(np.frombuffer(raw[-24:], "<f4"), [1, 2, 3, 4, 5, 6.5])
+        r = subprocess.run([exe, "convert", os.path.join(d, "missing.csv"), os.path.join(d, "y.dnb")],
+                           capture_output=True, text=True, timeout=60)
+        assert r.returncode == 2 and r.stderr.startswith("error: ")
     if not torch.cuda.is_available():
-        r = subprocess.run([exe, "bench", "--algo", "kmeans", "--synthetic", "100x4"], capture_output=True,
+        r = subprocess.run([exe, "bench", "kmeans", "--synthetic", "100x4"], capture_output=True,
                            text=True, timeout=60)
-        assert r.returncode == 1 and r.stderr.startswith("dnd: ")
-
+        assert r.returncode == 2 and r.stderr.startswith("error: ")

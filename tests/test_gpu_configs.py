@@ -149,3 +149,20 @@ def test_cfg5_kmeanspp_full_size(comm, oracle):
     xh = a.tile.cpu().numpy()
     want = oracle.kmeanspp_indices(xh, k, seed)
     assert np.array_equal(got, want), (got, want)
+
+
+def test_cfg1_fit_is_bitwise_repeatable(comm):
+    """the fit must not depend on run-to-run scheduling.  The
+    persistent kernel hands out part of its tiles dynamically, so its sums are
+    integer fixed point (order-independent); two fits at cfg1 size, and one on
+    data with tiny magnitudes (bits far below the fixed-point step), must agree
+    to the last bit."""
+    n, m, k = 5_000_000, 18, 8
+    x = dnd.random_uniform((n, m), 0, 42, comm)
+    a = dnd.kmeans_fit(x, k, 20, 0.0, 42)
+    b = dnd.kmeans_fit(x, k, 20, 0.0, 42)
+    assert np.array_equal(a.centroids, b.centroids) and a.inertia_trace == b.inertia_trace
+    xs = dnd.DndArray(x.shape, 0, comm, x.tile * 1e-6)
+    c = dnd.kmeans_fit(xs, k, 10, 0.0, 42)
+    d = dnd.kmeans_fit(xs, k, 10, 0.0, 42)
+    assert np.array_equal(c.centroids, d.centroids) and c.inertia_trace == d.inertia_trace

@@ -19,9 +19,14 @@ def test_cpp_dropin_reference_cases():
     assert " 0 failed" in r.stdout
 
 
-def _dnd(*args):
+def _run(*args):
     subprocess.run(["make", "-C", os.path.join(ROOT, "cpp")], check=True, capture_output=True)
-    r = subprocess.run([os.path.join(ROOT, "cpp", "build", "dnd"), *args], capture_output=True, text=True, timeout=600)
+    return subprocess.run([os.path.join(ROOT, "cpp", "build", "dnd"), *args], capture_output=True, text=True,
+                          timeout=600)
+
+
+def _dnd(*args):
+    r = _run(*args)
     assert r.returncode == 0, r.stderr[-3000:]
     return json.loads(r.stdout.strip().splitlines()[-1])
 
@@ -34,18 +39,29 @@ def _ranks():
 @pytest.mark.parametrize("algo", ["kmeans", "cdist", "moments"])
 def test_cli_bench_report_shape(algo):
     """`dnd bench` keeps the reference report keys (tools/bench.cpp:118-128)."""
-    rep = _dnd("bench", "--algo", algo, "--synthetic", "20000x18", "--runs", "3", "--ranks", str(_ranks()))
+    rep = _dnd("bench", algo, "--synthetic", "20000x18", "--runs", "3", "--ranks", str(_ranks()))
     for key in ("algo", "ranks", "split", "params", "warmup_runs", "timed_runs", "mean_seconds", "std_seconds"):
         assert key in rep
     assert rep["algo"] == algo and rep["timed_runs"] == 3
     assert rep["mean_seconds"] > 0 and rep["std_seconds"] >= 0
 
 
-@pytest.mark.parametrize("algo", ["kmeans", "cdist", "moments"])
-def test_cli_verify_distributed_vs_single(algo):
-    """`dnd verify`: P ranks against one rank within the gate (tools/verify.cpp)."""
-    rep = _dnd("verify", "--algo", algo, "--synthetic", "3000x18", "--ranks", str(_ranks()))
-    assert rep["pass"] is True, rep
+@pytest.mark.parametrize("algo", ["kmeans", "cdist", "moments", "lasso"])
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_cli_verify_distributed_vs_single(algo, ranks):
+    """`dnd verify ALGO`: P ranks against one rank, the reference's gate lines
+    (tools/verify.cpp:283-300); 3 ranks share GPUs on a 1-2 GPU box."""
+    r = _run("verify", algo, "--synthetic", "3000x18", "--ranks", str(ranks))
+    print(r.stdout)
+    assert r.returncode == 0 and r.stdout.strip().splitlines()[-1] == "result: OK", r.stdout + r.stderr[-2000:]
+
+
+def test_cli_verify_catches_an_injected_combiner_fault():
+    """verify --inject-combiner-fault (verify.cpp:57-73): the corrupted moments
+    combiner must FAIL the gate (exit 1) -- the gate is not vacuous."""
+    r = _run("verify", "moments", "--synthetic", "3000x18", "--ranks", "3", "--inject-combiner-fault")
+    print(r.stdout)
+    assert r.returncode == 1 and "FAIL" in r.stdout, r.stdout + r.stderr[-2000:]
 
 
 def test_cli_bench_from_dnb_file(tmp_path):
@@ -57,8 +73,7 @@ def test_cli_bench_from_dnb_file(tmp_path):
     path = tmp_path / "x.dnb"
     with open(path, "wb") as f:
         f.write(b"DNB1" + bytes([1, 2]) + np.array(x.shape, "<u8").tobytes() + x.tobytes())
-    rep = _dnd("bench", "--algo", "kmeans", "--data", str(path), "--runs", "2", "--ranks", str(_ranks()))
+    rep = _dnd("bench", "kmeans", "--data", str(path), "--runs", "2", "--ranks", str(_ranks()))
     assert rep["params"]["rows"] == 20000 and rep["params"]["cols"] == 18
-    r = subprocess.run([os.path.join(ROOT, "cpp", "build", "dnd"), "bench", "--data", str(tmp_path / "nope.dnb")],
-                       capture_output=True, text=True, timeout=60)
-    assert r.returncode == 1 and "cannot open" in r.stderr
+    r = _run("bench", "kmeans", "--data", str(tmp_path / "nope.dnb"))
+    assert r.returncode == 2 and "cannot open" in r.stderr
