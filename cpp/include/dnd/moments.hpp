@@ -49,16 +49,19 @@ inline MomentState local_moments(const Tile<double>& t) {
     return s;
 }
 
-/// Welford per column of a 2-D host tile along axis 0 (moments.cpp:100-114).
+/// Welford along `axis` of a 2-D host tile (moments.cpp:100-114): axis 0 gives
+/// one state slot per column, axis 1 one per row; count = the axis extent.
 inline MomentState local_moments_axis(const Tile<double>& t, int axis) {
-    if (t.ndim() != 2 || axis != 0) throw ValueError("local_moments_axis: 2-D tiles along axis 0");
+    if (t.ndim() != 2 || (axis != 0 && axis != 1)) throw ValueError("local_moments_axis: 2-D tiles, axis 0 or 1");
     const index_t rows = t.extents[0], m = t.extents[1];
-    MomentState s = MomentState::identity(static_cast<std::size_t>(m));
-    s.count = rows;
-    for (index_t c = 0; c < m; ++c) {
+    const index_t slots = axis == 0 ? m : rows, extent = axis == 0 ? rows : m;
+    MomentState s = MomentState::identity(static_cast<std::size_t>(slots));
+    s.count = extent;
+    for (index_t c = 0; c < slots; ++c) {
         double mu = 0.0, m2 = 0.0;
-        for (index_t r = 0; r < rows; ++r) {
-            const double v = t.data[static_cast<std::size_t>(r * m + c)];
+        for (index_t r = 0; r < extent; ++r) {
+            const double v = axis == 0 ? t.data[static_cast<std::size_t>(r * m + c)]
+                                       : t.data[static_cast<std::size_t>(c * m + r)];
             const double d = v - mu;
             mu += d / static_cast<double>(r + 1);
             m2 += d * (v - mu);
@@ -122,16 +125,50 @@ double stddev(const DndArray<T>& a, std::int64_t ddof = 0) {
     return std::sqrt(var(a, ddof));
 }
 
-/// Along the split axis (axis 0): combined across ranks, result replicated
-/// (moments.cpp:41-52).  Other axes are off the B200 path.
+namespace detail {
+/// The per-row statistic of a 2-D array (axis 1, off the GPU hot path: the
+/// reference's axis_statistic, moments.cpp:33-52): each rank reduces its
+/// tile's rows; a column split combines the rank states in rank order into a
+/// replicated result, a row split keeps the rows split (1-D, split 0).
+template <typename T, typename F>
+DndArray<double> axis1_statistic(const DndArray<T>& a, F value) {
+    const Tile<T> h = a.tile();
+    Tile<double> t{h.extents, std::vector<double>(h.data.begin(), h.data.end())};
+    MomentState s = local_moments_axis(t, 1);
+    if (a.split() == std::optional<int>(1)) {
+        s = a.comm().allreduce(
+            s, [](MomentState acc, const MomentState& v) { return combine(acc, v); },
+            MomentState::identity(s.arity()));
+    }
+    std::vector<double> out(s.arity());
+    for (std::size_t i = 0; i < out.size(); ++i) out[i] = value(s, i);
+    const index_t n = a.shape()[0];
+    if (a.split() == std::optional<int>(0)) {
+        auto r = empty_like_shape<double>({n}, 0, a.comm());
+        if (!out.empty())
+            check(dndc_memcpy(a.comm().handle(), r.device_data(), out.data(), out.size() * sizeof(double),
+                              DNDC_COPY_H2D));
+        return r;
+    }
+    return from_global(out, {n}, std::nullopt, a.comm());
+}
+}  // namespace detail
+
+/// Along the split axis (axis 0): combined across ranks by the device pass and
+/// the rank-order fold, result replicated (moments.cpp:41-52).  Axis 1 of a
+/// 2-D array is reduced per row (detail::axis1_statistic).
 template <typename T>
 DndArray<double> mean_axis(const DndArray<T>& a, int axis) {
-    if (axis != 0 || a.ndim() != 2) throw ValueError("mean_axis: axis 0 of a 2-D array on the B200 path");
+    if (a.ndim() != 2 || (axis != 0 && axis != 1)) throw ValueError("mean_axis: axis 0 or 1 of a 2-D array");
+    if (axis == 1) return detail::axis1_statistic(a, [](const MomentState& s, std::size_t i) { return s.mean[i]; });
     return detail::replicated_vector(detail::global_state(a, 0).mean, a);
 }
 template <typename T>
 DndArray<double> var_axis(const DndArray<T>& a, int axis, std::int64_t ddof = 0) {
-    if (axis != 0 || a.ndim() != 2) throw ValueError("var_axis: axis 0 of a 2-D array on the B200 path");
+    if (a.ndim() != 2 || (axis != 0 && axis != 1)) throw ValueError("var_axis: axis 0 or 1 of a 2-D array");
+    if (axis == 1)
+        return detail::axis1_statistic(
+            a, [ddof](const MomentState& s, std::size_t i) { return detail::variance_from(s, i, ddof, "var_axis"); });
     const MomentState s = detail::global_state(a, 0);
     std::vector<double> v(s.arity());
     for (std::size_t i = 0; i < v.size(); ++i) v[i] = detail::variance_from(s, i, ddof, "var_axis");
@@ -139,7 +176,11 @@ DndArray<double> var_axis(const DndArray<T>& a, int axis, std::int64_t ddof = 0)
 }
 template <typename T>
 DndArray<double> stddev_axis(const DndArray<T>& a, int axis, std::int64_t ddof = 0) {
-    if (axis != 0 || a.ndim() != 2) throw ValueError("stddev_axis: axis 0 of a 2-D array on the B200 path");
+    if (a.ndim() != 2 || (axis != 0 && axis != 1)) throw ValueError("stddev_axis: axis 0 or 1 of a 2-D array");
+    if (axis == 1)
+        return detail::axis1_statistic(a, [ddof](const MomentState& s, std::size_t i) {
+            return std::sqrt(detail::variance_from(s, i, ddof, "stddev_axis"));
+        });
     const MomentState s = detail::global_state(a, 0);
     std::vector<double> v(s.arity());
     for (std::size_t i = 0; i < v.size(); ++i) v[i] = std::sqrt(detail::variance_from(s, i, ddof, "stddev_axis"));

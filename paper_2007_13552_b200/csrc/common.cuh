@@ -201,23 +201,12 @@ __device__ __forceinline__ float sqrt_approx(float v) {
     return r;
 }
 
-// Packed fp32 FMA (sm_100 FFMA2): two independent fmaf's in one instruction.
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-    unsigned long long r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;"
-        : "=l"(r)
-        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)),
-          "l"(*reinterpret_cast<const unsigned long long*>(&c)));
-    return *reinterpret_cast<const float2*>(&r);
-}
+// Packed fp32 FMA / add (sm_100 FFMA2 / FADD2): two independent fmaf's in one
+// instruction.  The CUDA intrinsics, not inline asm: the asm's 64-bit operand
+// packing cost ~30 extra moves per row in the k-means scores (ncu, r2).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
-    unsigned long long r;
-    asm("add.rn.f32x2 %0, %1, %2;"
-        : "=l"(r)
-        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
-    return *reinterpret_cast<const float2*>(&r);
-}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 
 __device__ __forceinline__ void st_stream(float* p, float v) {
     asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");

@@ -524,13 +524,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 
+// try_wait with a suspend-time hint (ns): the warp sleeps until the phase
+// completes instead of re-polling (the plain poll loop was ~40 issue slots per
+// 32 rows of the k-means kernels under ncu, r2).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 
@@ -1529,12 +1532,11 @@ __global__ void kmeans_reset_kernel(int* flags, unsigned long long* refined, uns
 // Zero state of one persistent fit (kmeans_persist.cuh): the three fixed-point
 // accumulators, the arrival counter / release word, flags and the refined count.
 __global__ void persist_reset_kernel(int* flags, unsigned long long* refined, unsigned long long* acc, int n_acc,
-                                     unsigned* arrive, unsigned* go, unsigned* tile_ctr, int n_ctr) {
+                                     unsigned* words, int n_words, unsigned* tile_ctr, int n_ctr) {
     for (int i = threadIdx.x; i < n_acc; i += blockDim.x) acc[i] = 0ull;
     for (int i = threadIdx.x; i < n_ctr; i += blockDim.x) tile_ctr[i] = 0u;
+    for (int i = threadIdx.x; i < n_words; i += blockDim.x) words[i] = 0u;
     if (threadIdx.x == 0) {
-        *arrive = 0u;
-        *go = 0u;
         flags[0] = flags[2];
         flags[1] = 0;
         flags[3] = 0;
@@ -1917,22 +1919,27 @@ static UpdArgs upd_args(const KmBuffers& b, int k, int m, int world, const doubl
     return a;
 }
 
-// ---- the persistent one-launch fit (kmeans_persist.cuh)
-struct PersistPlan {
+// ---- the persistent fit (kmeans_persist.cuh): the full iterations in one
+// cooperative launch (R = 2 rows per thread: counting sort of the tile), the
+// delta iterations in a second, leaner one (R rows per thread, no sort)
+struct PersistLaunch {
     void (*fn)(PersistParams) = nullptr;
     int grid = 0, static_tiles = 0;
     size_t smem = 0;
     const char* name = "";
 };
+struct PersistPlan {
+    PersistLaunch full, delta;
+};
 
 // Grid = CTAs that fit per SM x SMs (capped by the tile count), all
 // co-resident (cooperative launch: the kernel's grid barrier needs it).
-template <int D, int K, int NST, int MINB>
-static bool try_persist(dndc_ctx* ctx, int64_t n, PersistPlan& P, const char* name) {
+template <int D, int K, int R, int NST, int MINB, int MODE>
+static bool try_persist(dndc_ctx* ctx, int64_t n, PersistLaunch& P, const char* name) {
     using namespace persist;
-    void (*fn)(PersistParams) = kmeans_persist_kernel<D, K, NST, MINB>;
-    const int64_t ntiles = std::max<int64_t>(ceil_div(n, TILE), 1);
-    const size_t smem = static_cast<size_t>(persist_layout<D, K, NST>().total);
+    void (*fn)(PersistParams) = kmeans_persist_kernel<D, K, R, NST, MINB, MODE>;
+    const int64_t ntiles = std::max<int64_t>(ceil_div(n, THREADS * R), 1);
+    const size_t smem = static_cast<size_t>(persist_layout<D, K, R, NST>().total);
     if (smem > 227 * 1024) return false;
     DNDC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int occ = 0;
@@ -1950,16 +1957,27 @@ static bool try_persist(dndc_ctx* ctx, int64_t n, PersistPlan& P, const char* na
     return true;
 }
 
-// DNDC_PERSIST=0 disables the one-launch fit; DNDC_PERSIST=s2b4|s3b3|s4b2 picks
-// the (stages, CTAs/SM) instantiation (A/B timing).
+// Iterations that sum every row before the delta iterations take over
+// (DNDC_FULL_ITERS overrides; at least 1: a delta needs previous labels).
+static int persist_full_iters() {
+    const char* e = std::getenv("DNDC_FULL_ITERS");
+    return e ? std::max(1, std::atoi(e)) : KS_FULL_ITERS;
+}
+
+// DNDC_PERSIST=0 disables the persistent fit; DNDC_PERSIST_DELTA=r4|r4s3
+// picks the delta kernel's (rows per thread, stages) instantiation (A/B timing).
 static bool plan_persist(dndc_ctx* ctx, int k, int m, int64_t n_local, PersistPlan& P) {
     const char* e = std::getenv("DNDC_PERSIST");
-    const std::string v = e ? e : "";
-    if (v == "0") return false;
+    if (e && std::string(e) == "0") return false;
     if (m == 18 && k == 8) {
-        if (v == "s3b3") return try_persist<18, 8, 3, 3>(ctx, n_local, P, "kmeans_persist_kernel<18,8,3,3>");
-        if (v == "s4b2") return try_persist<18, 8, 4, 2>(ctx, n_local, P, "kmeans_persist_kernel<18,8,4,2>");
-        return try_persist<18, 8, 2, 4>(ctx, n_local, P, "kmeans_persist_kernel<18,8,2,4>");
+        using namespace persist;
+        if (!try_persist<18, 8, 2, 2, 4, FULL_ONLY>(ctx, n_local, P.full, "kmeans_persist_kernel<18,8,R2,S2,full>"))
+            return false;
+        const char* d = std::getenv("DNDC_PERSIST_DELTA");
+        const std::string v = d ? d : "";
+        if (v == "r4s3") return try_persist<18, 8, 4, 3, 2, DELTA_ONLY>(ctx, n_local, P.delta, "kmeans_persist_kernel<18,8,R4,S3,delta>");
+        if (v == "r4") return try_persist<18, 8, 4, 2, 3, DELTA_ONLY>(ctx, n_local, P.delta, "kmeans_persist_kernel<18,8,R4,S2,delta>");
+        return try_persist<18, 8, 2, 2, 4, DELTA_ONLY>(ctx, n_local, P.delta, "kmeans_persist_kernel<18,8,R2,S2,delta>");
     }
     return false;
 }
@@ -2025,57 +2043,66 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     // (slots are allocated here, outside the capture: cudaMalloc is not capturable)
     unsigned long long* acc3 =
         persist ? static_cast<unsigned long long*>(ctx->slot("km_pacc", sizeof(unsigned long long) * 3 * S)) : nullptr;
-    unsigned* words = persist ? static_cast<unsigned*>(ctx->slot("km_pwords", sizeof(unsigned) * 4)) : nullptr;
+    unsigned* words = persist ? static_cast<unsigned*>(ctx->slot("km_pwords", sizeof(unsigned) * 4)) : nullptr;  // arrive/go x 2 launches
     double* gst = persist ? static_cast<double*>(ctx->slot("km_pgstats", sizeof(double) * 2 * S)) : nullptr;
     unsigned* tctr = persist ? static_cast<unsigned*>(ctx->slot("km_ptiles", sizeof(unsigned) * max_iter)) : nullptr;
-    const int64_t lab_stride = (n_local + 15) / 16 * 16;
-    int8_t* plab = persist ? static_cast<int8_t*>(ctx->slot("km_plab", 2 * static_cast<size_t>(lab_stride))) : nullptr;
+    int8_t* plab = persist ? static_cast<int8_t*>(ctx->slot("km_plab", static_cast<size_t>(n_local))) : nullptr;
     unsigned long long* pmarks = nullptr;
     if (persist && std::getenv("DNDC_PERSIST_TRACE")) {
-        ctx->persist_trace_len = static_cast<int64_t>(max_iter) * (2 * PP.grid + 2);
-        ctx->persist_trace_grid = PP.grid;
+        const int tg = std::max(PP.full.grid, PP.delta.grid);
+        ctx->persist_trace_len = static_cast<int64_t>(max_iter) * (2 * tg + 2);
+        ctx->persist_trace_grid = tg;
         pmarks = static_cast<unsigned long long*>(
             ctx->slot("km_pmarks", sizeof(unsigned long long) * ctx->persist_trace_len));
     }
     auto record_persist = [&](cudaStream_t st) {
-        persist_reset_kernel<<<1, 256, 0, st>>>(b.flags, b.refined, acc3, 3 * S, words, words + 1, tctr, max_iter);
+        persist_reset_kernel<<<1, 256, 0, st>>>(b.flags, b.refined, acc3, 3 * S, words, 4, tctr, max_iter);
+        const int F = std::max(1, std::min(persist_full_iters(), max_iter));
         PersistParams pp{};
         pp.x = reinterpret_cast<const float*>(x_local);
         pp.n = n_local;
         pp.max_iter = max_iter;
-        pp.full_iters = std::max(1, std::min(KS_FULL_ITERS, max_iter));
+        pp.full_iters = F;
         pp.tol = tol;
         pp.c64_init = b.c64;
         pp.c64_out = b.c64;
+        pp.run_io = b.running;
         pp.trace = b.trace;
         pp.disp = b.disp;
         pp.flags = b.flags;
         pp.sx2 = b.sx2;
         pp.acc = acc3;
-        pp.arrive = words;
-        pp.go = words + 1;
         pp.gstats = gst;
         pp.refined = b.refined;
         pp.world = ctx->world;
         pp.rank = ctx->rank;
         pp.peers = ctx->world > 1 ? ctx->peer_bases_dev : nullptr;
         pp.labels = plab;
-        pp.lab_stride = lab_stride;
         pp.tile_ctr = tctr;
-        pp.static_tiles = PP.static_tiles;
         pp.trace_marks = pmarks;
+        pp.trace_grid = ctx->persist_trace_grid;
         if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[0], st, cudaEventRecordExternal));
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(PP.grid);
-        cfg.blockDim = dim3(persist::THREADS);
-        cfg.dynamicSmemBytes = PP.smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        DNDC_CUDA(cudaLaunchKernelEx(&cfg, PP.fn, pp));
+        auto launch = [&](const PersistLaunch& L, int it0, int it1, unsigned* arrive, unsigned* go) {
+            PersistParams q = pp;
+            q.it_begin = it0;
+            q.it_end = it1;
+            q.arrive = arrive;
+            q.go = go;
+            q.static_tiles = L.static_tiles;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(L.grid);
+            cfg.blockDim = dim3(persist::THREADS);
+            cfg.dynamicSmemBytes = L.smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+            attr[0].val.cooperative = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            DNDC_CUDA(cudaLaunchKernelEx(&cfg, L.fn, q));
+        };
+        launch(PP.full, 0, F, words, words + 1);
+        if (F < max_iter) launch(PP.delta, F, max_iter, words + 2, words + 3);
         if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[1], st, cudaEventRecordExternal));
     };
     auto record = [&](cudaStream_t st) {
@@ -2162,10 +2189,10 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     DNDC_CUDA(cudaStreamWaitEvent(s, ctx->ev_b, 0));
     // reset + per iteration: assign (fused) | [tile reset,] assign, reduce, update
     // (persistent: reset + the one cooperative launch)
-    ctx->launches += persist ? 2ull : 1 + (fuse ? 1ull : A.small ? 4ull : 3ull) * max_iter;
+    ctx->launches += persist ? (max_iter > persist_full_iters() ? 3ull : 2ull) : 1 + (fuse ? 1ull : A.small ? 4ull : 3ull) * max_iter;
     if (ctx->world > 1) ctx->counters.allgathers += max_iter;
     }
-    ctx->last_kernel = persist ? PP.name : "";
+    ctx->last_kernel = persist ? (max_iter > persist_full_iters() ? PP.delta.name : PP.full.name) : "";
 
     // ---- results
     const size_t hb = sizeof(double) * (k * m + max_iter) + 64;

@@ -49,16 +49,24 @@
 #pragma once
 
 namespace persist {
-constexpr int THREADS = 128, W = THREADS / 32, R = 2, TILE = THREADS * R, VW = W * R, SCR = 8;
+// SCR: changed rows a warp queues (values + labels) before it moves them
+// between the clusters' sums in one pass (the per-row cost of small batches
+// was ~70 issue slots per changed row, r2 ncu)
+constexpr int THREADS = 128, W = THREADS / 32, SCR = 32;
+// MODE of an instantiation: iterations that accumulate every row (full), only
+// the rows whose label changed (delta), or both in one launch
+enum { BOTH = 0, FULL_ONLY = 1, DELTA_ONLY = 2 };
 }
 
 struct PersistParams {
     const float* x;
     int64_t n;                   // rows of this rank's shard
     int max_iter, full_iters;
+    int it_begin, it_end;        // this launch runs iterations [it_begin, it_end)
     double tol;
-    const double* c64_init;      // seeded centroids (k*m)
-    double* c64_out;             // final master centroids
+    const double* c64_init;      // centroids before iteration it_begin (k*m)
+    double* c64_out;             // centroids after the last iteration run (may alias c64_init)
+    double* run_io;              // running sums/counts [S]: read at it_begin (delta), written at the end
     double* trace;               // [max_iter] inertia
     double* disp;                // [max_iter] max centroid displacement
     int* flags;                  // [0] stopped early, [1] iterations run, [2] invalid input, [3] timeout
@@ -70,13 +78,13 @@ struct PersistParams {
     unsigned long long* refined; // rows re-decided in f64 (all iterations)
     int world, rank;
     void* const* peers;          // world > 1: exchange regions of every rank (NVLink)
-    int8_t* labels;              // 2 x lab_stride: labels of iteration i in buffer i & 1
-    int64_t lab_stride;          // n rounded up to 16 (bulk copies need 16-byte aligned sources)
+    int8_t* labels;              // [n] each row's label, updated in place (delta: changed rows only)
     unsigned* tile_ctr;          // [max_iter] dynamic tile counters (zero at launch)
     int static_tiles;            // J0: static tiles per CTA per iteration
     // optional %globaltimer trace (DNDC_PERSIST_TRACE): per iteration and CTA
     // [0] tiles done, [1] barrier passed; per iteration (CTA 0) [2] start, [3] update done
     unsigned long long* trace_marks;
+    int trace_grid;  // row stride of trace_marks: 2 * trace_grid + 2 per iteration
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -90,10 +98,10 @@ struct PersistLayout {
         lbars, total;
 };
 
-template <int D, int K, int NST>
+template <int D, int K, int R, int NST>
 __host__ __device__ constexpr PersistLayout persist_layout() {
     using namespace persist;
-    constexpr int KD = K * D, S = KD + K, DP = (D + 3) / 4 * 4;
+    constexpr int KD = K * D, S = KD + K, DP = (D + 3) / 4 * 4, TILE = THREADS * R, VW = W * R;
     PersistLayout l{};
     int o = 0;
     auto take = [&](int bytes) {
@@ -107,7 +115,7 @@ __host__ __device__ constexpr PersistLayout persist_layout() {
     l.scr = take(W * SCR * D * 4 > (KD + K) * 8 ? W * SCR * D * 4 : (KD + K) * 8);  // also old c / |c|^2 in the update
     l.scl = take(W * 2 * SCR * 4);
     l.cnt = take(VW * K * 4);
-    l.tab = take((K * DP + K) * 4);
+    l.tab = take((K * DP + 2 * K) * 4);
     l.run = take(S * 8);
     l.c64 = take(KD * 8);
     l.cn64 = take(K * 8);
@@ -135,7 +143,7 @@ __device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
 
 // fp32 top-2 of R rows against the table in shared memory: T = [K][DP] of
 // -2 c (DP = D rounded up to 4, 16-byte rows: one LDS.128 feeds 2R FFMA2) and
-// [K] |c|^2.  Same operation chain as small_top2 (so the same error bound).
+// [K] pairs (|c|^2, 0).  Same operation chain as small_top2 (so the same error bound).
 template <int D, int K, int R>
 __device__ __forceinline__ void persist_top2(const float2 (&xv)[R][D / 2], const float* __restrict__ T,
                                              float (&b1)[R], float (&b2)[R], int (&i1)[R]) {
@@ -152,9 +160,11 @@ __device__ __forceinline__ void persist_top2(const float2 (&xv)[R][D / 2], const
         float2 sp[JG][R];
 #pragma unroll
         for (int u = 0; u < JG; ++u) {
-            const float cn = T[K * DP + j0 + u];
+            // (|c_j|^2, 0) as one pair from the table: the first FFMA2 adds it
+            // directly (no register moves to build the accumulator)
+            const float2 cn = *reinterpret_cast<const float2*>(T + K * DP + 2 * (j0 + u));
 #pragma unroll
-            for (int h = 0; h < R; ++h) sp[u][h] = make_float2(cn, 0.f);
+            for (int h = 0; h < R; ++h) sp[u][h] = cn;
         }
 #pragma unroll
         for (int f4 = 0; f4 < DP / 4; ++f4) {
@@ -199,7 +209,8 @@ __device__ __forceinline__ void persist_tables(const double* c64, double* cn64, 
             n32 += static_cast<double>(c32) * static_cast<double>(c32);
         }
         for (int f = D; f < DP; ++f) tab[j * DP + f] = 0.f;
-        tab[K * DP + j] = static_cast<float>(n32);
+        tab[K * DP + 2 * j] = static_cast<float>(n32);
+        tab[K * DP + 2 * j + 1] = 0.f;
         cn64[j] = n64;
         cmax = sqrt(n32);
         cnmax = static_cast<double>(static_cast<float>(n32));
@@ -214,15 +225,16 @@ __device__ __forceinline__ void persist_tables(const double* c64, double* cn64, 
     }
 }
 
-template <int D, int K, int NST, int MINB>
+template <int D, int K, int R, int NST, int MINB, int MODE>
 __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(PersistParams p) {
     using namespace persist;
     static_assert(D % 2 == 0 && D <= 64 && K <= 32, "persistent kernel shape");
+    constexpr int TILE = THREADS * R, VW = W * R;
     constexpr int L = D / 2;                 // lanes per row in the run sums (float2 each)
     constexpr int GR = L <= 32 ? 32 / L : 1; // rows summed in parallel per warp
     constexpr int KD = K * D, S = KD + K;
     constexpr int JW = (K + W - 1) / W;      // clusters owned per warp in the run sums
-    constexpr PersistLayout LY = persist_layout<D, K, NST>();
+    constexpr PersistLayout LY = persist_layout<D, K, R, NST>();
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* tiles = reinterpret_cast<float*>(smem_raw + LY.tiles);
@@ -263,7 +275,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             mbar_init(&lbars[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        *s_git = 0;
+        *s_git = p.it_begin;
         *s_gj = 0;
     }
     if (tid < NST) {
@@ -272,6 +284,8 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
         lcnt[tid] = 0;
     }
     for (int e = tid; e < KD; e += THREADS) c64s[e] = p.c64_init[e];
+    if (MODE == DELTA_ONLY)
+        for (int e = tid; e < S; e += THREADS) run[e] = p.run_io[e];
     __syncthreads();
     persist_tables<D, K>(c64s, cn64s, tab, misc);
     // fixed-point scale of the sums: n max|x| < 2^e
@@ -291,7 +305,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
     auto issue = [&](int s, int cur) {
         int git = *s_git;
         int64_t tile = -1;
-        while (git < p.max_iter) {
+        while (git < p.it_end) {
             const int j = *s_gj;
             if (j < J0) {
                 const int64_t t = blockIdx.x + static_cast<int64_t>(j) * G;
@@ -318,10 +332,10 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             return;
         }
         const int64_t rows = min(static_cast<int64_t>(TILE), p.n - tile * TILE);
-        const bool want_lab = git >= p.full_iters;  // delta iteration: previous labels needed
+        const bool want_lab = MODE == DELTA_ONLY || (MODE == BOTH && git >= p.full_iters);  // delta: previous labels
         if (want_lab && git <= cur) {
             bulk_load2(tiles + s * TILE * D, p.x + tile * TILE * D, static_cast<uint32_t>(rows * D * 4),
-                       slab + s * TILE, p.labels + static_cast<int64_t>((git - 1) & 1) * p.lab_stride + tile * TILE,
+                       slab + s * TILE, p.labels + tile * TILE,
                        static_cast<uint32_t>(rows), &bars[s]);
         } else {
             bulk_load(tiles + s * TILE * D, p.x + tile * TILE * D, static_cast<uint32_t>(rows * D * 4), &bars[s]);
@@ -333,7 +347,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
         const int64_t tile = stile[s];
         const int64_t rows = min(static_cast<int64_t>(TILE), p.n - tile * TILE);
         int8_t* dst = slab + s * TILE;
-        const int8_t* src = p.labels + static_cast<int64_t>((git - 1) & 1) * p.lab_stride + tile * TILE;
+        const int8_t* src = p.labels + tile * TILE;
         const uint32_t body = static_cast<uint32_t>(rows) & ~15u;
         for (uint32_t b = body; b < static_cast<uint32_t>(rows); ++b) dst[b] = src[b];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -348,18 +362,19 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                 : "memory");
     };
     if (tid == 0)
-        for (int s = 0; s < NST; ++s) issue(s, 0);
+        for (int s = 0; s < NST; ++s) issue(s, p.it_begin);
     __syncthreads();
 
-    const bool invalid = p.flags[2] != 0;
+    const bool invalid = p.flags[0] != 0;  // invalid input, or converged in an earlier launch
     unsigned long long refined = 0;
     int64_t g = 0;  // stages consumed so far (stage g % NST, phase (g / NST) & 1)
     const int gq = lane / L, q = lane % L;
     bool stop = invalid;
-    for (int it = 0; it < p.max_iter && !stop; ++it) {
-        const bool full = it < p.full_iters;
-        unsigned long long* tm = p.trace_marks ? p.trace_marks + static_cast<int64_t>(it) * (2 * G + 2) : nullptr;
-        if (tm && blockIdx.x == 0 && tid == 0) tm[2 * G] = gtimer();
+    for (int it = p.it_begin; it < p.it_end && !stop; ++it) {
+        const bool full = MODE == FULL_ONLY || (MODE == BOTH && it < p.full_iters);
+        const int TG = p.trace_grid;
+        unsigned long long* tm = p.trace_marks ? p.trace_marks + static_cast<int64_t>(it) * (2 * TG + 2) : nullptr;
+        if (tm && blockIdx.x == 0 && tid == 0) tm[2 * TG] = gtimer();
         const float tau = 4.f * static_cast<float>(D + 3) * 0x1.0p-24f *
                           (static_cast<float>(misc[1]) +
                            2.f * sqrtf(static_cast<float>(D)) * xabs_f * static_cast<float>(misc[0]));
@@ -374,7 +389,25 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
         long long wsum[JW][2];
 #pragma unroll
         for (int jj = 0; jj < JW; ++jj) wsum[jj][0] = wsum[jj][1] = 0ll;
-        int8_t* lab_out = p.labels + static_cast<int64_t>(it & 1) * p.lab_stride;
+        int8_t* lab_out = p.labels;
+        int qn = 0;  // rows in this warp's change queue (warp-uniform)
+        auto flush_queue = [&]() {
+            __syncwarp();
+            const float* wscr = scr + warp * SCR * D;
+            const int* wscl = scl + warp * 2 * SCR;
+            long long* acc = wacc + warp * KD;
+            for (int c = 0; c < qn; ++c) {
+                const int nl = wscl[2 * c], ol = wscl[2 * c + 1];
+                if (lane < K) cnt_delta += (lane == nl) - (lane == ol);
+#pragma unroll
+                for (int f = lane; f < D; f += 32) {
+                    const long long v = __float2ll_rn(wscr[c * D + f] * qscale);
+                    acc[nl * D + f] += v;
+                    if (ol >= 0) acc[ol * D + f] -= v;
+                }
+            }
+            __syncwarp();
+        };
 
         for (;; ++g) {
             const int s = static_cast<int>(g % NST);
@@ -411,7 +444,19 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                 }
                 float b1[R], b2[R];
                 int i1[R];
+#ifdef KP_EXP_STREAM
+#pragma unroll
+                for (int h = 0; h < R; ++h) {  // timing experiment only: stream, no scores
+                    float a = 0.f;
+#pragma unroll
+                    for (int f = 0; f < L; ++f) a += xv[h][f].x + xv[h][f].y;
+                    b1[h] = a;
+                    b2[h] = a + 1e30f;
+                    i1[h] = prevl[h] < 0 ? 0 : prevl[h];
+                }
+#else
                 persist_top2<D, K, R>(xv, tab, b1, b2, i1);
+#endif
 #pragma unroll
                 for (int h = 0; h < R; ++h) {
                     const int row = tid + h * THREADS;
@@ -424,51 +469,33 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                             label[h] = ref_argmin<float>(p.x + gr * D, D, c64s, cn64s, K);
                             ++refined;
                         }
-                        lab_out[gr] = static_cast<int8_t>(label[h]);
+                        if (label[h] != prevl[h]) lab_out[gr] = static_cast<int8_t>(label[h]);
                     }
                 }
-                // changed rows: their fixed-point values moved from the old
-                // cluster's sums to the new one's, lane = feature (int64: any order)
-                float* wscr = scr + warp * SCR * D;
-                int* wscl = scl + warp * 2 * SCR;
-                long long* acc = wacc + warp * KD;
+                // changed rows: queued per warp (values + labels), moved from the
+                // old cluster's sums to the new one's when the queue fills or the
+                // iteration ends, lane = feature, int64 fixed point (any order)
+#ifdef KP_EXP_NOACC
+                continue;  // timing experiment only: no accumulation of changed rows
+#endif
 #pragma unroll
                 for (int h = 0; h < R; ++h) {
                     const bool ch = label[h] < K && label[h] != prevl[h];
-                    unsigned mask = __ballot_sync(FULL, ch);
-                    while (mask) {
-                        unsigned batch = mask;
-                        if (__popc(batch) > SCR) {
-                            batch = 0u;
-                            unsigned rest = mask;
-#pragma unroll
-                            for (int i = 0; i < SCR; ++i) {
-                                batch |= rest & (0u - rest);
-                                rest &= rest - 1u;
-                            }
-                        }
-                        mask &= ~batch;
-                        if ((batch >> lane) & 1u) {
-                            const int pos = __popc(batch & ((1u << lane) - 1u));
-#pragma unroll
-                            for (int f = 0; f < L; ++f) *reinterpret_cast<float2*>(wscr + pos * D + 2 * f) = xv[h][f];
-                            wscl[2 * pos] = label[h];
-                            wscl[2 * pos + 1] = prevl[h];
-                        }
-                        __syncwarp();
-                        const int nch = __popc(batch);
-                        for (int c = 0; c < nch; ++c) {
-                            const int nl = wscl[2 * c], ol = wscl[2 * c + 1];
-                            if (lane < K) cnt_delta += (lane == nl) - (lane == ol);
-#pragma unroll
-                            for (int f = lane; f < D; f += 32) {
-                                const long long v = __float2ll_rn(wscr[c * D + f] * qscale);
-                                acc[nl * D + f] += v;
-                                if (ol >= 0) acc[ol * D + f] -= v;
-                            }
-                        }
-                        __syncwarp();
+                    const unsigned mask = __ballot_sync(FULL, ch);
+                    if (!mask) continue;
+                    if (qn + __popc(mask) > SCR) {
+                        flush_queue();
+                        qn = 0;
                     }
+                    if (ch) {
+                        const int pos = qn + __popc(mask & ((1u << lane) - 1u));
+                        float* dst = scr + (warp * SCR + pos) * D;
+#pragma unroll
+                        for (int f = 0; f < L; ++f) *reinterpret_cast<float2*>(dst + 2 * f) = xv[h][f];
+                        scl[(warp * SCR + pos) * 2] = label[h];
+                        scl[(warp * SCR + pos) * 2 + 1] = prevl[h];
+                    }
+                    qn += __popc(mask);
                 }
                 continue;
             }
@@ -587,6 +614,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             }
             if (tid == 0) consumed[s] = 0xFFFFFFFFu;  // released at the next tile's count barrier
         }
+        if (!full && qn > 0) flush_queue();
         __syncthreads();  // every warp is done with this iteration's tiles
         // a full iteration hands its last stage back only now (it was the sort buffer)
         if (full && tid == 0 && g > 0 && consumed[(g - 1) % NST] == 0xFFFFFFFFu) {
@@ -630,7 +658,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
         __syncthreads();
 
         // ---- grid barrier (+ the cross-rank exchange on the last arrival)
-        const unsigned target = static_cast<unsigned>(G) * static_cast<unsigned>(it + 1);
+        const unsigned target = static_cast<unsigned>(G) * static_cast<unsigned>(it + 1 - p.it_begin);
         if (tid == 0) {
             __threadfence();
             const unsigned old = atomicAdd(p.arrive, 1u);
@@ -678,10 +706,10 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             }
             __threadfence();
             __syncthreads();
-            if (tid == 0) st_release_gpu_u32(p.go, static_cast<unsigned>(it + 1));
+            if (tid == 0) st_release_gpu_u32(p.go, static_cast<unsigned>(it + 1 - p.it_begin));
         } else if (tid == 0) {
             const unsigned* word = p.world > 1 ? p.go : p.arrive;
-            const unsigned want = p.world > 1 ? static_cast<unsigned>(it + 1) : target;
+            const unsigned want = p.world > 1 ? static_cast<unsigned>(it + 1 - p.it_begin) : target;
             const long long t0 = clock64();
             while (ld_acquire_gpu_u32(word) < want) {
                 __nanosleep(32);
@@ -693,7 +721,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             __threadfence();
         }
         __syncthreads();
-        if (tm && tid == 0) tm[G + blockIdx.x] = gtimer();
+        if (tm && tid == 0) tm[TG + blockIdx.x] = gtimer();
         // ---- the folded stats of this iteration -> stat (every CTA the same bits)
         if (p.world > 1) {
             for (int e = tid; e < S; e += THREADS) stat[e] = __ldcg(p.gstats + (it & 1) * S + e);
@@ -751,7 +779,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
         }
         persist_tables<D, K>(c64s, cn64s, tab, misc);
         __syncthreads();
-        if (tm && blockIdx.x == 0 && tid == 0) tm[2 * G + 1] = gtimer();
+        if (tm && blockIdx.x == 0 && tid == 0) tm[2 * TG + 1] = gtimer();
         stop = misc[2] != 0.0;
         // tiles of the next iteration already staged: their previous labels are final now
         if (!stop && tid == 0) {
@@ -768,6 +796,8 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             mbar_wait(&bars[h % NST], static_cast<uint32_t>((h / NST) & 1));
     }
     if (refined) atomicAdd(p.refined, refined);
-    if (blockIdx.x == 0)
+    if (blockIdx.x == 0) {
         for (int e = tid; e < KD; e += THREADS) p.c64_out[e] = c64s[e];
+        for (int e = tid; e < S; e += THREADS) p.run_io[e] = run[e];
+    }
 }

@@ -73,6 +73,23 @@ def main():
     c_ref, t_ref, _ = O.kmeans_fit(O.uniform_f32(n2, 18, 42).astype(np.float64), 8, 10, 0.0, 42, p)
     report("kmeans_fit 200k x 18", rel_dev(model.centroids, c_ref) <= 1e-5 and rel_dev(model.inertia_trace, t_ref) <= 1e-5,
            f"centroids dev={rel_dev(model.centroids, c_ref):.2e} trace dev={rel_dev(model.inertia_trace, t_ref):.2e}")
+    # BASELINE config 1 at full size over p GPUs vs the unmodified reference
+    # (8-rank golden): centroids at 1e-5, labels/counts exact, and the
+    # persistent kernel's in-kernel NVLink exchange bit-identical on every rank
+    gold = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                                "reference_golden.npz"))
+    cgold = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                                 "cfg_golden.npz"))
+    x1 = dnd.random_uniform((5_000_000, 18), 0, 42, comm)
+    m1c = dnd.kmeans_fit(x1, 8, 20, 0.0, 42)
+    lab1 = dnd.gather(dnd.kmeans_predict(m1c, x1))
+    counts = np.bincount(lab1, minlength=8)
+    all1 = [None] * p
+    dist.all_gather_object(all1, m1c.centroids)
+    report("cfg1 5M x 18 vs reference", rel_dev(m1c.centroids, gold["cfg1_centroids"]) <= 1e-5
+           and np.array_equal(counts, cgold["cfg1_counts"]) and all(np.array_equal(all1[0], c) for c in all1),
+           f"dev={rel_dev(m1c.centroids, gold['cfg1_centroids']):.2e} counts_equal={np.array_equal(counts, cgold['cfg1_counts'])}")
+    del x1
     # identical bits on every rank (rank-order fold on every GPU)
     allc = [None] * p
     dist.all_gather_object(allc, model.centroids)

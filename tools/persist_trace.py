@@ -41,12 +41,13 @@ def main():
         return
     m = buf[:n].reshape(args.iters, 2 * G + 2).astype(np.int64)
     t0 = m[0, 2 * G]
-    print(f"grid {G} CTAs; times in us from the first iteration's start")
+    print(f"trace stride {G} CTAs (grids may differ per launch; unused slots are 0); times in us")
     print("iter    start   tiles: first   median     last  released  upd_done  iter_us")
     for it in range(args.iters):
         st = (m[it, 2 * G] - t0) / 1e3
-        td = (m[it, :G] - t0) / 1e3
-        rel = (m[it, G:2 * G] - t0) / 1e3
+        td_raw, rel_raw = m[it, :G], m[it, G:2 * G]
+        td = (td_raw[td_raw > 0] - t0) / 1e3
+        rel = (rel_raw[rel_raw > 0] - t0) / 1e3
         up = (m[it, 2 * G + 1] - t0) / 1e3
         print(f"{it:4d} {st:8.1f}  {td.min():8.1f} {np.median(td):8.1f} {td.max():8.1f}  {rel.max():8.1f}  "
               f"{up:8.1f}  {up - st:7.1f}")
