@@ -740,7 +740,11 @@ __device__ void fused_tail(const FuseArgs& f, const double* part, int S, int KD,
             const long long t0 = clock64();
             while (ld_acquire_sys(mine) < epoch) {
                 __nanosleep(64);
-                if (clock64() - t0 > 40000000000ll) __trap();  // a peer never arrived (~20 s)
+                if (clock64() - t0 > 40000000000ll) {  // a peer never arrived (~20 s): TimeoutError, no trap
+                    atomicExch(f.upd.flags + 3, 1);
+                    atomicExch(f.upd.flags, 1);  // every later launch of the fit returns at once
+                    break;
+                }
             }
         }
         __syncthreads();
@@ -1526,6 +1530,7 @@ __global__ void kmeans_reset_kernel(int* flags, unsigned long long* refined, uns
     for (int i = 0; i < S; ++i) acc64[i] = 0ull;
     flags[0] = flags[2];  // invalid input (validate_fold_kernel): every iteration is skipped
     flags[1] = 0;
+    flags[3] = 0;  // peer timeout (fused exchange)
     *refined = 0ull;
 }
 
@@ -2043,7 +2048,8 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     // (slots are allocated here, outside the capture: cudaMalloc is not capturable)
     unsigned long long* acc3 =
         persist ? static_cast<unsigned long long*>(ctx->slot("km_pacc", sizeof(unsigned long long) * 3 * S)) : nullptr;
-    unsigned* words = persist ? static_cast<unsigned*>(ctx->slot("km_pwords", sizeof(unsigned) * 4)) : nullptr;  // arrive/go x 2 launches
+    // per launch: [0] root arrival, [1..32] group arrivals, [33] go -> 40 words x 2 launches
+    unsigned* words = persist ? static_cast<unsigned*>(ctx->slot("km_pwords", sizeof(unsigned) * 80)) : nullptr;
     double* gst = persist ? static_cast<double*>(ctx->slot("km_pgstats", sizeof(double) * 2 * S)) : nullptr;
     unsigned* tctr = persist ? static_cast<unsigned*>(ctx->slot("km_ptiles", sizeof(unsigned) * max_iter)) : nullptr;
     int8_t* plab = persist ? static_cast<int8_t*>(ctx->slot("km_plab", static_cast<size_t>(n_local))) : nullptr;
@@ -2056,7 +2062,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
             ctx->slot("km_pmarks", sizeof(unsigned long long) * ctx->persist_trace_len));
     }
     auto record_persist = [&](cudaStream_t st) {
-        persist_reset_kernel<<<1, 256, 0, st>>>(b.flags, b.refined, acc3, 3 * S, words, 4, tctr, max_iter);
+        persist_reset_kernel<<<1, 256, 0, st>>>(b.flags, b.refined, acc3, 3 * S, words, 80, tctr, max_iter);
         const int F = std::max(1, std::min(persist_full_iters(), max_iter));
         PersistParams pp{};
         pp.x = reinterpret_cast<const float*>(x_local);
@@ -2101,8 +2107,8 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
             cfg.numAttrs = 1;
             DNDC_CUDA(cudaLaunchKernelEx(&cfg, L.fn, q));
         };
-        launch(PP.full, 0, F, words, words + 1);
-        if (F < max_iter) launch(PP.delta, F, max_iter, words + 2, words + 3);
+        launch(PP.full, 0, F, words, words + 33);
+        if (F < max_iter) launch(PP.delta, F, max_iter, words + 40, words + 73);
         if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[1], st, cudaEventRecordExternal));
     };
     auto record = [&](cudaStream_t st) {
@@ -2130,8 +2136,11 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
             }
             if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[2 * it], st, cudaEventRecordExternal));
             if (A.small && !fuse) zero_u32_kernel<<<1, 32, 0, st>>>(tile_ctr, 1);
+            // static tile assignment (no tile counter): every CTA's f64 partial
+            // covers the same rows in every run, so the fit is bit-repeatable
+            // (the dynamic counter made it depend on arrival order)
             A.launch(b, x_local, n_local, m, k, true, nullptr, true, st, delta ? lab8 : nullptr, lab8,
-                     fuse ? &fa : nullptr, A.small ? tile_ctr : nullptr);
+                     fuse ? &fa : nullptr, nullptr);
             if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[2 * it + 1], st, cudaEventRecordExternal));
             if (fuse) continue;
             reduce_partials_kernel<<<(S + 7) / 8, 256, 0, st>>>(b.partials, A.grid_for(delta), S, b.stats, b.flags);

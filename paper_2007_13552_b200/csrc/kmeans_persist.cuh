@@ -72,7 +72,7 @@ struct PersistParams {
     int* flags;                  // [0] stopped early, [1] iterations run, [2] invalid input, [3] timeout
     const double* sx2;           // [2] global sum |x|^2, [3] max |x| of the shard
     unsigned long long* acc;     // 3 x S fixed-point accumulators (zero at launch)
-    unsigned* arrive;            // grid arrival counter (zero at launch)
+    unsigned* arrive;            // [33] grid arrival: root + 32 group counters (zero at launch)
     unsigned* go;                // world > 1: iterations released by the finaliser (zero at launch)
     double* gstats;              // world > 1: 2 x S rank-folded stats
     unsigned long long* refined; // rows re-decided in f64 (all iterations)
@@ -658,11 +658,19 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
         __syncthreads();
 
         // ---- grid barrier (+ the cross-rank exchange on the last arrival)
-        const unsigned target = static_cast<unsigned>(G) * static_cast<unsigned>(it + 1 - p.it_begin);
+        // two-level arrival: CTA b counts in group b % NG, the last of a group in
+        // the root word (592 same-address atomics serialised at one L2 slice)
+        const int NG = G < 32 ? G : 32;
+        const unsigned round = static_cast<unsigned>(it + 1 - p.it_begin);
+        const unsigned target = static_cast<unsigned>(NG) * round;
         if (tid == 0) {
             __threadfence();
-            const unsigned old = atomicAdd(p.arrive, 1u);
-            *s_last = old == target - 1u;
+            const int grp = blockIdx.x % NG;
+            const unsigned gsize = static_cast<unsigned>((G - 1 - grp) / NG + 1);
+            const unsigned oldg = atomicAdd(p.arrive + 1 + grp, 1u);
+            int last = 0;
+            if (oldg == gsize * round - 1u) last = atomicAdd(p.arrive, 1u) == target - 1u ? 1 : 0;
+            *s_last = last;
         }
         __syncthreads();
         if (p.world > 1 && *s_last) {
@@ -712,46 +720,42 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             const unsigned want = p.world > 1 ? static_cast<unsigned>(it + 1 - p.it_begin) : target;
             const long long t0 = clock64();
             while (ld_acquire_gpu_u32(word) < want) {
-                __nanosleep(32);
+                __nanosleep(20);
                 if (clock64() - t0 > 40000000000ll) {
                     atomicExch(p.flags + 3, 1);
                     break;
                 }
             }
-            __threadfence();
         }
         __syncthreads();
         if (tm && tid == 0) tm[TG + blockIdx.x] = gtimer();
-        // ---- the folded stats of this iteration -> stat (every CTA the same bits)
-        if (p.world > 1) {
-            for (int e = tid; e < S; e += THREADS) stat[e] = __ldcg(p.gstats + (it & 1) * S + e);
-        } else {
-            for (int e = tid; e < S; e += THREADS) {
+        // ---- the folded stats of this iteration, added to the running sums
+        // (delta iterations) -- every CTA the same bits -- and the old state
+        for (int e = tid; e < S; e += THREADS) {
+            double v;
+            if (p.world > 1) {
+                v = __ldcg(p.gstats + (it & 1) * S + e);
+            } else {
                 const long long qv = static_cast<long long>(__ldcg(acc_it + e));
-                stat[e] = e < KD ? ldexp(static_cast<double>(qv), -shift) : static_cast<double>(qv);
+                v = e < KD ? ldexp(static_cast<double>(qv), -shift) : static_cast<double>(qv);
             }
+            if (!full) v += run[e];  // delta iterations: changes added to the running sums
+            run[e] = v;
+            if (e < KD) cold[e] = c64s[e];
         }
-        for (int e = tid; e < KD; e += THREADS) cold[e] = c64s[e];
         if (tid < K) cnold[tid] = cn64s[tid];
         __syncthreads();
         if (__ldcv(p.flags + 3)) {
             stop = true;
             break;
         }
-        // ---- update (cluster.cpp:123-150), identical in every CTA
-        for (int e = tid; e < S; e += THREADS) {
-            double v = stat[e];
-            if (!full) v += run[e];  // delta iterations: changes added to the running sums
-            run[e] = v;
-        }
-        __syncthreads();
-        for (int e = tid; e < KD; e += THREADS) {
-            const int cl = e / D;
-            const double count = run[KD + cl];
-            c64s[e] = count > 0.0 ? run[e] / count : cold[e];  // empty cluster keeps its centroid
-        }
-        __syncthreads();
+        // ---- update (cluster.cpp:123-150) by warp 0, identical in every CTA
         if (warp == 0) {
+            for (int e = lane; e < KD; e += 32) {
+                const double count = run[KD + e / D];
+                c64s[e] = count > 0.0 ? run[e] / count : cold[e];  // empty cluster keeps its centroid
+            }
+            __syncwarp();
             double inertia_part = 0.0, dmax = 0.0;
             if (lane < K) {
                 const double count = run[KD + lane];
@@ -776,8 +780,8 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                 }
                 misc[2] = dmax < p.tol ? 1.0 : 0.0;
             }
+            persist_tables<D, K>(c64s, cn64s, tab, misc);
         }
-        persist_tables<D, K>(c64s, cn64s, tab, misc);
         __syncthreads();
         if (tm && blockIdx.x == 0 && tid == 0) tm[2 * TG + 1] = gtimer();
         stop = misc[2] != 0.0;

@@ -44,6 +44,7 @@ struct LassoCtl {
     int done;
     int sweep;          // sweeps completed
     int pending_j;      // NCCL fallback: coordinate whose update waits for the allreduce
+    int timeout;        // a peer never arrived at the NVLink sum: every later step is a no-op
 };
 
 struct LassoArgs {
@@ -110,7 +111,11 @@ static __device__ double peer_sum(const LassoArgs& a, double v, unsigned long lo
         const long long t0 = clock64();
         while (ld_acquire_sys_u64(mine) < epoch) {
             __nanosleep(64);
-            if (clock64() - t0 > 40000000000ll) __trap();  // a peer never arrived (~20 s)
+            if (clock64() - t0 > 40000000000ll) {  // a peer never arrived (~20 s): TimeoutError, no trap
+                a.ctl->timeout = 1;
+                a.ctl->done = 1;
+                break;
+            }
         }
     }
     __syncthreads();
@@ -338,7 +343,7 @@ static void lasso_fit(dndc_ctx* ctx, const double* x, int64_t rows, int64_t n_gl
     if (bad_total != 0.0) value_error("lasso_fit: column 0 must be the all-ones bias column");
     mark("allreduce");
 
-    LassoCtl c0{0.0, 0.0, 0.0, 0.0, -1, 0, 0, 0};
+    LassoCtl c0{0.0, 0.0, 0.0, 0.0, -1, 0, 0, 0, 0};
     DNDC_CUDA(cudaMemcpyAsync(ctl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
     DNDC_CUDA(cudaMemsetAsync(w, 0, sizeof(double) * m, s));
     DNDC_CUDA(cudaMemsetAsync(trace, 0, sizeof(double) * sweeps, s));
@@ -367,6 +372,7 @@ static void lasso_fit(dndc_ctx* ctx, const double* x, int64_t rows, int64_t n_gl
         DNDC_CUDA(cudaMemcpyAsync(w_host, w, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
         DNDC_CUDA(cudaMemcpyAsync(trace_host, trace, sizeof(double) * sweeps, cudaMemcpyDeviceToHost, s));
         DNDC_CUDA(cudaStreamSynchronize(s));
+        if (ch.timeout) throw Error(DNDC_ETIMEOUT, "lasso_fit: a peer rank did not arrive at the coordinate sum");
         *sweeps_run = ch.sweep;
         return;
     }
@@ -410,6 +416,9 @@ static void lasso_fit(dndc_ctx* ctx, const double* x, int64_t rows, int64_t n_gl
     DNDC_CUDA(cudaMemcpyAsync(trace_host, trace, sizeof(double) * sweeps, cudaMemcpyDeviceToHost, s));
     DNDC_CUDA(cudaStreamSynchronize(s));
     mark("sweeps");
+    if (ch.timeout)
+        throw Error(DNDC_ETIMEOUT, "lasso_fit: a peer rank did not arrive at the NVLink coordinate sum within the "
+                                   "deadlock timeout (transport.cpp:76-93)");
     *sweeps_run = ch.sweep;
 }
 
