@@ -2000,7 +2000,28 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
                     std::to_string(ext[ctx->rank]));
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
-    const Assigner<T> A = plan<T>(ctx, k, m, n_local, x_local);
+    Assigner<T> A = plan<T>(ctx, k, m, n_local, x_local);
+    // the kernel choice fixes the stats protocol (fused NVLink exchange,
+    // delta vs full sums): every rank must take the same one
+    PersistPlan PP;
+    bool persist = sizeof(T) == 4 && A.small && (ctx->world == 1 || ctx->p2p) && n_local > 0 &&
+                   plan_persist(ctx, k, m, n_local, PP);
+    if (ctx->world > 1) {
+        const int code = (persist ? 1 : 0) | (A.small ? 2 : 0) | (A.tc ? 4 : 0) | (A.tc && A.tc_delta ? 8 : 0);
+        int* dcode = static_cast<int*>(ctx->slot("km_plan", sizeof(int) * (ctx->world + 1)));
+        DNDC_CUDA(cudaMemcpyAsync(dcode + ctx->world, &code, sizeof(int), cudaMemcpyHostToDevice, s));
+        xport_allgather(ctx, dcode + ctx->world, dcode, sizeof(int), s);
+        std::vector<int> all(ctx->world);
+        DNDC_CUDA(cudaMemcpyAsync(all.data(), dcode, sizeof(int) * ctx->world, cudaMemcpyDeviceToHost, s));
+        DNDC_CUDA(cudaStreamSynchronize(s));
+        for (int r = 1; r < ctx->world; ++r)
+            if (all[r] != all[0]) {  // disagreement (e.g. an empty shard): the generic full-sum path everywhere
+                A = Assigner<T>{};
+                A.gen = plan_assign<T>(ctx, k, m, n_local);
+                persist = false;
+                break;
+            }
+    }
     const KmBuffers b = buffers(ctx, k, m, max_iter, A.max_grid());
     const int S = k * m + k;
 
@@ -2039,10 +2060,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     // one launch per iteration (fused tail) on one GPU or with the NVLink
     // peer exchange; otherwise assign -> reduce -> NCCL allgather -> update
     const bool fuse = A.small && (ctx->world == 1 || ctx->p2p) && !std::getenv("DNDC_NO_FUSE");
-    // the whole loop in one cooperative launch where the shape has an instantiation
-    PersistPlan PP;
-    const bool persist = sizeof(T) == 4 && A.small && (ctx->world == 1 || ctx->p2p) && n_local > 0 &&
-                         plan_persist(ctx, k, m, n_local, PP);
+    // (persist: the whole loop in cooperative launches, planned above)
     const int ncounters = 2;
     unsigned* tile_ctr = b.counters + 1;
     // (slots are allocated here, outside the capture: cudaMalloc is not capturable)

@@ -48,6 +48,24 @@
 // readers passed barrier it-1; its first writers wait for barrier it).
 #pragma once
 
+// -DDNDC_CHECKS: device-side bounds checks of the persistent kernel (labels,
+// tiles, queue slots, accumulator indices) for the checked build that
+// tools/sanitize_smoke.py runs (compute-sanitizer is closed on this pool)
+#ifdef DNDC_CHECKS
+#define PCHECK(cond)                                                                              \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("PCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, \
+                   threadIdx.x, #cond);                                                           \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define PCHECK(cond) \
+    do {             \
+    } while (0)
+#endif
+
 namespace persist {
 // SCR: changed rows a warp queues (values + labels) before it moves them
 // between the clusters' sums in one pass (the per-row cost of small batches
@@ -325,6 +343,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             *s_git = git;
             *s_gj = 0;
         }
+        PCHECK(tile < ntiles && git <= p.it_end);
         stile[s] = tile;
         siter[s] = git;
         if (tile < 0) {  // nothing left in the fit: an empty stage ends the consumer's loop
@@ -398,6 +417,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             long long* acc = wacc + warp * KD;
             for (int c = 0; c < qn; ++c) {
                 const int nl = wscl[2 * c], ol = wscl[2 * c + 1];
+                PCHECK(nl >= 0 && nl < K && ol >= -1 && ol < K && nl != ol);
                 if (lane < K) cnt_delta += (lane == nl) - (lane == ol);
 #pragma unroll
                 for (int f = lane; f < D; f += 32) {
@@ -431,6 +451,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                 for (int h = 0; h < R; ++h) {
                     const int row = tid + h * THREADS;
                     prevl[h] = row0 + row < p.n ? static_cast<int>(slab[s * TILE + row]) : -1;
+                    PCHECK(prevl[h] >= -1 && prevl[h] < K);
                 }
                 __threadfence_block();
                 __syncwarp();
@@ -489,6 +510,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                     }
                     if (ch) {
                         const int pos = qn + __popc(mask & ((1u << lane) - 1u));
+                        PCHECK(pos < SCR && label[h] >= 0 && label[h] < K);
                         float* dst = scr + (warp * SCR + pos) * D;
 #pragma unroll
                         for (int f = 0; f < L; ++f) *reinterpret_cast<float2*>(dst + 2 * f) = xv[h][f];
