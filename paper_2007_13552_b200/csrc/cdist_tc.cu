@@ -215,7 +215,9 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
             cdtc_tile_of(t, nrb, ncb, rb, cb);
             const int64_t row0 = rb * BM, col0 = cb * BN;
             const int b = static_cast<int>(tcount & 1);
+#ifndef CDTC_EXP_STOREONLY
             tc::mbar_wait(&tfull[b], static_cast<uint32_t>((tcount / 2) & 1));
+#endif
             tc::tc_fence_after();
             const int64_t gi = row0 + r;
             const float xni = gi < p.nx ? __ldg(p.xn + gi) : 0.f;
@@ -245,7 +247,11 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 const int c0 = cc * BC;
                 float v[BC];
 #pragma unroll
+#ifdef CDTC_EXP_STOREONLY
+                for (int h = 0; h < BC; ++h) v[h] = 0.25f * static_cast<float>(h);  // timing experiment: stores only
+#else
                 for (int h = 0; h < BC / 16; ++h) tc::tmem_ld16(trow + c0 + 16 * h, *reinterpret_cast<float(*)[16]>(v + 16 * h));
+#endif
                 const int64_t gc = col0 + c0;
                 float4 ycur[BC / 4];
 #pragma unroll

@@ -35,11 +35,12 @@
 // Per-iteration protocol (S = k*m + k stats):
 //   tiles    -> CTA int64 partials -> atomicAdd into acc[it % 3] (integer adds commute)
 //   barrier  world == 1: arrival counter reaches G (it + 1), every CTA reads
-//            acc[it % 3] from L2.  world > 1: the last CTA to arrive converts,
-//            stores the rank's stats into every peer's exchange region over
-//            NVLink, waits for every rank's flag (bounded: ~20 s, then flags[3]
-//            = timeout instead of a trap), folds ranks 0..p-1 in order into
-//            gstats and releases the grid through `go`.
+//            acc[it % 3] from L2.  world > 1: the last CTA to arrive converts
+//            and stores the rank's stats into every rank's exchange region over
+//            NVLink, then releases one flag per rank; every CTA of every rank
+//            waits for all ranks' flags in its own region (bounded: ~20 s, then
+//            flags[3] = timeout instead of a trap) and folds ranks 0..p-1 in
+//            order itself -- one NVLink hop, no second release word.
 //   update   every CTA: running sums (+= changes in delta iterations),
 //            c_j = S_j / n_j or kept when empty (cluster.cpp:125-133), reference
 //            order |c_j|^2, fp32 table, the fp32 error-bound inputs; CTA 0
@@ -385,6 +386,8 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
     __syncthreads();
 
     const bool invalid = p.flags[0] != 0;  // invalid input, or converged in an earlier launch
+    // exchange epoch before this launch's first iteration (read before barrier 0)
+    const unsigned long long xbase = p.world > 1 ? *(xchg_flags(p.peers[p.rank], p.world) + p.world) : 0ull;
     unsigned long long refined = 0;
     int64_t g = 0;  // stages consumed so far (stage g % NST, phase (g / NST) & 1)
     const int gq = lane / L, q = lane % L;
@@ -695,53 +698,40 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             *s_last = last;
         }
         __syncthreads();
+        // world > 1: the exchange epoch of this iteration (every CTA read the
+        // base before barrier 0; only the finaliser advances the stored epoch)
+        const unsigned long long epoch = xbase + static_cast<unsigned long long>(it + 1 - p.it_begin);
+        const int xslot = static_cast<int>(epoch & 1);
         if (p.world > 1 && *s_last) {
-            // finaliser: this rank's stats to every peer over NVLink, rank-order fold
-            unsigned long long* s_epoch = reinterpret_cast<unsigned long long*>(misc + 10);
-            if (tid == 0) {
-                __threadfence();
-                unsigned long long* ep = xchg_flags(p.peers[p.rank], p.world) + p.world;
-                *s_epoch = *ep + 1;
-                *ep = *s_epoch;
-            }
-            __syncthreads();
-            const unsigned long long epoch = *s_epoch;
-            const int slot = static_cast<int>(epoch & 1);
+            // finaliser: this rank's stats into every rank's exchange region
+            // (NVLink stores; its own too), then one release flag per rank
+            if (tid == 0) *(xchg_flags(p.peers[p.rank], p.world) + p.world) = epoch;
             for (int e = tid; e < S; e += THREADS) {
                 const long long qv = static_cast<long long>(__ldcg(acc_it + e));
                 const double v = e < KD ? ldexp(static_cast<double>(qv), -shift) : static_cast<double>(qv);
-                for (int r = 0; r < p.world; ++r) xchg_recv(p.peers[r], slot, p.world, p.rank)[e] = v;
+                for (int r = 0; r < p.world; ++r) xchg_recv(p.peers[r], xslot, p.world, p.rank)[e] = v;
             }
             __threadfence_system();
             __syncthreads();
+            if (tid < p.world) st_release_sys(xchg_flags(p.peers[tid], p.world) + p.rank, epoch);
+        }
+        if (p.world > 1) {
+            // every CTA waits for every rank's stats in its own region (no
+            // second hop through a release word) and folds them itself below
             if (tid < p.world) {
-                st_release_sys(xchg_flags(p.peers[tid], p.world) + p.rank, epoch);
                 const unsigned long long* mine_f = xchg_flags(p.peers[p.rank], p.world) + tid;
                 const long long t0 = clock64();
                 while (ld_acquire_sys(mine_f) < epoch) {
-                    __nanosleep(64);
-                    if (clock64() - t0 > 40000000000ll) {  // a peer never arrived (~20 s): TimeoutError
+                    __nanosleep(32);
+                    if (clock64() - t0 > 40000000000ll) {  // a rank never arrived (~20 s): TimeoutError, no trap
                         atomicExch(p.flags + 3, 1);
                         break;
                     }
                 }
             }
-            __syncthreads();
-            __threadfence();
-            const double* recv = xchg_recv(p.peers[p.rank], slot, p.world, 0);
-            for (int e = tid; e < S; e += THREADS) {
-                double v = 0.0;
-                for (int r = 0; r < p.world; ++r) v += __ldcv(recv + static_cast<int64_t>(r) * XCHG_STATS + e);
-                p.gstats[(it & 1) * S + e] = v;
-            }
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) st_release_gpu_u32(p.go, static_cast<unsigned>(it + 1 - p.it_begin));
         } else if (tid == 0) {
-            const unsigned* word = p.world > 1 ? p.go : p.arrive;
-            const unsigned want = p.world > 1 ? static_cast<unsigned>(it + 1 - p.it_begin) : target;
             const long long t0 = clock64();
-            while (ld_acquire_gpu_u32(word) < want) {
+            while (ld_acquire_gpu_u32(p.arrive) < target) {
                 __nanosleep(20);
                 if (clock64() - t0 > 40000000000ll) {
                     atomicExch(p.flags + 3, 1);
@@ -753,10 +743,12 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
         if (tm && tid == 0) tm[TG + blockIdx.x] = gtimer();
         // ---- the folded stats of this iteration, added to the running sums
         // (delta iterations) -- every CTA the same bits -- and the old state
+        const double* xrecv = p.world > 1 ? xchg_recv(p.peers[p.rank], xslot, p.world, 0) : nullptr;
         for (int e = tid; e < S; e += THREADS) {
             double v;
-            if (p.world > 1) {
-                v = __ldcg(p.gstats + (it & 1) * S + e);
+            if (p.world > 1) {  // rank-order fold (transport.hpp:136-148), identical in every CTA of every rank
+                v = 0.0;
+                for (int r = 0; r < p.world; ++r) v += __ldcv(xrecv + static_cast<int64_t>(r) * XCHG_STATS + e);
             } else {
                 const long long qv = static_cast<long long>(__ldcg(acc_it + e));
                 v = e < KD ? ldexp(static_cast<double>(qv), -shift) : static_cast<double>(qv);

@@ -22,10 +22,21 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     args = ap.parse_args()
     os.environ.setdefault("DNDC_PERSIST_TRACE", "1")
+    import torch
+
     import paper_2007_13552_b200.api as dnd
     from paper_2007_13552_b200 import _lib
 
-    comm = dnd.Communicator(0)
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world > 1:  # under torchrun: one rank per GPU, rank 0 prints its own timeline
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        comm = dnd.Communicator.from_torch_distributed(local)
+    else:
+        comm = dnd.Communicator(0)
     x = dnd.random_uniform((args.rows, 18), 0, 42, comm)
     for _ in range(3):
         dnd.kmeans_fit(x, 8, args.iters, 0.0, 42)
@@ -38,6 +49,8 @@ def main():
     G = grid.value
     if n == 0:
         print("no trace (DNDC_PERSIST_TRACE unset or not the persistent kernel)")
+        return
+    if int(os.environ.get("RANK", 0)) != 0:
         return
     m = buf[:n].reshape(args.iters, 2 * G + 2).astype(np.int64)
     t0 = m[0, 2 * G]
