@@ -1702,6 +1702,7 @@ struct Assigner {
             tp.done = use_done ? b.flags : nullptr;
             tp.prev = tc_delta ? prev : nullptr;
             tp.lab8 = tc_delta ? lab8 : nullptr;
+            tp.xabs = b.sx2 + 3;
             tfn<<<sgrid, tthreads, tsmem, st>>>(tmap, tp);
         } else if (small) {
             DNDC_CUDA(cudaMemcpyToSymbolAsync(c_km_table, b.ctab, sizeof(float) * (k * d + k),

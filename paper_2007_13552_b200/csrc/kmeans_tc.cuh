@@ -36,6 +36,7 @@ struct TcParams {
     const int* done;
     const int8_t* prev;   // delta iterations: last iteration's labels (null: full accumulation)
     int8_t* lab8;         // this iteration's labels (fit only; null in predict)
+    const double* xabs;   // max |x| of the shard: the int64 fixed-point scale of the sums
 };
 
 __host__ __device__ constexpr int tc_pow2_cols(int c) {
@@ -66,22 +67,19 @@ struct TcCfg {
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
     static constexpr int OFF_CN = OFF_BLO + B_BYTES;
     static constexpr int OFF_CNT = OFF_CN + ((K * 4 + 15) / 16) * 16;
-    // per-warpgroup f64 cluster sums (each warp owns clusters wq, wq+4, ...)
+    // one int64 fixed-point accumulator per CTA: [K*D] sums, [K] counts,
+    // shared by the warpgroups (integer atomics: any order gives the same bits)
     static constexpr int OFF_ACC = OFF_CNT + WGS * ((VW * K * 4 + 15) / 16) * 16;
-    static constexpr int OFF_BAR = OFF_ACC + WGS * K * D * 8;
+    static constexpr int OFF_BAR = OFF_ACC + (K * D + K) * 8;
     static constexpr int NBARS = 2 * S + 3 * WGS;
     static constexpr int OFF_TMEM = OFF_BAR + NBARS * 8;
     static constexpr int SMEM = OFF_TMEM + 16;
     static_assert(NS % 16 == 0 && NS <= 256, "MMA N (P*K) must be a multiple of 16, <= 256");
     static_assert(D % 2 == 0 && D <= 64 && K <= 64, "tc kernel shape");
-    static_assert(WGS * K * D * 8 <= WGS * WORK_BYTES, "final combine scratch");
     static_assert(OFF_TMEM + 16 <= 232448, "shared memory");
     static_assert(TILE_BYTES % 1024 == 0 && WORK_BYTES % 1024 == 0, "SW128 tiles need 1024-byte alignment");
-    // delta iterations reuse the count area: 4 counts, 4 warps' slot lists (u8)
-    // and the new/old label per slot (i8); shapes where it does not fit run
-    // full accumulation every iteration
-    static constexpr bool DELTA_OK = P == 1 && K <= 127 && TROWS <= 256 &&
-                                     16 + 4 * 32 * P + 2 * TROWS <= ((VW * K * 4 + 15) / 16) * 16;
+    // delta iterations: each warp moves its own changed rows (int8 labels)
+    static constexpr bool DELTA_OK = P == 1 && K <= 127;
 };
 
 template <int D, int K, int P, int WG_>
@@ -209,14 +207,17 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
         const uint32_t bar_id = 1 + wg;
         const float cmax = p.bounds[0], cnmax = p.bounds[1];
         constexpr float ERR = 4.f * (static_cast<float>(3 * C::KC) * 0x1.0p-24f + 3.f * 0x1.0p-20f);
-        long long count_acc[KL];
-#pragma unroll
-        for (int u = 0; u < KL; ++u) count_acc[u] = 0;
         unsigned long long refined = 0;
         const int g = lane / L, q = lane % L;
-        // cluster sums in shared memory (registers would spill at K = 64)
-        double* acc = reinterpret_cast<double*>(smem + C::OFF_ACC) + wg * KD;
-        for (int e = t; e < KD; e += 128) acc[e] = 0.0;
+        // cluster sums: int64 fixed point at 2^-(61-e), n max|x| < 2^e, shared by
+        // the warpgroups (atomics; integer adds commute)
+        long long* acc = reinterpret_cast<long long*>(smem + C::OFF_ACC);
+        for (int e = tid; e < KD + K; e += C::EPI) acc[e] = 0ll;
+        int e2 = 0;
+        frexp(static_cast<double>(p.n) * (p.xabs ? *p.xabs : 1.0) + 1.0, &e2);
+        const int shift = 61 - e2;
+        const float qscale = ldexpf(1.f, shift);
+        tc::named_sync(3, C::EPI);  // zeroed before any warpgroup adds
 
         for (int64_t it = wg; it < my_tiles; it += WGS) {
             const int st = static_cast<int>(it % S);
@@ -498,69 +499,37 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             if (C::DELTA_OK && p.prev) {
                 // ---------------- delta iteration: only rows whose label changed,
                 // +x into the new cluster and -x out of the old one (the update
-                // adds these to the running sums).  A changed row is parked in
-                // its own thread's lo rows of `work` (free: the tile's MMAs
-                // completed; a warp only writes its own rows, so a slower warp
-                // still deciding near-ties in its own rows is not disturbed),
-                // feature f at K-block f/32, column f%32, unswizzled; a compact
-                // list per warp in row order; every warp walks the whole list and
-                // applies the entries of the clusters it owns (j % 4 == wq), so
-                // each cluster's updates land in row order from one warp.
-                int* qn = cnt;                                                   // [4] counts
-                uint8_t* lst = reinterpret_cast<uint8_t*>(cnt + 4);              // [4][32 * P] slots
-                int8_t* nl = reinterpret_cast<int8_t*>(lst + 4 * 32 * P);        // [TROWS] new label
-                int8_t* ol = nl + C::TROWS;                                      // [TROWS] old label
-                int nq = 0;
+                // adds these to the running sums), each warp on its own: the
+                // changed row is parked in the warp's own rows of `work` (free:
+                // the tile's MMAs completed), lanes over features, int64 atomics
+                // -- no warpgroup barrier, no cross-warp list walk
+                float* wrow = work + wq * 32 * 32;  // this warp's first row slot (K-block 0)
 #pragma unroll
                 for (int h = 0; h < P; ++h) {
                     const bool ch = label[h] < K && label[h] != oldl[h];
-                    const unsigned fm = __ballot_sync(FULL, ch);
-                    if (ch) {
-                        const int slot = t * P + h;
+                    unsigned fm = __ballot_sync(FULL, ch);
+                    while (fm) {
+                        const int src = __ffs(fm) - 1;
+                        fm &= fm - 1;
+                        if (lane == src) {
 #pragma unroll
-                        for (int f = 0; f < D; ++f) work[(f / 32) * PR * 32 + slot * 32 + f % 32] = xval(h * D + f);
-                        nl[slot] = static_cast<int8_t>(label[h]);
-                        ol[slot] = static_cast<int8_t>(oldl[h]);
-                        lst[wq * 32 * P + nq + __popc(fm & ((1u << lane) - 1u))] = static_cast<uint8_t>(slot);
-                    }
-                    nq += __popc(fm);
-                }
-                if (lane == 0) qn[wq] = nq;
-                tc::named_sync(bar_id, 128);
-                for (int w = 0; w < 4; ++w) {
-                    const int cw = qn[w];
-                    for (int i = 0; i < cw; ++i) {
-                        const int slot = lst[w * 32 * P + i];
-                        const int jn = nl[slot], jo = ol[slot];
-                        // features 2*lane, 2*lane+1 (same K-block: 32 is even)
-                        const float2 xv2 = lane < L ? *reinterpret_cast<const float2*>(
-                                                          work + ((2 * lane) / 32) * PR * 32 + slot * 32 + (2 * lane) % 32)
-                                                    : make_float2(0.f, 0.f);
-                        if (jn % 4 == wq && lane < L) {
-                            double2* a = reinterpret_cast<double2*>(acc + jn * D + 2 * lane);
-                            double2 v = *a;
-                            v.x += static_cast<double>(xv2.x);
-                            v.y += static_cast<double>(xv2.y);
-                            *a = v;
+                            for (int f = 0; f < D; ++f) wrow[(f / 32) * PR * 32 + f % 32] = xval(h * D + f);
                         }
-                        if (jo >= 0 && jo % 4 == wq && lane < L) {
-                            double2* a = reinterpret_cast<double2*>(acc + jo * D + 2 * lane);
-                            double2 v = *a;
-                            v.x -= static_cast<double>(xv2.x);
-                            v.y -= static_cast<double>(xv2.y);
-                            *a = v;
+                        __syncwarp();
+                        const int jn = __shfl_sync(FULL, label[h], src), jo = __shfl_sync(FULL, oldl[h], src);
+                        for (int f = lane; f < D; f += 32) {
+                            const long long qv = __float2ll_rn(wrow[(f / 32) * PR * 32 + f % 32] * qscale);
+                            atomicAdd(reinterpret_cast<unsigned long long*>(acc + jn * D + f), static_cast<unsigned long long>(qv));
+                            if (jo >= 0)
+                                atomicAdd(reinterpret_cast<unsigned long long*>(acc + jo * D + f), static_cast<unsigned long long>(-qv));
                         }
-                        if (wq == 0) {
-#pragma unroll
-                            for (int u = 0; u < KL; ++u) {
-                                if (jn / 32 == u && lane == jn % 32) count_acc[u] += 1;
-                                if (jo >= 0 && jo / 32 == u && lane == jo % 32) count_acc[u] -= 1;
-                            }
+                        if (lane == 0) {
+                            atomicAdd(reinterpret_cast<unsigned long long*>(acc + KD + jn), 1ull);
+                            if (jo >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(acc + KD + jo), ~0ull);
                         }
+                        __syncwarp();
                     }
                 }
-                // the next tile's split rewrites `work`: all warps must be done reading it
-                tc::named_sync(bar_id, 128);
                 continue;
             }
 
@@ -605,7 +574,9 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                     }
                     start[u] = carry + incl - total[u];
                     carry += __shfl_sync(FULL, incl, 31);
-                    if (wq == 0) count_acc[u] += total[u];
+                    if (wq == 0 && lane + 32 * u < K && total[u])
+                        atomicAdd(reinterpret_cast<unsigned long long*>(acc + KD + lane + 32 * u),
+                                  static_cast<unsigned long long>(total[u]));
                 }
             }
             // scatter rows into label order (features from registers) -- the lo
@@ -673,12 +644,11 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                             part[u].y += vy;
                         }
                     }
-                    if (g == 0 && q < L) {
-                        double2* a = reinterpret_cast<double2*>(acc + js[u] * D + 2 * q);
-                        double2 v = *a;
-                        v.x += part[u].x;
-                        v.y += part[u].y;
-                        *a = v;
+                    if (g == 0 && q < L) {  // the tile's run sum, once rounded to fixed point
+                        atomicAdd(reinterpret_cast<unsigned long long*>(acc + js[u] * D + 2 * q),
+                                  static_cast<unsigned long long>(llrint(ldexp(part[u].x, shift))));
+                        atomicAdd(reinterpret_cast<unsigned long long*>(acc + js[u] * D + 2 * q + 1),
+                                  static_cast<unsigned long long>(llrint(ldexp(part[u].y, shift))));
                     }
                 }
             }
@@ -687,32 +657,12 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
         }
         if (refined) atomicAdd(p.refined, refined);
         if (accumulate) {
-            // combine the warpgroups in a fixed order (wg 0 + wg 1): sums from
-            // shared memory, counts parked by wg 1
-            double* park = reinterpret_cast<double*>(smem + C::OFF_WORK);
-            tc::named_sync(3, C::EPI);  // every warpgroup is past its last tile
-            if (wg == 1 && wq == 0) {
-#pragma unroll
-                for (int u = 0; u < KL; ++u)
-                    if (lane + 32 * u < K) park[lane + 32 * u] = static_cast<double>(count_acc[u]);
-            }
+            // every warpgroup is past its last tile: the CTA's fixed-point sums
+            // and counts -> its f64 partial row (summed over CTAs in CTA order)
             tc::named_sync(3, C::EPI);
-            if (wg == 0) {
-                double* out = p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K);
-                const double* acc0 = reinterpret_cast<const double*>(smem + C::OFF_ACC);
-                for (int e = t; e < KD; e += 128) {
-                    double v = acc0[e];
-#pragma unroll
-                    for (int w = 1; w < WGS; ++w) v += acc0[w * KD + e];
-                    out[e] = v;
-                }
-                if (wq == 0)
-#pragma unroll
-                    for (int u = 0; u < KL; ++u)
-                        if (lane + 32 * u < K)
-                            out[KD + lane + 32 * u] =
-                                static_cast<double>(count_acc[u]) + (WGS > 1 ? park[lane + 32 * u] : 0.0);
-            }
+            double* out = p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K);
+            for (int e = tid; e < KD + K; e += C::EPI)
+                out[e] = e < KD ? ldexp(static_cast<double>(acc[e]), -shift) : static_cast<double>(acc[e]);
         }
     }
     tc::tc_fence_before();
