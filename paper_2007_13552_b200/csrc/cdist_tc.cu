@@ -215,9 +215,7 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
             cdtc_tile_of(t, nrb, ncb, rb, cb);
             const int64_t row0 = rb * BM, col0 = cb * BN;
             const int b = static_cast<int>(tcount & 1);
-#ifndef CDTC_EXP_STOREONLY
             tc::mbar_wait(&tfull[b], static_cast<uint32_t>((tcount / 2) & 1));
-#endif
             tc::tc_fence_after();
             const int64_t gi = row0 + r;
             const float xni = gi < p.nx ? __ldg(p.xn + gi) : 0.f;

@@ -66,10 +66,10 @@ struct TcCfg {
     static constexpr int OFF_BHI = OFF_WORK + WGS * WORK_BYTES;
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
     static constexpr int OFF_CN = OFF_BLO + B_BYTES;
-    static constexpr int OFF_CNT = OFF_CN + ((K * 4 + 15) / 16) * 16;
+    static constexpr int OFF_CNT = OFF_CN + ((K * 4 + 15) / 16) * 16;  // u16 tile counts per warpgroup
     // one int64 fixed-point accumulator per CTA: [K*D] sums, [K] counts,
     // shared by the warpgroups (integer atomics: any order gives the same bits)
-    static constexpr int OFF_ACC = OFF_CNT + WGS * ((VW * K * 4 + 15) / 16) * 16;
+    static constexpr int OFF_ACC = OFF_CNT + WGS * ((VW * K * 2 + 15) / 16) * 16;
     static constexpr int OFF_BAR = OFF_ACC + (K * D + K) * 8;
     static constexpr int NBARS = 2 * S + 3 * WGS;
     static constexpr int OFF_TMEM = OFF_BAR + NBARS * 8;
@@ -172,8 +172,12 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                 }
                 const int st = static_cast<int>(it % S), w = static_cast<int>(it % WGS);
                 const int64_t use = it / WGS;  // this warpgroup's use index
-                tc::mbar_wait(&loready[w], static_cast<uint32_t>(use & 1));
+                // the two MMAs on the raw tile (hi.Bhi + hi.Blo) go out as soon as
+                // the tile has landed and the accumulator is free; only lo.Bhi
+                // waits for the warpgroup's split, so the warpgroup then waits for
+                // one third of the MMAs instead of all of them
                 if (use >= 1) tc::mbar_wait(&dempty[w], static_cast<uint32_t>((use - 1) & 1));
+                tc::mbar_wait(&full[st], static_cast<uint32_t>((it / S) & 1));
                 tc::tc_fence_after();
                 const uint32_t a0 = tc::smem_u32(tiles + st * (C::TILE_BYTES / 4));
                 const uint32_t l0 = tc::smem_u32(smem + C::OFF_WORK + w * C::WORK_BYTES);
@@ -183,15 +187,24 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                 for (int ks = 0; ks < C::KC / 8; ++ks) {
                     const uint32_t ko = (ks / 4) * PR * 128 + (ks % 4) * 32;  // K-block, then bytes inside the atom
                     const uint64_t ahi = tc::smem_desc(a0 + ko, 16, 1024, 2);
-                    const uint64_t alo = tc::smem_desc(l0 + ko, 16, 1024, 2);
                     const uint64_t bh = tc::smem_desc(bh0 + ks * 2 * NS * 16, NS * 16, 128);
                     const uint64_t bl = tc::smem_desc(bl0 + ks * 2 * NS * 16, NS * 16, 128);
                     tc::mma_tf32(dt, ahi, bh, idesc, ks > 0);
 #ifndef KT_EXP_ONEMMA
                     tc::mma_tf32(dt, ahi, bl, idesc, 1);
-                    tc::mma_tf32(dt, alo, bh, idesc, 1);
 #endif
                 }
+                tc::mbar_wait(&loready[w], static_cast<uint32_t>(use & 1));
+                tc::tc_fence_after();
+#ifndef KT_EXP_ONEMMA
+#pragma unroll
+                for (int ks = 0; ks < C::KC / 8; ++ks) {
+                    const uint32_t ko = (ks / 4) * PR * 128 + (ks % 4) * 32;
+                    const uint64_t alo = tc::smem_desc(l0 + ko, 16, 1024, 2);
+                    const uint64_t bh = tc::smem_desc(bh0 + ks * 2 * NS * 16, NS * 16, 128);
+                    tc::mma_tf32(dt, alo, bh, idesc, 1);
+                }
+#endif
                 tc::mma_commit(&dfull[w]);
                 // the stage is free once its MMAs retire (the split already read
                 // it): released here rather than after the epilogue's readback
@@ -203,7 +216,7 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
         // ------------------------------------------------ epilogue warpgroups
         const int wg = warp / 4, wq = warp % 4, t = tid % 128;  // t = packed row = TMEM lane
         float* work = reinterpret_cast<float*>(smem + C::OFF_WORK + wg * C::WORK_BYTES);
-        int* cnt = reinterpret_cast<int*>(smem + C::OFF_CNT + wg * ((VW * K * 4 + 15) / 16) * 16);
+        unsigned short* cnt = reinterpret_cast<unsigned short*>(smem + C::OFF_CNT + wg * ((VW * K * 2 + 15) / 16) * 16);
         const uint32_t bar_id = 1 + wg;
         const float cmax = p.bounds[0], cnmax = p.bounds[1];
         constexpr float ERR = 4.f * (static_cast<float>(3 * C::KC) * 0x1.0p-24f + 3.f * 0x1.0p-20f);
@@ -226,8 +239,10 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             const float* xt = tiles + st * (C::TILE_BYTES / 4);
             tc::mbar_wait(&full[st], static_cast<uint32_t>((it / S) & 1));
 
-            // split: lo = x - trunc_tf32(x); the raw row stays in registers
+            // split: lo = x - trunc_tf32(x); the raw row stays in registers; the
+            // row's |x|^2 (error bound) in four independent fp32 chains
             float4 xr[NCH];
+            float4 xq = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
                 // 16-byte chunk c of row t: K-block c/8, chunk (c%8) ^ (t%8) of the row's 128-byte line
@@ -240,6 +255,10 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                 l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
                 l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
                 *reinterpret_cast<float4*>(work + off) = l;
+                xq.x = fmaf(v.x, v.x, xq.x);
+                xq.y = fmaf(v.y, v.y, xq.y);
+                xq.z = fmaf(v.z, v.z, xq.z);
+                xq.w = fmaf(v.w, v.w, xq.w);
             }
             tc::fence_async_smem();
             tc::named_sync(bar_id, 128);
@@ -253,9 +272,13 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             float xx[P];
 #pragma unroll
             for (int h = 0; h < P; ++h) {
-                xx[h] = 0.f;
+                if (P == 1) {
+                    xx[h] = (xq.x + xq.y) + (xq.z + xq.w);
+                } else {
+                    xx[h] = 0.f;
 #pragma unroll
-                for (int f = 0; f < D; ++f) xx[h] = fmaf(xval(h * D + f), xval(h * D + f), xx[h]);
+                    for (int f = 0; f < D; ++f) xx[h] = fmaf(xval(h * D + f), xval(h * D + f), xx[h]);
+                }
 #ifdef KT_EXP_NOXX
                 xx[h] = 16.f;
 #endif
@@ -280,7 +303,7 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                 }
             }
             // (32-column loads where NS allows: one TMEM round trip per 32 scores)
-            constexpr int QC = NS % 32 == 0 ? 32 : 16;
+            constexpr int QC = (NS % 32 == 0 && WGS < 3) ? 32 : 16;  // 3 warpgroups: 152 registers per thread
 #pragma unroll
 #ifdef KT_EXP_NOSCORE
             for (int q16 = 0; q16 < 1; ++q16) {
@@ -542,7 +565,7 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             for (int h = 0; h < P; ++h) {
                 mine[h] = __match_any_sync(FULL, label[h]);
                 rank[h] = __popc(mine[h] & ((1u << lane) - 1u));
-                if (rank[h] == 0 && label[h] < K) cnt[(h * 4 + wq) * K + label[h]] = __popc(mine[h]);
+                if (rank[h] == 0 && label[h] < K) cnt[(h * 4 + wq) * K + label[h]] = static_cast<unsigned short>(__popc(mine[h]));
             }
             tc::named_sync(bar_id, 128);
             int total[KL], before[KL][P], start[KL];
