@@ -1748,12 +1748,7 @@ static bool pick_small(void (*&fn)(SmallParams), void (*&dfn)(SmallParams), size
 template <int D, int K, int P>
 static void pick_tc(Assigner<float>& A) {
     const char* w = std::getenv("DNDC_TC_WGS");
-    if (w && w[0] == '3') {
-        A.tfn = kmeans_tc_kernel<D, K, P, 3>;
-        A.tsmem = TcCfg<D, K, P, 3>::SMEM;
-        A.tthreads = TcCfg<D, K, P, 3>::THREADS;
-        A.tc_delta = TcCfg<D, K, P, 3>::DELTA_OK;
-    } else if (w && w[0] == '1') {
+    if (w && w[0] == '1') {
         A.tfn = kmeans_tc_kernel<D, K, P, 1>;
         A.tsmem = TcCfg<D, K, P, 1>::SMEM;
         A.tthreads = TcCfg<D, K, P, 1>::THREADS;

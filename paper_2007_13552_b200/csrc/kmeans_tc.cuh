@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
         frexp(static_cast<double>(p.n) * (p.xabs ? *p.xabs : 1.0) + 1.0, &e2);
         const int shift = 61 - e2;
         const float qscale = ldexpf(1.f, shift);
-        tc::named_sync(3, C::EPI);  // zeroed before any warpgroup adds
+        tc::named_sync(15, C::EPI);  // zeroed before any warpgroup adds
 
         for (int64_t it = wg; it < my_tiles; it += WGS) {
             const int st = static_cast<int>(it % S);
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                 }
             }
             // (32-column loads where NS allows: one TMEM round trip per 32 scores)
-            constexpr int QC = (NS % 32 == 0 && WGS < 3) ? 32 : 16;  // 3 warpgroups: 152 registers per thread
+            constexpr int QC = NS % 32 == 0 ? 32 : 16;
 #pragma unroll
 #ifdef KT_EXP_NOSCORE
             for (int q16 = 0; q16 < 1; ++q16) {
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
         if (accumulate) {
             // every warpgroup is past its last tile: the CTA's fixed-point sums
             // and counts -> its f64 partial row (summed over CTAs in CTA order)
-            tc::named_sync(3, C::EPI);
+            tc::named_sync(15, C::EPI);
             double* out = p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K);
             for (int e = tid; e < KD + K; e += C::EPI)
                 out[e] = e < KD ? ldexp(static_cast<double>(acc[e]), -shift) : static_cast<double>(acc[e]);
