@@ -160,14 +160,18 @@ __device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// fp32 top-2 of R rows against the table in shared memory: T = [K][DP] of
-// -2 c (DP = D rounded up to 4, 16-byte rows: one LDS.128 feeds 2R FFMA2) and
-// [K] pairs (|c|^2, 0).  Same operation chain as small_top2 (so the same error bound).
+// fp32 top-2 of R rows against the table in shared memory, clusters in pairs:
+// T[p*2D + 2f + (j&1)] = -2 c_j,f for the pair p = j/2 (one LDS.128 = two
+// features of both clusters), T[K*D + j] = |c_j|^2.  A pair's two scores
+// accumulate in one float2: FFMA2 with the feature x_f as a broadcast scalar
+// operand and the (|c_j|^2, |c_j+1|^2) pair as the first addend -- no
+// accumulator moves, no combining add.  s_j = |c_j|^2 + sum_f x_f (-2 c_j,f)
+// is one sequential fp32 chain of D FMAs (the error bound's model).
 template <int D, int K, int R>
 __device__ __forceinline__ void persist_top2(const float2 (&xv)[R][D / 2], const float* __restrict__ T,
                                              float (&b1)[R], float (&b2)[R], int (&i1)[R]) {
-    constexpr int L = D / 2, DP = (D + 3) / 4 * 4;
-    constexpr int JG = K % 2 == 0 ? 2 : 1;
+    static_assert(K % 2 == 0 && D % 2 == 0, "cluster pairs, feature pairs");
+    constexpr int L = D / 2;
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         b1[h] = FLT_MAX;
@@ -175,38 +179,31 @@ __device__ __forceinline__ void persist_top2(const float2 (&xv)[R][D / 2], const
         i1[h] = 0;
     }
 #pragma unroll
-    for (int j0 = 0; j0 < K; j0 += JG) {
-        float2 sp[JG][R];
+    for (int pr = 0; pr < K / 2; ++pr) {
+        const float2 cn = *reinterpret_cast<const float2*>(T + K * D + 2 * pr);
+        float2 sp[R];
 #pragma unroll
-        for (int u = 0; u < JG; ++u) {
-            // (|c_j|^2, 0) as one pair from the table: the first FFMA2 adds it
-            // directly (no register moves to build the accumulator)
-            const float2 cn = *reinterpret_cast<const float2*>(T + K * DP + 2 * (j0 + u));
+        for (int h = 0; h < R; ++h) sp[h] = cn;
 #pragma unroll
-            for (int h = 0; h < R; ++h) sp[u][h] = cn;
-        }
+        for (int g = 0; g < L; ++g) {
+            const float4 c = *reinterpret_cast<const float4*>(T + pr * 2 * D + 4 * g);
 #pragma unroll
-        for (int f4 = 0; f4 < DP / 4; ++f4) {
-#pragma unroll
-            for (int u = 0; u < JG; ++u) {
-                const float4 c = *reinterpret_cast<const float4*>(T + (j0 + u) * DP + 4 * f4);
-#pragma unroll
-                for (int h = 0; h < R; ++h) {
-                    sp[u][h] = ffma2(xv[h][2 * f4], make_float2(c.x, c.y), sp[u][h]);
-                    if (2 * f4 + 1 < L) sp[u][h] = ffma2(xv[h][2 * f4 + 1], make_float2(c.z, c.w), sp[u][h]);
-                }
+            for (int h = 0; h < R; ++h) {
+                sp[h] = __ffma2_rn(make_float2(xv[h][g].x, xv[h][g].x), make_float2(c.x, c.y), sp[h]);
+                sp[h] = __ffma2_rn(make_float2(xv[h][g].y, xv[h][g].y), make_float2(c.z, c.w), sp[h]);
             }
         }
 #pragma unroll
-        for (int u = 0; u < JG; ++u)
+        for (int h = 0; h < R; ++h) {
 #pragma unroll
-            for (int h = 0; h < R; ++h) {
-                const float sc = sp[u][h].x + sp[u][h].y;
+            for (int u = 0; u < 2; ++u) {
+                const float sc = u ? sp[h].y : sp[h].x;
                 const bool lt = sc < b1[h];
                 b2[h] = fminf(b2[h], fmaxf(b1[h], sc));
                 b1[h] = fminf(b1[h], sc);
-                i1[h] = lt ? j0 + u : i1[h];
+                i1[h] = lt ? 2 * pr + u : i1[h];
             }
+        }
     }
 }
 
@@ -215,7 +212,6 @@ __device__ __forceinline__ void persist_top2(const float2 (&xv)[R][D / 2], const
 // table and the error-bound inputs (misc[0] max |c|, misc[1] max fp32 |c|^2).
 template <int D, int K>
 __device__ __forceinline__ void persist_tables(const double* c64, double* cn64, float* tab, double* misc) {
-    constexpr int DP = (D + 3) / 4 * 4;
     const int j = threadIdx.x;
     double cmax = 0.0, cnmax = 0.0;
     if (j < K) {
@@ -224,12 +220,10 @@ __device__ __forceinline__ void persist_tables(const double* c64, double* cn64, 
             const double cf = c64[j * D + f];
             n64 = add_rn(n64, mul_rn(cf, cf));
             const float c32 = static_cast<float>(cf);
-            tab[j * DP + f] = -2.f * c32;
+            tab[(j / 2) * 2 * D + 2 * f + (j & 1)] = -2.f * c32;  // cluster-pair layout (persist_top2)
             n32 += static_cast<double>(c32) * static_cast<double>(c32);
         }
-        for (int f = D; f < DP; ++f) tab[j * DP + f] = 0.f;
-        tab[K * DP + 2 * j] = static_cast<float>(n32);
-        tab[K * DP + 2 * j + 1] = 0.f;
+        tab[K * D + j] = static_cast<float>(n32);
         cn64[j] = n64;
         cmax = sqrt(n32);
         cnmax = static_cast<double>(static_cast<float>(n32));
