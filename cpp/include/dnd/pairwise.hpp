@@ -52,7 +52,7 @@ DndArray<T> cdist(const DndArray<T>& x) {
 
 /// Distances between the rows of x (split=0) and y (pairwise.cpp:87-100).
 /// y replicated: communication-free.  y split=0: its shards travel the ring
-/// (fp32) instead of the reference's allgather; f64 gathers y first.
+/// (device to device) instead of the reference's allgather.
 template <typename T>
 DndArray<T> cdist_xy(const DndArray<T>& x, const DndArray<T>& y) {
     static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "cdist_xy: float or double");
@@ -77,8 +77,7 @@ DndArray<T> cdist_xy(const DndArray<T>& x, const DndArray<T>& y) {
     } else if constexpr (std::is_same_v<T, float>) {
         detail::check(dndc_cdist_xy_ring_f32(h, xl, rows, y.device_data(), y.lshape()[0], ny, m, out.device_data()));
     } else {
-        const auto yr = from_global(gather(y), y.shape(), std::nullopt, y.comm());
-        detail::check(dndc_cdist_xy_f64(h, xl, rows, yr.device_data(), ny, m, out.device_data()));
+        detail::check(dndc_cdist_xy_ring_f64(h, xl, rows, y.device_data(), y.lshape()[0], ny, m, out.device_data()));
     }
     detail::check(dndc_synchronize(h));
     return out;

@@ -200,6 +200,9 @@ int dndc_cdist_xy_f64(dndc_ctx* ctx, const double* x_local, int64_t n_local, con
 int dndc_cdist_xy_ring_f32(dndc_ctx* ctx, const float* x_local, int64_t nx_local,
                            const float* y_local, int64_t ny_local, int64_t ny_global, int64_t m,
                            float* out);
+int dndc_cdist_xy_ring_f64(dndc_ctx* ctx, const double* x_local, int64_t nx_local,
+                           const double* y_local, int64_t ny_local, int64_t ny_global, int64_t m,
+                           double* out);
 
 /* ------------------------------------------------------ A8-A12: k-means */
 /* kmeans_init_indices (cluster.cpp:60-75), host only, O(k) memory. */
@@ -243,6 +246,8 @@ int dndc_kmeans_predict_f64(dndc_ctx* ctx, const double* x, int64_t n, int64_t m
  * Communication-free: reduce with dndc_allreduce_f64 for the global step. */
 int dndc_kmeans_step_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m, const double* centroids_host,
                          int k, double* stats_host, int32_t* labels);
+int dndc_kmeans_step_f64(dndc_ctx* ctx, const double* x, int64_t n, int64_t m, const double* centroids_host,
+                         int k, double* stats_host, int32_t* labels);
 
 /* Statistics of the most recent kmeans_fit/predict on this context: rows whose
  * fp32 top-2 gap fell inside the error bound and were re-decided in f64. */
@@ -285,6 +290,9 @@ int dndc_moments_axis0_f64(dndc_ctx* ctx, const double* x_local, int64_t n_local
 /* D^2 seeding as defined in DESIGN.md (not in the reference),
  * collective; k global row indices (host). */
 int dndc_kmeanspp_indices_f32(dndc_ctx* ctx, const float* x_local, int64_t n_local,
+                              int64_t n_global, int64_t m, int k, uint64_t seed,
+                              int64_t* indices_host);
+int dndc_kmeanspp_indices_f64(dndc_ctx* ctx, const double* x_local, int64_t n_local,
                               int64_t n_global, int64_t m, int k, uint64_t seed,
                               int64_t* indices_host);
 

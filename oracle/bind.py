@@ -62,6 +62,7 @@ class Oracle:
         L.dno_local_moments_axis0.argtypes = [_P, _i64, _i64, _P, _P, _P]
         L.dno_welford_axis0_f32_continue.argtypes = [_P, _i64, _i64, _P, _P, _P]
         L.dno_kmeanspp_indices_f32.argtypes = [_P, _i64, _i64, _i32, _i32, _u64, _P]
+        L.dno_kmeanspp_indices_f64.argtypes = [_P, _i64, _i64, _i32, _i32, _u64, _P]
         L.dno_lasso_fit.argtypes = [_P, _P, _i64, _i64, _i32, _f64, _i32, _f64, _P, _P, _P]
         L.dno_soft_threshold.argtypes = [_f64, _f64]
         L.dno_soft_threshold.restype = _f64
@@ -175,10 +176,12 @@ class Oracle:
         return int(cnt[0]), mean, m2
 
     def kmeanspp_indices(self, x, k, seed, p=1):
-        x = np.ascontiguousarray(x, np.float32)
+        """float64 input runs the same definition on the doubles; anything else as float32."""
+        f64 = np.asarray(x).dtype == np.float64
+        x = np.ascontiguousarray(x, np.float64 if f64 else np.float32)
         out = np.empty(k, np.int64)
-        if self.lib.dno_kmeanspp_indices_f32(_ptr(x), x.shape[0], x.shape[1], p, k, seed,
-                                             _ptr(out)) != 0:
+        fn = self.lib.dno_kmeanspp_indices_f64 if f64 else self.lib.dno_kmeanspp_indices_f32
+        if fn(_ptr(x), x.shape[0], x.shape[1], p, k, seed, _ptr(out)) != 0:
             raise ValueError("kmeanspp: k out of range")
         return out
 

@@ -461,17 +461,19 @@ static double kpp_lane_sum(const double* v, int64_t count, int64_t stride_elems)
     return lanes[0];
 }
 
-static double kpp_dist2(const float* a, const float* b, int64_t m) {
+/* D2 of rows i and j of x (f32 or f64 elements, the same f64 chain) */
+static double kpp_dist2(const void* x, int f64, int64_t i, int64_t j, int64_t m) {
     double acc = 0.0;
     for (int64_t f = 0; f < m; ++f) {
-        const double d = (double)a[f] - (double)b[f];
+        const double d = f64 ? ((const double*)x)[i * m + f] - ((const double*)x)[j * m + f]
+                             : (double)((const float*)x)[i * m + f] - (double)((const float*)x)[j * m + f];
         acc += d * d;
     }
     return acc;
 }
 
-int dno_kmeanspp_indices_f32(const float* x, int64_t n, int64_t m, int p, int k, uint64_t seed,
-                             int64_t* indices) {
+static int kmeanspp_indices(const void* x, int f64, int64_t n, int64_t m, int p, int k, uint64_t seed,
+                            int64_t* indices) {
     if (k < 1 || (int64_t)k > n || p < 1) return -1;
     /* blocks and groups are laid out per rank shard (chunk_map), concatenated
      * in rank order; p = 1 is one shard covering all rows. */
@@ -507,7 +509,7 @@ int dno_kmeanspp_indices_f32(const float* x, int64_t n, int64_t m, int p, int k,
     double* S = (double*)malloc(sizeof(double) * (size_t)(nblocks + 1));
     double* T = (double*)malloc(sizeof(double) * (size_t)(ngroups + 1));
     dno_kmeans_init_indices(n, 1, seed, &indices[0]);
-    for (int64_t i = 0; i < n; ++i) d2[i] = kpp_dist2(x + i * m, x + indices[0] * m, m);
+    for (int64_t i = 0; i < n; ++i) d2[i] = kpp_dist2(x, f64, i, indices[0], m);
     for (int j = 1; j < k; ++j) {
         for (int64_t b = 0; b < nblocks; ++b) S[b] = kpp_lane_sum(d2 + blo[b], bcnt[b], 1);
         double W = 0.0;
@@ -551,13 +553,23 @@ int dno_kmeanspp_indices_f32(const float* x, int64_t n, int64_t m, int p, int k,
         }
         indices[j] = pick;
         for (int64_t i = 0; i < n; ++i) {
-            const double d = kpp_dist2(x + i * m, x + pick * m, m);
+            const double d = kpp_dist2(x, f64, i, pick, m);
             if (d < d2[i]) d2[i] = d;
         }
     }
     free(off); free(ext); free(blo); free(bcnt); free(g0); free(g1);
     free(d2); free(S); free(T);
     return 0;
+}
+
+int dno_kmeanspp_indices_f32(const float* x, int64_t n, int64_t m, int p, int k, uint64_t seed,
+                             int64_t* indices) {
+    return kmeanspp_indices(x, 0, n, m, p, k, seed, indices);
+}
+
+int dno_kmeanspp_indices_f64(const double* x, int64_t n, int64_t m, int p, int k, uint64_t seed,
+                             int64_t* indices) {
+    return kmeanspp_indices(x, 1, n, m, p, k, seed, indices);
 }
 
 /* ------------------------------------------------------------ LASSO (F4)

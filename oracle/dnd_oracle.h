@@ -88,6 +88,8 @@ int dno_moments_axis0(const double* x, int64_t n, int64_t m, int p, int64_t ddof
  * kernel it pins.  indices: k global row ids. x is fp32 (the device dtype). */
 int dno_kmeanspp_indices_f32(const float* x, int64_t n, int64_t m, int p, int k, uint64_t seed,
                              int64_t* indices);
+int dno_kmeanspp_indices_f64(const double* x, int64_t n, int64_t m, int p, int k, uint64_t seed,
+                             int64_t* indices);
 
 /* LASSO coordinate descent (regression.cpp:19-102) */
 double dno_soft_threshold(double rho, double t);

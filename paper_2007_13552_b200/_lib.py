@@ -75,6 +75,7 @@ _SIGS = {
     "dndc_file_write_from_device": [_P, C.c_char_p, _u64, _P, C.c_size_t],
     "dndc_allreduce_f64": [_P, _P, _i64],
     "dndc_kmeans_step_f32": [_P, _P, _i64, _i64, _P, _i32, _P, _P],
+    "dndc_kmeans_step_f64": [_P, _P, _i64, _i64, _P, _i32, _P, _P],
     "dndc_fill_uniform_f32": [_P, _u64, _i64, _i64, _i64, _P],
     "dndc_fill_uniform_f64": [_P, _u64, _i64, _i64, _i64, _P],
     "dndc_row_norms_f32": [_P, _P, _i64, _i64, _P],
@@ -86,6 +87,7 @@ _SIGS = {
     "dndc_cdist_xy_f32": [_P, _P, _i64, _P, _i64, _i64, _P],
     "dndc_cdist_xy_f64": [_P, _P, _i64, _P, _i64, _i64, _P],
     "dndc_cdist_xy_ring_f32": [_P, _P, _i64, _P, _i64, _i64, _i64, _P],
+    "dndc_cdist_xy_ring_f64": [_P, _P, _i64, _P, _i64, _i64, _i64, _P],
     "dndc_kmeans_init_indices": [_i64, _i32, _u64, _P],
     "dndc_kmeans_init_centroids_f32": [_P, _P, _i64, _i64, _i64, _i32, _u64, _P],
     "dndc_kmeans_fit_f32": [_P, _P, _i64, _i64, _i64, _i32, _i32, _f64, _u64, _P, _P, _P, _P],
@@ -99,6 +101,7 @@ _SIGS = {
     "dndc_moments_axis0_f32": [_P, _P, _i64, _i64, _P, _P, _P],
     "dndc_moments_axis0_f64": [_P, _P, _i64, _i64, _P, _P, _P],
     "dndc_kmeanspp_indices_f32": [_P, _P, _i64, _i64, _i64, _i32, _u64, _P],
+    "dndc_kmeanspp_indices_f64": [_P, _P, _i64, _i64, _i64, _i32, _u64, _P],
     "dndc_kmeans_last_kernel": [_P],
     "dndc_kmeans_persist_trace": [_P, _P, _i64, _P],
     "dndc_group_create": [_i32, _i64, C.POINTER(_P)],

@@ -253,6 +253,8 @@ def gather(a: DndArray) -> np.ndarray:
 
 
 def _fn(name: str, t: torch.Tensor):
+    if t.dtype not in _SUFFIX:
+        raise ValueError(f"{name[5:]}: float32 or float64 input required, got {t.dtype}")
     return getattr(lib(), f"{name}_{_SUFFIX[t.dtype]}")
 
 
@@ -320,10 +322,8 @@ def cdist_xy(x: DndArray, y: DndArray) -> DndArray:
         check(_fn("dndc_cdist_xy", x.tile)(x.comm.handle, _ptr(x.tile), nx_local, _ptr(y.tile), y.shape[0], m,
                                            _ptr(out)))
     else:
-        if x.tile.dtype != torch.float32:
-            raise ValueError("cdist_xy: the ring over split y is implemented for float32")
-        check(lib().dndc_cdist_xy_ring_f32(x.comm.handle, _ptr(x.tile), nx_local, _ptr(y.tile), y.tile.shape[0],
-                                           y.shape[0], m, _ptr(out)))
+        check(_fn("dndc_cdist_xy_ring", x.tile)(x.comm.handle, _ptr(x.tile), nx_local, _ptr(y.tile),
+                                                y.tile.shape[0], y.shape[0], m, _ptr(out)))
     return DndArray((x.shape[0], y.shape[0]), x.split, x.comm, out)
 
 
@@ -470,12 +470,10 @@ def kmeanspp_indices(x: DndArray, k: int, seed: int) -> np.ndarray:
     """k-means++ seeding (BASELINE config 5; definition in DESIGN.md)."""
     _require_2d(x, "kmeanspp")
     x = _rows(x)
-    if x.tile.dtype != torch.float32:
-        raise ValueError("kmeanspp: float32 input required")
     comm, n_local, n_global = _shard(x)
     out = np.empty(max(k, 1), np.int64)
-    check(lib().dndc_kmeanspp_indices_f32(comm.handle, _ptr(x.tile), n_local, n_global, x.shape[1], int(k),
-                                          int(seed) & 0xFFFFFFFFFFFFFFFF, out.ctypes.data))
+    check(_fn("dndc_kmeanspp_indices", x.tile)(comm.handle, _ptr(x.tile), n_local, n_global, x.shape[1], int(k),
+                                               int(seed) & 0xFFFFFFFFFFFFFFFF, out.ctypes.data))
     return out[:k]
 
 

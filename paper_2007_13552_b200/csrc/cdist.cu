@@ -549,4 +549,12 @@ int dndc_cdist_xy_ring_f32(dndc_ctx* ctx, const float* x_local, int64_t nx_local
     });
 }
 
+int dndc_cdist_xy_ring_f64(dndc_ctx* ctx, const double* x_local, int64_t nx_local,
+                           const double* y_local, int64_t ny_local, int64_t ny_global, int64_t m,
+                           double* out) {
+    return guard([&] {
+        dndc::cdist_ring<double>(ctx, x_local, nx_local, y_local, ny_local, ny_global, m, out, false);
+    });
+}
+
 }  // extern "C"

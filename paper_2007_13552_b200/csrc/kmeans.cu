@@ -2291,13 +2291,14 @@ static void kmeans_predict(dndc_ctx* ctx, const T* x, int64_t n, int64_t m64, co
 
 // One assignment/accumulation pass against given centroids: local stats and
 // local inertia (sum |x|^2 + sum_j n_j |c_j|^2 - 2 c_j . S_j, the fit's form).
-static void kmeans_step(dndc_ctx* ctx, const float* x, int64_t n, int64_t m64, const double* cent_host, int k,
+template <typename T>
+static void kmeans_step(dndc_ctx* ctx, const T* x, int64_t n, int64_t m64, const double* cent_host, int k,
                         double* stats_host, int32_t* labels) {
     if (k < 1) value_error("kmeans_step: k must be positive");
     if (n < 0 || m64 < 1) value_error("kmeans_step: bad extents");
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
-    const Assigner<float> A = plan<float>(ctx, k, m, n, x);
+    const Assigner<T> A = plan<T>(ctx, k, m, n, x);
     const KmBuffers b = buffers(ctx, k, m, 1, A.grid());
     const int S = k * m + k;
     double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * std::max(k * m, S + 4)));
@@ -2308,7 +2309,7 @@ static void kmeans_step(dndc_ctx* ctx, const float* x, int64_t n, int64_t m64, c
     DNDC_CUDA(cudaMemsetAsync(b.sx2, 0, sizeof(double) * 4, s));
     derive_tables(ctx, b, k, m);
     if (n > 0) {
-        scan_input<float>(ctx, b, x, n * m, s);
+        scan_input<T>(ctx, b, x, n * m, s);
         A.launch(b, x, n, m, k, true, labels, false, s);
         DNDC_LAUNCHED(ctx);
         reduce_partials_kernel<<<(S + 7) / 8, 256, 0, s>>>(b.partials, A.grid(), S, b.stats, nullptr);
@@ -2435,7 +2436,12 @@ int dndc_kmeans_predict_f64(dndc_ctx* ctx, const double* x, int64_t n, int64_t m
 
 int dndc_kmeans_step_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m, const double* centroids_host,
                          int k, double* stats_host, int32_t* labels) {
-    return guard([&] { dndc::kmeans_step(ctx, x, n, m, centroids_host, k, stats_host, labels); });
+    return guard([&] { dndc::kmeans_step<float>(ctx, x, n, m, centroids_host, k, stats_host, labels); });
+}
+
+int dndc_kmeans_step_f64(dndc_ctx* ctx, const double* x, int64_t n, int64_t m, const double* centroids_host,
+                         int k, double* stats_host, int32_t* labels) {
+    return guard([&] { dndc::kmeans_step<double>(ctx, x, n, m, centroids_host, k, stats_host, labels); });
 }
 
 int dndc_kmeans_time_assign_f32(dndc_ctx* ctx, const float* x, int64_t n, int64_t m, int k, int reps,

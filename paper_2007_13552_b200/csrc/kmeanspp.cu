@@ -16,6 +16,7 @@
 // and the picked row (exact zero-filled allreduce) travel.
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -25,7 +26,8 @@ constexpr int KPP_BLOCK = 2048;
 constexpr int KPP_GROUP = 1024;
 constexpr uint64_t KPP_SALT = 0x5851f42d4c957f2dULL;
 
-__device__ __forceinline__ double kpp_dist2(const float* __restrict__ xr, const float* c, int m) {
+template <typename T>
+__device__ __forceinline__ double kpp_dist2(const T* __restrict__ xr, const T* c, int m) {
     double acc = 0.0;
     for (int f = 0; f < m; ++f) {
         const double dd = sub_rn(static_cast<double>(xr[f]), static_cast<double>(c[f]));
@@ -43,9 +45,10 @@ __device__ __forceinline__ double warp_butterfly(double v) {
 // D2 of one row against the newest pick: sequential over features in f64,
 // product rounded before the add (the oracle's order).  M > 0: compile-time
 // width (all loads issued up front, float4 when aligned); M == 0: runtime.
-template <int M>
-__device__ __forceinline__ double kpp_row(const float* __restrict__ xr, const float* c, int m) {
-    if constexpr (M > 0) {
+// f64 input: the same chain on the doubles as they are.
+template <int M, typename T>
+__device__ __forceinline__ double kpp_row(const T* __restrict__ xr, const T* c, int m) {
+    if constexpr (M > 0 && std::is_same_v<T, float>) {
         float v[M];
         if constexpr (M % 4 == 0) {
 #pragma unroll
@@ -74,11 +77,12 @@ __device__ __forceinline__ double kpp_row(const float* __restrict__ xr, const fl
 
 // One warp per 2048-row block of the local shard; lane l owns rows l, l+32, ...
 // (the summation order of the definition), two rows in flight per lane.
-template <int M>
-__global__ void kpp_update_kernel(const float* __restrict__ x, int64_t n, int m,
-                                  const float* __restrict__ crow, double* __restrict__ d2, int first,
+template <int M, typename T>
+__global__ void kpp_update_kernel(const T* __restrict__ x, int64_t n, int m,
+                                  const T* __restrict__ crow, double* __restrict__ d2, int first,
                                   double* __restrict__ S, int64_t nblocks) {
-    extern __shared__ float c_sh[];
+    extern __shared__ __align__(16) unsigned char kpp_sh[];
+    T* c_sh = reinterpret_cast<T*>(kpp_sh);
     for (int f = threadIdx.x; f < m; f += blockDim.x) c_sh[f] = crow[f];
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -89,8 +93,8 @@ __global__ void kpp_update_kernel(const float* __restrict__ x, int64_t n, int m,
     double acc = 0.0;
     for (int64_t i = lo + lane; i < hi; i += 64) {
         const int64_t i2 = i + 32;
-        const double da = kpp_row<M>(x + i * m, c_sh, m);
-        const double db = i2 < hi ? kpp_row<M>(x + i2 * m, c_sh, m) : 0.0;
+        const double da = kpp_row<M, T>(x + i * m, c_sh, m);
+        const double db = i2 < hi ? kpp_row<M, T>(x + i2 * m, c_sh, m) : 0.0;
         double va = da, vb = db;
         if (!first) {
             va = da < d2[i] ? da : d2[i];
@@ -168,10 +172,11 @@ __global__ void kpp_select_group_kernel(const double* __restrict__ Tall, int wor
 
 // Owner rank: blocks of the chosen group, then rows of the chosen block.
 // out: [0] global row index, [1..m] the row (zeros on non-owners).
+template <typename T>
 __global__ void kpp_select_row_kernel(const double* __restrict__ sel, int rank, const double* __restrict__ S,
                                       int64_t nblocks, const double* __restrict__ d2, int64_t n,
-                                      int64_t row_off, const float* __restrict__ x, int m,
-                                      double* __restrict__ out, float* __restrict__ crow) {
+                                      int64_t row_off, const T* __restrict__ x, int m,
+                                      double* __restrict__ out) {
     __shared__ int64_t pick_sh;
     if (threadIdx.x == 0) {
         int64_t pick = -1;
@@ -223,20 +228,23 @@ __global__ void kpp_select_row_kernel(const double* __restrict__ sel, int rank, 
         out[1 + f] = pick >= 0 ? static_cast<double>(x[pick * m + f]) : 0.0;
 }
 
-__global__ void kpp_unpack_kernel(const double* __restrict__ in, int m, float* __restrict__ crow,
+template <typename T>
+__global__ void kpp_unpack_kernel(const double* __restrict__ in, int m, T* __restrict__ crow,
                                   int64_t* __restrict__ idx_out, int j) {
-    for (int f = threadIdx.x; f < m; f += blockDim.x) crow[f] = static_cast<float>(in[1 + f]);
+    for (int f = threadIdx.x; f < m; f += blockDim.x) crow[f] = static_cast<T>(in[1 + f]);
     if (threadIdx.x == 0) idx_out[j] = static_cast<int64_t>(in[0]);
 }
 
-__global__ void kpp_first_row_kernel(const float* __restrict__ x, int64_t lo, int64_t hi, int m,
+template <typename T>
+__global__ void kpp_first_row_kernel(const T* __restrict__ x, int64_t lo, int64_t hi, int m,
                                      int64_t g, double* __restrict__ out) {
     for (int f = threadIdx.x; f < m; f += blockDim.x)
         out[1 + f] = (g >= lo && g < hi) ? static_cast<double>(x[(g - lo) * m + f]) : 0.0;
     if (threadIdx.x == 0) out[0] = (g >= lo && g < hi) ? static_cast<double>(g) : 0.0;
 }
 
-static void kmeanspp(dndc_ctx* ctx, const float* x, int64_t n_local, int64_t n_global, int64_t m64, int k,
+template <typename E>
+static void kmeanspp(dndc_ctx* ctx, const E* x, int64_t n_local, int64_t n_global, int64_t m64, int k,
                      uint64_t seed, int64_t* idx_host) {
     if (k < 1 || static_cast<int64_t>(k) > n_global)
         value_error("kmeanspp: k=" + std::to_string(k) + " out of range for n=" + std::to_string(n_global));
@@ -261,7 +269,7 @@ static void kmeanspp(dndc_ctx* ctx, const float* x, int64_t n_local, int64_t n_g
     int64_t* gc = static_cast<int64_t*>(ctx->slot("kpp_gc", sizeof(int64_t) * p));
     double* sel = static_cast<double*>(ctx->slot("kpp_sel", sizeof(double) * 4));
     double* pk = static_cast<double*>(ctx->slot("kpp_pick", sizeof(double) * (m + 1)));
-    float* crow = static_cast<float*>(ctx->slot("kpp_crow", sizeof(float) * std::max(m, 1)));
+    E* crow = static_cast<E*>(ctx->slot("kpp_crow", sizeof(double) * std::max(m, 1)));
     int64_t* didx = static_cast<int64_t*>(ctx->slot("kpp_idx", sizeof(int64_t) * k));
 
     int64_t* hgc = static_cast<int64_t*>(ctx->host_staging(sizeof(int64_t) * p));
@@ -275,10 +283,10 @@ static void kmeanspp(dndc_ctx* ctx, const float* x, int64_t n_local, int64_t n_g
         const uint64_t draw = splitmix64(seed ^ splitmix64(0x6b8b4567u));
         first = static_cast<int64_t>(draw % static_cast<uint64_t>(n_global));
     }
-    kpp_first_row_kernel<<<1, 128, 0, s>>>(x, off[ctx->rank], off[ctx->rank] + n_local, m, first, pk);
+    kpp_first_row_kernel<E><<<1, 128, 0, s>>>(x, off[ctx->rank], off[ctx->rank] + n_local, m, first, pk);
     DNDC_LAUNCHED(ctx);
     allreduce_sum_f64(ctx, pk, m + 1, s);
-    kpp_unpack_kernel<<<1, 128, 0, s>>>(pk, m, crow, didx, 0);
+    kpp_unpack_kernel<E><<<1, 128, 0, s>>>(pk, m, crow, didx, 0);
     DNDC_LAUNCHED(ctx);
     DNDC_CUDA(cudaStreamSynchronize(s));  // hgc staging reuse below
 
@@ -286,13 +294,17 @@ static void kmeanspp(dndc_ctx* ctx, const float* x, int64_t n_local, int64_t n_g
     for (int j = 1; j < k; ++j) {
         if (nblocks > 0) {
             const unsigned g = static_cast<unsigned>(ceil_div(nblocks, wpb));
-            const size_t sm = sizeof(float) * m;
+            const size_t sm = sizeof(E) * m;
             const bool a16 = reinterpret_cast<uintptr_t>(x) % 16 == 0;
-            if (m == 32 && a16) kpp_update_kernel<32><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
-            else if (m == 64 && a16) kpp_update_kernel<64><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
-            else if (m == 16 && a16) kpp_update_kernel<16><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
-            else if (m == 18) kpp_update_kernel<18><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
-            else kpp_update_kernel<0><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+            if constexpr (std::is_same_v<E, float>) {
+                if (m == 32 && a16) kpp_update_kernel<32, E><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+                else if (m == 64 && a16) kpp_update_kernel<64, E><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+                else if (m == 16 && a16) kpp_update_kernel<16, E><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+                else if (m == 18) kpp_update_kernel<18, E><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+                else kpp_update_kernel<0, E><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+            } else {
+                kpp_update_kernel<0, E><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
+            }
             DNDC_LAUNCHED(ctx);
             kpp_group_kernel<<<static_cast<unsigned>(ceil_div(ngroups, wpb)), 32 * wpb, 0, s>>>(S, nblocks, T,
                                                                                                ngroups);
@@ -302,11 +314,11 @@ static void kmeanspp(dndc_ctx* ctx, const float* x, int64_t n_local, int64_t n_g
         const double u = uniform01(seed ^ KPP_SALT, static_cast<uint64_t>(j));
         kpp_select_group_kernel<<<1, 32, 0, s>>>(Tall, p, gmax, gc, u, n_global, sel);
         DNDC_LAUNCHED(ctx);
-        kpp_select_row_kernel<<<1, 128, 0, s>>>(sel, ctx->rank, S, nblocks, d2, n_local, off[ctx->rank], x, m,
-                                                pk, crow);
+        kpp_select_row_kernel<E><<<1, 128, 0, s>>>(sel, ctx->rank, S, nblocks, d2, n_local, off[ctx->rank], x, m,
+                                                   pk);
         DNDC_LAUNCHED(ctx);
         allreduce_sum_f64(ctx, pk, m + 1, s);
-        kpp_unpack_kernel<<<1, 128, 0, s>>>(pk, m, crow, didx, j);
+        kpp_unpack_kernel<E><<<1, 128, 0, s>>>(pk, m, crow, didx, j);
         DNDC_LAUNCHED(ctx);
     }
     int64_t* h = static_cast<int64_t*>(ctx->host_staging(sizeof(int64_t) * k));
@@ -320,5 +332,11 @@ static void kmeanspp(dndc_ctx* ctx, const float* x, int64_t n_local, int64_t n_g
 extern "C" int dndc_kmeanspp_indices_f32(dndc_ctx* ctx, const float* x_local, int64_t n_local,
                                          int64_t n_global, int64_t m, int k, uint64_t seed,
                                          int64_t* indices_host) {
-    return dndc::guard([&] { dndc::kmeanspp(ctx, x_local, n_local, n_global, m, k, seed, indices_host); });
+    return dndc::guard([&] { dndc::kmeanspp<float>(ctx, x_local, n_local, n_global, m, k, seed, indices_host); });
+}
+
+extern "C" int dndc_kmeanspp_indices_f64(dndc_ctx* ctx, const double* x_local, int64_t n_local,
+                                         int64_t n_global, int64_t m, int k, uint64_t seed,
+                                         int64_t* indices_host) {
+    return dndc::guard([&] { dndc::kmeanspp<double>(ctx, x_local, n_local, n_global, m, k, seed, indices_host); });
 }

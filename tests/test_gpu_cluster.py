@@ -181,20 +181,20 @@ def test_kernel_variants_agree(comm, oracle, n, m, k, monkeypatch):
         assert np.array_equal(labels, oracle.kmeans_predict(xh.astype(np.float64), model.centroids)), kind
 
 
-def test_kmeans_step_c_abi(comm, oracle):
-    # dndc_kmeans_step_f32: one assign/accumulate pass, local stats
-    import ctypes as C
-
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_kmeans_step_c_abi(comm, oracle, dt):
+    # dndc_kmeans_step_f32/_f64: one assign/accumulate pass, local stats
     from paper_2007_13552_b200 import _lib
 
     n, m, k = 5003, 18, 8
-    xh = oracle.uniform_f32(n, m, 11)
+    xh = oracle.uniform_f32(n, m, 11) if dt == "f32" else oracle.uniform_f64(n, m, 11)
     x = dnd.from_global(xh, (n, m), 0, comm)
     cents = np.ascontiguousarray(oracle.uniform_f64(k, m, 12))
     stats = np.zeros(k * m + k + 1)
     labels = torch.empty(n, dtype=torch.int32, device="cuda")
-    _lib.check(_lib.lib().dndc_kmeans_step_f32(comm.handle, x.tile.data_ptr(), n, m, cents.ctypes.data, k,
-                                              stats.ctypes.data, labels.data_ptr()))
+    fn = getattr(_lib.lib(), f"dndc_kmeans_step_{dt}")
+    _lib.check(fn(comm.handle, x.tile.data_ptr(), n, m, cents.ctypes.data, k, stats.ctypes.data,
+                  labels.data_ptr()))
     lab = labels.cpu().numpy()
     x64 = xh.astype(np.float64)
     assert np.array_equal(lab, oracle.kmeans_predict(x64, cents))

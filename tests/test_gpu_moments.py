@@ -81,6 +81,15 @@ def test_kmeanspp_matches_oracle(comm, oracle, n, m, k, seed):
     assert np.array_equal(got, oracle.kmeanspp_indices(xh, k, seed))
 
 
+@pytest.mark.parametrize("n,m,k,seed", [(5000, 8, 8, 11), (70_001, 18, 8, 3), (2048 * 1024 + 77, 4, 5, 9)])
+def test_kmeanspp_f64_matches_oracle(comm, oracle, n, m, k, seed):
+    # dndc_kmeanspp_indices_f64 (the f64 entry point of SURVEY 8(b))
+    xh = oracle.uniform_f64(n, m, seed + 100)
+    x = dnd.from_global(xh, (n, m), 0, comm)
+    got = dnd.kmeanspp_indices(x, k, seed)
+    assert np.array_equal(got, oracle.kmeanspp_indices(xh, k, seed))
+
+
 def test_kmeanspp_duplicate_rows_fallback(comm, oracle):
     # all rows identical: W == 0 after the first pick -> the documented fallback
     xh = np.ones((100, 4), np.float32)

@@ -54,6 +54,14 @@ def test_cdist_f64_is_bit_exact(comm, golden):
     assert np.array_equal(dnd.gather(dnd.cdist_xy(x, y)), golden["cdist_xy"])
 
 
+def test_cdist_xy_split_y_f64_is_bit_exact(comm, golden):
+    # y split=0 in f64: the device ring (dndc_cdist_xy_ring_f64) instead of the
+    # reference's allgather (pairwise.cpp:94); same bits as y replicated
+    x = dnd.from_global(golden["cdist_x"], golden["cdist_x"].shape, 0, comm)
+    y = dnd.from_global(golden["cdist_y"], golden["cdist_y"].shape, 0, comm)
+    assert np.array_equal(dnd.gather(dnd.cdist_xy(x, y)), golden["cdist_xy"])
+
+
 def test_cdist_f32_within_gate(comm, golden):
     xd = golden["cdist_x"]  # fp32-valued data widened to f64
     x = dnd.from_global(xd, xd.shape, 0, comm, dtype=torch.float32)

@@ -164,6 +164,11 @@ def test_kmeanspp_oracle_properties(oracle):
     assert a[0] == oracle.kmeans_init_indices(5000, 1, 11)[0]
     # rank layout changes the summation blocks only
     assert len(set(oracle.kmeanspp_indices(x, 8, 11, p=3).tolist())) == 8
+    # the f64 entry point runs the same chain on the doubles: f32-valued rows
+    # give the same picks, other doubles a valid distinct set
+    assert np.array_equal(oracle.kmeanspp_indices(x.astype(np.float64), 8, 11), a)
+    x64 = oracle.uniform_f64(5000, 8, 3)
+    assert len(set(oracle.kmeanspp_indices(x64, 8, 11).tolist())) == 8
 
 
 def _lasso_problem(n, m, seed):

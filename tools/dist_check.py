@@ -65,6 +65,10 @@ def main():
     y64 = dnd.random_uniform((300, 5), 0, 45, comm, dtype=torch.float64)
     d64 = dnd.gather(dnd.cdist(y64))
     report("cdist f64 ring bit-exact", np.array_equal(d64, O.cdist(O.uniform_f64(300, 5, 45), p)))
+    yy64 = dnd.random_uniform((211, 5), 0, 46, comm, dtype=torch.float64)
+    dxy64 = dnd.gather(dnd.cdist_xy(y64, yy64))
+    report("cdist_xy f64 ring (split y) bit-exact",
+           np.array_equal(dxy64, O.cdist_xy(O.uniform_f64(300, 5, 45), O.uniform_f64(211, 5, 46))))
 
     # k-means: cfg1 shape at 200k rows, 10 iterations, vs the oracle at the same p
     n2 = 200_000
@@ -124,6 +128,10 @@ def main():
     # k-means++ (per-rank block layout)
     kp = dnd.kmeanspp_indices(xk, 8, 5)
     report("kmeanspp", np.array_equal(kp, O.kmeanspp_indices(O.uniform_f32(n2, 18, 42), 8, 5, p)), str(kp.tolist()))
+    xk64 = dnd.random_uniform((50_001, 6), 0, 47, comm, dtype=torch.float64)
+    kp64 = dnd.kmeanspp_indices(xk64, 8, 5)
+    report("kmeanspp f64", np.array_equal(kp64, O.kmeanspp_indices(O.uniform_f64(50_001, 6, 47), 8, 5, p)),
+           str(kp64.tolist()))
     # empty shards: p > n
     tiny = dnd.from_global(np.array([0.0, 0.1, 10.0], np.float32), (3, 1), 0, comm)
     mt = dnd.kmeans_fit(tiny, 2, 4, 0.0, 7)
