@@ -1672,6 +1672,14 @@ struct Assigner {
     bool tc = false;
     bool tc_delta = false;  // the tc instantiation supports delta iterations (TcCfg::DELTA_OK)
     void (*tfn)(CUtensorMap, TcParams) = nullptr;
+    void (*rfn)(TcRefineParams) = nullptr;  // near-tie refine after each tc launch
+    unsigned* rq_ctl = nullptr;
+    uint64_t* rq_row = nullptr;
+    unsigned long long* rq_cand = nullptr;
+    float* rq_x = nullptr;
+    long long* racc = nullptr;
+    unsigned rq_cap = 0;
+    int rgrid = 0, rthreads = 0;
     CUtensorMap tmap{};
     size_t tsmem = 0;
     int tthreads = 0;
@@ -1681,7 +1689,8 @@ struct Assigner {
     size_t ssmem = 0;
     int sgrid = 0, dgrid = 0, slot = 0;
 
-    int grid() const { return (small || tc) ? sgrid : gen.grid; }
+    // partial rows a launch writes (tc: one per CTA + the refine kernel's)
+    int grid() const { return tc ? sgrid + 1 : small ? sgrid : gen.grid; }
     // the grid of a launch (delta iterations run the delta-only kernel)
     int grid_for(bool delta) const { return (small && delta && dfn) ? dgrid : grid(); }
     int max_grid() const { return std::max(grid(), small ? dgrid : 0); }
@@ -1703,7 +1712,31 @@ struct Assigner {
             tp.prev = tc_delta ? prev : nullptr;
             tp.lab8 = tc_delta ? lab8 : nullptr;
             tp.xabs = b.sx2 + 3;
+            tp.rq_ctl = rq_cap ? rq_ctl : nullptr;  // none: inline refine, the refine kernel finds no entries
+            tp.rq_row = rq_row;
+            tp.rq_cand = rq_cand;
+            tp.rq_x = rq_x;
+            tp.rq_cap = rq_cap;
             tfn<<<sgrid, tthreads, tsmem, st>>>(tmap, tp);
+            TcRefineParams rp{};
+            rp.n = n;
+            rp.c64 = b.c64;
+            rp.cn64 = b.cn64;
+            rp.bounds = b.bounds;
+            rp.xabs = b.sx2 + 3;
+            rp.ctl = rq_ctl;
+            rp.qrow = rq_row;
+            rp.qcand = rq_cand;
+            rp.qx = rq_x;
+            rp.cap = rq_cap;
+            rp.labels = labels;
+            rp.lab8 = tp.lab8;
+            rp.racc = racc;
+            rp.partial = accumulate ? b.partials + static_cast<int64_t>(sgrid) * (static_cast<int64_t>(k) * d + k)
+                                    : nullptr;
+            rp.refined = b.refined;
+            rp.done = tp.done;
+            rfn<<<rgrid, rthreads, 0, st>>>(rp);
         } else if (small) {
             DNDC_CUDA(cudaMemcpyToSymbolAsync(c_km_table, b.ctab, sizeof(float) * (k * d + k),
                                               sizeof(float) * KS_TABLE * slot, cudaMemcpyDeviceToDevice, st));
@@ -1760,6 +1793,8 @@ static void pick_tc(Assigner<float>& A) {
         A.tc_delta = TcCfg<D, K, P, 2>::DELTA_OK;
     }
     if (std::getenv("DNDC_TC_NO_DELTA")) A.tc_delta = false;
+    A.rfn = kmeans_tc_refine_kernel<D, K>;
+    A.rthreads = tc_refine_threads<D, K>();
 }
 
 // DNDC_KMEANS_KERNEL=tc|small|generic overrides the automatic choice (tests, A/B timing).
@@ -1794,6 +1829,23 @@ static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n, const T* x) {
             per_sm = std::max(1, std::min(per_sm, 2));
             const int64_t tiles = std::max<int64_t>(ceil_div(n / P, 128), 1);
             A.sgrid = static_cast<int>(std::min<int64_t>(tiles, static_cast<int64_t>(ctx->num_sms) * per_sm));
+            // near-tie queue (DNDC_TC_QUEUE=0: refine inside the tc kernel) and
+            // the refine kernel's accumulator; zeroed here, then the refine
+            // kernel leaves them zero after every launch
+            A.rq_cap = std::getenv("DNDC_TC_QUEUE") && std::getenv("DNDC_TC_QUEUE")[0] == '0'
+                           ? 0u
+                           : static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(n / 4, 4096), 1 << 22));
+            A.rq_ctl = static_cast<unsigned*>(ctx->slot("km_rq_ctl", sizeof(unsigned) * 4));
+            A.rq_row = static_cast<uint64_t*>(ctx->slot("km_rq_row", sizeof(uint64_t) * std::max(A.rq_cap, 1u)));
+            A.rq_x = static_cast<float*>(ctx->slot("km_rq_x", sizeof(float) * d * std::max(A.rq_cap, 1u)));
+            A.rq_cand = static_cast<unsigned long long*>(
+                ctx->slot("km_rq_cand", sizeof(unsigned long long) * std::max(A.rq_cap, 1u)));
+            A.racc = static_cast<long long*>(ctx->slot("km_racc", sizeof(long long) * (k * d + k)));
+            DNDC_CUDA(cudaMemsetAsync(A.rq_ctl, 0, sizeof(unsigned) * 4, ctx->stream));
+            DNDC_CUDA(cudaMemsetAsync(A.racc, 0, sizeof(long long) * (k * d + k), ctx->stream));
+            int rper_sm = 1;
+            DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper_sm, A.rfn, A.rthreads, 0));
+            A.rgrid = ctx->num_sms * std::max(rper_sm, 1);
             return A;
         }
     }
@@ -2172,7 +2224,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     if (ctx->group) {
         // ranks sharing GPUs: the stats exchange is host-staged, not capturable
         record(s);  // (allgather_f64 counts itself here)
-        ctx->launches += 1 + (A.small ? 4ull : 3ull) * max_iter;
+        ctx->launches += 1 + ((A.small || A.tc) ? 4ull : 3ull) * max_iter;
     }
     cudaStream_t gs = ctx->own_stream;
     char keybuf[256];
@@ -2217,7 +2269,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     DNDC_CUDA(cudaStreamWaitEvent(s, ctx->ev_b, 0));
     // reset + per iteration: assign (fused) | [tile reset,] assign, reduce, update
     // (persistent: reset + the one cooperative launch)
-    ctx->launches += persist ? (max_iter > persist_full_iters() ? 3ull : 2ull) : 1 + (fuse ? 1ull : A.small ? 4ull : 3ull) * max_iter;
+    ctx->launches += persist ? (max_iter > persist_full_iters() ? 3ull : 2ull) : 1 + (fuse ? 1ull : (A.small || A.tc) ? 4ull : 3ull) * max_iter;
     if (ctx->world > 1) ctx->counters.allgathers += max_iter;
     }
     ctx->last_kernel = persist ? (max_iter > persist_full_iters() ? PP.delta.name : PP.full.name) : "";
@@ -2282,6 +2334,7 @@ static void kmeans_predict(dndc_ctx* ctx, const T* x, int64_t n, int64_t m64, co
         if (A.small || A.tc) scan_input<T>(ctx, b, x, n * m, s);
         A.launch(b, x, n, m, k, false, labels, false, s);
         DNDC_LAUNCHED(ctx);
+        if (A.tc) ctx->launches++;  // + the near-tie refine kernel
     }
     unsigned long long* hr = reinterpret_cast<unsigned long long*>(h);
     DNDC_CUDA(cudaMemcpyAsync(hr, b.refined, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -2312,6 +2365,7 @@ static void kmeans_step(dndc_ctx* ctx, const T* x, int64_t n, int64_t m64, const
         scan_input<T>(ctx, b, x, n * m, s);
         A.launch(b, x, n, m, k, true, labels, false, s);
         DNDC_LAUNCHED(ctx);
+        if (A.tc) ctx->launches++;  // + the near-tie refine kernel
         reduce_partials_kernel<<<(S + 7) / 8, 256, 0, s>>>(b.partials, A.grid(), S, b.stats, nullptr);
         DNDC_LAUNCHED(ctx);
     }

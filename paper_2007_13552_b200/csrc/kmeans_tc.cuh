@@ -37,7 +37,125 @@ struct TcParams {
     const int8_t* prev;   // delta iterations: last iteration's labels (null: full accumulation)
     int8_t* lab8;         // this iteration's labels (fit only; null in predict)
     const double* xabs;   // max |x| of the shard: the int64 fixed-point scale of the sums
+    // near-tie queue (null: refine inline): rows whose fp32 top-2 gap is inside
+    // the error bound go to kmeans_tc_refine_kernel with their candidate mask
+    unsigned* rq_ctl;             // [0] entries, [1] refine-kernel ticket
+    uint64_t* rq_row;             // row | (uint8)(decided label + 1) << 48 | (uint8)last label << 56
+    unsigned long long* rq_cand;  // candidate clusters
+    float* rq_x;                  // the row itself (D floats): no gather from X later
+    unsigned rq_cap;
 };
+
+// label of a row handed to the refine kernel (not written, not accumulated here)
+template <int K>
+constexpr int tc_deferred() { return K + 1; }
+
+// The exact decision for one near-tie row, by one warp (result warp-uniform):
+// `row` (D floats, shared memory) against the candidate clusters `cm`.
+// (1) fast filter: f64 distances with the lanes over the features (any
+// summation order).  Its error and the reference's are both <= (D+2)*2^-53*S,
+// S = |x|^2 + max|c|^2 + 2|x|max|c|, so a winner whose margin over the
+// runner-up (and over the clamp at 0) exceeds 2^-40*S is the reference's
+// choice, sqrt rounding included.  (2) otherwise the reference's own operation
+// order (cluster.cpp:44-56 via ref_distance), lanes over the candidates, with
+// its lowest-index tie rule.
+template <int D, int K>
+__device__ __forceinline__ int tc_refine_warp(const float* row, uint64_t cm, const double* __restrict__ c64,
+                                              const double* __restrict__ cn64, float cnmax, float cmax,
+                                              unsigned long long* fallback_ctr) {
+    const int lane = threadIdx.x & 31;
+    constexpr int FL = (D + 31) / 32;
+    double xf[FL];
+    double xn = 0.0;
+#pragma unroll
+    for (int u = 0; u < FL; ++u) {
+        const int f = lane + 32 * u;
+        xf[u] = f < D ? static_cast<double>(row[f]) : 0.0;
+        xn = fma(xf[u], xf[u], xn);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) xn += __shfl_xor_sync(FULL, xn, o);
+    double d1 = DBL_MAX, d2 = DBL_MAX;
+    int best = K;
+    for (uint64_t rest = cm; rest;) {
+        int js[4];
+        double gp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            js[q] = rest ? __ffsll(static_cast<long long>(rest)) - 1 : -1;
+            rest &= rest - 1;
+            gp[q] = 0.0;
+            const double* cq = c64 + static_cast<int64_t>(js[q] < 0 ? 0 : js[q]) * D;
+#pragma unroll
+            for (int u = 0; u < FL; ++u) {
+                const int f = lane + 32 * u;
+                if (f < D) gp[q] = fma(xf[u], __ldg(cq + f), gp[q]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) gp[q] += __shfl_xor_sync(FULL, gp[q], o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (js[q] < 0) continue;
+            const double dq = xn + cn64[js[q]] - 2.0 * gp[q];
+            if (dq < d1) {
+                d2 = d1;
+                d1 = dq;
+                best = js[q];
+            } else if (dq < d2) {
+                d2 = dq;
+            }
+        }
+    }
+    const double margin =
+        0x1.0p-40 * (xn + static_cast<double>(cnmax) + 2.0 * sqrt(xn) * static_cast<double>(cmax));
+    const bool decided = d1 > margin && d2 - d1 > margin;
+    if (decided) return best;
+    if (fallback_ctr && lane == 0) atomicAdd(fallback_ctr, 1ull);
+    double bd = 0.0;
+    best = K;
+    for (uint64_t rest = cm; rest;) {  // rounds of up to 32 candidates, ascending j
+        uint64_t mm = rest;
+        for (int i = 0; i < lane && mm; ++i) mm &= mm - 1;
+        const int j = mm ? __ffsll(static_cast<long long>(mm)) - 1 : -1;
+        for (int i = 0; i < 32 && rest; ++i) rest &= rest - 1;
+        const double* c = c64 + static_cast<int64_t>(j < 0 ? 0 : j) * D;
+        double xs = 0.0, g = 0.0;
+        // batches of 16 features: the centroid loads are issued ahead of the
+        // two serial f64 chains (one L1 round trip per batch, not per step)
+        constexpr int FB = D % 16 == 0 ? 16 : D % 8 == 0 ? 8 : 2;
+#pragma unroll
+        for (int f0 = 0; f0 < D; f0 += FB) {
+            double2 cb[FB / 2];
+#pragma unroll
+            for (int u = 0; u < FB / 2; ++u) cb[u] = __ldg(reinterpret_cast<const double2*>(c + f0) + u);
+#pragma unroll
+            for (int u = 0; u < FB; ++u) {
+                const double xv = static_cast<double>(row[f0 + u]);
+                xs = add_rn(xs, mul_rn(xv, xv));
+                g = add_rn(g, mul_rn(xv, u % 2 ? cb[u / 2].y : cb[u / 2].x));
+            }
+        }
+        double dj = j < 0 ? 0.0 : ref_distance(xs, cn64[j], g);
+        int jj = j < 0 ? K : j;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_xor_sync(FULL, dj, o);
+            const int oj = __shfl_xor_sync(FULL, jj, o);
+            if (oj < K && (jj == K || od < dj || (od == dj && oj < jj))) {
+                dj = od;
+                jj = oj;
+            }
+        }
+        if (jj < K && (best == K || dj < bd)) {  // later rounds hold larger j: strict <
+            bd = dj;
+            best = jj;
+        }
+    }
+    return best;
+}
 
 __host__ __device__ constexpr int tc_pow2_cols(int c) {
     return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
@@ -51,7 +169,7 @@ struct TcCfg {
     static constexpr int NS = P * K;                  // MMA N: score slots
     static constexpr int PR = 128;                    // packed rows per tile (MMA M)
     static constexpr int TROWS = PR * P;              // data rows per tile
-    static constexpr int S = K * D >= 4096 ? 2 : 3;  // TMA stages (2 leaves room for the sums)
+    static constexpr int S = 3;                       // TMA stages
     static constexpr int WGS = WG_;                   // epilogue warpgroups
     static constexpr int EPI = 128 * WGS;
     static constexpr int THREADS = EPI + 32;          // + the producer / MMA warp
@@ -67,10 +185,7 @@ struct TcCfg {
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
     static constexpr int OFF_CN = OFF_BLO + B_BYTES;
     static constexpr int OFF_CNT = OFF_CN + ((K * 4 + 15) / 16) * 16;  // u16 tile counts per warpgroup
-    // one int64 fixed-point accumulator per CTA: [K*D] sums, [K] counts,
-    // shared by the warpgroups (integer atomics: any order gives the same bits)
-    static constexpr int OFF_ACC = OFF_CNT + WGS * ((VW * K * 2 + 15) / 16) * 16;
-    static constexpr int OFF_BAR = OFF_ACC + (K * D + K) * 8;
+    static constexpr int OFF_BAR = OFF_CNT + WGS * ((VW * K * 2 + 15) / 16) * 16;
     static constexpr int NBARS = 2 * S + 3 * WGS;
     static constexpr int OFF_TMEM = OFF_BAR + NBARS * 8;
     static constexpr int SMEM = OFF_TMEM + 16;
@@ -222,10 +337,16 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
         constexpr float ERR = 4.f * (static_cast<float>(3 * C::KC) * 0x1.0p-24f + 3.f * 0x1.0p-20f);
         unsigned long long refined = 0;
         const int g = lane / L, q = lane % L;
-        // cluster sums: int64 fixed point at 2^-(61-e), n max|x| < 2^e, shared by
-        // the warpgroups (atomics; integer adds commute)
-        long long* acc = reinterpret_cast<long long*>(smem + C::OFF_ACC);
-        for (int e = tid; e < KD + K; e += C::EPI) acc[e] = 0ll;
+        // cluster sums: int64 fixed point at 2^-(61-e), n max|x| < 2^e, in the
+        // CTA's own partial row (global, L2-resident; converted to f64 in place
+        // at the end), shared by the warpgroups.  Integer adds commute, and
+        // global reductions are fire-and-forget RED at L2 -- shared memory has
+        // no native 64-bit add (a CAS loop that stalled the warp).
+        long long* acc = accumulate ? reinterpret_cast<long long*>(p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K))
+                                    : nullptr;
+        if (accumulate)
+            for (int e = tid; e < KD + K; e += C::EPI) acc[e] = 0ll;
+        __threadfence();
         int e2 = 0;
         frexp(static_cast<double>(p.n) * (p.xabs ? *p.xabs : 1.0) + 1.0, &e2);
         const int shift = 61 - e2;
@@ -237,6 +358,14 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             const int64_t use = it / WGS;
             const int64_t prow0 = (blockIdx.x + it * gridDim.x) * PR;
             const float* xt = tiles + st * (C::TILE_BYTES / 4);
+            // last iteration's labels, loaded now: the global round trip overlaps
+            // the split and the MMAs instead of holding up the accumulator release
+            int oldl[P];
+#pragma unroll
+            for (int h = 0; h < P; ++h) {
+                const int64_t row = (prow0 + t) * P + h;
+                oldl[h] = (p.prev && row < p.n) ? static_cast<int>(p.prev[row]) : -1;
+            }
             tc::mbar_wait(&full[st], static_cast<uint32_t>((it / S) & 1));
 
             // split: lo = x - trunc_tf32(x); the raw row stays in registers; the
@@ -267,6 +396,32 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             auto xval = [&](int c) {
                 const float4 v4 = xr[c / 4];
                 return (c % 4 == 0) ? v4.x : (c % 4 == 1) ? v4.y : (c % 4 == 2) ? v4.z : v4.w;
+            };
+            // hands the rows of this warp with `want` to the refine kernel's
+            // queue (row, last label, the decided label or none, candidates, the
+            // row itself); false for the lanes whose row did not fit
+            auto enqueue = [&](int h, bool want, uint64_t cm, int newl) -> bool {
+                const unsigned fm = __ballot_sync(FULL, want);
+                if (!p.rq_ctl || !fm) return false;
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(p.rq_ctl, static_cast<unsigned>(__popc(fm)));
+                base = __shfl_sync(FULL, base, 0);
+                const unsigned pos = base + static_cast<unsigned>(__popc(fm & ((1u << lane) - 1u)));
+                if (!want || pos >= p.rq_cap) return false;
+                p.rq_row[pos] = static_cast<uint64_t>((prow0 + t) * P + h) |
+                                (static_cast<uint64_t>(static_cast<uint8_t>(oldl[h])) << 56) |
+                                (static_cast<uint64_t>(static_cast<uint8_t>(newl + 1)) << 48);
+                p.rq_cand[pos] = cm;
+                float* qx = p.rq_x + static_cast<int64_t>(pos) * D;
+                if constexpr (P == 1 && D % 4 == 0) {
+#pragma unroll
+                    for (int c = 0; c < D / 4; ++c) reinterpret_cast<float4*>(qx)[c] = xr[c];
+                } else {
+#pragma unroll
+                    for (int f = 0; f < D; f += 2)
+                        *reinterpret_cast<float2*>(qx + f) = make_float2(xval(h * D + f), xval(h * D + f + 1));
+                }
+                return true;
             };
             // per-row |x|^2 for the error bound (fp32; only scales the bound)
             float xx[P];
@@ -366,131 +521,29 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                         if (cn[j] + v[i] <= b1[h] + tau[h]) cand[h] |= 1ull << j;
                     }
                 }
-                // warp-cooperative exact decision: the flagged rows one at a
-                // time, the lanes spread over that row's candidates (one f64
-                // dot-product chain each, the row broadcast by shuffles), then
-                // a warp argmin with the reference's lowest-index tie rule.
-                // (A per-lane ref_argmin_cand ran ncand + 1 serial chains in a
-                // divergent branch and cost half the kernel at K = 64.)
+                // near-tie rows go to the refine kernel (one warp per row over a
+                // balanced queue) instead of stalling this warp -- and with it
+                // the warpgroup's next MMA -- for the f64 decision; only a
+                // queue overflow refines here
 #pragma unroll
                 for (int h = 0; h < P; ++h) {
-                    unsigned fm = __ballot_sync(FULL, flag[h]);
+                    if (enqueue(h, flag[h], cand[h], -1)) label[h] = tc_deferred<K>();
+                    unsigned fm = __ballot_sync(FULL, flag[h] && label[h] != tc_deferred<K>());
+                    // warp-cooperative exact decision, one flagged row at a time
+                    // (the row parked in this warp's rows of the lo buffer: free,
+                    // the tile's MMAs completed)
                     while (fm) {
                         const int src = __ffs(fm) - 1;
                         fm &= fm - 1;
                         const uint64_t cm = __shfl_sync(FULL, cand[h], src);
-                        // (1) fast filter: f64 distances with the lanes over the
-                        // features (any summation order).  Its error and the
-                        // reference's are both <= (D+2)*2^-53*S, S = |x|^2 +
-                        // max|c|^2 + 2|x|max|c|, so a winner whose margin over
-                        // the runner-up (and over the clamp at 0) exceeds
-                        // 2^-40*S is the reference's choice, sqrt rounding
-                        // included.  The row goes through this warp's own rows
-                        // of the lo buffer (free: the tile's MMAs completed).
                         float* scr = work + wq * 32 * 32;
                         if (lane == src) {
 #pragma unroll
                             for (int f = 0; f < D; ++f) scr[f] = xval(h * D + f);
                         }
                         __syncwarp();
-                        constexpr int FL = (D + 31) / 32;
-                        double xf[FL];
-                        double xn = 0.0;
-#pragma unroll
-                        for (int u = 0; u < FL; ++u) {
-                            const int f = lane + 32 * u;
-                            xf[u] = f < D ? static_cast<double>(scr[f]) : 0.0;
-                            xn = fma(xf[u], xf[u], xn);
-                        }
+                        const int best = tc_refine_warp<D, K>(scr, cm, p.c64, p.cn64, cnmax, cmax, nullptr);
                         __syncwarp();
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) xn += __shfl_xor_sync(FULL, xn, o);
-                        double d1 = DBL_MAX, d2 = DBL_MAX;
-                        int best = K;
-                        for (uint64_t rest = cm; rest;) {
-                            int js[4];
-                            double gp[4];
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                js[q] = rest ? __ffsll(static_cast<long long>(rest)) - 1 : -1;
-                                rest &= rest - 1;
-                                gp[q] = 0.0;
-                                const double* cq = p.c64 + static_cast<int64_t>(js[q] < 0 ? 0 : js[q]) * D;
-#pragma unroll
-                                for (int u = 0; u < FL; ++u) {
-                                    const int f = lane + 32 * u;
-                                    if (f < D) gp[q] = fma(xf[u], __ldg(cq + f), gp[q]);
-                                }
-                            }
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                                for (int q = 0; q < 4; ++q) gp[q] += __shfl_xor_sync(FULL, gp[q], o);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                if (js[q] < 0) continue;
-                                const double dq = xn + p.cn64[js[q]] - 2.0 * gp[q];
-                                if (dq < d1) {
-                                    d2 = d1;
-                                    d1 = dq;
-                                    best = js[q];
-                                } else if (dq < d2) {
-                                    d2 = dq;
-                                }
-                            }
-                        }
-                        const double margin =
-                            0x1.0p-40 * (xn + static_cast<double>(cnmax) + 2.0 * sqrt(xn) * static_cast<double>(cmax));
-                        const bool decided = d1 > margin && d2 - d1 > margin;
-#ifdef KT_EXP_COUNT_FALLBACK
-                        if (!decided && lane == src) atomicAdd(p.refined + 1, 1ull);
-#endif
-                        // (2) otherwise the reference's own operation order
-                        double bd = 0.0;
-                        if (!decided) best = K;
-                        for (uint64_t rest = decided ? 0 : cm; rest;) {  // rounds of up to 32 candidates, ascending j
-                            uint64_t mm = rest;
-                            for (int i = 0; i < lane && mm; ++i) mm &= mm - 1;
-                            const int j = mm ? __ffsll(static_cast<long long>(mm)) - 1 : -1;
-                            for (int i = 0; i < 32 && rest; ++i) rest &= rest - 1;
-                            const double* c = p.c64 + static_cast<int64_t>(j < 0 ? 0 : j) * D;
-                            double xn = 0.0, g = 0.0;
-                            // batches of 16 features: the centroid loads and the
-                            // row broadcast are issued ahead of the two serial
-                            // f64 chains (one L1 round trip per batch, not per step)
-                            constexpr int FB = D % 16 == 0 ? 16 : D % 8 == 0 ? 8 : 2;
-#pragma unroll
-                            for (int f0 = 0; f0 < D; f0 += FB) {
-                                double2 cb[FB / 2];
-                                float xb[FB];
-#pragma unroll
-                                for (int u = 0; u < FB / 2; ++u)
-                                    cb[u] = __ldg(reinterpret_cast<const double2*>(c + f0) + u);
-#pragma unroll
-                                for (int u = 0; u < FB; ++u) xb[u] = __shfl_sync(FULL, xval(h * D + f0 + u), src);
-#pragma unroll
-                                for (int u = 0; u < FB; ++u) {
-                                    const double xf = static_cast<double>(xb[u]);
-                                    xn = add_rn(xn, mul_rn(xf, xf));
-                                    g = add_rn(g, mul_rn(xf, u % 2 ? cb[u / 2].y : cb[u / 2].x));
-                                }
-                            }
-                            double dj = j < 0 ? 0.0 : ref_distance(xn, p.cn64[j], g);
-                            int jj = j < 0 ? K : j;
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) {
-                                const double od = __shfl_xor_sync(FULL, dj, o);
-                                const int oj = __shfl_xor_sync(FULL, jj, o);
-                                if (oj < K && (jj == K || od < dj || (od == dj && oj < jj))) {
-                                    dj = od;
-                                    jj = oj;
-                                }
-                            }
-                            if (jj < K && (best == K || dj < bd)) {  // later rounds hold larger j: strict <
-                                bd = dj;
-                                best = jj;
-                            }
-                        }
                         if (lane == src) {
                             label[h] = best;
                             ++refined;
@@ -498,38 +551,37 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                     }
                 }
             }
+            // every score has been read: the accumulator goes back to the MMA
+            // issuer before the label stores and the accumulation
+            tc::tc_fence_before();
+            tc::mbar_arrive(&dempty[wg]);
             if (p.labels) {
 #pragma unroll
                 for (int h = 0; h < P; ++h) {
                     const int64_t row = (prow0 + t) * P + h;
-                    if (row < p.n) p.labels[row] = label[h];
+                    if (row < p.n && label[h] < K) p.labels[row] = label[h];
                 }
             }
-            int oldl[P];
 #pragma unroll
             for (int h = 0; h < P; ++h) {
                 const int64_t row = (prow0 + t) * P + h;
-                oldl[h] = -1;
-                if (row < p.n) {
-                    if (p.prev) oldl[h] = p.prev[row];
-                    if (p.lab8) p.lab8[row] = static_cast<int8_t>(label[h]);
-                }
+                if (row < p.n && label[h] < K && p.lab8) p.lab8[row] = static_cast<int8_t>(label[h]);
             }
-            tc::tc_fence_before();
-            tc::mbar_arrive(&dempty[wg]);
             if (!accumulate) continue;
 
             if (C::DELTA_OK && p.prev) {
                 // ---------------- delta iteration: only rows whose label changed,
                 // +x into the new cluster and -x out of the old one (the update
-                // adds these to the running sums), each warp on its own: the
-                // changed row is parked in the warp's own rows of `work` (free:
-                // the tile's MMAs completed), lanes over features, int64 atomics
-                // -- no warpgroup barrier, no cross-warp list walk
+                // adds these to the running sums).  They go to the refine
+                // kernel's queue like the near-ties (it accumulates them off this
+                // warpgroup's MMA critical path); a full queue falls back to the
+                // warp itself: the changed row parked in the warp's own rows of
+                // `work` (free: the tile's MMAs completed), lanes over features
                 float* wrow = work + wq * 32 * 32;  // this warp's first row slot (K-block 0)
 #pragma unroll
                 for (int h = 0; h < P; ++h) {
-                    const bool ch = label[h] < K && label[h] != oldl[h];
+                    bool ch = label[h] < K && label[h] != oldl[h];
+                    if (enqueue(h, ch, 0ull, label[h])) ch = false;
                     unsigned fm = __ballot_sync(FULL, ch);
                     while (fm) {
                         const int src = __ffs(fm) - 1;
@@ -681,14 +733,151 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
         if (refined) atomicAdd(p.refined, refined);
         if (accumulate) {
             // every warpgroup is past its last tile: the CTA's fixed-point sums
-            // and counts -> its f64 partial row (summed over CTAs in CTA order)
+            // and counts -> its f64 partial row, in place (summed over CTAs in
+            // CTA order)
+            __threadfence();
             tc::named_sync(15, C::EPI);
             double* out = p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K);
-            for (int e = tid; e < KD + K; e += C::EPI)
-                out[e] = e < KD ? ldexp(static_cast<double>(acc[e]), -shift) : static_cast<double>(acc[e]);
+            for (int e = tid; e < KD + K; e += C::EPI) {
+                const long long v = __ldcg(acc + e);
+                out[e] = e < KD ? ldexp(static_cast<double>(v), -shift) : static_cast<double>(v);
+            }
         }
     }
     tc::tc_fence_before();
     __syncthreads();
     if (warp == CTRL) tc::tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------- near-tie refine
+// Runs after kmeans_tc_kernel in the same stream: one warp per queued row (the
+// rows whose fp32 top-2 gap fell inside the error bound, ~2% at cfg3), the
+// exact decision of tc_refine_warp, then what the tc kernel skipped for the
+// row: labels / lab8, and its accumulation -- every row in a full iteration,
+// +x / -x when the label changed in a delta iteration -- as int64 fixed point
+// (the tc kernel's scale; integer adds commute, so the result does not depend
+// on which warp took which row).  The last CTA turns the sums into partial row
+// `partial` (after the tc kernel's per-CTA rows) and resets the queue and the
+// accumulator for the next launch.
+struct TcRefineParams {
+    int64_t n;
+    const double* c64;
+    const double* cn64;
+    const float* bounds;
+    const double* xabs;
+    unsigned* ctl;                 // [0] queue entries, [1] ticket
+    const uint64_t* qrow;          // row | (uint8)(decided label + 1) << 48 | (uint8)last label << 56
+    const unsigned long long* qcand;
+    const float* qx;
+    unsigned cap;
+    int32_t* labels;
+    int8_t* lab8;
+    long long* racc;               // K*D sums, K counts (zero between launches)
+    double* partial;               // null: predict (no accumulation)
+    unsigned long long* refined;
+    const int* done;
+};
+
+template <int D, int K>
+__host__ __device__ constexpr int tc_refine_threads() { return 512; }
+
+// rows are accumulated in a per-CTA shared int64 copy first (global atomics
+// on the K*D sums from every warp contended at L2: 200 us per launch at cfg3),
+// then the CTA adds its nonzero entries to racc once
+template <int D, int K>
+__global__ void __launch_bounds__(512) kmeans_tc_refine_kernel(TcRefineParams p) {
+    constexpr int KD = K * D, WPB = tc_refine_threads<D, K>() / 32;
+    __shared__ float rows[WPB][D];
+    __shared__ long long sacc[KD + K];
+    __shared__ bool last;
+    for (int e = threadIdx.x; e < KD + K; e += blockDim.x) sacc[e] = 0ll;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool skip = p.done && *p.done;
+    const unsigned count = skip ? 0u : min(p.ctl[0], p.cap);
+    int e2 = 0;
+    frexp(static_cast<double>(p.n) * (p.xabs ? *p.xabs : 1.0) + 1.0, &e2);
+    const int shift = 61 - e2;
+    const float qscale = ldexpf(1.f, shift);
+    const float cmax = p.bounds[0], cnmax = p.bounds[1];
+    float* row = rows[warp];
+    constexpr int FPL = (D + 31) / 32;
+    // the next entry is loaded while this one is decided (the queue is
+    // contiguous and L2-resident: it was written by the tc kernel just before)
+    auto fetch = [&](unsigned ee, uint64_t& v, uint64_t& c, float (&xv)[FPL]) {
+        v = p.qrow[ee];
+        c = p.qcand[ee];
+#pragma unroll
+        for (int u = 0; u < FPL; ++u) {
+            const int f = lane + 32 * u;
+            xv[u] = f < D ? p.qx[static_cast<int64_t>(ee) * D + f] : 0.f;
+        }
+    };
+    const unsigned stride = gridDim.x * WPB;
+    unsigned e = blockIdx.x * WPB + warp;
+    uint64_t v = 0, cm = 0;
+    unsigned nref = 0;  // entries decided here (the rest only accumulate)
+    float xa[FPL];
+    if (e < count) fetch(e, v, cm, xa);
+    for (; e < count; e += stride) {
+        uint64_t vn = 0, cn = 0;
+        float xn[FPL];
+        if (e + stride < count) fetch(e + stride, vn, cn, xn);
+#pragma unroll
+        for (int u = 0; u < FPL; ++u)
+            if (lane + 32 * u < D) row[lane + 32 * u] = xa[u];
+        __syncwarp();
+        const int64_t r = static_cast<int64_t>(v & ((1ull << 48) - 1));
+        const int old = static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(v >> 56)));
+        const int dec = static_cast<int>((v >> 48) & 0xff) - 1;  // decided label (changed row) or -1
+        int best = dec;
+        if (dec < 0) {
+            best = tc_refine_warp<D, K>(row, cm, p.c64, p.cn64, cnmax, cmax, nullptr);
+            ++nref;
+            if (lane == 0) {
+                if (p.labels) p.labels[r] = best;
+                if (p.lab8) p.lab8[r] = static_cast<int8_t>(best);
+            }
+        }
+        __syncwarp();
+        if (p.partial && best != old) {
+            for (int f = lane; f < D; f += 32) {
+                const long long qv = __float2ll_rn(row[f] * qscale);
+                atomicAdd(reinterpret_cast<unsigned long long*>(sacc + best * D + f), static_cast<unsigned long long>(qv));
+                if (old >= 0)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(sacc + old * D + f), static_cast<unsigned long long>(-qv));
+            }
+            if (lane == 0) {
+                atomicAdd(reinterpret_cast<unsigned long long*>(sacc + KD + best), 1ull);
+                if (old >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(sacc + KD + old), ~0ull);
+            }
+        }
+        __syncwarp();
+        v = vn;
+        cm = cn;
+#pragma unroll
+        for (int u = 0; u < FPL; ++u) xa[u] = xn[u];
+    }
+    if (lane == 0 && nref) atomicAdd(p.refined, static_cast<unsigned long long>(nref));
+    __syncthreads();
+    if (p.partial && blockIdx.x * WPB < count) {
+        for (int e = threadIdx.x; e < KD + K; e += blockDim.x)
+            if (sacc[e]) atomicAdd(reinterpret_cast<unsigned long long*>(p.racc + e), static_cast<unsigned long long>(sacc[e]));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(p.ctl + 1, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int e = threadIdx.x; e < KD + K; e += blockDim.x) {
+        const long long v = static_cast<long long>(atomicExch(reinterpret_cast<unsigned long long*>(p.racc + e), 0ull));
+        if (p.partial) p.partial[e] = e < KD ? ldexp(static_cast<double>(v), -shift) : static_cast<double>(v);
+    }
+    if (threadIdx.x == 0) {
+        p.ctl[0] = 0;
+        p.ctl[1] = 0;
+    }
 }

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--per", type=float, default=1.0)
     ap.add_argument("--top", type=int, default=40)
     ap.add_argument("--launch", type=int, default=None, help="only the N-th captured launch (0-based)")
+    ap.add_argument("--by-stall", action="store_true", help="order lines by stall samples")
     args = ap.parse_args()
     cmd = ["ncu", "-i", args.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
     if args.launch is not None:
@@ -59,7 +60,8 @@ def main():
     totw = sum(v[1] for v in agg.values()) or 1.0
     print(f"total warp instructions {tot:.4g} ({tot / args.per:.1f} per unit)")
     print("opcodes:", ", ".join(f"{o} {n / args.per:.1f}" for o, n in ops.most_common(16)))
-    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[: args.top]:
+    key = (lambda kv: -kv[1][1]) if args.by_stall else (lambda kv: -kv[1][0])
+    for k, v in sorted(agg.items(), key=key)[: args.top]:
         print(f"{v[0] / args.per:8.1f} {100 * v[1] / totw:5.1f}%stall  {k[0]}:{k[1]}  {v[2].strip()[:90]}")
 
 
