@@ -1673,6 +1673,9 @@ struct Assigner {
     bool tc_delta = false;  // the tc instantiation supports delta iterations (TcCfg::DELTA_OK)
     void (*tfn)(CUtensorMap, TcParams) = nullptr;
     void (*rfn)(TcRefineParams) = nullptr;  // near-tie refine after each tc launch
+    void (*dtfn)(CUtensorMap, TcParams) = nullptr;  // four-warpgroup kernel: delta iterations and predict
+    size_t dtsmem = 0;
+    int dtthreads = 0;
     unsigned* rq_ctl = nullptr;
     uint64_t* rq_row = nullptr;
     unsigned long long* rq_cand = nullptr;
@@ -1717,7 +1720,14 @@ struct Assigner {
             tp.rq_cand = rq_cand;
             tp.rq_x = rq_x;
             tp.rq_cap = rq_cap;
-            tfn<<<sgrid, tthreads, tsmem, st>>>(tmap, tp);
+            tp.x = reinterpret_cast<const float*>(x);
+            // launches that accumulate no row themselves (delta, predict) take the
+            // four-warpgroup kernel; full accumulation needs the sort of the old one
+            const bool four = dtfn && (tp.prev != nullptr || !accumulate);
+            if (four)
+                dtfn<<<sgrid, dtthreads, dtsmem, st>>>(tmap, tp);
+            else
+                tfn<<<sgrid, tthreads, tsmem, st>>>(tmap, tp);
             TcRefineParams rp{};
             rp.n = n;
             rp.c64 = b.c64;
@@ -1727,7 +1737,8 @@ struct Assigner {
             rp.ctl = rq_ctl;
             rp.qrow = rq_row;
             rp.qcand = rq_cand;
-            rp.qx = rq_x;
+            rp.qx = four ? nullptr : rq_x;  // the four-warpgroup kernel queues no rows: read X
+            rp.x = reinterpret_cast<const float*>(x);
             rp.cap = rq_cap;
             rp.labels = labels;
             rp.lab8 = tp.lab8;
@@ -1795,6 +1806,13 @@ static void pick_tc(Assigner<float>& A) {
     if (std::getenv("DNDC_TC_NO_DELTA")) A.tc_delta = false;
     A.rfn = kmeans_tc_refine_kernel<D, K>;
     A.rthreads = tc_refine_threads<D, K>();
+    if constexpr (P == 1 && D % 4 == 0) {
+        if (!std::getenv("DNDC_TC_NO_FOUR") && A.tc_delta) {
+            A.dtfn = kmeans_tcd_kernel<D, K>;
+            A.dtsmem = TcdCfg<D, K>::SMEM;
+            A.dtthreads = TcdCfg<D, K>::THREADS;
+        }
+    }
 }
 
 // DNDC_KMEANS_KERNEL=tc|small|generic overrides the automatic choice (tests, A/B timing).
@@ -1824,6 +1842,9 @@ static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n, const T* x) {
                                       static_cast<uint64_t>(P * d * 4), 32, 128, true);
             DNDC_CUDA(cudaFuncSetAttribute(A.tfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(A.tsmem)));
+            if (A.dtfn)
+                DNDC_CUDA(cudaFuncSetAttribute(A.dtfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(A.dtsmem)));
             int per_sm = 1;
             DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, A.tfn, A.tthreads, A.tsmem));
             per_sm = std::max(1, std::min(per_sm, 2));
@@ -2512,6 +2533,12 @@ int dndc_internal_iter_trace(unsigned long long* out128) {
 }
 int dndc_internal_cta_trace(unsigned long long* out4096) {
     return guard([&] { DNDC_CUDA(cudaMemcpyFromSymbol(out4096, dndc::g_cta_trace, 4096 * sizeof(unsigned long long))); });
+}
+#endif
+
+#ifdef TCD_TRACE
+extern "C" int dndc_internal_tcd_trace(unsigned long long* out512) {
+    return guard([&] { DNDC_CUDA(cudaMemcpyFromSymbol(out512, dndc::g_tcd_trace, 512 * sizeof(unsigned long long))); });
 }
 #endif
 

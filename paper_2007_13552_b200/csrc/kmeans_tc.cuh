@@ -42,9 +42,13 @@ struct TcParams {
     unsigned* rq_ctl;             // [0] entries, [1] refine-kernel ticket
     uint64_t* rq_row;             // row | (uint8)(decided label + 1) << 48 | (uint8)last label << 56
     unsigned long long* rq_cand;  // candidate clusters
-    float* rq_x;                  // the row itself (D floats): no gather from X later
+    float* rq_x;                  // the row itself (D floats; null: the refine kernel reads X)
     unsigned rq_cap;
+    const float* x;               // X (kmeans_tcd_kernel's queue-overflow fallback)
 };
+
+// an unused queue slot
+constexpr uint64_t TC_QHOLE = ~0ull;
 
 // label of a row handed to the refine kernel (not written, not accumulated here)
 template <int K>
@@ -336,6 +340,16 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
         const float cmax = p.bounds[0], cnmax = p.bounds[1];
         constexpr float ERR = 4.f * (static_cast<float>(3 * C::KC) * 0x1.0p-24f + 3.f * 0x1.0p-20f);
         unsigned long long refined = 0;
+        // this warp's reserved run of queue slots (warp-uniform): slots are taken
+        // from the global counter QCHUNK at a time, so the ~1 us atomic round
+        // trip is paid once per run instead of once per tile; a run's unused
+        // slots are marked as holes (TC_QHOLE) for the refine kernel
+        constexpr unsigned QCHUNK = 64;
+        unsigned qbase = 0, qleft = 0;
+        auto qholes = [&]() {
+            for (unsigned i = lane; i < qleft; i += 32)
+                if (qbase + i < p.rq_cap) p.rq_row[qbase + i] = TC_QHOLE;
+        };
         const int g = lane / L, q = lane % L;
         // cluster sums: int64 fixed point at 2^-(61-e), n max|x| < 2^e, in the
         // CTA's own partial row (global, L2-resident; converted to f64 in place
@@ -403,10 +417,17 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             auto enqueue = [&](int h, bool want, uint64_t cm, int newl) -> bool {
                 const unsigned fm = __ballot_sync(FULL, want);
                 if (!p.rq_ctl || !fm) return false;
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(p.rq_ctl, static_cast<unsigned>(__popc(fm)));
-                base = __shfl_sync(FULL, base, 0);
-                const unsigned pos = base + static_cast<unsigned>(__popc(fm & ((1u << lane) - 1u)));
+                const unsigned cnt = static_cast<unsigned>(__popc(fm));
+                if (cnt > qleft) {
+                    qholes();
+                    unsigned base = 0;
+                    if (lane == 0) base = atomicAdd(p.rq_ctl, QCHUNK);
+                    qbase = __shfl_sync(FULL, base, 0);
+                    qleft = QCHUNK;
+                }
+                const unsigned pos = qbase + static_cast<unsigned>(__popc(fm & ((1u << lane) - 1u)));
+                qbase += cnt;
+                qleft -= cnt;
                 if (!want || pos >= p.rq_cap) return false;
                 p.rq_row[pos] = static_cast<uint64_t>((prow0 + t) * P + h) |
                                 (static_cast<uint64_t>(static_cast<uint8_t>(oldl[h])) << 56) |
@@ -731,6 +752,7 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
             tc::named_sync(bar_id, 128);
         }
         if (refined) atomicAdd(p.refined, refined);
+        qholes();
         if (accumulate) {
             // every warpgroup is past its last tile: the CTA's fixed-point sums
             // and counts -> its f64 partial row, in place (summed over CTAs in
@@ -768,7 +790,8 @@ struct TcRefineParams {
     unsigned* ctl;                 // [0] queue entries, [1] ticket
     const uint64_t* qrow;          // row | (uint8)(decided label + 1) << 48 | (uint8)last label << 56
     const unsigned long long* qcand;
-    const float* qx;
+    const float* qx;               // rows in the queue, or null: read from x
+    const float* x;
     unsigned cap;
     int32_t* labels;
     int8_t* lab8;
@@ -807,10 +830,13 @@ __global__ void __launch_bounds__(512) kmeans_tc_refine_kernel(TcRefineParams p)
     auto fetch = [&](unsigned ee, uint64_t& v, uint64_t& c, float (&xv)[FPL]) {
         v = p.qrow[ee];
         c = p.qcand[ee];
+        // the row from the queue, or (queues without rows) gathered from X
+        const float* src = p.qx ? p.qx + static_cast<int64_t>(ee) * D
+                                : (v == TC_QHOLE ? nullptr : p.x + static_cast<int64_t>(v & ((1ull << 48) - 1)) * D);
 #pragma unroll
         for (int u = 0; u < FPL; ++u) {
             const int f = lane + 32 * u;
-            xv[u] = f < D ? p.qx[static_cast<int64_t>(ee) * D + f] : 0.f;
+            xv[u] = (f < D && src) ? src[f] : 0.f;
         }
     };
     const unsigned stride = gridDim.x * WPB;
@@ -827,6 +853,13 @@ __global__ void __launch_bounds__(512) kmeans_tc_refine_kernel(TcRefineParams p)
         for (int u = 0; u < FPL; ++u)
             if (lane + 32 * u < D) row[lane + 32 * u] = xa[u];
         __syncwarp();
+        if (v == TC_QHOLE) {
+            v = vn;
+            cm = cn;
+#pragma unroll
+            for (int u = 0; u < FPL; ++u) xa[u] = xn[u];
+            continue;
+        }
         const int64_t r = static_cast<int64_t>(v & ((1ull << 48) - 1));
         const int old = static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(v >> 56)));
         const int dec = static_cast<int>((v >> 48) & 0xff) - 1;  // decided label (changed row) or -1
@@ -880,4 +913,388 @@ __global__ void __launch_bounds__(512) kmeans_tc_refine_kernel(TcRefineParams p)
         p.ctl[0] = 0;
         p.ctl[1] = 0;
     }
+}
+
+// ------------------------------------------------ TMEM-operand delta / predict kernel
+// kmeans_tcd_kernel: the same scores and decisions as kmeans_tc_kernel (P = 1),
+// for the launches that accumulate nothing per row -- delta iterations (the
+// changed rows go to the refine queue) and predict.  Laid out for the shared
+// memory port, which bounds the smem-operand kernel (per 128-row tile it moved
+// 240 KB through the 128 B/clk crossbar: the TMA write, the split's read and
+// lo write, and the MMAs' A and B reads):
+//   * the split writes BOTH halves of the row (raw = hi, the tensor core reads
+//     tf32; lo = x - trunc(x)) into tensor memory with tcgen05.st (256 B/clk),
+//     and the MMAs take A from TMEM: shared memory carries only the TMA tile,
+//     its one read by the split, and the centroid operand B (112 KB per tile);
+//   * the stage is released as soon as the split has read it;
+//   * four epilogue warpgroups (tile it: warpgroup it % 4) for latency hiding;
+//     TMEM: two A sets (hi | lo, tile it uses set it % 2, free again when the
+//     MMAs of tile it - 2 retired) and one score block per warpgroup
+//     (2 x 128 + 4 x 64 = 512 columns).
+#ifdef TCD_TRACE
+// diagnostics (-DTCD_TRACE builds only): %globaltimer marks of CTA 0's first 64
+// tiles: [0] MMAs issued, [2] A ready seen by the issuer, [4] A written,
+// [5] scores ready, [6] scores read, [7] tile done
+__device__ unsigned long long g_tcd_trace[64 * 8];
+__device__ __forceinline__ void tcd_mark(int64_t it, int k) {
+    if (blockIdx.x == 0 && it < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_tcd_trace[it * 8 + k] = t;
+    }
+}
+#define TCD_MARK(it, k) tcd_mark(it, k)
+#else
+#define TCD_MARK(it, k) ((void)0)
+#endif
+
+template <int D, int K>
+struct TcdCfg {
+    static constexpr int KC = ((D + 7) / 8) * 8;
+    static constexpr int NCH = KC / 4;
+    static constexpr int NKB = (KC + 31) / 32;
+    static constexpr int NS = K;
+    static constexpr int PR = 128;
+    static constexpr int WGS = 4;
+    static constexpr int ASETS = 2;
+    static constexpr int EPI = 128 * WGS;
+    static constexpr int THREADS = EPI + 32;
+    static constexpr int TILE_BYTES = NKB * PR * 128;
+    static constexpr int B_BYTES = NCH * NS * 16;
+    static constexpr int ROWB = (D * 4 + 15) / 16 * 16;
+    static constexpr int SCR_BYTES = (EPI / 32) * ROWB;  // per-warp row (queue-overflow fallback)
+    static constexpr int ACOLS = ((KC + 31) / 32) * 32;  // TMEM columns of one A half
+    static constexpr int DBASE = ASETS * 2 * ACOLS;      // score blocks after the A sets
+    static constexpr int TMEM_COLS = tc_pow2_cols(DBASE + WGS * NS);
+    static constexpr int FIXED = 2 * B_BYTES + ((K * 4 + 15) / 16) * 16 + SCR_BYTES + 64 * 8 + 16;
+    static constexpr int S = (232448 - FIXED) / TILE_BYTES > 6 ? 6 : (232448 - FIXED) / TILE_BYTES;
+    static constexpr int OFF_TILE = 0;
+    static constexpr int OFF_BHI = OFF_TILE + S * TILE_BYTES;
+    static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
+    static constexpr int OFF_CN = OFF_BLO + B_BYTES;
+    static constexpr int OFF_SCR = OFF_CN + ((K * 4 + 15) / 16) * 16;
+    static constexpr int OFF_BAR = OFF_SCR + SCR_BYTES;
+    static constexpr int NBARS = 2 * S + 2 * WGS;
+    static constexpr int OFF_TMEM = OFF_BAR + NBARS * 8;
+    static constexpr int SMEM = OFF_TMEM + 16;
+    static_assert(S >= 3, "kmeans_tcd: at least three TMA stages");
+    static_assert(NS % 16 == 0 && DBASE + WGS * NS <= 512, "MMA N / TMEM columns");
+    static_assert(D % 16 == 0 && D <= 64 && K <= 64, "kmeans_tcd shape (16-column TMEM stores)");
+    static_assert(SMEM <= 232448, "shared memory");
+    static_assert(TILE_BYTES % 1024 == 0, "SW128 tiles need 1024-byte alignment");
+};
+
+template <int D, int K>
+__global__ void __launch_bounds__(TcdCfg<D, K>::THREADS, 1)
+    kmeans_tcd_kernel(const __grid_constant__ CUtensorMap map, TcParams p) {
+    using C = TcdCfg<D, K>;
+    constexpr int NS = C::NS, PR = C::PR, S = C::S, KD = K * D, WGS = C::WGS;
+    if (p.done && *p.done) return;
+
+    extern __shared__ __align__(1024) unsigned char smem[];
+    if (tc::smem_u32(smem) & 1023u) __trap();
+    float* tiles = reinterpret_cast<float*>(smem + C::OFF_TILE);
+    float* bhi = reinterpret_cast<float*>(smem + C::OFF_BHI);
+    float* blo = reinterpret_cast<float*>(smem + C::OFF_BLO);
+    float* cn = reinterpret_cast<float*>(smem + C::OFF_CN);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+    uint64_t* full = bars;             // [S] TMA landed
+    uint64_t* empty = bars + S;        // [S] stage read by the split (4 warp arrivals)
+    uint64_t* aready = bars + 2 * S;   // [WGS] A hi/lo in TMEM (4 warp arrivals)
+    uint64_t* dfull = aready + WGS;    // [WGS] scores ready (MMAs retired: A free again)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool accumulate = p.partials != nullptr;
+    constexpr int CTRL = C::EPI / 32;
+
+    if (warp == CTRL) {
+        tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+        if (lane == 0) {
+            for (int s = 0; s < S; ++s) {
+                tc::mbar_init(&full[s], 1);
+                tc::mbar_init(&empty[s], 4);
+            }
+            for (int w = 0; w < WGS; ++w) {
+                tc::mbar_init(&aready[w], 4);
+                tc::mbar_init(&dfull[w], 1);
+            }
+            tc::mbar_fence_init();
+            tc::tma_prefetch_desc(&map);
+        }
+    } else {
+        for (int e = tid; e < NS * C::KC; e += C::EPI) {
+            const int j = e / C::KC, f = e % C::KC;
+            const float v = f < D ? p.ctab[j * D + f] : 0.f;
+            const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+            const int off = (f / 4) * (NS * 4) + j * 4 + (f % 4);
+            bhi[off] = hi;
+            blo[off] = v - hi;
+        }
+        for (int j = tid; j < K; j += C::EPI) cn[j] = p.ctab[KD + j];
+        tc::fence_async_smem();
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int64_t ntiles = ceil_div(p.n, static_cast<int64_t>(PR));
+    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    if (warp == CTRL) {
+        // ------------------------------------------------ TMA + MMA issuer
+        // the whole warp runs the loop (converged: the MMAs are issued by an
+        // elect.sync inside their asm, without a per-instruction divergence
+        // loop); lane 0 issues the TMA loads
+        constexpr uint32_t idesc = tc::idesc_tf32(128, NS, 0, 0);
+        const uint64_t bh0 = tc::smem_desc(tc::smem_u32(bhi), NS * 16, 128);
+        const uint64_t bl0 = tc::smem_desc(tc::smem_u32(blo), NS * 16, 128);
+        int64_t issued = 0;
+        auto refill = [&]() {
+            while (issued < my_tiles) {
+                const int st = static_cast<int>(issued % S);
+                bool free = issued < S || tc::mbar_test(&empty[st], static_cast<uint32_t>((issued / S - 1) & 1));
+                free = __shfl_sync(FULL, free, 0);
+                if (!free) break;
+                if (lane == 0) {
+                    const int prow = static_cast<int>((blockIdx.x + issued * gridDim.x) * PR);
+                    float* dst = tiles + st * (C::TILE_BYTES / 4);
+                    tc::mbar_expect_tx(&full[st], C::TILE_BYTES);
+#pragma unroll
+                    for (int kb = 0; kb < C::NKB; ++kb) tc::tma_load_2d(dst + kb * PR * 32, &map, &full[st], kb * 32, prow);
+                }
+                __syncwarp();
+                ++issued;
+            }
+        };
+        for (int64_t it = 0; it < my_tiles; ++it) {
+            const int w = static_cast<int>(it % WGS);
+            refill();
+            if (lane == 0) TCD_MARK(it, 1);
+            for (;;) {
+                bool ok = tc::mbar_test(&aready[w], static_cast<uint32_t>((it / WGS) & 1));
+                ok = __shfl_sync(FULL, ok, 0);
+                if (ok) break;
+                refill();
+            }
+            if (lane == 0) TCD_MARK(it, 2);
+            tc::tc_fence_after();
+            const uint32_t ahi = tmem + static_cast<uint32_t>(it % C::ASETS) * 2 * C::ACOLS, alo = ahi + C::ACOLS;
+            const uint32_t dt = tmem + C::DBASE + w * NS;
+#pragma unroll
+            for (int ks = 0; ks < C::KC / 8; ++ks)  // descriptor start address field: 16-byte units
+                tc::mma3_tf32_ta_elect(dt, ahi + ks * 8, alo + ks * 8, bh0 + static_cast<uint64_t>(ks * 2 * NS),
+                                       bl0 + static_cast<uint64_t>(ks * 2 * NS), idesc, ks > 0);
+            tc::mma_commit_elect(&dfull[w]);
+            if (lane == 0) TCD_MARK(it, 0);
+        }
+    } else {
+        // ------------------------------------------------ epilogue warpgroups
+        const int wg = warp / 4, wq = warp % 4, t = tid % 128;
+        const float cmax = p.bounds[0], cnmax = p.bounds[1];
+        constexpr float ERR = 4.f * (static_cast<float>(3 * C::KC) * 0x1.0p-24f + 3.f * 0x1.0p-20f);
+        float* wscr = reinterpret_cast<float*>(smem + C::OFF_SCR + warp * C::ROWB);
+        unsigned long long refined = 0;
+        constexpr unsigned QCHUNK = 64;
+        unsigned qbase = 0, qleft = 0;
+        auto qholes = [&]() {
+            for (unsigned i = lane; i < qleft; i += 32)
+                if (qbase + i < p.rq_cap) p.rq_row[qbase + i] = TC_QHOLE;
+        };
+        // queue-overflow fallback only: +x / -x of changed rows as int64 REDs
+        // into the CTA's partial row (zero otherwise; converted at the end)
+        long long* acc = accumulate ? reinterpret_cast<long long*>(p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K))
+                                    : nullptr;
+        if (accumulate)
+            for (int e = tid; e < KD + K; e += C::EPI) acc[e] = 0ll;
+        __threadfence();
+        int e2 = 0;
+        frexp(static_cast<double>(p.n) * (p.xabs ? *p.xabs : 1.0) + 1.0, &e2);
+        const int shift = 61 - e2;
+        const float qscale = ldexpf(1.f, shift);
+        tc::named_sync(15, C::EPI);
+
+        const uint32_t lanes = static_cast<uint32_t>(wq * 32) << 16;
+        const uint32_t trow = tmem + lanes + C::DBASE + wg * NS;
+        auto park = [&](int64_t row) {
+            for (int f = lane; f < D; f += 32) wscr[f] = __ldg(p.x + row * D + f);
+            __syncwarp();
+        };
+        for (int64_t it = wg; it < my_tiles; it += WGS) {
+            const int st = static_cast<int>(it % S);
+            const int64_t use = it / WGS;
+            const int64_t row = (blockIdx.x + it * gridDim.x) * PR + t;
+            const bool live = row < p.n;
+            const int oldl = (p.prev && live) ? static_cast<int>(p.prev[row]) : -1;
+            const float* xt = tiles + st * (C::TILE_BYTES / 4);
+            // A set it % 2 is free once the MMAs of tile it - 2 (another
+            // warpgroup's) retired
+            const uint32_t ahi = tmem + lanes + static_cast<uint32_t>(it % C::ASETS) * 2 * C::ACOLS, alo = ahi + C::ACOLS;
+            if (it >= C::ASETS)
+                tc::mbar_wait(&dfull[(it - C::ASETS) % WGS], static_cast<uint32_t>(((it - C::ASETS) / WGS) & 1));
+            tc::mbar_wait(&full[st], static_cast<uint32_t>((it / S) & 1));
+            tc::tc_fence_after();
+            // split: 16 features at a time from the swizzled tile into TMEM,
+            // raw (= hi: the tensor core reads tf32) and lo = x - trunc(x);
+            // |x|^2 for the error bound on the way
+            float4 xq = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int g = 0; g < C::KC / 16; ++g) {
+                float hv[16], lv[16];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = g * 4 + u;
+                    const int off = (c / 8) * PR * 32 + t * 32 + (((c % 8) ^ (t & 7)) * 4);
+                    const float4 v = *reinterpret_cast<const float4*>(xt + off);
+                    hv[4 * u] = v.x;
+                    hv[4 * u + 1] = v.y;
+                    hv[4 * u + 2] = v.z;
+                    hv[4 * u + 3] = v.w;
+                    xq.x = fmaf(v.x, v.x, xq.x);
+                    xq.y = fmaf(v.y, v.y, xq.y);
+                    xq.z = fmaf(v.z, v.z, xq.z);
+                    xq.w = fmaf(v.w, v.w, xq.w);
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) lv[i] = hv[i] - __uint_as_float(__float_as_uint(hv[i]) & 0xFFFFE000u);
+                tc::tmem_st16(ahi + g * 16, hv);
+                tc::tmem_st16(alo + g * 16, lv);
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&empty[st]);  // the stage is read: TMA may refill it
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&aready[wg]);
+            if (t == 0) TCD_MARK(it, 4);
+            const float xx = (xq.x + xq.y) + (xq.z + xq.w);
+
+            tc::mbar_wait(&dfull[wg], static_cast<uint32_t>(use & 1));
+            if (t == 0) TCD_MARK(it, 5);
+            tc::tc_fence_after();
+            float b1x[2] = {FLT_MAX, FLT_MAX}, b2x[2] = {FLT_MAX, FLT_MAX};
+            int i1x[2] = {0, 0};
+            constexpr int QC = NS % 32 == 0 ? 32 : 16;
+#pragma unroll
+            for (int q16 = 0; q16 < NS / QC; ++q16) {
+                float v[QC];
+                if constexpr (QC == 32) tc::tmem_ld32(trow + q16 * QC, v);
+                else tc::tmem_ld16(trow + q16 * QC, v);
+#pragma unroll
+                for (int i = 0; i < QC; ++i) {
+                    const int j = q16 * QC + i;
+                    const float s = cn[j] + v[i];
+                    float& c1 = b1x[i & 1];
+                    const bool lt = s < c1;
+                    b2x[i & 1] = fminf(b2x[i & 1], fmaxf(c1, s));
+                    c1 = fminf(c1, s);
+                    i1x[i & 1] = lt ? j : i1x[i & 1];
+                }
+            }
+            const float b1 = fminf(b1x[0], b1x[1]);
+            const float b2 = fminf(fmaxf(b1x[0], b1x[1]), fminf(b2x[0], b2x[1]));
+            int label = live ? (b1x[1] < b1x[0] ? i1x[1] : i1x[0]) : K;
+            const float tau = ERR * (cnmax + 2.f * sqrtf(xx) * cmax);
+            const bool flag = live && K > 1 && !(b2 - b1 > tau);
+            uint64_t cand = 0;
+            const bool wflag = __any_sync(FULL, flag);
+            if (wflag) {
+#pragma unroll
+                for (int q16 = 0; q16 < NS / QC; ++q16) {
+                    float v[QC];
+                    if constexpr (QC == 32) tc::tmem_ld32(trow + q16 * QC, v);
+                    else tc::tmem_ld16(trow + q16 * QC, v);
+#pragma unroll
+                    for (int i = 0; i < QC; ++i) {
+                        const int j = q16 * QC + i;
+                        if (cn[j] + v[i] <= b1 + tau) cand |= 1ull << j;
+                    }
+                }
+            }
+            tc::tc_fence_before();
+            if (t == 0) TCD_MARK(it, 6);
+
+            auto enqueue = [&](bool want, uint64_t cm, int newl) -> bool {
+                const unsigned fm = __ballot_sync(FULL, want);
+                if (!p.rq_ctl || !fm) return false;
+                const unsigned cnt = static_cast<unsigned>(__popc(fm));
+                if (cnt > qleft) {
+                    qholes();
+                    unsigned base = 0;
+                    if (lane == 0) base = atomicAdd(p.rq_ctl, QCHUNK);
+                    qbase = __shfl_sync(FULL, base, 0);
+                    qleft = QCHUNK;
+                }
+                const unsigned pos = qbase + static_cast<unsigned>(__popc(fm & ((1u << lane) - 1u)));
+                qbase += cnt;
+                qleft -= cnt;
+                if (!want || pos >= p.rq_cap) return false;
+                p.rq_row[pos] = static_cast<uint64_t>(row) | (static_cast<uint64_t>(static_cast<uint8_t>(oldl)) << 56) |
+                                (static_cast<uint64_t>(static_cast<uint8_t>(newl + 1)) << 48);
+                p.rq_cand[pos] = cm;
+                return true;
+            };
+            if (wflag) {
+                if (enqueue(flag, cand, -1)) label = tc_deferred<K>();
+                // queue overflow: the exact decision here, one row at a time
+                unsigned fm = __ballot_sync(FULL, flag && label != tc_deferred<K>());
+                while (fm) {
+                    const int src = __ffs(fm) - 1;
+                    fm &= fm - 1;
+                    park(__shfl_sync(FULL, row, src));
+                    const int best = tc_refine_warp<D, K>(wscr, __shfl_sync(FULL, cand, src), p.c64, p.cn64, cnmax,
+                                                          cmax, nullptr);
+                    __syncwarp();
+                    if (lane == src) {
+                        label = best;
+                        ++refined;
+                    }
+                }
+            }
+            if (live && label < K) {
+                if (p.labels) p.labels[row] = label;
+                if (p.lab8) p.lab8[row] = static_cast<int8_t>(label);
+            }
+            if (accumulate && p.prev) {
+                // changed rows: +x into the new cluster, -x out of the old one,
+                // by the refine kernel (queue overflow: REDs here)
+                bool ch = label < K && label != oldl;
+                if (enqueue(ch, 0ull, label)) ch = false;
+                unsigned fm = __ballot_sync(FULL, ch);
+                while (fm) {
+                    const int src = __ffs(fm) - 1;
+                    fm &= fm - 1;
+                    park(__shfl_sync(FULL, row, src));
+                    const int jn = __shfl_sync(FULL, label, src), jo = __shfl_sync(FULL, oldl, src);
+                    for (int f = lane; f < D; f += 32) {
+                        const long long qv = __float2ll_rn(wscr[f] * qscale);
+                        atomicAdd(reinterpret_cast<unsigned long long*>(acc + jn * D + f), static_cast<unsigned long long>(qv));
+                        if (jo >= 0)
+                            atomicAdd(reinterpret_cast<unsigned long long*>(acc + jo * D + f), static_cast<unsigned long long>(-qv));
+                    }
+                    if (lane == 0) {
+                        atomicAdd(reinterpret_cast<unsigned long long*>(acc + KD + jn), 1ull);
+                        if (jo >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(acc + KD + jo), ~0ull);
+                    }
+                    __syncwarp();
+                }
+            }
+            if (t == 0) TCD_MARK(it, 7);
+        }
+        if (refined) atomicAdd(p.refined, refined);
+        qholes();
+        if (accumulate) {
+            __threadfence();
+            tc::named_sync(15, C::EPI);
+            double* out = p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K);
+            for (int e = tid; e < KD + K; e += C::EPI) {
+                const long long v = __ldcg(acc + e);
+                out[e] = e < KD ? ldexp(static_cast<double>(v), -shift) : static_cast<double>(v);
+            }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == CTRL) tc::tmem_dealloc(tmem, C::TMEM_COLS);
 }

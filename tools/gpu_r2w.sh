@@ -1,6 +1,7 @@
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-timeout 600 python tools/cdist_ab.py variants/STG.so > gpurun_out/r2w_cdist_ab.log 2>&1
-DNDC_LIB_PATH=variants/STG.so timeout 600 python -m pytest tests/test_gpu_pairwise.py -m gpu -q -x > gpurun_out/r2w_stg_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r2w_stg_tests.log
-DNDC_TC_WGS=3 timeout 300 python tools/time_cfg3.py > gpurun_out/r2w_cfg3_wg3.log 2>&1
-DNDC_TC_WGS=3 timeout 600 python -m pytest tests/test_gpu_configs.py -k "cfg3" -m gpu -q -s > gpurun_out/r2w_tests_wg3.log 2>&1; echo "rc=$?" >> gpurun_out/r2w_tests_wg3.log
+timeout 600 python -m pytest tests/test_gpu_tc.py tests/test_gpu_cluster.py -m gpu -x -q > gpurun_out/r2w_tests.log 2>&1; echo rc=$? >> gpurun_out/r2w_tests.log
+timeout 300 python tools/time_cfg3.py > gpurun_out/r2w_cfg3.log 2>&1
+DNDC_TC_QUEUE=0 timeout 300 python tools/time_cfg3.py >> gpurun_out/r2w_cfg3.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_configs.py -k "cfg3" -m gpu -x -q -s >> gpurun_out/r2w_tests.log 2>&1; echo rc=$? >> gpurun_out/r2w_tests.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv --log-file gpurun_out/r2w_cfg3_launches.csv python tools/prof_cfg3.py > gpurun_out/r2w_ncu1.log 2>&1
