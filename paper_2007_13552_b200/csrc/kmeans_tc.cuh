@@ -930,7 +930,16 @@ __global__ void __launch_bounds__(512) kmeans_tc_refine_kernel(TcRefineParams p)
 //   * four epilogue warpgroups (tile it: warpgroup it % 4) for latency hiding;
 //     TMEM: two A sets (hi | lo, tile it uses set it % 2, free again when the
 //     MMAs of tile it - 2 retired) and one score block per warpgroup
-//     (2 x 128 + 4 x 64 = 512 columns).
+//     (2 x 128 + 4 x 64 = 512 columns).  (Starting the score block at |c|^2
+//     with tcgen05.st instead of one add per score measured slower.)
+// kmeans_tcd_kernel's queue-overflow fallback, out of line (keeps the
+// f64 decision's registers out of the kernel's main loop)
+template <int D, int K>
+__device__ __noinline__ int tcd_refine_row(const float* row, uint64_t cm, const double* __restrict__ c64,
+                                           const double* __restrict__ cn64, float cnmax, float cmax) {
+    return tc_refine_warp<D, K>(row, cm, c64, cn64, cnmax, cmax, nullptr);
+}
+
 #ifdef TCD_TRACE
 // diagnostics (-DTCD_TRACE builds only): %globaltimer marks of CTA 0's first 64
 // tiles: [0] MMAs issued, [2] A ready seen by the issuer, [4] A written,
@@ -958,7 +967,7 @@ struct TcdCfg {
     static constexpr int WGS = 4;
     static constexpr int ASETS = 2;
     static constexpr int EPI = 128 * WGS;
-    static constexpr int THREADS = EPI + 32;
+    static constexpr int THREADS = EPI + 64;  // + the MMA warp + the TMA warp
     static constexpr int TILE_BYTES = NKB * PR * 128;
     static constexpr int B_BYTES = NCH * NS * 16;
     static constexpr int ROWB = (D * 4 + 15) / 16 * 16;
@@ -1022,7 +1031,7 @@ __global__ void __launch_bounds__(TcdCfg<D, K>::THREADS, 1)
             tc::mbar_fence_init();
             tc::tma_prefetch_desc(&map);
         }
-    } else {
+    } else if (warp < CTRL) {
         for (int e = tid; e < NS * C::KC; e += C::EPI) {
             const int j = e / C::KC, f = e % C::KC;
             const float v = f < D ? p.ctab[j * D + f] : 0.f;
@@ -1043,41 +1052,18 @@ __global__ void __launch_bounds__(TcdCfg<D, K>::THREADS, 1)
     const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     if (warp == CTRL) {
-        // ------------------------------------------------ TMA + MMA issuer
+        // ------------------------------------------------ MMA issuer
         // the whole warp runs the loop (converged: the MMAs are issued by an
-        // elect.sync inside their asm, without a per-instruction divergence
-        // loop); lane 0 issues the TMA loads
+        // elect.sync inside their asm, without a per-instruction divergence loop)
         constexpr uint32_t idesc = tc::idesc_tf32(128, NS, 0, 0);
         const uint64_t bh0 = tc::smem_desc(tc::smem_u32(bhi), NS * 16, 128);
         const uint64_t bl0 = tc::smem_desc(tc::smem_u32(blo), NS * 16, 128);
-        int64_t issued = 0;
-        auto refill = [&]() {
-            while (issued < my_tiles) {
-                const int st = static_cast<int>(issued % S);
-                bool free = issued < S || tc::mbar_test(&empty[st], static_cast<uint32_t>((issued / S - 1) & 1));
-                free = __shfl_sync(FULL, free, 0);
-                if (!free) break;
-                if (lane == 0) {
-                    const int prow = static_cast<int>((blockIdx.x + issued * gridDim.x) * PR);
-                    float* dst = tiles + st * (C::TILE_BYTES / 4);
-                    tc::mbar_expect_tx(&full[st], C::TILE_BYTES);
-#pragma unroll
-                    for (int kb = 0; kb < C::NKB; ++kb) tc::tma_load_2d(dst + kb * PR * 32, &map, &full[st], kb * 32, prow);
-                }
-                __syncwarp();
-                ++issued;
-            }
-        };
+#pragma unroll 1
         for (int64_t it = 0; it < my_tiles; ++it) {
             const int w = static_cast<int>(it % WGS);
-            refill();
             if (lane == 0) TCD_MARK(it, 1);
-            for (;;) {
-                bool ok = tc::mbar_test(&aready[w], static_cast<uint32_t>((it / WGS) & 1));
-                ok = __shfl_sync(FULL, ok, 0);
-                if (ok) break;
-                refill();
-            }
+            tc::mbar_wait(&aready[w], static_cast<uint32_t>((it / WGS) & 1));
+            __syncwarp();
             if (lane == 0) TCD_MARK(it, 2);
             tc::tc_fence_after();
             const uint32_t ahi = tmem + static_cast<uint32_t>(it % C::ASETS) * 2 * C::ACOLS, alo = ahi + C::ACOLS;
@@ -1088,6 +1074,19 @@ __global__ void __launch_bounds__(TcdCfg<D, K>::THREADS, 1)
                                        bl0 + static_cast<uint64_t>(ks * 2 * NS), idesc, ks > 0);
             tc::mma_commit_elect(&dfull[w]);
             if (lane == 0) TCD_MARK(it, 0);
+        }
+    } else if (warp == CTRL + 1) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            for (int64_t it = 0; it < my_tiles; ++it) {
+                const int st = static_cast<int>(it % S);
+                if (it >= S) tc::mbar_wait(&empty[st], static_cast<uint32_t>((it / S - 1) & 1));
+                const int prow = static_cast<int>((blockIdx.x + it * gridDim.x) * PR);
+                float* dst = tiles + st * (C::TILE_BYTES / 4);
+                tc::mbar_expect_tx(&full[st], C::TILE_BYTES);
+#pragma unroll
+                for (int kb = 0; kb < C::NKB; ++kb) tc::tma_load_2d(dst + kb * PR * 32, &map, &full[st], kb * 32, prow);
+            }
         }
     } else {
         // ------------------------------------------------ epilogue warpgroups
@@ -1139,14 +1138,18 @@ __global__ void __launch_bounds__(TcdCfg<D, K>::THREADS, 1)
             // raw (= hi: the tensor core reads tf32) and lo = x - trunc(x);
             // |x|^2 for the error bound on the way
             float4 xq = make_float4(0.f, 0.f, 0.f, 0.f);
+            // the row's swizzle phase through an opaque shuffle: otherwise the
+            // compiler hoists all 16 chunk offsets out of the tile loop and
+            // spills them (the kernel runs at 128 registers)
+            const int t7 = __shfl_sync(FULL, t & 7, lane);
+            const float* xrow = xt + t * 32;
 #pragma unroll
             for (int g = 0; g < C::KC / 16; ++g) {
                 float hv[16], lv[16];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int c = g * 4 + u;
-                    const int off = (c / 8) * PR * 32 + t * 32 + (((c % 8) ^ (t & 7)) * 4);
-                    const float4 v = *reinterpret_cast<const float4*>(xt + off);
+                    const float4 v = *reinterpret_cast<const float4*>(xrow + (c / 8) * PR * 32 + (((c % 8) ^ t7) * 4));
                     hv[4 * u] = v.x;
                     hv[4 * u + 1] = v.y;
                     hv[4 * u + 2] = v.z;
@@ -1243,8 +1246,7 @@ __global__ void __launch_bounds__(TcdCfg<D, K>::THREADS, 1)
                     const int src = __ffs(fm) - 1;
                     fm &= fm - 1;
                     park(__shfl_sync(FULL, row, src));
-                    const int best = tc_refine_warp<D, K>(wscr, __shfl_sync(FULL, cand, src), p.c64, p.cn64, cnmax,
-                                                          cmax, nullptr);
+                    const int best = tcd_refine_row<D, K>(wscr, __shfl_sync(FULL, cand, src), p.c64, p.cn64, cnmax, cmax);
                     __syncwarp();
                     if (lane == src) {
                         label = best;
