@@ -1674,6 +1674,8 @@ struct Assigner {
     void (*tfn)(CUtensorMap, TcParams) = nullptr;
     void (*rfn)(TcRefineParams) = nullptr;  // near-tie refine after each tc launch
     void (*dtfn)(CUtensorMap, TcParams) = nullptr;  // four-warpgroup kernel: delta iterations and predict
+    void (*afn)(TcAccumParams) = nullptr;  // full iterations with it: the sums from the final labels
+    size_t asmem = 0;
     size_t dtsmem = 0;
     int dtthreads = 0;
     unsigned* rq_ctl = nullptr;
@@ -1683,6 +1685,7 @@ struct Assigner {
     long long* racc = nullptr;
     unsigned rq_cap = 0;
     int rgrid = 0, rthreads = 0;
+    size_t rsmem = 0;
     CUtensorMap tmap{};
     size_t tsmem = 0;
     int tthreads = 0;
@@ -1724,10 +1727,18 @@ struct Assigner {
             // launches that accumulate no row themselves (delta, predict) take the
             // four-warpgroup kernel; full accumulation needs the sort of the old one
             const bool four = dtfn && (tp.prev != nullptr || !accumulate);
-            if (four)
+            // full iterations with the labels buffer: labels by the TMEM kernel,
+            // then the sums of every row by kmeans_tc_accum_kernel
+            const bool split_full = dtfn && afn && accumulate && tp.prev == nullptr && tp.lab8 != nullptr;
+            if (split_full) {
+                TcParams lp = tp;
+                lp.partials = nullptr;
+                dtfn<<<sgrid, dtthreads, dtsmem, st>>>(tmap, lp);
+            } else if (four) {
                 dtfn<<<sgrid, dtthreads, dtsmem, st>>>(tmap, tp);
-            else
+            } else {
                 tfn<<<sgrid, tthreads, tsmem, st>>>(tmap, tp);
+            }
             TcRefineParams rp{};
             rp.n = n;
             rp.c64 = b.c64;
@@ -1737,17 +1748,28 @@ struct Assigner {
             rp.ctl = rq_ctl;
             rp.qrow = rq_row;
             rp.qcand = rq_cand;
-            rp.qx = four ? nullptr : rq_x;  // the four-warpgroup kernel queues no rows: read X
+            rp.qx = (four || split_full) ? nullptr : rq_x;  // the TMEM kernel queues no rows: read X
             rp.x = reinterpret_cast<const float*>(x);
             rp.cap = rq_cap;
             rp.labels = labels;
             rp.lab8 = tp.lab8;
             rp.racc = racc;
-            rp.partial = accumulate ? b.partials + static_cast<int64_t>(sgrid) * (static_cast<int64_t>(k) * d + k)
-                                    : nullptr;
+            rp.partial = accumulate && !split_full
+                             ? b.partials + static_cast<int64_t>(sgrid) * (static_cast<int64_t>(k) * d + k)
+                             : nullptr;
             rp.refined = b.refined;
             rp.done = tp.done;
-            rfn<<<rgrid, rthreads, 0, st>>>(rp);
+            rfn<<<rgrid, rthreads, rsmem, st>>>(rp);
+            if (split_full) {
+                TcAccumParams ap{};
+                ap.x = reinterpret_cast<const float*>(x);
+                ap.n = n;
+                ap.lab8 = tp.lab8;
+                ap.xabs = b.sx2 + 3;
+                ap.partials = b.partials;
+                ap.done = tp.done;
+                afn<<<sgrid, 512, asmem, st>>>(ap);
+            }
         } else if (small) {
             DNDC_CUDA(cudaMemcpyToSymbolAsync(c_km_table, b.ctab, sizeof(float) * (k * d + k),
                                               sizeof(float) * KS_TABLE * slot, cudaMemcpyDeviceToDevice, st));
@@ -1806,11 +1828,19 @@ static void pick_tc(Assigner<float>& A) {
     if (std::getenv("DNDC_TC_NO_DELTA")) A.tc_delta = false;
     A.rfn = kmeans_tc_refine_kernel<D, K>;
     A.rthreads = tc_refine_threads<D, K>();
+    A.rsmem = TcRefineSmem<D, K>::BYTES;
+    DNDC_CUDA(cudaFuncSetAttribute(A.rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(A.rsmem)));
     if constexpr (P == 1 && D % 4 == 0) {
         if (!std::getenv("DNDC_TC_NO_FOUR") && A.tc_delta) {
             A.dtfn = kmeans_tcd_kernel<D, K>;
             A.dtsmem = TcdCfg<D, K>::SMEM;
             A.dtthreads = TcdCfg<D, K>::THREADS;
+            if (!std::getenv("DNDC_TC_OLD_FULL")) {
+                A.afn = kmeans_tc_accum_kernel<D, K>;
+                A.asmem = TcAccumCfg<D, K>::SMEM;
+                DNDC_CUDA(cudaFuncSetAttribute(A.afn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(A.asmem)));
+            }
         }
     }
 }
@@ -1865,7 +1895,7 @@ static Assigner<T> plan(dndc_ctx* ctx, int k, int d, int64_t n, const T* x) {
             DNDC_CUDA(cudaMemsetAsync(A.rq_ctl, 0, sizeof(unsigned) * 4, ctx->stream));
             DNDC_CUDA(cudaMemsetAsync(A.racc, 0, sizeof(long long) * (k * d + k), ctx->stream));
             int rper_sm = 1;
-            DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper_sm, A.rfn, A.rthreads, 0));
+            DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper_sm, A.rfn, A.rthreads, A.rsmem));
             A.rgrid = ctx->num_sms * std::max(rper_sm, 1);
             return A;
         }
@@ -2122,7 +2152,8 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     // small kernel: every iteration records int8 labels; the first ones
     // accumulate full sums, later ones only the rows whose label changed
     const bool use_delta = A.small || (A.tc && A.tc_delta);
-    int8_t* lab8 = use_delta ? static_cast<int8_t*>(ctx->slot("km_lab8", std::max<int64_t>(n_local, 1))) : nullptr;
+    // (+64: kmeans_tc_accum_kernel bulk-copies labels in 16-byte multiples)
+    int8_t* lab8 = use_delta ? static_cast<int8_t*>(ctx->slot("km_lab8", std::max<int64_t>(n_local, 1) + 64)) : nullptr;
     if (!ctx->km) ctx->km = new KMeansState();
     KMeansState* km = ctx->km;
     if (km->timing && km->ev.size() < 2 * static_cast<size_t>(max_iter)) {
@@ -2203,6 +2234,9 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
         if (F < max_iter) launch(PP.delta, F, max_iter, words + 40, words + 73);
         if (km->timing) DNDC_CUDA(cudaEventRecordWithFlags(km->ev[1], st, cudaEventRecordExternal));
     };
+    // tc full iterations with the labels buffer launch one kernel more (the sums pass)
+    const unsigned long long split_full_iters =
+        (A.tc && A.afn && lab8) ? static_cast<unsigned long long>(std::min(KS_FULL_ITERS, max_iter)) : 0ull;
     auto record = [&](cudaStream_t st) {
         if (persist) {
             record_persist(st);
@@ -2245,7 +2279,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     if (ctx->group) {
         // ranks sharing GPUs: the stats exchange is host-staged, not capturable
         record(s);  // (allgather_f64 counts itself here)
-        ctx->launches += 1 + ((A.small || A.tc) ? 4ull : 3ull) * max_iter;
+        ctx->launches += 1 + ((A.small || A.tc) ? 4ull : 3ull) * max_iter + split_full_iters;
     }
     cudaStream_t gs = ctx->own_stream;
     char keybuf[256];
@@ -2290,7 +2324,8 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     DNDC_CUDA(cudaStreamWaitEvent(s, ctx->ev_b, 0));
     // reset + per iteration: assign (fused) | [tile reset,] assign, reduce, update
     // (persistent: reset + the one cooperative launch)
-    ctx->launches += persist ? (max_iter > persist_full_iters() ? 3ull : 2ull) : 1 + (fuse ? 1ull : (A.small || A.tc) ? 4ull : 3ull) * max_iter;
+    ctx->launches += persist ? (max_iter > persist_full_iters() ? 3ull : 2ull)
+                             : 1 + (fuse ? 1ull : (A.small || A.tc) ? 4ull : 3ull) * max_iter + split_full_iters;
     if (ctx->world > 1) ctx->counters.allgathers += max_iter;
     }
     ctx->last_kernel = persist ? (max_iter > persist_full_iters() ? PP.delta.name : PP.full.name) : "";

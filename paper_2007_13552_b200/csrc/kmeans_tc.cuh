@@ -804,18 +804,57 @@ struct TcRefineParams {
 template <int D, int K>
 __host__ __device__ constexpr int tc_refine_threads() { return 512; }
 
-// rows are accumulated in a per-CTA shared int64 copy first (global atomics
-// on the K*D sums from every warp contended at L2: 200 us per launch at cfg3),
-// then the CTA adds its nonzero entries to racc once
+// shared memory of kmeans_tc_refine_kernel (dynamic): transposed f64
+// centroids, |c|^2, the int64 sums, and one queue chunk's bookkeeping
+template <int D, int K>
+struct TcRefineSmem {
+    static constexpr int CH = 1024, NW = tc_refine_threads<D, K>() / 32;
+    static constexpr int OFF_CT = 0;                                  // double [D][K]
+    static constexpr int OFF_CN = OFF_CT + D * K * 8;                 // double [K]
+    static constexpr int OFF_ACC = OFF_CN + K * 8;                    // long long [K*D + K]
+    static constexpr int OFF_QV = OFF_ACC + (K * D + K) * 8;          // uint64 [CH]
+    static constexpr int OFF_LST = OFF_QV + CH * 8;                   // u16 [2 CH]
+    static constexpr int OFF_UND = OFF_LST + 2 * CH * 2;              // u16 [CH]
+    static constexpr int OFF_CNT = OFF_UND + CH * 2;                  // int [2K] counts, [2K+1] starts, [2K] cursors, [1] nund
+    static constexpr int OFF_NLAB = OFF_CNT + (6 * K + 2) * 4;        // int8 [CH]
+    static constexpr int OFF_ROWS = (OFF_NLAB + CH + 15) / 16 * 16;   // float [NW][D]
+    static constexpr int BYTES = OFF_ROWS + NW * D * 4;
+};
+
+// The queue is taken in chunks of CH entries per CTA.  In a chunk:
+// (1) the near-tie rows are decided one LANE per row (the row in registers, f64
+//     distances to its candidate clusters from a transposed shared copy of the
+//     centroids); only rows the f64 filter cannot separate go to the
+//     warp-cooperative reference-order decision (tc_refine_warp);
+// (2) the rows whose label changed are bucketed by cluster (+x under the new
+//     label, -x under the old one), a counting sort in shared memory;
+// (3) the bucketed list is split evenly over the warps; each sums its range
+//     in registers, eight rows in flight, and adds a run to the shared int64
+//     sums only where its cluster changes (no atomic per row).
+// Rows come from the queue (qx) or are read from X.  At the end the CTA adds
+// its sums to racc; the last CTA converts racc into the partial row and
+// resets the queue.
 template <int D, int K>
 __global__ void __launch_bounds__(512) kmeans_tc_refine_kernel(TcRefineParams p) {
-    constexpr int KD = K * D, WPB = tc_refine_threads<D, K>() / 32;
-    __shared__ float rows[WPB][D];
-    __shared__ long long sacc[KD + K];
+    using L = TcRefineSmem<D, K>;
+    constexpr int KD = K * D, NT = tc_refine_threads<D, K>(), NW = L::NW, CH = L::CH;
+    constexpr int FPL = (D + 31) / 32;
+    static_assert(K <= 127 && D % 2 == 0, "int8 labels, float2 rows");
+    extern __shared__ __align__(16) unsigned char rsm[];
+    double* cT = reinterpret_cast<double*>(rsm + L::OFF_CT);
+    double* cnS = reinterpret_cast<double*>(rsm + L::OFF_CN);
+    long long* sacc = reinterpret_cast<long long*>(rsm + L::OFF_ACC);
+    uint64_t* qv = reinterpret_cast<uint64_t*>(rsm + L::OFF_QV);
+    unsigned short* lst = reinterpret_cast<unsigned short*>(rsm + L::OFF_LST);
+    unsigned short* und = reinterpret_cast<unsigned short*>(rsm + L::OFF_UND);
+    int* cnt = reinterpret_cast<int*>(rsm + L::OFF_CNT);
+    int* start = cnt + 2 * K;
+    int* cur = start + 2 * K + 1;
+    int* nund = cur + 2 * K;
+    signed char* nlab = reinterpret_cast<signed char*>(rsm + L::OFF_NLAB);
+    float* rows = reinterpret_cast<float*>(rsm + L::OFF_ROWS);
     __shared__ bool last;
-    for (int e = threadIdx.x; e < KD + K; e += blockDim.x) sacc[e] = 0ll;
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool skip = p.done && *p.done;
     const unsigned count = skip ? 0u : min(p.ctl[0], p.cap);
     int e2 = 0;
@@ -823,93 +862,242 @@ __global__ void __launch_bounds__(512) kmeans_tc_refine_kernel(TcRefineParams p)
     const int shift = 61 - e2;
     const float qscale = ldexpf(1.f, shift);
     const float cmax = p.bounds[0], cnmax = p.bounds[1];
-    float* row = rows[warp];
-    constexpr int FPL = (D + 31) / 32;
-    // the next entry is loaded while this one is decided (the queue is
-    // contiguous and L2-resident: it was written by the tc kernel just before)
-    auto fetch = [&](unsigned ee, uint64_t& v, uint64_t& c, float (&xv)[FPL]) {
-        v = p.qrow[ee];
-        c = p.qcand[ee];
-        // the row from the queue, or (queues without rows) gathered from X
-        const float* src = p.qx ? p.qx + static_cast<int64_t>(ee) * D
-                                : (v == TC_QHOLE ? nullptr : p.x + static_cast<int64_t>(v & ((1ull << 48) - 1)) * D);
-#pragma unroll
-        for (int u = 0; u < FPL; ++u) {
-            const int f = lane + 32 * u;
-            xv[u] = (f < D && src) ? src[f] : 0.f;
-        }
+    constexpr uint64_t RMASK = (1ull << 48) - 1;
+    auto src_of = [&](unsigned e, uint64_t v) -> const float* {
+        return p.qx ? p.qx + static_cast<int64_t>(e) * D : p.x + static_cast<int64_t>(v & RMASK) * D;
     };
-    const unsigned stride = gridDim.x * WPB;
-    unsigned e = blockIdx.x * WPB + warp;
-    uint64_t v = 0, cm = 0;
-    unsigned nref = 0;  // entries decided here (the rest only accumulate)
-    float xa[FPL];
-    if (e < count) fetch(e, v, cm, xa);
-    for (; e < count; e += stride) {
-        uint64_t vn = 0, cn = 0;
-        float xn[FPL];
-        if (e + stride < count) fetch(e + stride, vn, cn, xn);
-#pragma unroll
-        for (int u = 0; u < FPL; ++u)
-            if (lane + 32 * u < D) row[lane + 32 * u] = xa[u];
-        __syncwarp();
-        if (v == TC_QHOLE) {
-            v = vn;
-            cm = cn;
-#pragma unroll
-            for (int u = 0; u < FPL; ++u) xa[u] = xn[u];
-            continue;
+    const unsigned nchunks = (count + CH - 1) / CH;
+    if (blockIdx.x < nchunks) {
+        for (int e = tid; e < KD; e += NT) cT[(e % D) * K + e / D] = p.c64[e];
+        for (int j = tid; j < K; j += NT) cnS[j] = p.cn64[j];
+        for (int e = tid; e < KD + K; e += NT) sacc[e] = 0;
+    }
+    unsigned nref = 0;
+    for (unsigned c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const unsigned e0 = c * CH;
+        const int ne = static_cast<int>(min(static_cast<unsigned>(CH), count - e0));
+        for (int i = tid; i < 2 * K; i += NT) cnt[i] = 0;
+        if (tid == 0) *nund = 0;
+        __syncthreads();
+        for (int i = tid; i < ne; i += NT) {
+            const uint64_t v = p.qrow[e0 + i];
+            qv[i] = v;
+            int dec = -2;
+            if (v != TC_QHOLE) {
+                dec = static_cast<int>((v >> 48) & 0xff) - 1;
+                if (dec < 0) und[atomicAdd(nund, 1)] = static_cast<unsigned short>(i);
+            }
+            nlab[i] = static_cast<signed char>(dec);
         }
-        const int64_t r = static_cast<int64_t>(v & ((1ull << 48) - 1));
-        const int old = static_cast<int>(static_cast<int8_t>(static_cast<uint8_t>(v >> 56)));
-        const int dec = static_cast<int>((v >> 48) & 0xff) - 1;  // decided label (changed row) or -1
-        int best = dec;
-        if (dec < 0) {
-            best = tc_refine_warp<D, K>(row, cm, p.c64, p.cn64, cnmax, cmax, nullptr);
-            ++nref;
-            if (lane == 0) {
+        __syncthreads();
+        // (1) near-ties, lane per row
+        const int nu = *nund;
+        for (int base = warp * 32; base < nu; base += NW * 32) {
+            const int k = base + lane;
+            const bool active = k < nu;
+            const int i = active ? und[k] : 0;
+            const uint64_t v = qv[i];
+            const uint64_t cm = active ? p.qcand[e0 + i] : 0ull;
+            float xr[D];
+            {
+                const float* src = active ? src_of(e0 + i, v) : nullptr;
+                if constexpr (D % 4 == 0) {
+#pragma unroll
+                    for (int q = 0; q < D / 4; ++q) {
+                        const float4 t = active ? reinterpret_cast<const float4*>(src)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        xr[4 * q] = t.x;
+                        xr[4 * q + 1] = t.y;
+                        xr[4 * q + 2] = t.z;
+                        xr[4 * q + 3] = t.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < D / 2; ++q) {
+                        const float2 t = active ? reinterpret_cast<const float2*>(src)[q] : make_float2(0.f, 0.f);
+                        xr[2 * q] = t.x;
+                        xr[2 * q + 1] = t.y;
+                    }
+                }
+            }
+            double xn = 0.0;
+#pragma unroll
+            for (int f = 0; f < D; ++f) xn = fma(static_cast<double>(xr[f]), static_cast<double>(xr[f]), xn);
+            double d1 = DBL_MAX, d2 = DBL_MAX;
+            int best = K;
+            for (uint64_t rest = cm; rest;) {
+                int js[4];
+                double g[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    js[q] = rest ? __ffsll(static_cast<long long>(rest)) - 1 : -1;
+                    rest &= rest - 1;
+                    g[q] = 0.0;
+                }
+                const int j0 = js[0] < 0 ? 0 : js[0], j1 = js[1] < 0 ? 0 : js[1];
+                const int j2 = js[2] < 0 ? 0 : js[2], j3 = js[3] < 0 ? 0 : js[3];
+#pragma unroll
+                for (int f = 0; f < D; ++f) {
+                    const double xf = static_cast<double>(xr[f]);
+                    const double* col = cT + f * K;
+                    g[0] = fma(xf, col[j0], g[0]);
+                    g[1] = fma(xf, col[j1], g[1]);
+                    g[2] = fma(xf, col[j2], g[2]);
+                    g[3] = fma(xf, col[j3], g[3]);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (js[q] < 0) continue;
+                    const double dq = xn + cnS[js[q]] - 2.0 * g[q];
+                    if (dq < d1) {
+                        d2 = d1;
+                        d1 = dq;
+                        best = js[q];
+                    } else if (dq < d2) {
+                        d2 = dq;
+                    }
+                }
+            }
+            const double margin =
+                0x1.0p-40 * (xn + static_cast<double>(cnmax) + 2.0 * sqrt(xn) * static_cast<double>(cmax));
+            const bool decided = active && d1 > margin && d2 - d1 > margin;
+            // not separable by the filter: the reference's operation order, one
+            // row at a time, warp-cooperative
+            unsigned fm = __ballot_sync(FULL, active && !decided);
+            while (fm) {
+                const int src = __ffs(fm) - 1;
+                fm &= fm - 1;
+                float* rw = rows + warp * D;
+                if (lane == src) {
+#pragma unroll
+                    for (int f = 0; f < D; ++f) rw[f] = xr[f];
+                }
+                __syncwarp();
+                const int b = tc_refine_warp<D, K>(rw, __shfl_sync(FULL, cm, src), p.c64, p.cn64, cnmax, cmax, nullptr);
+                __syncwarp();
+                if (lane == src) best = b;
+            }
+            if (active) {
+                nlab[i] = static_cast<signed char>(best);
+                ++nref;
+                const int64_t r = static_cast<int64_t>(v & RMASK);
                 if (p.labels) p.labels[r] = best;
                 if (p.lab8) p.lab8[r] = static_cast<int8_t>(best);
             }
         }
-        __syncwarp();
-        if (p.partial && best != old) {
-            for (int f = lane; f < D; f += 32) {
-                const long long qv = __float2ll_rn(row[f] * qscale);
-                atomicAdd(reinterpret_cast<unsigned long long*>(sacc + best * D + f), static_cast<unsigned long long>(qv));
-                if (old >= 0)
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sacc + old * D + f), static_cast<unsigned long long>(-qv));
+        __syncthreads();
+        if (p.partial) {
+            // (2) buckets: + new label, - last label (rows whose label changed)
+            for (int i = tid; i < ne; i += NT) {
+                const int nl = nlab[i], old = static_cast<int8_t>(static_cast<uint8_t>(qv[i] >> 56));
+                if (nl >= 0 && nl != old) {
+                    atomicAdd(&cnt[nl], 1);
+                    if (old >= 0) atomicAdd(&cnt[K + old], 1);
+                }
             }
-            if (lane == 0) {
-                atomicAdd(reinterpret_cast<unsigned long long*>(sacc + KD + best), 1ull);
-                if (old >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(sacc + KD + old), ~0ull);
+            __syncthreads();
+            if (warp == 0) {
+                int carry = 0;
+                for (int b = 0; b < 2 * K; b += 32) {
+                    const int v = b + lane < 2 * K ? cnt[b + lane] : 0;
+                    int incl = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int t = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= o) incl += t;
+                    }
+                    if (b + lane < 2 * K) {
+                        start[b + lane] = carry + incl - v;
+                        cur[b + lane] = carry + incl - v;
+                    }
+                    carry += __shfl_sync(FULL, incl, 31);
+                }
+                if (lane == 0) start[2 * K] = carry;
+            }
+            __syncthreads();
+            for (int i = tid; i < ne; i += NT) {
+                const int nl = nlab[i], old = static_cast<int8_t>(static_cast<uint8_t>(qv[i] >> 56));
+                if (nl >= 0 && nl != old) {
+                    lst[atomicAdd(&cur[nl], 1)] = static_cast<unsigned short>(i);
+                    if (old >= 0) lst[atomicAdd(&cur[K + old], 1)] = static_cast<unsigned short>(i);
+                }
+            }
+            __syncthreads();
+            // (3) an even share of the bucketed list per warp, runs summed in registers
+            const int total = start[2 * K];
+            const int lo = static_cast<int>(static_cast<int64_t>(total) * warp / NW);
+            const int hi = static_cast<int>(static_cast<int64_t>(total) * (warp + 1) / NW);
+            if (lo < hi) {
+                int bk = 0;
+                while (start[bk + 1] <= lo) ++bk;
+                int bend = start[bk + 1], runs = 0;
+                long long acc[FPL];
+#pragma unroll
+                for (int f = 0; f < FPL; ++f) acc[f] = 0;
+                auto flush = [&]() {
+                    const int j = bk < K ? bk : bk - K;
+                    const bool neg = bk >= K;
+#pragma unroll
+                    for (int f = 0; f < FPL; ++f) {
+                        const int ff = lane + 32 * f;
+                        if (ff < D && acc[f])
+                            atomicAdd(reinterpret_cast<unsigned long long*>(sacc + j * D + ff),
+                                      static_cast<unsigned long long>(neg ? -acc[f] : acc[f]));
+                        acc[f] = 0;
+                    }
+                    if (lane == 0 && runs)
+                        atomicAdd(reinterpret_cast<unsigned long long*>(sacc + KD + j),
+                                  static_cast<unsigned long long>(neg ? -static_cast<long long>(runs) : runs));
+                    runs = 0;
+                };
+                for (int b = lo; b < hi; b += 8) {
+                    float xv[8][FPL];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int idx = b + q < hi ? lst[b + q] : -1;
+                        const float* src = idx >= 0 ? src_of(e0 + idx, qv[idx]) : nullptr;
+#pragma unroll
+                        for (int f = 0; f < FPL; ++f) {
+                            const int ff = lane + 32 * f;
+                            xv[q][f] = (src && ff < D) ? src[ff] : 0.f;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (b + q >= hi) break;
+                        while (b + q >= bend) {
+                            flush();
+                            ++bk;
+                            bend = start[bk + 1];
+                        }
+#pragma unroll
+                        for (int f = 0; f < FPL; ++f) acc[f] += __float2ll_rn(xv[q][f] * qscale);
+                        ++runs;
+                    }
+                }
+                flush();
             }
         }
-        __syncwarp();
-        v = vn;
-        cm = cn;
-#pragma unroll
-        for (int u = 0; u < FPL; ++u) xa[u] = xn[u];
+        __syncthreads();
     }
+    nref = __reduce_add_sync(FULL, nref);  // lane per row: every lane counted its own
     if (lane == 0 && nref) atomicAdd(p.refined, static_cast<unsigned long long>(nref));
-    __syncthreads();
-    if (p.partial && blockIdx.x * WPB < count) {
-        for (int e = threadIdx.x; e < KD + K; e += blockDim.x)
+    if (p.partial && blockIdx.x < nchunks) {
+        for (int e = tid; e < KD + K; e += NT)
             if (sacc[e]) atomicAdd(reinterpret_cast<unsigned long long*>(p.racc + e), static_cast<unsigned long long>(sacc[e]));
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         __threadfence();
         last = atomicAdd(p.ctl + 1, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
-    for (int e = threadIdx.x; e < KD + K; e += blockDim.x) {
+    for (int e = tid; e < KD + K; e += blockDim.x) {
         const long long v = static_cast<long long>(atomicExch(reinterpret_cast<unsigned long long*>(p.racc + e), 0ull));
         if (p.partial) p.partial[e] = e < KD ? ldexp(static_cast<double>(v), -shift) : static_cast<double>(v);
     }
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         p.ctl[0] = 0;
         p.ctl[1] = 0;
     }
@@ -1299,4 +1487,185 @@ __global__ void __launch_bounds__(TcdCfg<D, K>::THREADS, 1)
     tc::tc_fence_before();
     __syncthreads();
     if (warp == CTRL) tc::tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ------------------------------------------------ full-iteration accumulation
+// kmeans_tc_accum_kernel: the per-cluster sums of EVERY row from the final
+// labels (lab8), for the full iterations of the tc path: kmeans_tcd_kernel
+// (labels only) + the refine kernel (near-ties) decide, then this kernel
+// streams X once more.  Chunks of ROWS rows arrive by 1-D bulk copy into a
+// two-stage ring; each chunk is counting-sorted by label in shared memory and
+// the sorted list is split evenly over the warps, which sum their runs in
+// registers (lanes over the features) and add a run to the CTA's int64 sums
+// only where the label changes.  The CTA's sums become its partial row (f64,
+// exact conversion of the integer, summed over CTAs in CTA order as before);
+// CTA 0 also clears the refine kernel's row.  Deterministic: static chunk
+// assignment, integer sums.
+struct TcAccumParams {
+    const float* x;
+    int64_t n;
+    const int8_t* lab8;
+    const double* xabs;
+    double* partials;   // rows [0, gridDim.x) + the zeroed row gridDim.x
+    const int* done;
+};
+
+template <int D, int K>
+struct TcAccumCfg {
+    static constexpr int ROWS = 256, S = 3, THREADS = 512, NW = THREADS / 32;
+    static constexpr int OFF_X = 0;                                   // float [S][ROWS][D]
+    static constexpr int OFF_ACC = OFF_X + S * ROWS * D * 4;          // long long [K*D + K]
+    static constexpr int OFF_LST = OFF_ACC + (K * D + K) * 8;         // u16 [ROWS]
+    static constexpr int OFF_LAB = OFF_LST + ROWS * 2;                // int8 [S][ROWS] (bulk-copied with the rows)
+    static constexpr int OFF_CNT = (OFF_LAB + S * ROWS + 15) / 16 * 16;  // int [K] counts, [K+1] starts, [K] cursors
+    static constexpr int OFF_BAR = (OFF_CNT + (3 * K + 1) * 4 + 15) / 16 * 16;
+    static constexpr int SMEM = OFF_BAR + S * 8;
+    static_assert(SMEM <= 232448, "shared memory");
+};
+
+template <int D, int K>
+__global__ void __launch_bounds__(512, 1) kmeans_tc_accum_kernel(TcAccumParams p) {
+    using C = TcAccumCfg<D, K>;
+    constexpr int KD = K * D, ROWS = C::ROWS, S = C::S, NT = C::THREADS, NW = C::NW;
+    constexpr int FPL = (D + 31) / 32;
+    if (p.done && *p.done) return;
+    extern __shared__ __align__(16) unsigned char asmem[];
+    float* xs = reinterpret_cast<float*>(asmem + C::OFF_X);
+    long long* sacc = reinterpret_cast<long long*>(asmem + C::OFF_ACC);
+    unsigned short* lst = reinterpret_cast<unsigned short*>(asmem + C::OFF_LST);
+    signed char* lab = reinterpret_cast<signed char*>(asmem + C::OFF_LAB);
+    int* cnt = reinterpret_cast<int*>(asmem + C::OFF_CNT);
+    int* start = cnt + K;
+    int* cur = start + K + 1;
+    uint64_t* full = reinterpret_cast<uint64_t*>(asmem + C::OFF_BAR);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int e2 = 0;
+    frexp(static_cast<double>(p.n) * (p.xabs ? *p.xabs : 1.0) + 1.0, &e2);
+    const int shift = 61 - e2;
+    const float qscale = ldexpf(1.f, shift);
+    const int64_t nchunks = (p.n + ROWS - 1) / ROWS;
+    const int64_t my = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    for (int e = tid; e < KD + K; e += NT) sacc[e] = 0;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) tc::mbar_init(&full[s], 1);
+        tc::mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t k) {  // chunk k of this CTA into stage k % S
+        const int64_t r0 = (blockIdx.x + k * gridDim.x) * ROWS;
+        const int64_t nr = min(static_cast<int64_t>(ROWS), p.n - r0);
+        const uint32_t bytes = static_cast<uint32_t>(nr * D * 4);
+        const uint32_t lbytes = static_cast<uint32_t>((nr + 15) / 16 * 16);  // labels: 16-byte multiple (r0 % 16 == 0)
+        const int st = static_cast<int>(k % S);
+        tc::mbar_expect_tx(&full[st], bytes + lbytes);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                tc::smem_u32(xs + st * ROWS * D)),
+            "l"(p.x + r0 * D), "r"(bytes), "r"(tc::smem_u32(&full[st]))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                tc::smem_u32(lab + st * ROWS)),
+            "l"(p.lab8 + r0), "r"(lbytes), "r"(tc::smem_u32(&full[st]))
+            : "memory");
+    };
+    if (tid == 0)
+        for (int64_t k = 0; k < min(my, static_cast<int64_t>(S)); ++k) issue(k);
+    for (int64_t k = 0; k < my; ++k) {
+        const int st = static_cast<int>(k % S);
+        const int64_t r0 = (blockIdx.x + k * gridDim.x) * ROWS;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(ROWS), p.n - r0));
+        for (int i = tid; i < K; i += NT) cnt[i] = 0;
+        const signed char* lb = lab + st * ROWS;
+        tc::mbar_wait(&full[st], static_cast<uint32_t>((k / S) & 1));
+        __syncthreads();
+        for (int i = tid; i < nr; i += NT) {
+            const int l = lb[i];
+            if (l >= 0 && l < K) atomicAdd(&cnt[l], 1);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int carry = 0;
+            for (int b = 0; b < K; b += 32) {
+                const int v = b + lane < K ? cnt[b + lane] : 0;
+                int incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                if (b + lane < K) {
+                    start[b + lane] = carry + incl - v;
+                    cur[b + lane] = carry + incl - v;
+                }
+                carry += __shfl_sync(FULL, incl, 31);
+            }
+            if (lane == 0) start[K] = carry;
+        }
+        __syncthreads();
+        for (int i = tid; i < nr; i += NT) {
+            const int l = lb[i];
+            if (l >= 0 && l < K) lst[atomicAdd(&cur[l], 1)] = static_cast<unsigned short>(i);
+        }
+        __syncthreads();
+        const float* xc = xs + st * ROWS * D;
+        const int total = start[K];
+        const int lo = total * warp / NW, hi = total * (warp + 1) / NW;
+        if (lo < hi) {
+            int bk = 0;
+            while (start[bk + 1] <= lo) ++bk;
+            int bend = start[bk + 1], runs = 0;
+            long long acc[FPL];
+#pragma unroll
+            for (int f = 0; f < FPL; ++f) acc[f] = 0;
+            auto flush = [&]() {
+#pragma unroll
+                for (int f = 0; f < FPL; ++f) {
+                    const int ff = lane + 32 * f;
+                    if (ff < D && acc[f])
+                        atomicAdd(reinterpret_cast<unsigned long long*>(sacc + bk * D + ff),
+                                  static_cast<unsigned long long>(acc[f]));
+                    acc[f] = 0;
+                }
+                if (lane == 0 && runs)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(sacc + KD + bk), static_cast<unsigned long long>(runs));
+                runs = 0;
+            };
+            for (int b = lo; b < hi; b += 8) {
+                float xv[8][FPL];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int idx = b + q < hi ? lst[b + q] : 0;
+#pragma unroll
+                    for (int f = 0; f < FPL; ++f) {
+                        const int ff = lane + 32 * f;
+                        xv[q][f] = ff < D ? xc[idx * D + ff] : 0.f;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (b + q >= hi) break;
+                    while (b + q >= bend) {
+                        flush();
+                        ++bk;
+                        bend = start[bk + 1];
+                    }
+#pragma unroll
+                    for (int f = 0; f < FPL; ++f) acc[f] += __float2ll_rn(xv[q][f] * qscale);
+                    ++runs;
+                }
+            }
+            flush();
+        }
+        __syncthreads();  // the stage is read: refill it
+        if (tid == 0 && k + S < my) issue(k + S);
+    }
+    __syncthreads();
+    double* out = p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K);
+    for (int e = tid; e < KD + K; e += NT)
+        out[e] = e < KD ? ldexp(static_cast<double>(sacc[e]), -shift) : static_cast<double>(sacc[e]);
+    if (blockIdx.x == 0) {
+        double* zr = p.partials + static_cast<int64_t>(gridDim.x) * (KD + K);
+        for (int e = tid; e < KD + K; e += NT) zr[e] = 0.0;
+    }
 }
