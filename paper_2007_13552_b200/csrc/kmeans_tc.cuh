@@ -1493,12 +1493,12 @@ __global__ void __launch_bounds__(TcdCfg<D, K>::THREADS, 1)
 // kmeans_tc_accum_kernel: the per-cluster sums of EVERY row from the final
 // labels (lab8), for the full iterations of the tc path: kmeans_tcd_kernel
 // (labels only) + the refine kernel (near-ties) decide, then this kernel
-// streams X once more.  Chunks of ROWS rows arrive by 1-D bulk copy into a
-// two-stage ring; each chunk is counting-sorted by label in shared memory and
-// the sorted list is split evenly over the warps, which sum their runs in
-// registers (lanes over the features) and add a run to the CTA's int64 sums
-// only where the label changes.  The CTA's sums become its partial row (f64,
-// exact conversion of the integer, summed over CTAs in CTA order as before);
+// streams X once more.  Chunks of ROWS rows and their labels arrive by 1-D
+// bulk copy into a three-stage ring; each chunk is counting-sorted by label in
+// shared memory and warp w sums the rows of its clusters (w, w + 16, ...) from
+// shared memory into int64 registers kept across all chunks (lanes over the
+// features; no atomics).  The sums become the CTA's partial row (f64 of the
+// exact integers, summed over CTAs in CTA order as before);
 // CTA 0 also clears the refine kernel's row.  Deterministic: static chunk
 // assignment, integer sums.
 struct TcAccumParams {
@@ -1512,10 +1512,9 @@ struct TcAccumParams {
 
 template <int D, int K>
 struct TcAccumCfg {
-    static constexpr int ROWS = 256, S = 3, THREADS = 512, NW = THREADS / 32;
+    static constexpr int ROWS = 256, S = 3, THREADS = 512, NW = THREADS / 32;  // 3 x 64 KB stages
     static constexpr int OFF_X = 0;                                   // float [S][ROWS][D]
-    static constexpr int OFF_ACC = OFF_X + S * ROWS * D * 4;          // long long [K*D + K]
-    static constexpr int OFF_LST = OFF_ACC + (K * D + K) * 8;         // u16 [ROWS]
+    static constexpr int OFF_LST = OFF_X + S * ROWS * D * 4;          // u16 [ROWS]
     static constexpr int OFF_LAB = OFF_LST + ROWS * 2;                // int8 [S][ROWS] (bulk-copied with the rows)
     static constexpr int OFF_CNT = (OFF_LAB + S * ROWS + 15) / 16 * 16;  // int [K] counts, [K+1] starts, [K] cursors
     static constexpr int OFF_BAR = (OFF_CNT + (3 * K + 1) * 4 + 15) / 16 * 16;
@@ -1531,7 +1530,6 @@ __global__ void __launch_bounds__(512, 1) kmeans_tc_accum_kernel(TcAccumParams p
     if (p.done && *p.done) return;
     extern __shared__ __align__(16) unsigned char asmem[];
     float* xs = reinterpret_cast<float*>(asmem + C::OFF_X);
-    long long* sacc = reinterpret_cast<long long*>(asmem + C::OFF_ACC);
     unsigned short* lst = reinterpret_cast<unsigned short*>(asmem + C::OFF_LST);
     signed char* lab = reinterpret_cast<signed char*>(asmem + C::OFF_LAB);
     int* cnt = reinterpret_cast<int*>(asmem + C::OFF_CNT);
@@ -1545,7 +1543,14 @@ __global__ void __launch_bounds__(512, 1) kmeans_tc_accum_kernel(TcAccumParams p
     const float qscale = ldexpf(1.f, shift);
     const int64_t nchunks = (p.n + ROWS - 1) / ROWS;
     const int64_t my = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    for (int e = tid; e < KD + K; e += NT) sacc[e] = 0;
+    constexpr int CPW = (K + NW - 1) / NW;  // clusters per warp
+    long long acc[CPW][FPL], accn[CPW];
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+        accn[u] = 0;
+#pragma unroll
+        for (int f = 0; f < FPL; ++f) acc[u][f] = 0;
+    }
     if (tid == 0) {
         for (int s = 0; s < S; ++s) tc::mbar_init(&full[s], 1);
         tc::mbar_fence_init();
@@ -1609,61 +1614,47 @@ __global__ void __launch_bounds__(512, 1) kmeans_tc_accum_kernel(TcAccumParams p
         }
         __syncthreads();
         const float* xc = xs + st * ROWS * D;
-        const int total = start[K];
-        const int lo = total * warp / NW, hi = total * (warp + 1) / NW;
-        if (lo < hi) {
-            int bk = 0;
-            while (start[bk + 1] <= lo) ++bk;
-            int bend = start[bk + 1], runs = 0;
-            long long acc[FPL];
+        // warp w owns clusters w, w + NW, ...: their sorted rows from shared
+        // memory into int64 registers kept across chunks (no atomics)
 #pragma unroll
-            for (int f = 0; f < FPL; ++f) acc[f] = 0;
-            auto flush = [&]() {
-#pragma unroll
-                for (int f = 0; f < FPL; ++f) {
-                    const int ff = lane + 32 * f;
-                    if (ff < D && acc[f])
-                        atomicAdd(reinterpret_cast<unsigned long long*>(sacc + bk * D + ff),
-                                  static_cast<unsigned long long>(acc[f]));
-                    acc[f] = 0;
-                }
-                if (lane == 0 && runs)
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sacc + KD + bk), static_cast<unsigned long long>(runs));
-                runs = 0;
-            };
-            for (int b = lo; b < hi; b += 8) {
+        for (int u = 0; u < CPW; ++u) {
+            const int j = warp + NW * u;
+            if (j >= K) continue;
+            const int b0 = start[j], b1 = start[j + 1];
+            for (int b = b0; b < b1; b += 8) {
                 float xv[8][FPL];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const int idx = b + q < hi ? lst[b + q] : 0;
+                    const int idx = b + q < b1 ? lst[b + q] : 0;
 #pragma unroll
                     for (int f = 0; f < FPL; ++f) {
                         const int ff = lane + 32 * f;
-                        xv[q][f] = ff < D ? xc[idx * D + ff] : 0.f;
+                        xv[q][f] = (ff < D && b + q < b1) ? xc[idx * D + ff] : 0.f;
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    if (b + q >= hi) break;
-                    while (b + q >= bend) {
-                        flush();
-                        ++bk;
-                        bend = start[bk + 1];
-                    }
+                for (int q = 0; q < 8; ++q)
 #pragma unroll
-                    for (int f = 0; f < FPL; ++f) acc[f] += __float2ll_rn(xv[q][f] * qscale);
-                    ++runs;
-                }
+                    for (int f = 0; f < FPL; ++f) acc[u][f] += __float2ll_rn(xv[q][f] * qscale);
             }
-            flush();
+            accn[u] += b1 - b0;
         }
         __syncthreads();  // the stage is read: refill it
         if (tid == 0 && k + S < my) issue(k + S);
     }
-    __syncthreads();
+    // each warp's clusters -> the CTA's partial row (f64 of the exact int64)
     double* out = p.partials + static_cast<int64_t>(blockIdx.x) * (KD + K);
-    for (int e = tid; e < KD + K; e += NT)
-        out[e] = e < KD ? ldexp(static_cast<double>(sacc[e]), -shift) : static_cast<double>(sacc[e]);
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+        const int j = warp + NW * u;
+        if (j >= K) continue;
+#pragma unroll
+        for (int f = 0; f < FPL; ++f) {
+            const int ff = lane + 32 * f;
+            if (ff < D) out[j * D + ff] = ldexp(static_cast<double>(acc[u][f]), -shift);
+        }
+        if (lane == 0) out[KD + j] = static_cast<double>(accn[u]);
+    }
     if (blockIdx.x == 0) {
         double* zr = p.partials + static_cast<int64_t>(gridDim.x) * (KD + K);
         for (int e = tid; e < KD + K; e += NT) zr[e] = 0.0;
