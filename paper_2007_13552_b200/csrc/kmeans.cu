@@ -1299,18 +1299,37 @@ __device__ void update_body(const UpdArgs& a, double* upd, double* sh) {
     const int S = k * d + k, KD = k * d;
     const bool staged = KD <= UPD_MAX_KD;
     if (staged) {
-        // allreduce(plus_vec) from the zero identity in rank order (cluster.cpp:123)
-        for (int e = threadIdx.x; e < S; e += blockDim.x) {
-            double v = 0.0;
-            for (int r = 0; r < world; ++r) v += gathered[static_cast<int64_t>(r) * a.gstride + e];
-            // delta iterations (small kernel): the stats are changes since the
-            // last iteration, added to the running per-cluster sums and counts
-            if (running) {
-                if (accum) v += a.rd_running[e];
-                running[e] = v;
+        // allreduce(plus_vec) from the zero identity in rank order (cluster.cpp:123).
+        // Eight elements per thread per pass, all loads before any store
+        // (running may alias rd_running: one at a time, every load waited
+        // behind the previous store -- 16 serial L2 round trips per thread)
+        constexpr int UB = 8;
+        for (int e0 = threadIdx.x; e0 < S; e0 += UB * blockDim.x) {
+            double gv[UB], rv[UB], cv[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int e = e0 + u * blockDim.x;
+                gv[u] = rv[u] = cv[u] = 0.0;
+                if (e < S) {
+                    for (int r = 0; r < world; ++r) gv[u] += gathered[static_cast<int64_t>(r) * a.gstride + e];
+                    if (running && accum) rv[u] = a.rd_running[e];
+                    if (e < KD) cv[u] = a.rd_c64[e];
+                }
             }
-            upd[e < KD ? e : KD + e] = v;
-            if (e < KD) upd[KD + e] = a.rd_c64[e];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int e = e0 + u * blockDim.x;
+                if (e >= S) break;
+                double v = gv[u];
+                // delta iterations: the stats are changes since the last
+                // iteration, added to the running per-cluster sums and counts
+                if (running) {
+                    if (accum) v += rv[u];
+                    running[e] = v;
+                }
+                upd[e < KD ? e : KD + e] = v;
+                if (e < KD) upd[KD + e] = cv[u];
+            }
         }
         __syncthreads();
         tail_mark(6);
