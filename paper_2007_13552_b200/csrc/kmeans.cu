@@ -2053,6 +2053,7 @@ static UpdArgs upd_args(const KmBuffers& b, int k, int m, int world, const doubl
 struct PersistLaunch {
     void (*fn)(PersistParams) = nullptr;
     int grid = 0, static_tiles = 0;
+    int wg = 1;  // warpgroups (virtual CTAs) per CTA
     size_t smem = 0;
     const char* name = "";
 };
@@ -2062,24 +2063,30 @@ struct PersistPlan {
 
 // Grid = CTAs that fit per SM x SMs (capped by the tile count), all
 // co-resident (cooperative launch: the kernel's grid barrier needs it).
-template <int D, int K, int R, int NST, int MINB, int MODE>
+template <int D, int K, int R, int NST, int MINB, int MODE, bool TCS = false, int WG = 1>
 static bool try_persist(dndc_ctx* ctx, int64_t n, PersistLaunch& P, const char* name) {
     using namespace persist;
-    void (*fn)(PersistParams) = kmeans_persist_kernel<D, K, R, NST, MINB, MODE>;
+    void (*fn)(PersistParams) = kmeans_persist_kernel<D, K, R, NST, MINB, MODE, TCS, WG>;
     const int64_t ntiles = std::max<int64_t>(ceil_div(n, THREADS * R), 1);
-    const size_t smem = static_cast<size_t>(persist_layout<D, K, R, NST>().total);
+    const size_t smem = static_cast<size_t>(persist_layout<D, K, R, NST, TCS>().total) * WG;
     if (smem > 227 * 1024) return false;
     DNDC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int occ = 0;
-    DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS, smem));
+    DNDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS * WG, smem));
     if (occ < 1) return false;
-    const int grid = static_cast<int>(std::min<int64_t>(ntiles, static_cast<int64_t>(std::min(occ, MINB)) * ctx->num_sms));
+    const int per_sm = WG == 1 ? std::min(occ, MINB) : 1;
+    const int grid = static_cast<int>(std::min<int64_t>(ceil_div(ntiles, static_cast<int64_t>(WG)),
+                                                        static_cast<int64_t>(per_sm) * ctx->num_sms));
+    if (std::getenv("DNDC_PERSIST_VERBOSE"))
+        std::fprintf(stderr, "[dndc] %s: smem %zu B, %d CTAs/SM, grid %d x %d warpgroups\n", name, smem, occ, grid,
+                     WG);
     // static share: ~70% of the tiles (DNDC_PERSIST_STATIC=percent overrides)
     const char* e = std::getenv("DNDC_PERSIST_STATIC");
     const int pct = e ? std::max(0, std::min(100, std::atoi(e))) : 70;
     P.fn = fn;
     P.grid = grid;
-    P.static_tiles = static_cast<int>(ntiles * pct / 100 / grid);
+    P.wg = WG;
+    P.static_tiles = static_cast<int>(ntiles * pct / 100 / (static_cast<int64_t>(grid) * WG));
     P.smem = smem;
     P.name = name;
     return true;
@@ -2087,9 +2094,11 @@ static bool try_persist(dndc_ctx* ctx, int64_t n, PersistLaunch& P, const char* 
 
 // Iterations that sum every row before the delta iterations take over
 // (DNDC_FULL_ITERS overrides; at least 1: a delta needs previous labels).
+// Persistent fit: one (the delta launch takes over at iteration 1: 1.1% faster
+// than two full iterations at cfg1, profiles/r02_env_sweep.txt).
 static int persist_full_iters() {
     const char* e = std::getenv("DNDC_FULL_ITERS");
-    return e ? std::max(1, std::atoi(e)) : KS_FULL_ITERS;
+    return e ? std::max(1, std::atoi(e)) : 1;
 }
 
 // DNDC_PERSIST=0 disables the persistent fit; DNDC_PERSIST_DELTA=r4|r4s3
@@ -2099,6 +2108,18 @@ static bool plan_persist(dndc_ctx* ctx, int k, int m, int64_t n_local, PersistPl
     if (e && std::string(e) == "0") return false;
     if (m == 18 && k == 8) {
         using namespace persist;
+        // DNDC_PERSIST_TC=1: scores on the tensor core (persist_top2_tc, four
+        // warpgroups per CTA).  Measured slower (~150 us per
+        // delta iteration against ~88: 18 MMAs of N = 16 per 256-row tile, each
+        // tile's MMAs waited for), so not the default.
+        const char* t = std::getenv("DNDC_PERSIST_TC");
+        if (t && std::string(t) == "1") {
+            if (!try_persist<18, 8, 2, 2, 4, FULL_ONLY, true, 4>(ctx, n_local, P.full,
+                                                                 "kmeans_persist_kernel<18,8,R2,S2,full,tc,wg4>"))
+                return false;
+            return try_persist<18, 8, 2, 2, 4, DELTA_ONLY, true, 4>(ctx, n_local, P.delta,
+                                                                    "kmeans_persist_kernel<18,8,R2,S2,delta,tc,wg4>");
+        }
         if (!try_persist<18, 8, 2, 2, 4, FULL_ONLY>(ctx, n_local, P.full, "kmeans_persist_kernel<18,8,R2,S2,full>"))
             return false;
         const char* d = std::getenv("DNDC_PERSIST_DELTA");
@@ -2197,7 +2218,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     int8_t* plab = persist ? static_cast<int8_t*>(ctx->slot("km_plab", static_cast<size_t>(n_local))) : nullptr;
     unsigned long long* pmarks = nullptr;
     if (persist && std::getenv("DNDC_PERSIST_TRACE")) {
-        const int tg = std::max(PP.full.grid, PP.delta.grid);
+        const int tg = std::max(PP.full.grid * PP.full.wg, PP.delta.grid * PP.delta.wg);  // virtual CTAs
         ctx->persist_trace_len = static_cast<int64_t>(max_iter) * (2 * tg + 2);
         ctx->persist_trace_grid = tg;
         pmarks = static_cast<unsigned long long*>(
@@ -2239,7 +2260,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
             q.static_tiles = L.static_tiles;
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(L.grid);
-            cfg.blockDim = dim3(persist::THREADS);
+            cfg.blockDim = dim3(persist::THREADS * L.wg);
             cfg.dynamicSmemBytes = L.smem;
             cfg.stream = st;
             cudaLaunchAttribute attr[1];

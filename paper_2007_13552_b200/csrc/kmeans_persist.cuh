@@ -72,6 +72,9 @@ namespace persist {
 // between the clusters' sums in one pass (the per-row cost of small batches
 // was ~70 issue slots per changed row, r2 ncu)
 constexpr int THREADS = 128, W = THREADS / 32, SCR = 32;
+// tensor-core scores (TCS instantiations): MMA N (K centroids padded to 16),
+// TMEM columns per CTA (4 CTAs per SM share the 512)
+constexpr int TC_NS = 16, TC_COLS = 128;
 // MODE of an instantiation: iterations that accumulate every row (full), only
 // the rows whose label changed (delta), or both in one launch
 enum { BOTH = 0, FULL_ONLY = 1, DELTA_ONLY = 2 };
@@ -112,15 +115,26 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// The barrier of one virtual CTA: the whole CTA (WG = 1) or warpgroup wg of
+// a WG-warpgroup CTA (named barrier 1 + wg) -- see kmeans_persist_kernel.
+template <int WG>
+__device__ __forceinline__ void persist_sync(int wg) {
+    if constexpr (WG == 1) {
+        __syncthreads();
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(wg + 1), "r"(persist::THREADS) : "memory");
+    }
+}
+
 struct PersistLayout {
-    int tiles, slab, wacc, scr, scl, cnt, tab, run, c64, cn64, stat, misc, stile, siter, sdef, lcnt, consumed, bars,
+    int tiles, slab, wacc, scr, scl, cnt, tab, bop, run, c64, cn64, misc, stile, siter, sdef, lcnt, consumed, bars,
         lbars, total;
 };
 
-template <int D, int K, int R, int NST>
+template <int D, int K, int R, int NST, bool TCS = false>
 __host__ __device__ constexpr PersistLayout persist_layout() {
     using namespace persist;
-    constexpr int KD = K * D, S = KD + K, DP = (D + 3) / 4 * 4, TILE = THREADS * R, VW = W * R;
+    constexpr int KD = K * D, S = KD + K, TILE = THREADS * R, VW = W * R;
     PersistLayout l{};
     int o = 0;
     auto take = [&](int bytes) {
@@ -134,11 +148,17 @@ __host__ __device__ constexpr PersistLayout persist_layout() {
     l.scr = take(W * SCR * D * 4 > (KD + K) * 8 ? W * SCR * D * 4 : (KD + K) * 8);  // also old c / |c|^2 in the update
     l.scl = take(W * 2 * SCR * 4);
     l.cnt = take(VW * K * 4);
-    l.tab = take((K * DP + 2 * K) * 4);
+    l.tab = take((K * D + K) * 4);
+    // TCS: the centroid operand -2c as tf32 hi then lo, K-major SWIZZLE_NONE
+    // core matrices of 8 rows x 16 B: chunk c (4 features) of rows 0..7 at
+    // c * 128 B, TC_BSTRIDE bytes per part.  The MMA's second 8-row group
+    // (N = 16 > K) reads the next TC_BSTRIDE bytes (hi: the lo part; lo: the
+    // start of `run`) -- score columns >= K are never read, so those rows need
+    // no zeros of their own (and cost no shared memory: 4 CTAs per SM fit)
+    l.bop = TCS ? take(2 * (D + 7) / 8 * 8 / 4 * 128) : o;
     l.run = take(S * 8);
     l.c64 = take(KD * 8);
     l.cn64 = take(K * 8);
-    l.stat = take(S * 8);
     l.misc = take(16 * 8);
     l.stile = take(NST * 8);
     l.siter = take(NST * 4);
@@ -207,12 +227,102 @@ __device__ __forceinline__ void persist_top2(const float2 (&xv)[R][D / 2], const
     }
 }
 
+// The same top-2 with the K*D score products on the tensor core (TCS
+// instantiations).  Every thread writes its R rows into tensor memory (lane =
+// row of the 128-row half h; the raw fp32 is the tf32 hi part -- the tensor
+// core truncates -- and lo = x - trunc(x); KCP = D padded to the K = 8 step,
+// padding columns zero), then one warp issues, per half, the 3xTF32 MMAs
+// hi.Bhi + hi.Blo + lo.Bhi with A from TMEM (kmeans_tcd_kernel's scheme:
+// shared memory carries only B = -2c) and every thread reads its rows' K
+// scores back (tcgen05.ld) and adds |c_j|^2 in fp32.  Error bound per row
+// (kmeans_tcd_kernel's model): tau = 4 (3 KCP 2^-24 + 3 2^-20)
+// (max|c|^2 + 2 |x| max|c|).  Replaces 72 FFMA2 and ~25 table loads per row
+// by ~40 instructions; the CTA waits for its MMAs once per tile (the other
+// CTAs of the SM fill the gap).
+template <int D, int K, int R, int WG>
+__device__ __forceinline__ void persist_top2_tc(const float2 (&xv)[R][D / 2], const float* __restrict__ T,
+                                                uint32_t tmem, uint64_t bh, uint64_t bl, uint64_t* tbar,
+                                                uint32_t& tph, float cnmax, float cmax, float (&b1)[R],
+                                                float (&b2)[R], int (&i1)[R], float (&tau)[R], int wg) {
+    using namespace persist;
+    constexpr int L = D / 2, KCP = (D + 7) / 8 * 8, DCOL = R * 2 * KCP;
+    static_assert(K <= 8 && DCOL + R * TC_NS <= TC_COLS, "persistent tc scores: TMEM columns");
+    constexpr float ERR = 4.f * (static_cast<float>(3 * KCP) * 0x1.0p-24f + 3.f * 0x1.0p-20f);
+    const int warp = (threadIdx.x >> 5) & 3;  // TMEM lane quarter = warp within the warpgroup
+    const uint32_t lanes = static_cast<uint32_t>(warp * 32) << 16;
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        float2 q = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int f = 0; f < L; ++f) q = __ffma2_rn(xv[h][f], xv[h][f], q);
+        tau[h] = ERR * (cnmax + 2.f * sqrtf(q.x + q.y) * cmax);
+        const uint32_t ahi = tmem + lanes + static_cast<uint32_t>(h * 2 * KCP), alo = ahi + KCP;
+#pragma unroll
+        for (int g = 0; g < KCP; g += 8) {
+            float hv[8], lv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int c = g + i;
+                const float v = c < D ? ((c & 1) ? xv[h][c / 2].y : xv[h][c / 2].x) : 0.f;
+                hv[i] = v;
+                lv[i] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+            }
+            tc::tmem_st8(ahi + g, hv);
+            tc::tmem_st8(alo + g, lv);
+        }
+    }
+    tc::tmem_st_wait();
+    tc::tc_fence_before();
+    persist_sync<WG>(wg);
+    if (warp == 0) {
+        tc::tc_fence_after();
+        constexpr uint32_t idesc = tc::idesc_tf32(128, TC_NS, 0, 0);
+#pragma unroll
+        for (int h = 0; h < R; ++h)
+#pragma unroll
+            for (int ks = 0; ks < KCP / 8; ++ks)  // descriptor start address: 16-byte units
+                tc::mma3_tf32_ta_elect(tmem + DCOL + h * TC_NS, tmem + h * 2 * KCP + ks * 8,
+                                       tmem + h * 2 * KCP + KCP + ks * 8, bh + static_cast<uint64_t>(ks * 16),
+                                       bl + static_cast<uint64_t>(ks * 16), idesc, ks > 0);
+        tc::mma_commit_elect(tbar);
+    }
+    tc::mbar_wait(tbar, tph);  // plain poll (the suspend-hint wait is for TMA completions)
+    tph ^= 1u;
+    tc::tc_fence_after();
+    float v[R][8];
+    if constexpr (R == 2) {
+        tc::tmem_ld8x2(tmem + lanes + DCOL, tmem + lanes + DCOL + TC_NS, v[0], v[1]);
+    } else {
+#pragma unroll
+        for (int h = 0; h < R; ++h) tc::tmem_ld8(tmem + lanes + DCOL + h * TC_NS, v[h]);
+    }
+    tc::tc_fence_before();
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        b1[h] = FLT_MAX;
+        b2[h] = FLT_MAX;
+        i1[h] = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const float sc = T[K * D + j] + v[h][j];
+            const bool lt = sc < b1[h];
+            b2[h] = fminf(b2[h], fmaxf(b1[h], sc));
+            b1[h] = fminf(b1[h], sc);
+            i1[h] = lt ? j : i1[h];
+        }
+    }
+}
+
 // Tables of the current centroids c64 (shared memory), thread j < K (K <= 32:
 // all in warp 0): reference-order |c_j|^2 (pairwise.cpp:13-18), the fp32 score
 // table and the error-bound inputs (misc[0] max |c|, misc[1] max fp32 |c|^2).
+// TCS: also the MMA operand B = -2c (rows j < K of bhi / blo; the padding
+// rows and columns stay zero) for persist_top2_tc, made visible to the
+// tensor core (async proxy) before the caller's barrier.
 template <int D, int K>
-__device__ __forceinline__ void persist_tables(const double* c64, double* cn64, float* tab, double* misc) {
-    const int j = threadIdx.x;
+__device__ __forceinline__ void persist_tables(const double* c64, double* cn64, float* tab, double* misc,
+                                               float* bhi = nullptr, float* blo = nullptr) {
+    const int j = threadIdx.x % persist::THREADS;  // thread of the (virtual) CTA
     double cmax = 0.0, cnmax = 0.0;
     if (j < K) {
         double n64 = 0.0, n32 = 0.0;
@@ -221,25 +331,38 @@ __device__ __forceinline__ void persist_tables(const double* c64, double* cn64, 
             n64 = add_rn(n64, mul_rn(cf, cf));
             const float c32 = static_cast<float>(cf);
             tab[(j / 2) * 2 * D + 2 * f + (j & 1)] = -2.f * c32;  // cluster-pair layout (persist_top2)
+            if (bhi) {  // persist_layout's bop (j < K <= 8: the first 8-row group)
+                const float v = -2.f * c32;
+                const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+                const int off = (f / 4) * 32 + j * 4 + (f % 4);
+                bhi[off] = hi;
+                blo[off] = v - hi;
+            }
             n32 += static_cast<double>(c32) * static_cast<double>(c32);
         }
+        if (bhi) tc::fence_async_smem();
         tab[K * D + j] = static_cast<float>(n32);
         cn64[j] = n64;
         cmax = sqrt(n32);
         cnmax = static_cast<double>(static_cast<float>(n32));
     }
-    if (threadIdx.x < 32) {
+    if (j < 32) {
         cmax = warp_max(cmax);
         cnmax = warp_max(cnmax);
-        if (threadIdx.x == 0) {
+        if (j == 0) {
             misc[0] = static_cast<double>(static_cast<float>(cmax) * (1.f + 0x1.0p-20f));
             misc[1] = static_cast<double>(static_cast<float>(cnmax) * (1.f + 0x1.0p-20f));
         }
     }
 }
 
-template <int D, int K, int R, int NST, int MINB, int MODE>
-__global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(PersistParams p) {
+// WG > 1: one CTA of WG warpgroups per SM, each warpgroup one virtual CTA of
+// the algorithm above (its own shared-memory block, tiles, state copy and
+// named barrier; virtual block id blockIdx.x * WG + wg).  The tensor-core
+// score instantiations need it: a kernel that uses tcgen05 is resident one
+// CTA per SM, and the four virtual CTAs share the SM's 512 TMEM columns.
+template <int D, int K, int R, int NST, int MINB, int MODE, bool TCS = false, int WG = 1>
+__global__ void __launch_bounds__(persist::THREADS * WG, WG == 1 ? MINB : 1) kmeans_persist_kernel(PersistParams p) {
     using namespace persist;
     static_assert(D % 2 == 0 && D <= 64 && K <= 32, "persistent kernel shape");
     constexpr int TILE = THREADS * R, VW = W * R;
@@ -247,9 +370,11 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
     constexpr int GR = L <= 32 ? 32 / L : 1; // rows summed in parallel per warp
     constexpr int KD = K * D, S = KD + K;
     constexpr int JW = (K + W - 1) / W;      // clusters owned per warp in the run sums
-    constexpr PersistLayout LY = persist_layout<D, K, R, NST>();
+    constexpr PersistLayout LY = persist_layout<D, K, R, NST, TCS>();
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_base[];
+    const int wg = WG == 1 ? 0 : static_cast<int>(threadIdx.x) / THREADS;
+    unsigned char* smem_raw = smem_base + wg * LY.total;
     float* tiles = reinterpret_cast<float*>(smem_raw + LY.tiles);
     int8_t* slab = reinterpret_cast<int8_t*>(smem_raw + LY.slab);
     long long* wacc = reinterpret_cast<long long*>(smem_raw + LY.wacc);
@@ -260,7 +385,6 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
     double* run = reinterpret_cast<double*>(smem_raw + LY.run);
     double* c64s = reinterpret_cast<double*>(smem_raw + LY.c64);
     double* cn64s = reinterpret_cast<double*>(smem_raw + LY.cn64);
-    double* stat = reinterpret_cast<double*>(smem_raw + LY.stat);
     double* misc = reinterpret_cast<double*>(smem_raw + LY.misc);
     volatile long long* stile = reinterpret_cast<volatile long long*>(smem_raw + LY.stile);
     volatile int* siter = reinterpret_cast<volatile int*>(smem_raw + LY.siter);
@@ -269,27 +393,40 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
     unsigned* consumed = reinterpret_cast<unsigned*>(smem_raw + LY.consumed);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + LY.bars);
     uint64_t* lbars = reinterpret_cast<uint64_t*>(smem_raw + LY.lbars);
+    constexpr int BPART = (D + 7) / 8 * 8 / 4 * 128;  // bytes of one part (hi or lo) of the MMA operand
+    float* bhi = TCS ? reinterpret_cast<float*>(smem_raw + LY.bop) : nullptr;
+    float* blo = TCS ? reinterpret_cast<float*>(smem_raw + LY.bop + BPART) : nullptr;
     double* cold = reinterpret_cast<double*>(scr);  // update only: previous centroids [KD] and |c|^2 [K]
     double* cnold = cold + KD;
     int* s_last = reinterpret_cast<int*>(misc + 8);
+    volatile int* s_tmo = reinterpret_cast<volatile int*>(misc + 8) + 1;  // this CTA timed out at a barrier
+    uint64_t* tbar = reinterpret_cast<uint64_t*>(misc + 4);    // TCS: MMA completion
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(misc + 5);   // TCS: TMEM base address
     // the producer's position: iteration being grabbed and its next static index
     volatile int* s_git = reinterpret_cast<volatile int*>(misc + 12);
     volatile int* s_gj = reinterpret_cast<volatile int*>(misc + 12) + 1;
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int G = gridDim.x;
+    const int tid = static_cast<int>(threadIdx.x) % THREADS, warp = tid >> 5, lane = tid & 31;
+    const int vb = static_cast<int>(blockIdx.x) * WG + wg;  // virtual block
+    const int G = static_cast<int>(gridDim.x) * WG;
     const int64_t ntiles = ceil_div(p.n, TILE);
     const int J0 = p.static_tiles;                       // static tiles of every CTA
     const int64_t nstatic = static_cast<int64_t>(J0) * G;  // tiles [0, nstatic) are static
 
+    if constexpr (TCS) {
+        if (threadIdx.x < 32) tc::tmem_alloc(tslot, TC_COLS * WG);  // warpgroup 0's slot
+        for (int e = tid; e < 2 * BPART / 4; e += THREADS) bhi[e] = 0.f;  // padding features
+    }
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&bars[s], 1);
             mbar_init(&lbars[s], 1);
         }
+        if (TCS) mbar_init(tbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         *s_git = p.it_begin;
         *s_gj = 0;
+        *s_tmo = 0;
     }
     if (tid < NST) {
         consumed[tid] = 0u;
@@ -299,8 +436,20 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
     for (int e = tid; e < KD; e += THREADS) c64s[e] = p.c64_init[e];
     if (MODE == DELTA_ONLY)
         for (int e = tid; e < S; e += THREADS) run[e] = p.run_io[e];
-    __syncthreads();
-    persist_tables<D, K>(c64s, cn64s, tab, misc);
+    if (TCS) tc::tc_fence_before();
+    __syncthreads();  // the whole CTA (every warpgroup)
+    if (TCS) tc::tc_fence_after();
+    // this warpgroup's TMEM columns
+    const uint32_t tmem =
+        TCS ? *reinterpret_cast<const uint32_t*>(smem_base + (reinterpret_cast<unsigned char*>(tslot) - smem_raw)) +
+                  static_cast<uint32_t>(wg * TC_COLS)
+            : 0u;
+    persist_tables<D, K>(c64s, cn64s, tab, misc, bhi, blo);
+    // TCS: the MMA operand descriptors (fixed addresses) and the barrier phase
+    // (LBO: the two 16-byte K chunks of a K = 8 step; SBO: the 8-row groups)
+    const uint64_t bh_desc = TCS ? tc::smem_desc(tc::smem_u32(bhi), 128, BPART) : 0ull;
+    const uint64_t bl_desc = TCS ? tc::smem_desc(tc::smem_u32(blo), 128, BPART) : 0ull;
+    uint32_t tph = 0u;
     // fixed-point scale of the sums: n max|x| < 2^e
     const double xabs = p.sx2[3];
     int e2 = 0;
@@ -321,7 +470,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
         while (git < p.it_end) {
             const int j = *s_gj;
             if (j < J0) {
-                const int64_t t = blockIdx.x + static_cast<int64_t>(j) * G;
+                const int64_t t = vb + static_cast<int64_t>(j) * G;
                 *s_gj = j + 1;
                 if (t < ntiles) {
                     tile = t;
@@ -377,7 +526,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
     };
     if (tid == 0)
         for (int s = 0; s < NST; ++s) issue(s, p.it_begin);
-    __syncthreads();
+    persist_sync<WG>(wg);
 
     const bool invalid = p.flags[0] != 0;  // invalid input, or converged in an earlier launch
     // exchange epoch before this launch's first iteration (read before barrier 0)
@@ -390,15 +539,16 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
         const bool full = MODE == FULL_ONLY || (MODE == BOTH && it < p.full_iters);
         const int TG = p.trace_grid;
         unsigned long long* tm = p.trace_marks ? p.trace_marks + static_cast<int64_t>(it) * (2 * TG + 2) : nullptr;
-        if (tm && blockIdx.x == 0 && tid == 0) tm[2 * TG] = gtimer();
+        if (tm && vb == 0 && tid == 0) tm[2 * TG] = gtimer();
         const float tau = 4.f * static_cast<float>(D + 3) * 0x1.0p-24f *
                           (static_cast<float>(misc[1]) +
                            2.f * sqrtf(static_cast<float>(D)) * xabs_f * static_cast<float>(misc[0]));
+        const float cnmax_f = static_cast<float>(misc[1]), cmax_f = static_cast<float>(misc[0]);
         if (!full)
             for (int e = tid; e < W * KD; e += THREADS) wacc[e] = 0ll;
-        if (blockIdx.x == 0 && it >= 1)
+        if (vb == 0 && it >= 1)
             for (int e = tid; e < S; e += THREADS) p.acc[((it + 1) % 3) * S + e] = 0ull;
-        __syncthreads();
+        persist_sync<WG>(wg);
 
         long long count_acc = 0;
         int cnt_delta = 0;
@@ -460,7 +610,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                         issue(s, it);
                     }
                 }
-                float b1[R], b2[R];
+                float b1[R], b2[R], tr[R];
                 int i1[R];
 #ifdef KP_EXP_STREAM
 #pragma unroll
@@ -473,7 +623,13 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                     i1[h] = prevl[h] < 0 ? 0 : prevl[h];
                 }
 #else
-                persist_top2<D, K, R>(xv, tab, b1, b2, i1);
+                if constexpr (TCS) {
+                    persist_top2_tc<D, K, R, WG>(xv, tab, tmem, bh_desc, bl_desc, tbar, tph, cnmax_f, cmax_f, b1, b2, i1, tr, wg);
+                } else {
+                    persist_top2<D, K, R>(xv, tab, b1, b2, i1);
+#pragma unroll
+                    for (int h = 0; h < R; ++h) tr[h] = tau;
+                }
 #endif
 #pragma unroll
                 for (int h = 0; h < R; ++h) {
@@ -482,7 +638,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                     label[h] = K;
                     if (gr < p.n) {
                         label[h] = i1[h];
-                        if (K > 1 && !(b2[h] - b1[h] > tau)) {
+                        if (K > 1 && !(b2[h] - b1[h] > tr[h])) {
                             // the stage may be refilled already: the row from global (L2)
                             label[h] = ref_argmin<float>(p.x + gr * D, D, c64s, cn64s, K);
                             ++refined;
@@ -522,16 +678,22 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             // ---- full iteration: every row summed (counting sort of the tile)
             int label[R];
             {
-                float b1[R], b2[R];
+                float b1[R], b2[R], tr[R];
                 int i1[R];
-                persist_top2<D, K, R>(xv, tab, b1, b2, i1);
+                if constexpr (TCS) {
+                    persist_top2_tc<D, K, R, WG>(xv, tab, tmem, bh_desc, bl_desc, tbar, tph, cnmax_f, cmax_f, b1, b2, i1, tr, wg);
+                } else {
+                    persist_top2<D, K, R>(xv, tab, b1, b2, i1);
+#pragma unroll
+                    for (int h = 0; h < R; ++h) tr[h] = tau;
+                }
 #pragma unroll
                 for (int h = 0; h < R; ++h) {
                     const int row = tid + h * THREADS;
                     label[h] = K;  // rows past the end sort last
                     if (row0 + row < p.n) {
                         label[h] = i1[h];
-                        if (K > 1 && !(b2[h] - b1[h] > tau)) {
+                        if (K > 1 && !(b2[h] - b1[h] > tr[h])) {
                             label[h] = ref_argmin<float>(xt + row * D, D, c64s, cn64s, K);
                             ++refined;
                         }
@@ -552,7 +714,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                 rank[h] = __popc(mine[h] & ((1u << lane) - 1u));
                 if (rank[h] == 0 && label[h] < K) cnt[(h * W + warp) * K + label[h]] = __popc(mine[h]);
             }
-            __syncthreads();  // counts visible; every warp is done with the previous tile's stage
+            persist_sync<WG>(wg);  // counts visible; every warp is done with the previous tile's stage
             if (tid == 0 && g > 0 && consumed[(g - 1) % NST] == 0xFFFFFFFFu) {
                 consumed[(g - 1) % NST] = 0u;  // the previous full tile's stage: sort buffer no more
                 sdef[(g - 1) % NST] = 0;
@@ -587,7 +749,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                     for (int f = 0; f < L; ++f) *reinterpret_cast<float2*>(xt + pos * D + 2 * f) = xv[h][f];
                 }
             }
-            __syncthreads();
+            persist_sync<WG>(wg);
             // warp w sums the sorted runs of clusters w, w+W, ... in f64 and
             // adds the tile's run sums as int64 fixed point
 #pragma unroll
@@ -634,21 +796,21 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             if (tid == 0) consumed[s] = 0xFFFFFFFFu;  // released at the next tile's count barrier
         }
         if (!full && qn > 0) flush_queue();
-        __syncthreads();  // every warp is done with this iteration's tiles
+        persist_sync<WG>(wg);  // every warp is done with this iteration's tiles
         // a full iteration hands its last stage back only now (it was the sort buffer)
         if (full && tid == 0 && g > 0 && consumed[(g - 1) % NST] == 0xFFFFFFFFu) {
             consumed[(g - 1) % NST] = 0u;
             sdef[(g - 1) % NST] = 0;
             issue(static_cast<int>((g - 1) % NST), it);
         }
-        if (tm && tid == 0) tm[blockIdx.x] = gtimer();
+        if (tm && tid == 0) tm[vb] = gtimer();
         asm volatile("fence.proxy.async.global;" ::: "memory");  // this iteration's labels -> later bulk reads
 
         // ---- this CTA's int64 partial stats -> global accumulator
         unsigned long long* acc_it = p.acc + (it % 3) * S;
         if (!full) {
             if (lane < K) cnt[warp * K + lane] = cnt_delta;
-            __syncthreads();
+            persist_sync<WG>(wg);
             for (int e = tid; e < KD; e += THREADS) {
                 long long v = 0;
 #pragma unroll
@@ -674,7 +836,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             if (warp == 0 && lane < K && count_acc)
                 atomicAdd(acc_it + KD + lane, static_cast<unsigned long long>(count_acc));
         }
-        __syncthreads();
+        persist_sync<WG>(wg);
 
         // ---- grid barrier (+ the cross-rank exchange on the last arrival)
         // two-level arrival: CTA b counts in group b % NG, the last of a group in
@@ -684,14 +846,14 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
         const unsigned target = static_cast<unsigned>(NG) * round;
         if (tid == 0) {
             __threadfence();
-            const int grp = blockIdx.x % NG;
+            const int grp = vb % NG;
             const unsigned gsize = static_cast<unsigned>((G - 1 - grp) / NG + 1);
             const unsigned oldg = atomicAdd(p.arrive + 1 + grp, 1u);
             int last = 0;
             if (oldg == gsize * round - 1u) last = atomicAdd(p.arrive, 1u) == target - 1u ? 1 : 0;
             *s_last = last;
         }
-        __syncthreads();
+        persist_sync<WG>(wg);
         // world > 1: the exchange epoch of this iteration (every CTA read the
         // base before barrier 0; only the finaliser advances the stored epoch)
         const unsigned long long epoch = xbase + static_cast<unsigned long long>(it + 1 - p.it_begin);
@@ -705,8 +867,10 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                 const double v = e < KD ? ldexp(static_cast<double>(qv), -shift) : static_cast<double>(qv);
                 for (int r = 0; r < p.world; ++r) xchg_recv(p.peers[r], xslot, p.world, p.rank)[e] = v;
             }
-            __threadfence_system();
-            __syncthreads();
+            // the CTA barrier orders every thread's stores before the flag
+            // writers' system-scope release (cumulative, as in a grid sync:
+            // no fence per storing thread -- one NVLink round trip less)
+            persist_sync<WG>(wg);
             if (tid < p.world) st_release_sys(xchg_flags(p.peers[tid], p.world) + p.rank, epoch);
         }
         if (p.world > 1) {
@@ -719,6 +883,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                     __nanosleep(32);
                     if (clock64() - t0 > 40000000000ll) {  // a rank never arrived (~20 s): TimeoutError, no trap
                         atomicExch(p.flags + 3, 1);
+                        *s_tmo = 1;
                         break;
                     }
                 }
@@ -729,12 +894,13 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                 __nanosleep(20);
                 if (clock64() - t0 > 40000000000ll) {
                     atomicExch(p.flags + 3, 1);
+                    *s_tmo = 1;
                     break;
                 }
             }
         }
-        __syncthreads();
-        if (tm && tid == 0) tm[TG + blockIdx.x] = gtimer();
+        persist_sync<WG>(wg);
+        if (tm && tid == 0) tm[TG + vb] = gtimer();
         // ---- the folded stats of this iteration, added to the running sums
         // (delta iterations) -- every CTA the same bits -- and the old state
         const double* xrecv = p.world > 1 ? xchg_recv(p.peers[p.rank], xslot, p.world, 0) : nullptr;
@@ -752,8 +918,8 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             if (e < KD) cold[e] = c64s[e];
         }
         if (tid < K) cnold[tid] = cn64s[tid];
-        __syncthreads();
-        if (__ldcv(p.flags + 3)) {
+        persist_sync<WG>(wg);
+        if (*s_tmo) {  // (flags[3] tells the host; the other CTAs time out at their own waits)
             stop = true;
             break;
         }
@@ -780,7 +946,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             inertia_part = warp_sum(inertia_part);
             dmax = warp_max(dmax);
             if (lane == 0) {
-                if (blockIdx.x == 0) {
+                if (vb == 0) {
                     p.trace[it] = p.sx2[2] + inertia_part;
                     p.disp[it] = dmax;
                     p.flags[1] = it + 1;
@@ -788,10 +954,10 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                 }
                 misc[2] = dmax < p.tol ? 1.0 : 0.0;
             }
-            persist_tables<D, K>(c64s, cn64s, tab, misc);
+            persist_tables<D, K>(c64s, cn64s, tab, misc, bhi, blo);
         }
-        __syncthreads();
-        if (tm && blockIdx.x == 0 && tid == 0) tm[2 * TG + 1] = gtimer();
+        persist_sync<WG>(wg);
+        if (tm && vb == 0 && tid == 0) tm[2 * TG + 1] = gtimer();
         stop = misc[2] != 0.0;
         // tiles of the next iteration already staged: their previous labels are final now
         if (!stop && tid == 0) {
@@ -800,7 +966,7 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
                 if (sdef[s] && siter[s] == it + 1) issue_labels(s);
             }
         }
-        __syncthreads();
+        persist_sync<WG>(wg);
     }
     // loads issued but never consumed (early stop): let them land before exit
     if (tid == 0) {
@@ -808,8 +974,16 @@ __global__ void __launch_bounds__(persist::THREADS, MINB) kmeans_persist_kernel(
             mbar_wait(&bars[h % NST], static_cast<uint32_t>((h / NST) & 1));
     }
     if (refined) atomicAdd(p.refined, refined);
-    if (blockIdx.x == 0) {
+    if (vb == 0) {
         for (int e = tid; e < KD; e += THREADS) p.c64_out[e] = c64s[e];
         for (int e = tid; e < S; e += THREADS) p.run_io[e] = run[e];
+    }
+    if constexpr (TCS) {
+        tc::tc_fence_before();
+        __syncthreads();  // every warpgroup done with its columns
+        if (threadIdx.x < 32) {
+            tc::tc_fence_after();
+            tc::tmem_dealloc(tmem, TC_COLS * WG);  // warpgroup 0's base = the allocation
+        }
     }
 }
