@@ -904,7 +904,7 @@ __global__ void __launch_bounds__(persist::THREADS * WG, WG == 1 ? MINB : 1) kme
         // ---- the folded stats of this iteration, added to the running sums
         // (delta iterations) -- every CTA the same bits -- and the old state
         const double* xrecv = p.world > 1 ? xchg_recv(p.peers[p.rank], xslot, p.world, 0) : nullptr;
-        for (int e = tid; e < S; e += THREADS) {
+        auto folded = [&](int e) {  // this iteration's stat e, plus the running value (delta iterations)
             double v;
             if (p.world > 1) {  // rank-order fold (transport.hpp:136-148), identical in every CTA of every rank
                 v = 0.0;
@@ -914,8 +914,24 @@ __global__ void __launch_bounds__(persist::THREADS * WG, WG == 1 ? MINB : 1) kme
                 v = e < KD ? ldexp(static_cast<double>(qv), -shift) : static_cast<double>(qv);
             }
             if (!full) v += run[e];  // delta iterations: changes added to the running sums
-            run[e] = v;
-            if (e < KD) cold[e] = c64s[e];
+            return v;
+        };
+        // the new centroids in the same pass (cluster.cpp:125-133): the thread of
+        // entry e folds its cluster's count itself (the same bits as the count's
+        // own entry); counts go to ncnt, so run[KD..] stays the old value until
+        // every thread has read it
+        double* ncnt = cnold + K;
+        for (int e = tid; e < S; e += THREADS) {
+            const double v = folded(e);
+            if (e < KD) {
+                const double count = folded(KD + e / D);
+                run[e] = v;
+                const double c_old = c64s[e];
+                cold[e] = c_old;
+                c64s[e] = count > 0.0 ? v / count : c_old;  // empty cluster keeps its centroid
+            } else {
+                ncnt[e - KD] = v;
+            }
         }
         if (tid < K) cnold[tid] = cn64s[tid];
         persist_sync<WG>(wg);
@@ -923,16 +939,16 @@ __global__ void __launch_bounds__(persist::THREADS * WG, WG == 1 ? MINB : 1) kme
             stop = true;
             break;
         }
-        // ---- update (cluster.cpp:123-150) by warp 0, identical in every CTA
+        // ---- rest of the update (cluster.cpp:123-150), identical in every CTA:
+        // warp 0 the tables, warp 1 inertia / displacement, warp 2 the counts
         if (warp == 0) {
-            for (int e = lane; e < KD; e += 32) {
-                const double count = run[KD + e / D];
-                c64s[e] = count > 0.0 ? run[e] / count : cold[e];  // empty cluster keeps its centroid
-            }
-            __syncwarp();
+            persist_tables<D, K>(c64s, cn64s, tab, misc, bhi, blo);
+        } else if (warp == 2) {
+            if (lane < K) run[KD + lane] = ncnt[lane];
+        } else if (warp == 1) {
             double inertia_part = 0.0, dmax = 0.0;
             if (lane < K) {
-                const double count = run[KD + lane];
+                const double count = ncnt[lane];
                 double dot = 0.0, dsq = 0.0;
                 for (int f = 0; f < D; ++f) {
                     const int e = lane * D + f;
@@ -954,7 +970,6 @@ __global__ void __launch_bounds__(persist::THREADS * WG, WG == 1 ? MINB : 1) kme
                 }
                 misc[2] = dmax < p.tol ? 1.0 : 0.0;
             }
-            persist_tables<D, K>(c64s, cn64s, tab, misc, bhi, blo);
         }
         persist_sync<WG>(wg);
         if (tm && vb == 0 && tid == 0) tm[2 * TG + 1] = gtimer();
