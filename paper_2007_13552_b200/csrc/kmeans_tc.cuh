@@ -801,14 +801,20 @@ struct TcRefineParams {
     const int* done;
 };
 
+#ifndef DNDC_REFINE_THREADS
+#define DNDC_REFINE_THREADS 512
+#endif
+#ifndef DNDC_REFINE_CH
+#define DNDC_REFINE_CH 1024
+#endif
 template <int D, int K>
-__host__ __device__ constexpr int tc_refine_threads() { return 512; }
+__host__ __device__ constexpr int tc_refine_threads() { return DNDC_REFINE_THREADS; }
 
 // shared memory of kmeans_tc_refine_kernel (dynamic): transposed f64
 // centroids, |c|^2, the int64 sums, and one queue chunk's bookkeeping
 template <int D, int K>
 struct TcRefineSmem {
-    static constexpr int CH = 1024, NW = tc_refine_threads<D, K>() / 32;
+    static constexpr int CH = DNDC_REFINE_CH, NW = tc_refine_threads<D, K>() / 32;
     static constexpr int OFF_CT = 0;                                  // double [D][K]
     static constexpr int OFF_CN = OFF_CT + D * K * 8;                 // double [K]
     static constexpr int OFF_ACC = OFF_CN + K * 8;                    // long long [K*D + K]
@@ -835,7 +841,7 @@ struct TcRefineSmem {
 // its sums to racc; the last CTA converts racc into the partial row and
 // resets the queue.
 template <int D, int K>
-__global__ void __launch_bounds__(512) kmeans_tc_refine_kernel(TcRefineParams p) {
+__global__ void __launch_bounds__(DNDC_REFINE_THREADS) kmeans_tc_refine_kernel(TcRefineParams p) {
     using L = TcRefineSmem<D, K>;
     constexpr int KD = K * D, NT = tc_refine_threads<D, K>(), NW = L::NW, CH = L::CH;
     constexpr int FPL = (D + 31) / 32;
