@@ -177,10 +177,13 @@ def measured_peaks():
 
 
 def ncu_traffic():
-    """dram bytes per launch of the assign kernel from the committed ncu summary."""
+    """dram bytes of the k-means loop (the unit `roofline.achieved` counts: 20
+    iterations) from the committed ncu capture of the persistent delta launch
+    (iterations 1-19, profiles/ncu_persist_delta_r02_final.json), scaled to 20
+    iterations."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_kmeans_assign.json")))
-        return d.get("dram_bytes_per_launch")
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_persist_delta_r02_final.json")))
+        return d.get("dram_bytes_per_launch") * ITERS / (ITERS - 1)
     except Exception:
         return None
 
@@ -489,7 +492,7 @@ def run_ours(args):
     byt = float(x.tile.shape[0]) * N_FEAT * 4
     roof.update({"traffic": ncu_traffic(),
                  "timing": "CUDA event nodes around the k-means loop kernel launch(es) inside one fit graph on "
-                           "the fit's stream (iterations 0-1 accumulate every row, later ones only rows whose "
+                           "the fit's stream (iteration 0 accumulates every row, later ones only rows whose "
                            "label changed)",
                  "per_iteration_kernel_full_accumulate_ms": ms_full.value,
                  "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json copy bandwidth)",

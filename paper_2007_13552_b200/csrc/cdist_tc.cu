@@ -315,7 +315,12 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 tc::fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
+#ifdef CDTC_STORE_EVICT_FIRST
+                    tc::tma_store_2d_hint(&mapo, box, static_cast<int>(gc), static_cast<int>(row0 + q * 32),
+                                          tc::l2_policy_evict_first());
+#else
                     tc::tma_store_2d(&mapo, box, static_cast<int>(gc), static_cast<int>(row0 + q * 32));
+#endif
                     tc::bulk_commit();
                 }
             }

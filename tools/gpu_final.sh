@@ -18,3 +18,11 @@ if [ "${NCU:-1}" = "1" ]; then
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-cdist --no-configs > $OUT/final_ncu_launch.log 2>&1
 fi
 tail -3 $OUT/final_pytest_gpu.log; tail -2 $OUT/final_smoke.log; cat $OUT/final_bench.json; cat $OUT/final_bench_ref.json
+# one full ncu capture of the dominant kernel (the persistent delta launch),
+# after its plain run exited 0
+if [ "${NCU:-1}" = "1" ]; then
+  timeout 300 python tools/prof_persist.py > $OUT/final_prof_plain.log 2>&1 && \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:kmeans_persist_kernel -s 5 -c 1 \
+      -o $OUT/final_prof_persist_delta -f python tools/prof_persist.py > $OUT/final_ncu_full.log 2>&1
+  echo "ncu full rc=$?" >> $OUT/final_ncu_full.log
+fi
