@@ -66,7 +66,10 @@ __host__ __device__ constexpr int smem_bytes(int nst, int epi, int bc) {
 constexpr int SMEM = smem_bytes(2, 8, 16);  // the largest configuration
 static_assert(smem_bytes(1, CDTC_EPI1, CDTC_BC1) <= SMEM, "smem layouts");
 constexpr int TMEM_COLS = 512;
-constexpr int GROUP = 16;  // rasterisation: GROUP x GROUP tile super-blocks
+#ifndef CDTC_GROUP
+#define CDTC_GROUP 16
+#endif
+constexpr int GROUP = CDTC_GROUP;  // rasterisation: GROUP row blocks x all column blocks per super-block
 }  // namespace cdtc
 
 struct CdtcParams {
@@ -315,7 +318,9 @@ __global__ void __launch_bounds__(cdtc::THREADS, 1)
                 tc::fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-#ifdef CDTC_STORE_EVICT_FIRST
+                    // evict_first: the distance matrix is streamed out, never re-read
+                    // here (cfg2: 42.9 -> 42.0 ms, tools/gpu_var_cdist.sh)
+#ifndef CDTC_STORE_NO_HINT
                     tc::tma_store_2d_hint(&mapo, box, static_cast<int>(gc), static_cast<int>(row0 + q * 32),
                                           tc::l2_policy_evict_first());
 #else
