@@ -2126,6 +2126,9 @@ static bool plan_persist(dndc_ctx* ctx, int k, int m, int64_t n_local, PersistPl
         const std::string v = d ? d : "";
         if (v == "r4s3") return try_persist<18, 8, 4, 3, 2, DELTA_ONLY>(ctx, n_local, P.delta, "kmeans_persist_kernel<18,8,R4,S3,delta>");
         if (v == "r4") return try_persist<18, 8, 4, 2, 3, DELTA_ONLY>(ctx, n_local, P.delta, "kmeans_persist_kernel<18,8,R4,S2,delta>");
+        if (v == "r1s3") return try_persist<18, 8, 1, 3, 4, DELTA_ONLY>(ctx, n_local, P.delta, "kmeans_persist_kernel<18,8,R1,S3,delta>");
+        if (v == "r1s4") return try_persist<18, 8, 1, 4, 4, DELTA_ONLY>(ctx, n_local, P.delta, "kmeans_persist_kernel<18,8,R1,S4,delta>");
+        if (v == "r2s3") return try_persist<18, 8, 2, 3, 3, DELTA_ONLY>(ctx, n_local, P.delta, "kmeans_persist_kernel<18,8,R2,S3,delta>");
         return try_persist<18, 8, 2, 2, 4, DELTA_ONLY>(ctx, n_local, P.delta, "kmeans_persist_kernel<18,8,R2,S2,delta>");
     }
     return false;
