@@ -251,3 +251,38 @@ def test_tc_predict_exact_ties_and_zero_distances(comm, oracle, n):
     want = oracle.kmeans_predict(xh.astype(np.float64), cents)
     assert np.array_equal(got, want)
     assert got[9] == 5 and got[3] == 3  # duplicated pairs resolve to the lower index
+
+
+_PERSIST_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, ".")
+import paper_2007_13552_b200.api as dnd
+comm = dnd.Communicator(0)
+x = dnd.random_uniform((300_000, 18), 0, 7, comm)
+m = dnd.kmeans_fit(x, 8, 12, 0.0, 5)
+labels = dnd.gather(dnd.kmeans_predict(m, x))
+np.savez(sys.argv[1], c=m.centroids, t=np.asarray(m.inertia_trace), l=labels)
+"""
+
+
+@pytest.mark.parametrize("env", [{"DNDC_PERSIST_TC": "1"}, {"DNDC_FULL_ITERS": "2"}, {"DNDC_PERSIST_STATIC": "100"}])
+def test_persistent_variants_bitwise_equal(tmp_path, env):
+    """The persistent cfg1-shape fit's variants -- tensor-core scores (four
+    warpgroups per CTA), two full iterations, a fully static tile schedule --
+    give the default's centroids, trace and labels bit for bit: the near-ties
+    are re-decided exactly and the sums are order-independent int64 fixed
+    point.  Each run in its own process (the fit graph is cached per shape)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for name, extra in (("default", {}), ("variant", env)):
+        path = tmp_path / f"{name}.npz"
+        e = {k: v for k, v in os.environ.items() if not k.startswith("DNDC_")}
+        e.update(extra)
+        subprocess.run([sys.executable, "-c", _PERSIST_CHILD, str(path)], cwd=root, env=e, check=True, timeout=600)
+        out[name] = np.load(path)
+    for key in ("c", "t", "l"):
+        assert np.array_equal(out["default"][key], out["variant"][key]), (env, key)
