@@ -2147,13 +2147,31 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
                     std::to_string(ext[ctx->rank]));
     const int m = static_cast<int>(m64);
     cudaStream_t s = ctx->stream;
+    // A shard that is not 16-byte aligned is copied to an aligned scratch
+    // buffer first (the bulk-copy / TMA kernels need the alignment), so that on
+    // every rank the kernel plan below follows from global facts only -- (k, m),
+    // the chunk_map extents, the environment -- and needs no cross-rank
+    // agreement in the common case.
+    if (ctx->world > 1 && n_local > 0 && reinterpret_cast<uintptr_t>(x_local) % 16 != 0) {
+        T* xa = static_cast<T*>(ctx->slot("km_xalign", sizeof(T) * static_cast<size_t>(n_local) * m));
+        DNDC_CUDA(cudaMemcpyAsync(xa, x_local, sizeof(T) * static_cast<size_t>(n_local) * m,
+                                  cudaMemcpyDeviceToDevice, s));
+        x_local = xa;
+    }
     Assigner<T> A = plan<T>(ctx, k, m, n_local, x_local);
     // the kernel choice fixes the stats protocol (fused NVLink exchange,
     // delta vs full sums): every rank must take the same one
     PersistPlan PP;
     bool persist = sizeof(T) == 4 && A.small && (ctx->world == 1 || ctx->p2p) && n_local > 0 &&
                    plan_persist(ctx, k, m, n_local, PP);
-    if (ctx->world > 1) {
+    // The plan differs between ranks only when some rank's shard is empty, or
+    // under a kernel override (forced tc packs row pairs: shard parity).  Every
+    // rank evaluates this rule from the same global facts, so all of them take
+    // the host-synchronised agreement below or none does (skipping it saves
+    // ~40 us per fit at N = 4: tools/gpu_plan_ab.sh).  DNDC_PLAN_AGREE=1 forces it.
+    bool agree = std::getenv("DNDC_PLAN_AGREE") != nullptr || !std::string(kernel_override()).empty();
+    for (int r = 0; r < ctx->world; ++r) agree = agree || ext[r] == 0;
+    if (ctx->world > 1 && agree) {
         const int code = (persist ? 1 : 0) | (A.small ? 2 : 0) | (A.tc ? 4 : 0) | (A.tc && A.tc_delta ? 8 : 0);
         int* dcode = static_cast<int*>(ctx->slot("km_plan", sizeof(int) * (ctx->world + 1)));
         DNDC_CUDA(cudaMemcpyAsync(dcode + ctx->world, &code, sizeof(int), cudaMemcpyHostToDevice, s));

@@ -265,13 +265,17 @@ np.savez(sys.argv[1], c=m.centroids, t=np.asarray(m.inertia_trace), l=labels)
 """
 
 
-@pytest.mark.parametrize("env", [{"DNDC_PERSIST_TC": "1"}, {"DNDC_FULL_ITERS": "2"}, {"DNDC_PERSIST_STATIC": "100"}])
-def test_persistent_variants_bitwise_equal(tmp_path, env):
-    """The persistent cfg1-shape fit's variants -- tensor-core scores (four
-    warpgroups per CTA), two full iterations, a fully static tile schedule --
-    give the default's centroids, trace and labels bit for bit: the near-ties
-    are re-decided exactly and the sums are order-independent int64 fixed
-    point.  Each run in its own process (the fit graph is cached per shape)."""
+@pytest.mark.parametrize("env,exact", [({"DNDC_PERSIST_TC": "1"}, True), ({"DNDC_PERSIST_STATIC": "100"}, True),
+                                       ({"DNDC_FULL_ITERS": "2"}, False)])
+def test_persistent_variants_agree(tmp_path, env, exact):
+    """The persistent cfg1-shape fit's variants against the default: tensor-core
+    scores (four warpgroups per CTA) and a fully static tile schedule give the
+    same centroids, trace and labels bit for bit (near-ties re-decided exactly;
+    sums are order-independent int64 fixed point, per tile in the full
+    iteration, per row in the delta ones).  A second full iteration rounds its
+    per-tile sums where the delta path rounds per row: the same labels, the
+    centroids within f64 rounding.  Each run in its own process (the fit graph
+    is cached per shape)."""
     import os
     import subprocess
     import sys
@@ -284,5 +288,9 @@ def test_persistent_variants_bitwise_equal(tmp_path, env):
         e.update(extra)
         subprocess.run([sys.executable, "-c", _PERSIST_CHILD, str(path)], cwd=root, env=e, check=True, timeout=600)
         out[name] = np.load(path)
-    for key in ("c", "t", "l"):
-        assert np.array_equal(out["default"][key], out["variant"][key]), (env, key)
+    assert np.array_equal(out["default"]["l"], out["variant"]["l"]), env
+    for key in ("c", "t"):
+        if exact:
+            assert np.array_equal(out["default"][key], out["variant"][key]), (env, key)
+        else:
+            assert rel_dev(out["variant"][key], out["default"][key]) <= 1e-13, (env, key)
