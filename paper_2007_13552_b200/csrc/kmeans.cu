@@ -1581,6 +1581,29 @@ __global__ void validate_fold_kernel(const double* all, int world, double* sx2, 
     flags[2] = bad > 0.0 ? 1 : 0;
 }
 
+// world x (sum |x|^2, non-finite count, the k init rows this rank owns, zeros
+// elsewhere) -> sx2[2], flags[2] (as validate_fold_kernel) and the initial
+// centroids: the rank-order sum of the rows (one owner each: exact) -- the
+// validation allgather and the init allreduce as one collective
+__global__ void validate_init_fold_kernel(const double* all, int world, int km, double* sx2, int* flags,
+                                          double* c64) {
+    const int per = 2 + km;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double sum = 0.0, bad = 0.0;
+        for (int r = 0; r < world; ++r) {
+            sum += all[static_cast<int64_t>(r) * per];
+            bad += all[static_cast<int64_t>(r) * per + 1];
+        }
+        sx2[2] = sum;
+        flags[2] = bad > 0.0 ? 1 : 0;
+    }
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < km; e += gridDim.x * blockDim.x) {
+        double v = 0.0;
+        for (int r = 0; r < world; ++r) v += all[static_cast<int64_t>(r) * per + 2 + e];
+        c64[e] = v;
+    }
+}
+
 // ----------------------------------------------------------------- host
 static KmBuffers buffers(dndc_ctx* ctx, int k, int m, int max_iter, int G) {
     KmBuffers b;
@@ -2194,13 +2217,37 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     // device: a non-finite value anywhere sets flags[2] (and the iterations
     // skip); the host raises after the single synchronisation at the end
     scan_input<T>(ctx, b, x_local, n_local * m, s);
-    allgather_f64(ctx, b.sx2, b.gathered, 2, s);  // gathered: scratch, world x 2
-    validate_fold_kernel<<<1, 32, 0, s>>>(b.gathered, ctx->world, b.sx2, b.flags);
-    DNDC_LAUNCHED(ctx);
+    const bool fused_init = ctx->world > 1 && !init_host && !ctx->group;
+    if (fused_init) {
+        // one collective for the validation stats and the initial centroids
+        // (the k seeded rows, each owned by one rank: cluster.cpp:60-81)
+        const int km = k * m;
+        double* pre = static_cast<double*>(ctx->slot("km_pre", sizeof(double) * (2 + km)));
+        double* pre_all = static_cast<double*>(ctx->slot("km_pre_all", sizeof(double) * (2 + km) * ctx->world));
+        const auto idx = init_indices(n_global, k, seed);
+        int64_t* didx = static_cast<int64_t*>(ctx->slot("km_idx", sizeof(int64_t) * k));
+        int64_t* hidx = static_cast<int64_t*>(ctx->host_staging(sizeof(int64_t) * k));
+        std::memcpy(hidx, idx.data(), sizeof(int64_t) * k);
+        DNDC_CUDA(cudaMemcpyAsync(didx, hidx, sizeof(int64_t) * k, cudaMemcpyHostToDevice, s));
+        DNDC_CUDA(cudaMemcpyAsync(pre, b.sx2, sizeof(double) * 2, cudaMemcpyDeviceToDevice, s));
+        gather_rows_kernel<T><<<std::max(1, std::min(1024, (km + 255) / 256)), 256, 0, s>>>(
+            x_local, off[ctx->rank], off[ctx->rank] + n_local, m, didx, k, pre + 2);
+        DNDC_LAUNCHED(ctx);
+        allgather_f64(ctx, pre, pre_all, static_cast<size_t>(2 + km), s);
+        validate_init_fold_kernel<<<std::max(1, std::min(64, (km + 255) / 256)), 256, 0, s>>>(
+            pre_all, ctx->world, km, b.sx2, b.flags, b.c64);
+        DNDC_LAUNCHED(ctx);
+    } else {
+        allgather_f64(ctx, b.sx2, b.gathered, 2, s);  // gathered: scratch, world x 2
+        validate_fold_kernel<<<1, 32, 0, s>>>(b.gathered, ctx->world, b.sx2, b.flags);
+        DNDC_LAUNCHED(ctx);
+    }
 
     // ---- initial centroids (no host round trip: the pinned staging buffer is
     // next written by the results copy, which is ordered after this upload)
-    if (init_host) {
+    if (fused_init) {
+        // (above)
+    } else if (init_host) {
         double* h = static_cast<double*>(ctx->host_staging(sizeof(double) * k * m));
         std::memcpy(h, init_host, sizeof(double) * k * m);
         DNDC_CUDA(cudaMemcpyAsync(b.c64, h, sizeof(double) * k * m, cudaMemcpyHostToDevice, s));
