@@ -3,28 +3,31 @@
 // Reference: kmeans_fit / assign_local / gather_rows / kmeans_predict
 // (cluster.cpp:27-172) on top of cdist_xy (pairwise.cpp:87-100).
 //
-// One iteration on one GPU is three launches, all captured in one CUDA graph
-// for the whole fit (tol == 0 never needs the host; tol > 0 sets a device
-// `done` flag that turns the remaining launches into no-ops):
+// Which kernels run a fit (plan<T>, plan_persist; the choice depends only on
+// global facts, so every rank takes the same one):
 //
-//   assign   persistent CTAs stream X once through a cp.async ring in shared
-//            memory.  Phase 1: lane = row; fp32 scores s_j = |c_j|^2 - 2 x.c_j
-//            against centroids staged in smem, top-2 tracking, and a rigorous
-//            fp32 error bound: rows whose top-2 gap falls inside it are
-//            re-decided with the reference's exact f64 arithmetic
-//            (distance_block + assign_local, products rounded before adds,
-//            strict < so the lowest index wins ties).  Phase 2: lane = feature;
-//            warp w owns clusters j = w, w+8, ...; per 32-row chunk a ballot
-//            selects the chunk's rows of cluster j and their features are summed
-//            in fp32 (<= 32 rows), then added into the CTA's f64 accumulators.
-//            No atomics: the result is deterministic for a given grid.
-//   reduce   per-stat sum over the CTA partials in CTA order (f64).
-//   update   [world > 1: after an NCCL allgather of the k*m + k stats] one CTA
-//            folds the ranks in order 0..p-1 (transport.hpp:136-148), forms
-//            the new f64 master centroids (empty clusters keep theirs,
-//            cluster.cpp:125-133), the inertia of the assignment just made,
-//            the displacement (cluster.cpp:139-150) and the fp32 tables of the
-//            next iteration.
+//   persistent  (fp32, the cfg1 shape d = 18, k = 8; kmeans_persist.cuh) the
+//               whole Lloyd loop in two cooperative launches -- iteration 0
+//               sums every row, the delta launch only the rows whose label
+//               changed -- with a grid barrier per iteration and, for
+//               world > 1, an NVLink exchange of the rank stats inside the
+//               kernel.  No relaunch, no host round trip.
+//   tc          (k d >= 1024, cfg3; kmeans_tc.cuh) per iteration in one CUDA
+//               graph: the tcgen05 3xTF32 scores/labels kernel, the refine
+//               kernel (near-ties decided exactly, changed rows summed), the
+//               accumulate kernel for full iterations, reduce + update.
+//   small / generic  the other shapes: one assign(+accumulate) launch per
+//               iteration (fused with the update on one GPU or over NVLink),
+//               else assign -> reduce -> NCCL allgather -> update.
+//
+// Common to all: fp32 scores s_j = |c_j|^2 - 2 x.c_j with a rigorous error
+// bound; rows whose top-2 gap falls inside it are re-decided with the
+// reference's exact f64 arithmetic (distance_block + assign_local, products
+// rounded before adds, strict < so the lowest index wins ties).  Sums are
+// int64 fixed point (order-independent: the fit is bit-repeatable), folded
+// over ranks in rank order 0..p-1 (transport.hpp:136-148); the update forms
+// the f64 master centroids (empty clusters keep theirs, cluster.cpp:125-133),
+// the inertia and the displacement (cluster.cpp:139-150).
 //
 // Inertia is not accumulated per row: with S_j, n_j the new sums/counts and c_j
 // the centroids used for the assignment,
