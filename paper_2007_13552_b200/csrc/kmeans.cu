@@ -540,6 +540,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// The row stream X of the bulk-copy k-means kernels: with DNDC_X_EVICT_FIRST
+// its copies carry an L2 evict_first policy (X is re-read only an iteration
+// later, after hundreds of MB; labels, stats and tables stay in L2).  Neutral
+// for the persistent cfg1 kernel (tools/gpu_var_xev.sh), so off by default;
+// the tensor-core path's TMA tiles take it by default (kmeans_tc.cuh).
+#ifdef DNDC_X_EVICT_FIRST
+#define X_BULK_HINT ".L2::cache_hint"
+#define X_BULK_POL , "l"(tc::l2_policy_evict_first())
+#define X_BULK_OPS ", %4"
+#else
+#define X_BULK_HINT ""
+#define X_BULK_POL
+#define X_BULK_OPS ""
+#endif
+
 // One thread: stream `bytes` (any multiple of 4) of global memory into smem,
 // completing on `bar`.  The 16-byte-aligned body goes through the bulk-copy
 // engine; a <16-byte tail is stored directly before the arrive.
@@ -551,9 +566,9 @@ __device__ __forceinline__ void bulk_load(float* dst, const float* src, uint32_t
                  : "memory");
     if (body)
         asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes" X_BULK_HINT " [%0], [%1], %2, [%3]" X_BULK_OPS ";" ::"r"(
                 smem_u32(dst)),
-            "l"(src), "r"(body), "r"(smem_u32(bar))
+            "l"(src), "r"(body), "r"(smem_u32(bar)) X_BULK_POL
             : "memory");
 }
 
@@ -568,9 +583,9 @@ __device__ __forceinline__ void bulk_load2(float* dst, const float* src, uint32_
                  : "memory");
     if (body)
         asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes" X_BULK_HINT " [%0], [%1], %2, [%3]" X_BULK_OPS ";" ::"r"(
                 smem_u32(dst)),
-            "l"(src), "r"(body), "r"(smem_u32(bar))
+            "l"(src), "r"(body), "r"(smem_u32(bar)) X_BULK_POL
             : "memory");
     if (body2)
         asm volatile(

@@ -286,7 +286,12 @@ __global__ void __launch_bounds__(TcCfg<D, K, P, WG_>::THREADS, 1)
                     tc::mbar_expect_tx(&full[st], C::TILE_BYTES);
                     float* dst = tiles + st * (C::TILE_BYTES / 4);
 #pragma unroll
-                    for (int kb = 0; kb < C::NKB; ++kb) tc::tma_load_2d(dst + kb * PR * 32, &map, &full[st], kb * 32, prow);
+    #ifndef DNDC_TC_NO_EVICT_FIRST  // X tiles leave L2 first (cfg3 shard: 0.532 -> 0.518 ms per iteration)
+                for (int kb = 0; kb < C::NKB; ++kb)
+                    tc::tma_load_2d_hint(dst + kb * PR * 32, &map, &full[st], kb * 32, prow, tc::l2_policy_evict_first());
+#else
+                for (int kb = 0; kb < C::NKB; ++kb) tc::tma_load_2d(dst + kb * PR * 32, &map, &full[st], kb * 32, prow);
+#endif
                     ++issued;
                 }
                 const int st = static_cast<int>(it % S), w = static_cast<int>(it % WGS);
@@ -1279,7 +1284,12 @@ __global__ void __launch_bounds__(TcdCfg<D, K>::THREADS, 1)
                 float* dst = tiles + st * (C::TILE_BYTES / 4);
                 tc::mbar_expect_tx(&full[st], C::TILE_BYTES);
 #pragma unroll
+#ifndef DNDC_TC_NO_EVICT_FIRST  // X tiles leave L2 first (cfg3 shard: 0.532 -> 0.518 ms per iteration)
+                for (int kb = 0; kb < C::NKB; ++kb)
+                    tc::tma_load_2d_hint(dst + kb * PR * 32, &map, &full[st], kb * 32, prow, tc::l2_policy_evict_first());
+#else
                 for (int kb = 0; kb < C::NKB; ++kb) tc::tma_load_2d(dst + kb * PR * 32, &map, &full[st], kb * 32, prow);
+#endif
             }
         }
     } else {
