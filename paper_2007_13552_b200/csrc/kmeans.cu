@@ -1464,6 +1464,129 @@ __global__ void __launch_bounds__(256) kmeans_update_kernel(UpdArgs a) {
     update_body(a, upd, sh);
 }
 
+// The same update spread over CTAs (per-iteration launches, d <= UPD_MC_MAXD):
+// CTA b takes clusters b, b + G, ...: the cluster's stats folded over the
+// ranks in rank order, running sums, new centroid, fp32 tables (element-
+// parallel), then the order-dependent chains (dot, |c_new - c_old|^2, |c|^2 in
+// f64 and fp32) by one thread.  Per-cluster inertia / displacement / norm
+// maxima go to `red`; the last CTA to finish reduces them exactly like
+// update_body (thread t holds clusters t, t + 256, ...; xor-butterfly per warp,
+// then the warps in order), so the results are bit-identical to it.  The
+// single-CTA kernel took ~27 us per cfg3 iteration (a latency chain: 64-step
+// loops over 64 clusters on two warps); this one a few.
+constexpr int UPD_MC_MAXD = 2048;
+__global__ void __launch_bounds__(256) kmeans_update_mc_kernel(UpdArgs a, double* red, unsigned* ticket) {
+    if (a.flags[0]) return;
+    const int k = a.k, d = a.d, dpad = a.dpad, world = a.world, KD = k * d;
+    extern __shared__ double us[];  // [d] sums, [d] old, [d] new
+    double* ss = us;
+    double* so = us + d;
+    double* sn = us + 2 * d;
+    __shared__ double scount;
+    __shared__ bool last;
+    for (int j = blockIdx.x; j < k; j += gridDim.x) {
+        // (1) fold, running sums, new centroid, tables: element-parallel
+        for (int f = threadIdx.x; f <= d; f += blockDim.x) {
+            const int e = f < d ? j * d + f : KD + j;
+            double v = 0.0;
+            for (int r = 0; r < world; ++r) v += a.gathered[static_cast<int64_t>(r) * a.gstride + e];
+            if (a.running) {
+                if (a.accum) v += a.rd_running[e];
+                a.running[e] = v;
+            }
+            if (f < d) {
+                ss[f] = v;
+                so[f] = a.rd_c64[e];
+            } else {
+                scount = v;
+            }
+        }
+        __syncthreads();
+        const double count = scount;
+        for (int f = threadIdx.x; f < dpad; f += blockDim.x) {
+            if (f < d) {
+                const double nxt = count > 0.0 ? ss[f] / count : so[f];  // cluster.cpp:125-133
+                sn[f] = nxt;
+                a.c64[j * d + f] = nxt;
+                const float c32 = static_cast<float>(nxt);
+                a.ct[static_cast<int64_t>(j) * dpad + f] = -2.f * c32;
+                if (a.ctab) a.ctab[j * d + f] = -2.f * c32;
+            } else {
+                a.ct[static_cast<int64_t>(j) * dpad + f] = 0.f;
+            }
+        }
+        __syncthreads();
+        // (2) the order-dependent sums of update_body, same operations
+        if (threadIdx.x == 0) {
+            const double cn_old = a.rd_cn64[j];  // (rd_cn64 may alias cn64, written below)
+            double dot = 0.0, dsq = 0.0, n64 = 0.0, n32 = 0.0;
+            for (int f = 0; f < d; ++f) {
+                const double sv = ss[f], old = so[f], nxt = sn[f];
+                dot += old * sv;
+                const double diff = nxt - old;
+                dsq = add_rn(dsq, mul_rn(diff, diff));  // cluster.cpp:142-146 order
+                n64 = add_rn(n64, mul_rn(nxt, nxt));    // row_norms order
+                const float c32 = static_cast<float>(nxt);
+                n32 += static_cast<double>(c32) * static_cast<double>(c32);
+            }
+            if (a.ctab) a.ctab[KD + j] = static_cast<float>(n32);
+            a.cn64[j] = n64;
+            a.cn32[j] = static_cast<float>(n32);
+            red[j] = count * cn_old - 2.0 * dot;  // uses the old |c_j|^2
+            red[k + j] = __dsqrt_rn(dsq);
+            red[2 * k + j] = sqrt(n32);
+            red[3 * k + j] = static_cast<double>(static_cast<float>(n32));
+        }
+        __syncthreads();
+    }
+    // (3) the last CTA: update_body's block reduction over the per-cluster values
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double inertia_part = 0.0, dmax = 0.0, cmax = 0.0, cnmax = 0.0;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        inertia_part += __ldcg(red + j);
+        dmax = fmax(dmax, __ldcg(red + k + j));
+        cmax = fmax(cmax, __ldcg(red + 2 * k + j));
+        cnmax = fmax(cnmax, __ldcg(red + 3 * k + j));
+    }
+    __shared__ double sh[32];
+    const double sx2_total = threadIdx.x == 0 ? a.rd_sx2[2] : 0.0;
+    inertia_part = warp_sum(inertia_part);
+    dmax = warp_max(dmax);
+    cmax = warp_max(cmax);
+    cnmax = warp_max(cnmax);
+    const int nw = (blockDim.x + 31) / 32;
+    if ((threadIdx.x & 31) == 0) {
+        const int w = threadIdx.x / 32;
+        sh[4 * w] = inertia_part;
+        sh[4 * w + 1] = dmax;
+        sh[4 * w + 2] = cmax;
+        sh[4 * w + 3] = cnmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double inertia = 0.0;
+        for (int w = 0; w < nw; ++w) {
+            inertia += sh[4 * w];
+            dmax = fmax(dmax, sh[4 * w + 1]);
+            cmax = fmax(cmax, sh[4 * w + 2]);
+            cnmax = fmax(cnmax, sh[4 * w + 3]);
+        }
+        a.trace[a.iter] = sx2_total + inertia;
+        a.disp[a.iter] = dmax;
+        a.flags[1] = a.iter + 1;
+        if (dmax < a.tol) a.flags[0] = 1;
+        a.bounds[0] = static_cast<float>(cmax) * (1.f + 0x1.0p-20f);
+        a.bounds[1] = static_cast<float>(cnmax) * (1.f + 0x1.0p-20f);
+        *ticket = 0u;  // the next launch starts from zero
+    }
+}
+
 static size_t update_smem(int k, int d) {
     const size_t kd = static_cast<size_t>(k) * d;
     const size_t bytes = kd <= UPD_MAX_KD ? (3 * kd + k) * sizeof(double) : 0;
@@ -2302,6 +2425,10 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
     double* gst = persist ? static_cast<double*>(ctx->slot("km_pgstats", sizeof(double) * 2 * S)) : nullptr;
     unsigned* tctr = persist ? static_cast<unsigned*>(ctx->slot("km_ptiles", sizeof(unsigned) * max_iter)) : nullptr;
     int8_t* plab = persist ? static_cast<int8_t*>(ctx->slot("km_plab", static_cast<size_t>(n_local))) : nullptr;
+    // multi-CTA update (per-iteration launches): per-cluster results + ticket
+    double* upd_red = static_cast<double*>(ctx->slot("km_upd_red", sizeof(double) * 4 * k));
+    unsigned* upd_ticket = static_cast<unsigned*>(ctx->slot("km_upd_ticket", sizeof(unsigned)));
+    DNDC_CUDA(cudaMemsetAsync(upd_ticket, 0, sizeof(unsigned), s));
     unsigned long long* pmarks = nullptr;
     if (persist && std::getenv("DNDC_PERSIST_TRACE")) {
         const int tg = std::max(PP.full.grid * PP.full.wg, PP.delta.grid * PP.delta.wg);  // virtual CTAs
@@ -2399,7 +2526,12 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
             if (ctx->world > 1) allgather_f64(ctx, b.stats, b.gathered, S, st);
             const UpdArgs ua = upd_args(b, k, m, ctx->world, ctx->world > 1 ? b.gathered : b.stats,
                                         use_delta ? b.running : nullptr, delta, it, tol);
-            kmeans_update_kernel<<<1, 256, update_smem(k, m), st>>>(ua);
+            if (m <= UPD_MC_MAXD && !std::getenv("DNDC_UPDATE_1CTA")) {
+                const int ug = std::min(k, ctx->num_sms);
+                kmeans_update_mc_kernel<<<ug, 256, sizeof(double) * 3 * m, st>>>(ua, upd_red, upd_ticket);
+            } else {
+                kmeans_update_kernel<<<1, 256, update_smem(k, m), st>>>(ua);
+            }
         }
     };
     if (ctx->group) {
