@@ -19,6 +19,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace dndc {
 
@@ -109,6 +110,115 @@ __global__ void kpp_update_kernel(const T* __restrict__ x, int64_t n, int m,
     }
     acc = warp_butterfly(acc);
     if (lane == 0) S[b] = acc;
+}
+
+// The same pass for 32-feature fp32 rows with the rows staged by TMA: the
+// per-lane float4 loads of kpp_update_kernel (lane = row, 128-byte rows) cost
+// 32 L1 wavefronts per warp instruction and bounded it near 4.2 TB/s.  Here
+// each warp streams its blocks in 64-row chunks (2-D TMA box {32, 64},
+// SWIZZLE_128B: chunk q of row r sits at q ^ (r & 7), so the lanes' 16-byte
+// shared-memory reads are conflict-free) through a KPP_NS-stage ring of its
+// own; lane l still takes rows l, l + 32 of every chunk, i.e. rows l, l + 32,
+// l + 64, ... of the block in order -- the same D2 values and the same sums.
+constexpr int KPP_WPB = 8, KPP_NS = 3, KPP_CH = 64;
+constexpr int KPP_CHUNK_BYTES = KPP_CH * 128;
+constexpr int KPP_TMA_SMEM = KPP_WPB * KPP_NS * KPP_CHUNK_BYTES + KPP_WPB * KPP_NS * 8 + 32 * 4 + 1024;
+
+__global__ void __launch_bounds__(32 * KPP_WPB, 1)
+    kpp_update_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t n, const float* __restrict__ crow,
+                          double* __restrict__ d2, int first, double* __restrict__ S, int64_t nblocks) {
+    extern __shared__ unsigned char kpp_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(kpp_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* ring = base + warp * KPP_NS * KPP_CHUNK_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + KPP_WPB * KPP_NS * KPP_CHUNK_BYTES) + warp * KPP_NS;
+    float* c_sh = reinterpret_cast<float*>(base + KPP_WPB * KPP_NS * KPP_CHUNK_BYTES + KPP_WPB * KPP_NS * 8);
+    if (threadIdx.x < 32) c_sh[threadIdx.x] = crow[threadIdx.x];
+    if (lane == 0) {
+        for (int st = 0; st < KPP_NS; ++st) tc::mbar_init(&bars[st], 1);
+        tc::mbar_fence_init();
+    }
+    __syncthreads();
+    float c[32];
+#pragma unroll
+    for (int f = 0; f < 32; ++f) c[f] = c_sh[f];
+
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * KPP_WPB + warp, tw = static_cast<int64_t>(gridDim.x) * KPP_WPB;
+    constexpr int CPB = KPP_BLOCK / KPP_CH;  // chunks per full block
+    // sequence index q of this warp -> (block, chunk); valid while inside the shard
+    auto item = [&](int64_t q, int64_t& b, int& ch) -> bool {
+        b = gw + (q / CPB) * tw;
+        ch = static_cast<int>(q % CPB);
+        return b < nblocks && b * KPP_BLOCK + static_cast<int64_t>(ch) * KPP_CH < n;
+    };
+    auto issue = [&](int64_t q) {
+        int64_t b;
+        int ch;
+        if (!item(q, b, ch)) return;
+        const int st = static_cast<int>(q % KPP_NS);
+        tc::fence_async_smem();
+        tc::mbar_expect_tx(&bars[st], KPP_CHUNK_BYTES);
+        tc::tma_load_2d(ring + st * KPP_CHUNK_BYTES, &map, &bars[st], 0,
+                        static_cast<int>(b * KPP_BLOCK + static_cast<int64_t>(ch) * KPP_CH));
+    };
+    if (lane == 0)
+        for (int64_t q = 0; q < KPP_NS; ++q) issue(q);
+    double acc = 0.0;
+    for (int64_t q = 0;; ++q) {
+        int64_t b;
+        int ch;
+        if (!item(q, b, ch)) break;
+        const int st = static_cast<int>(q % KPP_NS);
+        tc::mbar_wait(&bars[st], static_cast<uint32_t>((q / KPP_NS) & 1));
+        const unsigned char* buf = ring + st * KPP_CHUNK_BYTES;
+        const int64_t lo = b * KPP_BLOCK, hi = min(n, lo + KPP_BLOCK);
+        const int64_t r0 = lo + static_cast<int64_t>(ch) * KPP_CH;
+        double va[2];
+        bool ok[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h;
+            const int64_t i = r0 + r;
+            ok[h] = i < hi;
+            float v[32];
+#pragma unroll
+            for (int qq = 0; qq < 8; ++qq) {
+                const float4 t = *reinterpret_cast<const float4*>(buf + r * 128 + ((qq ^ (r & 7)) << 4));
+                v[4 * qq] = t.x;
+                v[4 * qq + 1] = t.y;
+                v[4 * qq + 2] = t.z;
+                v[4 * qq + 3] = t.w;
+            }
+            double dd2 = 0.0;
+#pragma unroll
+            for (int f = 0; f < 32; ++f) {
+                const double dd = sub_rn(static_cast<double>(v[f]), static_cast<double>(c[f]));
+                dd2 = add_rn(dd2, mul_rn(dd, dd));
+            }
+            va[h] = dd2;
+        }
+        __syncwarp();
+        if (lane == 0) issue(q + KPP_NS);  // the stage is read: refill it
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t i = r0 + lane + 32 * h;
+            if (ok[h]) {
+                double v = va[h];
+                if (!first) {
+                    const double old = d2[i];
+                    v = v < old ? v : old;
+                }
+                d2[i] = v;
+                acc = add_rn(acc, v);
+            }
+        }
+        // last chunk of the block: its sum
+        if (ch == CPB - 1 || r0 + KPP_CH >= hi) {
+            const double t = warp_butterfly(acc);
+            if (lane == 0) S[b] = t;
+            acc = 0.0;
+        }
+    }
 }
 
 // One warp per group of 1024 blocks.
@@ -291,12 +401,26 @@ static void kmeanspp(dndc_ctx* ctx, const E* x, int64_t n_local, int64_t n_globa
     DNDC_CUDA(cudaStreamSynchronize(s));  // hgc staging reuse below
 
     const int wpb = 8;
+    // fp32 rows of 32 features, 16-byte aligned: the TMA-staged pass
+    const bool tma = std::is_same_v<E, float> && m == 32 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+                     n_local > 0 && !std::getenv("DNDC_KPP_NO_TMA");
+    CUtensorMap kmap{};
+    int tgrid = 0;
+    if (tma) {
+        kmap = make_tmap_2d_f32(x, static_cast<uint64_t>(n_local), 32, 128, 32, KPP_CH, true);
+        DNDC_CUDA(cudaFuncSetAttribute(kpp_update_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       KPP_TMA_SMEM));
+        tgrid = static_cast<int>(std::min<int64_t>(ceil_div(nblocks, static_cast<int64_t>(KPP_WPB)), ctx->num_sms));
+    }
     for (int j = 1; j < k; ++j) {
         if (nblocks > 0) {
             const unsigned g = static_cast<unsigned>(ceil_div(nblocks, wpb));
             const size_t sm = sizeof(E) * m;
             const bool a16 = reinterpret_cast<uintptr_t>(x) % 16 == 0;
-            if constexpr (std::is_same_v<E, float>) {
+            if (tma) {
+                kpp_update_tma_kernel<<<tgrid, 32 * KPP_WPB, KPP_TMA_SMEM, s>>>(
+                    kmap, n_local, reinterpret_cast<const float*>(crow), d2, j == 1, S, nblocks);
+            } else if constexpr (std::is_same_v<E, float>) {
                 if (m == 32 && a16) kpp_update_kernel<32, E><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
                 else if (m == 64 && a16) kpp_update_kernel<64, E><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);
                 else if (m == 16 && a16) kpp_update_kernel<16, E><<<g, 32 * wpb, sm, s>>>(x, n_local, m, crow, d2, j == 1, S, nblocks);

@@ -73,8 +73,11 @@ def test_cfg5_moments_full_size(comm, oracle):
     assert close(sp.mean, mean_ref, 1e-12) and close(sp.m2 / 2_000_000, var_ref, 1e-12)
 
 
-@pytest.mark.parametrize("n,m,k,seed", [(5000, 8, 8, 11), (70_001, 32, 8, 3), (3, 2, 3, 1), (2048 * 1024 + 77, 4, 5, 9)])
+@pytest.mark.parametrize("n,m,k,seed", [(5000, 8, 8, 11), (70_001, 32, 8, 3), (3, 2, 3, 1), (2048 * 1024 + 77, 4, 5, 9),
+                                        (40, 32, 3, 5), (2 * 2048 + 64, 32, 4, 2), (2048 * 700 + 1, 32, 6, 8)])
 def test_kmeanspp_matches_oracle(comm, oracle, n, m, k, seed):
+    # m = 32 fp32 rows take the TMA-staged pass (kpp_update_tma_kernel): a shard
+    # shorter than one 64-row chunk, whole blocks + one chunk, more blocks than warps
     xh = oracle.uniform_f32(n, m, seed + 100)
     x = dnd.from_global(xh, (n, m), 0, comm)
     got = dnd.kmeanspp_indices(x, k, seed)
