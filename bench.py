@@ -369,7 +369,7 @@ def secondary_configs(dnd, _lib, comm, stream, barrier, dist, local, world, peak
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak * world, "unit": "GB/s",
                          "frac": gbs / (peak * world),
                          "algorithmic_bytes": byt, "bytes_rule": "(k-1) D^2 passes x (X read + f64 D^2 read/write)",
-                         "kernel": "kpp_update_kernel (fused D^2 update + block sums)"}}
+                         "kernel": "kpp_update_tma_kernel (fused D^2 update + block sums, TMA-staged rows)"}}
         del a5
     except Exception as exc:
         out.setdefault("moments_cfg5", {"error": f"{type(exc).__name__}: {exc}"[:300]})
