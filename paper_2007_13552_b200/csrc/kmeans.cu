@@ -1474,7 +1474,7 @@ __global__ void __launch_bounds__(256) kmeans_update_kernel(UpdArgs a) {
 // then the warps in order), so the results are bit-identical to it.  The
 // single-CTA kernel took ~27 us per cfg3 iteration (a latency chain: 64-step
 // loops over 64 clusters on two warps); this one a few.
-constexpr int UPD_MC_MAXD = 2048;
+constexpr int UPD_MC_MAXD = 1024;  // 3 d doubles of dynamic shared memory: 24 KB at most
 __global__ void __launch_bounds__(256) kmeans_update_mc_kernel(UpdArgs a, double* red, unsigned* ticket) {
     if (a.flags[0]) return;
     const int k = a.k, d = a.d, dpad = a.dpad, world = a.world, KD = k * d;
