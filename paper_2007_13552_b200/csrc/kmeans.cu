@@ -2363,7 +2363,7 @@ static void kmeans_fit(dndc_ctx* ctx, const T* x_local, int64_t n_local, int64_t
         // one collective for the validation stats and the initial centroids
         // (the k seeded rows, each owned by one rank: cluster.cpp:60-81)
         const int km = k * m;
-        double* pre = static_cast<double*>(ctx->slot("km_pre", sizeof(double) * (2 + km)));
+        double* pre = static_cast<double*>(ctx->slot("km_pre_init", sizeof(double) * (2 + km)));
         double* pre_all = static_cast<double*>(ctx->slot("km_pre_all", sizeof(double) * (2 + km) * ctx->world));
         const auto idx = init_indices(n_global, k, seed);
         int64_t* didx = static_cast<int64_t*>(ctx->slot("km_idx", sizeof(int64_t) * k));
